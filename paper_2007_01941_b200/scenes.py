@@ -1,0 +1,383 @@
+"""Seeded synthetic scenes for the five BASELINE.json configurations.
+
+The reference ships only a grid-city generator (`pkg/src/bamg/synth.py:506-558`);
+the benchmark scenes are new and follow SURVEY.md Appendix C, which resolves the
+ambiguous sentences of BASELINE.json (ring visibility window, street run
+placement, depth / field-of-view limits, centre-preserving noise).
+
+Shared conventions (Appendix C):
+
+* one ``np.random.default_rng(seed)`` per scene, draws in a fixed order;
+* camera frame z_c = -look, x_c = unit(up x z_c), y_c = z_c x x_c, R = rows,
+  t = -R c (the frame of `pkg/tests/conftest.py:33-41`);
+* f = 500, k1, k2 ~ N(0, 1e-2) (sigma; "N(0,1e-4)" read as a variance);
+* pixels = exact projection + N(0, 1 px);
+* initial guess: rotation <- Rot(xi) R with xi ~ N(0, 1e-2), centre + N(0, 1e-2),
+  t recomputed; points + N(0, 5e-2) (the centre-preserving convention of
+  `synth.py:449-463`);
+* every kept observation has depth >= 1 and normalised radius |p| <= 2 at the
+  ground truth and lies in front of its camera at the initial guess; points
+  with fewer than two cameras and cameras with no observation are dropped.
+
+Everything here is host-side input generation (numpy / scipy.spatial), not part
+of the measured path.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import hashlib
+
+import numpy as np
+from scipy.spatial import cKDTree
+from scipy.spatial.transform import Rotation
+
+FOCAL = 500.0
+MAX_RADIUS = 2.0
+MIN_DEPTH = 1.0
+
+
+@dataclasses.dataclass
+class Scene:
+    """Problem arrays in the reference's `BundleProblem` layout (problem.py:81-107)."""
+
+    name: str
+    camera_params: np.ndarray  # (nc, 9) initial guess
+    points: np.ndarray  # (np, 3) initial guess
+    cam_index: np.ndarray  # (k,) int64
+    pt_index: np.ndarray  # (k,) int64
+    pixels: np.ndarray  # (k, 2)
+    truth_cameras: np.ndarray | None = None
+    truth_points: np.ndarray | None = None
+    notes: str = ""
+
+    @property
+    def n_cameras(self) -> int:
+        return self.camera_params.shape[0]
+
+    @property
+    def n_points(self) -> int:
+        return self.points.shape[0]
+
+    @property
+    def n_observations(self) -> int:
+        return len(self.cam_index)
+
+    def digest(self) -> str:
+        h = hashlib.sha256()
+        for a in (self.camera_params, self.points, self.cam_index, self.pt_index, self.pixels):
+            h.update(np.ascontiguousarray(a).tobytes())
+        return h.hexdigest()[:16]
+
+    def arrays(self):
+        return (self.camera_params, self.points, self.cam_index, self.pt_index, self.pixels)
+
+
+# -- geometry helpers ---------------------------------------------------------
+
+
+def look_frames(centers: np.ndarray, looks: np.ndarray) -> np.ndarray:
+    """Rotation matrices (rows x_c, y_c, z_c) for cameras looking along ``looks``."""
+    z = -looks / np.linalg.norm(looks, axis=1, keepdims=True)
+    up = np.array([0.0, 0.0, 1.0])
+    x = np.cross(up[None, :], z)
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    y = np.cross(z, x)
+    return np.stack([x, y, z], axis=1)
+
+
+def _project_truth(R, t, f, k1, k2, cam, X):
+    """Camera-frame coordinates and pixels of points X seen by cameras ``cam``."""
+    pc = np.einsum("kij,kj->ki", R[cam], X) + t[cam]
+    z = pc[:, 2]
+    p = -pc[:, :2] / z[:, None]
+    n2 = np.einsum("ki,ki->k", p, p)
+    dist = 1.0 + k1[cam] * n2 + k2[cam] * n2 * n2
+    pix = (f[cam] * dist)[:, None] * p
+    return pc, p, pix
+
+
+def _finish(name, rng, centers, R, pts_true, cam, pt, notes=""):
+    """Filter observations, drop weak points / empty cameras, add noise, perturb."""
+    nc = centers.shape[0]
+    k1 = rng.normal(0.0, 1e-2, nc)
+    k2 = rng.normal(0.0, 1e-2, nc)
+    f = np.full(nc, FOCAL)
+    t = -np.einsum("nij,nj->ni", R, centers)
+
+    pc, p, _ = _project_truth(R, t, f, k1, k2, cam, pts_true[pt])
+    depth = -pc[:, 2]
+    ok = (depth >= MIN_DEPTH) & (np.max(np.abs(p), axis=1) <= MAX_RADIUS) & (
+        np.einsum("ki,ki->k", p, p) <= MAX_RADIUS**2
+    )
+    cam, pt = cam[ok], pt[ok]
+    # points seen at least twice, cameras seeing at least one point (multigrid.py:66-71)
+    for _ in range(4):
+        pc_cnt = np.bincount(pt, minlength=pts_true.shape[0])
+        keep = pc_cnt[pt] >= 2
+        cam, pt = cam[keep], pt[keep]
+        if keep.all():
+            break
+    used_pts = np.flatnonzero(np.bincount(pt, minlength=pts_true.shape[0]) > 0)
+    used_cams = np.flatnonzero(np.bincount(cam, minlength=nc) > 0)
+    pt_map = np.full(pts_true.shape[0], -1, np.int64)
+    pt_map[used_pts] = np.arange(len(used_pts))
+    cam_map = np.full(nc, -1, np.int64)
+    cam_map[used_cams] = np.arange(len(used_cams))
+    cam, pt = cam_map[cam], pt_map[pt]
+    centers, R, t, f, k1, k2 = (a[used_cams] for a in (centers, R, t, f, k1, k2))
+    pts_true = pts_true[used_pts]
+    nc, npts, k = len(used_cams), len(used_pts), len(cam)
+
+    # observation order: sorted by (point, camera) -- the reference keeps whatever
+    # order it is given (problem.py:84-86); the GPU path never relies on it.
+    order = np.lexsort((cam, pt))
+    cam, pt = cam[order].astype(np.int64), pt[order].astype(np.int64)
+
+    _, _, pix = _project_truth(R, t, f, k1, k2, cam, pts_true[pt])
+    pixels = pix + rng.normal(0.0, 1.0, pix.shape)
+
+    aa_true = Rotation.from_matrix(R).as_rotvec()
+    truth = np.concatenate([aa_true, t, f[:, None], k1[:, None], k2[:, None]], axis=1)
+
+    xi = rng.normal(0.0, 1e-2, (nc, 3))
+    rot0 = Rotation.from_rotvec(xi) * Rotation.from_matrix(R)
+    R0 = rot0.as_matrix()
+    c0 = centers + rng.normal(0.0, 1e-2, (nc, 3))
+    t0 = -np.einsum("nij,nj->ni", R0, c0)
+    cams0 = np.concatenate([rot0.as_rotvec(), t0, f[:, None], k1[:, None], k2[:, None]], axis=1)
+    pts0 = pts_true + rng.normal(0.0, 5e-2, pts_true.shape)
+
+    # the initial guess must evaluate (problem.py:211-213); drop the rare violators
+    z0 = np.einsum("kij,kj->ki", R0[cam], pts0[pt])[:, 2] + t0[cam, 2]
+    bad = z0 >= -1e-3
+    if bad.any():
+        keep = ~bad
+        cam, pt, pixels = cam[keep], pt[keep], pixels[keep]
+        notes += f" dropped {int(bad.sum())} obs behind at init;"
+    return Scene(name, cams0, pts0, cam, pt, pixels, truth, pts_true, notes.strip())
+
+
+# -- configs ------------------------------------------------------------------
+
+
+def ring(seed: int = 0, n_cameras: int = 49, n_points: int = 7776,
+         window_deg: float = 15.0) -> Scene:
+    """Config 1: cameras on a radius-10 circle looking at the origin (App. C.1)."""
+    rng = np.random.default_rng(seed)
+    theta = 2.0 * np.pi * np.arange(n_cameras) / n_cameras
+    centers = np.stack([10 * np.cos(theta), 10 * np.sin(theta), np.zeros(n_cameras)], 1)
+    R = look_frames(centers, -centers)
+    pts = rng.uniform(-2.0, 2.0, (n_points, 3))
+    az = np.arctan2(pts[:, 1], pts[:, 0])
+    d = np.angle(np.exp(1j * (theta[None, :] - az[:, None])))
+    pt_i, cam_i = np.nonzero(np.abs(d) <= np.deg2rad(window_deg))
+    return _finish("ring", rng, centers, R, pts, cam_i, pt_i,
+                   f"azimuth window +-{window_deg} deg")
+
+
+def street(seed: int = 0, n_cameras: int = 500, n_points: int = 150_000) -> Scene:
+    """Config 2: cameras along x looking +y, runs of 2+Geometric(0.35) (App. C.2)."""
+    rng = np.random.default_rng(seed)
+    centers = np.stack([np.arange(n_cameras, dtype=float), np.zeros(n_cameras),
+                        np.zeros(n_cameras)], 1)
+    R = look_frames(centers, np.tile([0.0, 1.0, 0.0], (n_cameras, 1)))
+    lo = np.array([0.0, 5.0, -5.0])
+    hi = np.array([float(n_cameras), 25.0, 5.0])
+    pts = rng.uniform(lo, hi, (n_points, 3))
+    L = np.minimum(2 + rng.geometric(0.35, n_points), n_cameras)
+    start = np.clip(np.round(pts[:, 0]).astype(np.int64) - L // 2, 0, n_cameras - L)
+    pt_i = np.repeat(np.arange(n_points), L)
+    off = np.arange(L.sum()) - np.repeat(np.cumsum(L) - L, L)
+    cam_i = np.repeat(start, L) + off
+    return _finish("street", rng, centers, R, pts, cam_i, pt_i, "L=2+geometric(0.35)")
+
+
+def _horizontal_looks(yaw):
+    return np.stack([np.cos(yaw), np.sin(yaw), np.zeros_like(yaw)], 1)
+
+
+def _nearest_visible(rng, centers, R, pts, k_nn, radius, n_pick, min_depth_frac=0.2,
+                     chunk=200_000):
+    """First ``n_pick`` in-front candidates among the ``k_nn`` nearest cameras."""
+    tree = cKDTree(centers[:, :2])
+    cams_out, pts_out = [], []
+    for lo in range(0, pts.shape[0], chunk):
+        P = pts[lo:lo + chunk]
+        dist, idx = tree.query(P[:, :2], k=k_nn, distance_upper_bound=radius, workers=-1)
+        valid = np.isfinite(dist)
+        idx = np.where(valid, idx, 0)
+        rel = P[:, None, :] - centers[idx]
+        Rk = R[idx]
+        pz = np.einsum("nkj,nkj->nk", Rk[:, :, 2, :], rel)
+        px = np.einsum("nkj,nkj->nk", Rk[:, :, 0, :], rel)
+        py = np.einsum("nkj,nkj->nk", Rk[:, :, 1, :], rel)
+        depth = -pz
+        d3 = np.linalg.norm(rel, axis=2)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            pr = np.maximum(np.abs(px), np.abs(py)) / np.maximum(depth, 1e-9)
+        ok = valid & (depth >= np.maximum(MIN_DEPTH, min_depth_frac * d3)) & (
+            pr <= 0.95 * MAX_RADIUS)
+        rank = np.cumsum(ok, axis=1)
+        take = ok & (rank <= n_pick[lo:lo + chunk, None])
+        pt_i, slot = np.nonzero(take)
+        cams_out.append(idx[pt_i, slot])
+        pts_out.append(pt_i + lo)
+    return np.concatenate(cams_out), np.concatenate(pts_out)
+
+
+def city(seed: int = 0, n_cameras: int = 4000, n_points: int = 1_000_000,
+         side: float = 200.0, radius: float = 15.0) -> Scene:
+    """Config 3: uniform plane, random yaw, 2+Poisson(4) nearest in range (App. C.3)."""
+    rng = np.random.default_rng(seed)
+    centers = np.stack([rng.uniform(0, side, n_cameras), rng.uniform(0, side, n_cameras),
+                        np.full(n_cameras, 1.5)], 1)
+    yaw = rng.uniform(0, 2 * np.pi, n_cameras)
+    R = look_frames(centers, _horizontal_looks(yaw))
+    pts = np.stack([rng.uniform(0, side, n_points), rng.uniform(0, side, n_points),
+                    rng.uniform(0, 20.0, n_points)], 1)
+    n_pick = 2 + rng.poisson(4.0, n_points)
+    cam_i, pt_i = _nearest_visible(rng, centers, R, pts, 48, radius, n_pick)
+    return _finish("city", rng, centers, R, pts, cam_i, pt_i,
+                   f"range {radius}, 48 nearest, depth>=max(1,0.2 d)")
+
+
+def _large_chunk(args):
+    seed, lo, P, n_pick, tree, centers, R, k_nn, radius = args
+    rng = np.random.default_rng([seed, 7, lo])
+    dist, idx = tree.query(P[:, :2], k=k_nn, distance_upper_bound=radius)
+    valid = np.isfinite(dist)
+    idx = np.where(valid, idx, 0)
+    rel = P[:, None, :] - centers[idx]
+    Rk = R[idx]
+    pz = np.einsum("nkj,nkj->nk", Rk[:, :, 2, :], rel)
+    depth = -pz
+    ok = valid & (depth >= np.maximum(MIN_DEPTH, 0.2 * np.linalg.norm(rel, axis=2)))
+    lim = 0.95 * MAX_RADIUS * depth
+    ok &= np.abs(np.einsum("nkj,nkj->nk", Rk[:, :, 0, :], rel)) <= lim
+    ok &= np.abs(np.einsum("nkj,nkj->nk", Rk[:, :, 1, :], rel)) <= lim
+    key = np.where(ok, rng.random(ok.shape), 2.0)
+    order = np.argsort(key, axis=1)
+    rank = np.empty_like(order)
+    np.put_along_axis(rank, order, np.arange(k_nn)[None, :].repeat(len(P), 0), axis=1)
+    take = ok & (rank < n_pick[:, None])
+    pt_i, slot = np.nonzero(take)
+    return idx[pt_i, slot], pt_i + lo
+
+
+def large(seed: int = 0, n_clusters: int = 40, cams_per_cluster: int = 325,
+          n_points: int = 4_500_000, k_nearest: int = 160, threads: int | None = None
+          ) -> Scene:
+    """Config 4: 40 Gaussian camera clusters, 2+Poisson(4.5) cameras (App. C.4).
+
+    Each point draws 2+Poisson(4.5) cameras without replacement from the in-front,
+    |p| <= 2 cameras among its ``k_nearest`` nearest (its own and neighbouring
+    clusters). ``k_nearest`` = 160 is the App. C.4 calibration: it puts S at
+    ~163 blocks per row (~2.1 M blocks at full size). The sample used for bounded
+    CPU timing keeps the per-cluster structure and shrinks ``n_clusters`` and
+    ``n_points`` proportionally. Candidate evaluation runs chunked over a thread
+    pool; every chunk draws from its own seeded stream, so the result does not
+    depend on the thread count.
+    """
+    import concurrent.futures as cf
+    import os
+
+    rng = np.random.default_rng(seed)
+    centres = rng.uniform(0, 1000.0, (n_clusters, 2))
+    nc = n_clusters * cams_per_cluster
+    cl = np.repeat(np.arange(n_clusters), cams_per_cluster)
+    xy = centres[cl] + rng.normal(0.0, 5.0, (nc, 2))
+    centers = np.concatenate([xy, np.full((nc, 1), 1.5)], 1)
+    yaw = rng.uniform(0, 2 * np.pi, nc)
+    R = look_frames(centers, _horizontal_looks(yaw))
+    pcl = rng.integers(0, n_clusters, n_points)
+    pxy = centres[pcl] + rng.normal(0.0, 10.0, (n_points, 2))
+    pts = np.concatenate([pxy, rng.uniform(0, 20.0, (n_points, 1))], 1)
+    n_pick = 2 + rng.poisson(4.5, n_points)
+    tree = cKDTree(centers[:, :2])
+    chunk = 50_000
+    jobs = [(seed, lo, pts[lo:lo + chunk], n_pick[lo:lo + chunk], tree, centers, R,
+             k_nearest, 60.0) for lo in range(0, n_points, chunk)]
+    with cf.ThreadPoolExecutor(threads or os.cpu_count()) as ex:
+        res = list(ex.map(_large_chunk, jobs))
+    cam_i = np.concatenate([r[0] for r in res])
+    pt_i = np.concatenate([r[1] for r in res])
+    return _finish("large", rng, centers, R, pts, cam_i, pt_i,
+                   f"k_nearest={k_nearest}, clusters={n_clusters}")
+
+
+def loop(seed: int = 0, n_cameras: int = 8000, n_points: int = 2_000_000,
+         bridge_frac: float = 0.005) -> Scene:
+    """Config 5: closed loop, forward-looking cameras, runs 7-10 behind (App. C.5)."""
+    rng = np.random.default_rng(seed)
+    rad = n_cameras / (2 * np.pi)
+    phi = np.arange(n_cameras) / rad
+    centers = np.stack([rad * np.cos(phi), rad * np.sin(phi), np.zeros(n_cameras)], 1)
+    tangent = np.stack([-np.sin(phi), np.cos(phi), np.zeros(n_cameras)], 1)
+    R = look_frames(centers, tangent)
+    s = rng.uniform(0, n_cameras, n_points)
+    rr = 10.0 * np.sqrt(rng.uniform(0, 1, n_points))
+    ang = rng.uniform(0, 2 * np.pi, n_points)
+    radial, height = rr * np.cos(ang), rr * np.sin(ang)
+    ps = s / rad
+    pts = np.stack([(rad + radial) * np.cos(ps), (rad + radial) * np.sin(ps), height], 1)
+    L = 2 + rng.geometric(0.5, n_points)
+    behind = rng.integers(7, 11, n_points)
+    pt_i = np.repeat(np.arange(n_points), L)
+    off = np.arange(L.sum()) - np.repeat(np.cumsum(L) - L, L)
+    cam_i = (np.floor(s).astype(np.int64)[pt_i] - behind[pt_i] - off) % n_cameras
+    nb = int(round(bridge_frac * n_points))
+    bp = rng.choice(n_points, nb, replace=False)
+    bc = (np.floor(s[bp]).astype(np.int64) - rng.integers(51, 101, nb)) % n_cameras
+    cam_i = np.concatenate([cam_i, bc])
+    pt_i = np.concatenate([pt_i, bp])
+    pair = np.unique(pt_i * n_cameras + cam_i)
+    pt_i, cam_i = pair // n_cameras, pair % n_cameras
+    return _finish("loop", rng, centers, R, pts, cam_i, pt_i,
+                   "L=2+geometric(0.5) (numpy support>=1), runs 7-10 behind")
+
+
+CONFIGS = {1: ring, 2: street, 3: city, 4: large, 5: loop}
+
+
+def config(n: int, **kw) -> Scene:
+    return CONFIGS[n](**kw)
+
+
+def random_problem(seed, n_cameras=5, n_points=15, pixel_noise=0.5, decoupled=False):
+    """Small ring problem with the shape of the reference test builder.
+
+    Same geometry recipe as `pkg/tests/conftest.py:10-70` (cameras on a radius-10
+    circle looking at a U[-2,2]^3 cloud, focal 500 +- 50, every point seen by at
+    least two cameras), re-expressed with vectorised draws; it is used for small
+    parity cases only.
+    """
+    rng = np.random.default_rng(seed)
+    groups = 2 if decoupled else 1
+    shift = np.array([60.0, 0.0, 0.0])
+    g_cam = np.arange(n_cameras) % groups
+    ang = 2 * np.pi * np.arange(n_cameras) / n_cameras + rng.uniform(-0.1, 0.1, n_cameras)
+    centers = np.stack([10 * np.cos(ang), 10 * np.sin(ang), rng.uniform(-1, 1, n_cameras)], 1)
+    centers += g_cam[:, None] * shift
+    R = look_frames(centers, g_cam[:, None] * shift - centers)
+    aa = Rotation.from_matrix(R).as_rotvec()
+    t = -np.einsum("nij,nj->ni", R, centers)
+    f = 500.0 + rng.uniform(-50, 50, n_cameras)
+    k1 = rng.uniform(-0.05, 0.0, n_cameras)
+    k2 = rng.uniform(0.0, 0.01, n_cameras)
+    cams = np.concatenate([aa, t, f[:, None], k1[:, None], k2[:, None]], 1)
+    pts = rng.uniform(-2, 2, (n_points, 3))
+    g_pt = np.arange(n_points) % groups
+    pts += g_pt[:, None] * shift
+    ci, pi = [], []
+    for p in range(n_points):
+        pool = np.flatnonzero(g_cam == g_pt[p])
+        m = rng.integers(2, len(pool) + 1)
+        sel = np.sort(rng.choice(pool, size=m, replace=False))
+        ci.extend(sel.tolist())
+        pi.extend([p] * m)
+    ci, pi = np.asarray(ci, np.int64), np.asarray(pi, np.int64)
+    _, _, pix = _project_truth(R, t, f, k1, k2, ci, pts[pi])
+    if pixel_noise:
+        pix = pix + rng.normal(0, pixel_noise, pix.shape)
+    return Scene("random", cams, pts, ci, pi, pix)
