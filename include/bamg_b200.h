@@ -1,0 +1,188 @@
+/*
+ * libbamg_b200 -- C ABI of the B200-native LM linear-solve path of arXiv 2007.01941.
+ *
+ * The reference (`/root/reference/pkg/src/bamg`, Python + numpy/scipy) has no
+ * native boundary of its own: every entry point below replaces a reference Python
+ * function (cited file:line) whose arithmetic ran in numpy / scipy.sparse / LAPACK.
+ * All pointers are DEVICE pointers unless named *_host; sizes are element counts;
+ * `stream` is a cudaStream_t (NULL = legacy default stream). Buffers are owned by
+ * the caller; the library allocates only stream-ordered scratch inside a call and
+ * the small workspace in `bamg_ctx`.
+ *
+ * Return value: 0 = ok, >0 = domain error (see the BAMG_ERR_* codes; index
+ * out-parameters carry details), <0 = CUDA / launch error. `bamg_last_error`
+ * returns the thread-local message of the last failure.
+ *
+ * Layout: observations are stored point-major (sorted by (point, camera));
+ * `cm_list` gives the point-major position of each observation in (camera, point)
+ * order (the reference's W block order). Block matrices are BSR with int32
+ * row pointers / column indices sorted per row and row-major fp64 blocks.
+ */
+#ifndef BAMG_B200_H
+#define BAMG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BAMG_ABI_VERSION 1
+
+#define BAMG_OK 0
+#define BAMG_ERR_INDEFINITE 1   /* IndefiniteBlockError (blockmat.py:25-39) */
+#define BAMG_ERR_BEHIND 2       /* BehindCameraError (problem.py:28-36) */
+#define BAMG_ERR_NOT_PD 3       /* coarsest operator not PD (multigrid.py:434-440) */
+#define BAMG_ERR_UNSUPPORTED 4  /* size outside the kernels' supported range */
+#define BAMG_ERR_CUDA (-1)
+
+typedef struct bamg_ctx bamg_ctx;
+
+int bamg_version(void);
+bamg_ctx* bamg_ctx_create(void);
+void bamg_ctx_destroy(bamg_ctx* ctx);
+int bamg_last_error(char* buf, size_t n);
+
+/* ---- primitives (replace numpy lexsort / cumsum / dot used across the path) ---- */
+int bamg_scan_exclusive_i32(bamg_ctx* ctx, const int32_t* in, int32_t* out, int64_t n, int32_t* total,
+                            void* stream);
+int bamg_sort_pairs_u32(bamg_ctx* ctx, const uint32_t* kin, const uint32_t* vin, uint32_t* kout,
+                        uint32_t* vout, int64_t n, int key_bits, void* stream);
+int bamg_segment_ptr(bamg_ctx* ctx, const int32_t* sorted_ids, int64_t n, int32_t nseg, int32_t* ptr,
+                     void* stream);
+int bamg_gather_rows_f64(bamg_ctx* ctx, const double* src, const int32_t* idx, int64_t n, int32_t width,
+                         double* dst, void* stream);
+int bamg_scatter_rows_f64(bamg_ctx* ctx, const double* src, const int32_t* idx, int64_t n, int32_t width,
+                          double* dst, void* stream);
+int bamg_gather_i32(bamg_ctx* ctx, const int32_t* src, const int32_t* idx, int64_t n, int32_t* dst,
+                    void* stream);
+int bamg_dot(bamg_ctx* ctx, const double* x, const double* y, int64_t n, double* out_dev, void* stream);
+int bamg_absmax(bamg_ctx* ctx, const double* x, int64_t n, double* out_dev, void* stream);
+int bamg_axpby(bamg_ctx* ctx, double a, const double* x, double b, double* y, int64_t n, void* stream);
+int bamg_negate(bamg_ctx* ctx, const double* a, double* b, int64_t n, void* stream);
+
+/* ---- observation structure (problem.py:81-107 keeps input order; this is the
+ *      device layout) and covisibility (schur.py:147-159, multigrid.py:52-80) ---- */
+int bamg_obs_orders(bamg_ctx* ctx, const int32_t* cam_idx, const int32_t* pt_idx, int64_t k, int32_t nc,
+                    int32_t npt, int32_t* pm_perm, int32_t* obs_cam_pm, int32_t* obs_pt_pm, int32_t* pt_ptr,
+                    int32_t* cm_list, int32_t* cam_ptr, void* stream);
+int bamg_covis_count(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* obs_pt_pm,
+                     const int32_t* pt_ptr, const int32_t* obs_cam_pm, int32_t nc, int32_t* row_counts,
+                     void* stream);
+int bamg_covis_fill(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* obs_pt_pm,
+                    const int32_t* pt_ptr, const int32_t* obs_cam_pm, int32_t nc, const int32_t* S_ptr,
+                    int32_t* S_col, void* stream);
+int bamg_shared_counts(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* obs_pt_pm,
+                       const int32_t* pt_ptr, const int32_t* obs_cam_pm, int32_t nc, const int32_t* S_ptr,
+                       const int32_t* S_col, int32_t max_row, int32_t* shared_cnt, void* stream);
+/* multigrid.py:52-80 visibility_strength; flags_dev[0] = cameras with no points,
+ * flags_dev[1] = int8-wrapped covisibility block count (schur.py:151-159). */
+int bamg_visibility_strength(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* S_ptr, const int32_t* S_col,
+                             const int32_t* shared_cnt, int32_t nc, int32_t* deg, int32_t* G_ptr, int32_t* G_col,
+                             double* G_val, int32_t* flags_dev, void* stream);
+
+/* ---- residuals / Jacobians: problem.py:202-219 (_project_arrays), 272-326 (evaluate) ---- */
+int bamg_evaluate(bamg_ctx* ctx, const double* cams, const double* pts, const int32_t* obs_cam,
+                  const int32_t* obs_pt, const double* pixels, int64_t k, int32_t huber, int32_t with_jacobian,
+                  double* F, double* E, double* res, double* w, uint8_t* behind, double* objective_dev,
+                  int32_t* n_behind_dev, void* stream);
+
+/* ---- normal blocks / damping / reduced system: problem.py:255-269, schur.py:38-47, 99-125 ---- */
+int bamg_normal_blocks(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* pt_ptr,
+                       const double* F, const double* E, const double* res, int32_t nc, int32_t npt,
+                       double* A_raw, double* g_cam, double* C_raw, double* g_pt, void* stream);
+int bamg_damping(bamg_ctx* ctx, const double* A_raw, const double* C_raw, int32_t nc, int32_t npt, double radius,
+                 double* d_cam, double* d_pt, void* stream);
+int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* pt_ptr,
+                      const double* F, const double* E, const double* A_raw, const double* C_raw,
+                      const double* g_cam, const double* g_pt, const double* d_cam, const double* d_pt,
+                      int32_t nc, int32_t npt, double* A, double* C, double* Cinv, double* Cb, double* H,
+                      double* qo, double* rhs, int32_t* bad_min_dev, void* stream);
+/* schur.py:84-86 implicit_matvec */
+int bamg_implicit_matvec(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* pt_ptr,
+                         const int32_t* obs_cam_pm, const double* F, const double* E, const double* A,
+                         const double* Cinv, const double* x, int32_t nc, int32_t npt, double* qo, double* y,
+                         void* stream);
+/* schur.py:171-173 back_substitute */
+int bamg_back_substitute(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs_cam_pm, const double* F,
+                         const double* E, const double* Cinv, const double* grad_pt, const double* dc,
+                         int32_t npt, double* dp, void* stream);
+/* schur.py:114-116 W blocks in reference BSR order (API view) */
+int bamg_materialize_W(bamg_ctx* ctx, const int32_t* cm_list, const double* F, const double* E, int64_t k,
+                       double* W, void* stream);
+
+/* ---- explicit S: schur.py:128-144 (+ blockmat.py:308-353) ---- */
+int bamg_schur_symbolic_sizes(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* S_ptr, const int32_t* S_col,
+                              int32_t nc, int32_t npt, int32_t* pair_off, int32_t* dpos, int32_t* up_off,
+                              int64_t* out_host, void* stream);
+int bamg_schur_symbolic(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs_cam_pm, const int32_t* S_ptr,
+                        const int32_t* S_col, int32_t nc, int32_t npt, int64_t nnz, const int32_t* pair_off,
+                        int64_t n_pairs, const int32_t* dpos, const int32_t* up_off, int32_t* pair_a,
+                        int32_t* pair_b, int32_t* blk_pair_ptr, int32_t* up_blk, int32_t* up_row,
+                        int32_t* up_tpos, void* stream);
+int bamg_schur_numeric(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const double* F,
+                       const double* E, const double* H, const double* A, const int32_t* dpos, int32_t nc,
+                       const int32_t* up_blk, const int32_t* up_tpos, int32_t n_up, const int32_t* blk_pair_ptr,
+                       const int32_t* pair_a, const int32_t* pair_b, double* S, void* stream);
+
+/* ---- BSR kernels: blockmat.py:295-299 (matvec), 91-129 (block-diagonal), 270-282 ---- */
+int bamg_bsr_spmv(bamg_ctx* ctx, int32_t bs, const int32_t* ptr, const int32_t* col, const double* blocks,
+                  const double* x, double* y, int32_t nbr, double* dot_out_dev, void* stream);
+int bamg_bsr_residual(bamg_ctx* ctx, int32_t bs, const int32_t* ptr, const int32_t* col, const double* blocks,
+                      const double* x, const double* b, double* r, int32_t nbr, void* stream);
+int bamg_block_chol_inv(bamg_ctx* ctx, const double* M, int32_t n, int32_t bs, double* L, double* inv,
+                        int32_t* bad_min_dev, void* stream);
+int bamg_blockdiag_apply(bamg_ctx* ctx, const double* M, const double* x, int32_t n, int32_t bs, double* y,
+                         void* stream);
+int bamg_diag_blocks(bamg_ctx* ctx, const int32_t* ptr, const int32_t* col, const double* blocks, int32_t nbr,
+                     int32_t bs, double* D, void* stream);
+
+/* ---- multigrid setup: multigrid.py:83-98, 127-176, 179-237, 409-471; problem.py:332-352 ---- */
+int bamg_operator_strength(bamg_ctx* ctx, const int32_t* ptr, const int32_t* col, const double* blocks, int32_t n,
+                           int64_t nnz, int32_t bs, double* nrm_work, double* dnorm_work, int32_t* G_ptr,
+                           int32_t* G_col, double* G_val, int32_t* flags_dev, void* stream);
+int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t* G_col, const double* G_val, int32_t n,
+                   int32_t max_size, int32_t* agg, int32_t* size_work, int32_t* n_agg_dev, void* stream);
+int bamg_aggregate_members(bamg_ctx* ctx, const int32_t* agg, int32_t n, int32_t n_agg, int32_t* agg_ptr,
+                           int32_t* members, void* stream);
+int bamg_gauge_nullspace(bamg_ctx* ctx, const double* cams, int32_t nc, double* K, void* stream);
+int bamg_prolongation_qr(bamg_ctx* ctx, const int32_t* agg_ptr, const int32_t* members, const double* K,
+                         int32_t n_agg, int32_t bs, int32_t max_members, double* Pblocks, double* Kc, int32_t* info,
+                         int32_t* padded_cnt, void* stream);
+int bamg_galerkin_pattern(bamg_ctx* ctx, const int32_t* agg_ptr, const int32_t* members, const int32_t* ptr,
+                          const int32_t* col, const int32_t* agg, int32_t n_agg, int32_t* Cptr_or_counts,
+                          int32_t* Ccol, void* stream);
+int bamg_galerkin_map(bamg_ctx* ctx, const int32_t* ptr, const int32_t* col, const int32_t* agg, int32_t n,
+                      int64_t nnz_fine, const int32_t* Cptr, const int32_t* Ccol, int64_t nnz_coarse,
+                      int32_t* fine_sorted, int32_t* cblk_ptr, int32_t* fine_row, void* stream);
+int bamg_galerkin_numeric(bamg_ctx* ctx, int32_t bs, const int32_t* cblk_ptr, const int32_t* fine_sorted,
+                          const int32_t* fine_row, const int32_t* col, const double* blocks, const double* P,
+                          int32_t n_agg, const int32_t* Cptr, const int32_t* Ccol, int64_t nnz_coarse,
+                          const int32_t* padded_cnt, double* out, void* stream);
+/* coarsest direct solve: multigrid.py:431-440 (cho_factor) / 477-478 (cho_solve) */
+int bamg_coarse_factor(bamg_ctx* ctx, const int32_t* ptr, const int32_t* col, const double* blocks, int32_t nbr,
+                       int32_t bs, double* dense, double* work, double* inv, int32_t* flag_dev, void* stream);
+int bamg_dense_gemv(bamg_ctx* ctx, const double* M, const double* x, int32_t n, double* y, void* stream);
+
+/* ---- smoother / V-cycle / PCG: multigrid.py:308-328, 474-483; solver.py:70-128 ---- */
+int bamg_cheb_step(bamg_ctx* ctx, int32_t bs, const int32_t* ptr, const int32_t* col, const double* blocks,
+                   const double* x_in, const double* b, const double* Dinv, double* d, double* x_out, int32_t nbr,
+                   double c1, double c2, int32_t divide, void* stream);
+int bamg_prolong(bamg_ctx* ctx, const int32_t* agg, const double* P, const double* xc, int32_t nf, int32_t bs,
+                 double* y, int32_t accumulate, void* stream);
+int bamg_restrict(bamg_ctx* ctx, const int32_t* agg_ptr, const int32_t* members, const double* P, const double* r,
+                  int32_t nagg, int32_t bs, double* bc, void* stream);
+int bamg_pcg_update(bamg_ctx* ctx, double* x, double* r, const double* p, const double* ap, double alpha,
+                    int64_t n, double* rr_dev, void* stream);
+int bamg_xpby(bamg_ctx* ctx, const double* z, double beta, double* p, int64_t n, void* stream);
+/* multigrid.py:281-284: largest eigenvalue of the Lanczos tridiagonal (host arrays) */
+double bamg_tridiag_max_eig(const double* a_host, const double* b_host, int32_t n);
+
+/* ---- driver helpers: rotation.py:124-137 canonicalize (solver.py:290, problem.py:106) ---- */
+int bamg_canonicalize(bamg_ctx* ctx, double* cams, int32_t n, int32_t stride, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BAMG_B200_H */

@@ -1,0 +1,540 @@
+// Block-sparse kernels for the solve phase: BSR SpMV (9x9 / 16x16, fused dot),
+// fused Chebyshev smoother steps, residual, prolongation / restriction, batched
+// block Cholesky + explicit inverse, block-diagonal apply, dense coarse factor.
+//
+// SpMV mapping: one warp per block row; BS lanes own the BS rows of a block and
+// 32/BS lane groups walk the row's blocks in an interleaved order; each lane streams
+// its 72 B (BS=9) / 128 B (BS=16) block row through L1 with the x sub-vector
+// broadcast, and the groups are combined with a fixed shuffle tree (deterministic).
+#include "common.cuh"
+#include "ctx.h"
+
+template <int BS>
+struct Lanes {
+  static constexpr int G = 32 / BS;  // lane groups per warp
+  static constexpr int USED = G * BS;
+};
+
+// Per-warp row product: returns (A x)_r in lanes with lane < BS (r = lane).
+template <int BS>
+__device__ __forceinline__ double warp_row_product(const int* __restrict__ ptr, const int* __restrict__ col,
+                                                   const double* __restrict__ blocks, const double* __restrict__ x,
+                                                   int row, int lane) {
+  constexpr int G = Lanes<BS>::G;
+  int g = lane / BS, r = lane - g * BS;
+  double acc = 0.0;
+  if (g < G) {
+    int b0 = ptr[row], b1 = ptr[row + 1];
+    for (int b = b0 + g; b < b1; b += G) {
+      const double* a = blocks + (int64_t)b * (BS * BS) + r * BS;
+      const double* xv = x + (int64_t)col[b] * BS;
+#pragma unroll
+      for (int c = 0; c < BS; ++c) acc = fma(__ldg(a + c), __ldg(xv + c), acc);
+    }
+  }
+  // combine groups: lane r += lane r + BS*k
+#pragma unroll
+  for (int k = 1; k < G; ++k) {
+    double t = __shfl_down_sync(FULL_MASK, acc, k * BS);
+    if (lane < BS) acc += t;
+  }
+  return acc;
+}
+
+// y = A x ; optionally dot_out = <x, y> (deterministic, grid_finish).
+template <int BS>
+__global__ void __launch_bounds__(128)
+k_bsr_spmv(const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ blocks,
+           const double* __restrict__ x, double* __restrict__ y, int nbr, double* partials, unsigned int* counter,
+           double* dot_out) {
+  __shared__ double scratch[33];
+  int lane = threadIdx.x & 31;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  double dsum = 0.0;
+  for (int row = warp; row < nbr; row += nwarps) {
+    double v = warp_row_product<BS>(ptr, col, blocks, x, row, lane);
+    if (lane < BS) {
+      y[(int64_t)row * BS + lane] = v;
+      if (dot_out) dsum = fma(x[(int64_t)row * BS + lane], v, dsum);
+    }
+  }
+  if (dot_out) {
+    dsum = block_sum(dsum, scratch);
+    grid_finish(partials, counter, dsum, scratch, dot_out);
+  }
+}
+
+// rows x: r = b - A x
+template <int BS>
+__global__ void __launch_bounds__(128)
+k_bsr_residual(const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ blocks,
+               const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r, int nbr) {
+  int lane = threadIdx.x & 31;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int row = warp; row < nbr; row += nwarps) {
+    double v = warp_row_product<BS>(ptr, col, blocks, x, row, lane);
+    if (lane < BS) r[(int64_t)row * BS + lane] = b[(int64_t)row * BS + lane] - v;
+  }
+}
+
+// Chebyshev step (multigrid.py:308-328), fused with the SpMV and the Jacobi apply:
+//   r = b - A x_in   (A == null: r = b)
+//   z = D^-1 r
+//   divide: d = z / c2          else: d = c1 d + c2 z
+//   x_out = x_in + d            (x_in == null: x_out = d)
+// x_out must not alias x_in (other rows read x_in).
+template <int BS>
+__global__ void __launch_bounds__(128)
+k_cheb_step(const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ blocks,
+            const double* __restrict__ x_in, const double* __restrict__ b, const double* __restrict__ Dinv,
+            double* __restrict__ d, double* __restrict__ x_out, int nbr, double c1, double c2, int divide) {
+  int lane = threadIdx.x & 31;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int row = warp; row < nbr; row += nwarps) {
+    double ax = 0.0;
+    if (blocks && x_in) ax = warp_row_product<BS>(ptr, col, blocks, x_in, row, lane);
+    int64_t base = (int64_t)row * BS;
+    double rr = (lane < BS) ? b[base + lane] - ax : 0.0;
+    // z_r = sum_c Dinv[r][c] r_c  (r_c broadcast from lane c)
+    double z = 0.0;
+    const double* Di = Dinv + (int64_t)row * BS * BS + (lane < BS ? lane : 0) * BS;
+#pragma unroll
+    for (int c = 0; c < BS; ++c) {
+      double rc = __shfl_sync(FULL_MASK, rr, c);
+      if (lane < BS) z = fma(Di[c], rc, z);
+    }
+    if (lane < BS) {
+      double dn = divide ? z / c2 : c1 * d[base + lane] + c2 * z;
+      d[base + lane] = dn;
+      x_out[base + lane] = (x_in ? x_in[base + lane] : 0.0) + dn;
+    }
+  }
+}
+
+static int spmv_grid(int nbr) { return grid_for((int64_t)nbr * 32, 128, 16); }
+
+extern "C" int bamg_bsr_spmv(bamg_ctx* ctx, int32_t bs, const int32_t* ptr, const int32_t* col,
+                             const double* blocks, const double* x, double* y, int32_t nbr, double* dot_out_dev,
+                             void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (nbr <= 0) return 0;
+  double* part = ctx ? ctx->partials : nullptr;
+  unsigned* ctr = ctx ? ctx->counters + BAMG_CTR_SPMV : nullptr;
+  int g = spmv_grid(nbr);
+  if (dot_out_dev && g > BAMG_MAX_PARTIALS) g = BAMG_MAX_PARTIALS;
+  switch (bs) {
+    case 9: k_bsr_spmv<9><<<g, 128, 0, st>>>(ptr, col, blocks, x, y, nbr, part, ctr, dot_out_dev); break;
+    case 16: k_bsr_spmv<16><<<g, 128, 0, st>>>(ptr, col, blocks, x, y, nbr, part, ctr, dot_out_dev); break;
+    case 3: k_bsr_spmv<3><<<g, 128, 0, st>>>(ptr, col, blocks, x, y, nbr, part, ctr, dot_out_dev); break;
+    case 1: k_bsr_spmv<1><<<g, 128, 0, st>>>(ptr, col, blocks, x, y, nbr, part, ctr, dot_out_dev); break;
+    default: bamg_set_error("bsr_spmv: unsupported square block size %d", bs); return BAMG_ERR_UNSUPPORTED;
+  }
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int bamg_bsr_residual(bamg_ctx* ctx, int32_t bs, const int32_t* ptr, const int32_t* col,
+                                 const double* blocks, const double* x, const double* b, double* r, int32_t nbr,
+                                 void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (nbr <= 0) return 0;
+  int g = spmv_grid(nbr);
+  switch (bs) {
+    case 9: k_bsr_residual<9><<<g, 128, 0, st>>>(ptr, col, blocks, x, b, r, nbr); break;
+    case 16: k_bsr_residual<16><<<g, 128, 0, st>>>(ptr, col, blocks, x, b, r, nbr); break;
+    case 1: k_bsr_residual<1><<<g, 128, 0, st>>>(ptr, col, blocks, x, b, r, nbr); break;
+    default: bamg_set_error("bsr_residual: unsupported block size %d", bs); return BAMG_ERR_UNSUPPORTED;
+  }
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int bamg_cheb_step(bamg_ctx* ctx, int32_t bs, const int32_t* ptr, const int32_t* col,
+                              const double* blocks, const double* x_in, const double* b, const double* Dinv, double* d,
+                              double* x_out, int32_t nbr, double c1, double c2, int32_t divide, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (nbr <= 0) return 0;
+  int g = spmv_grid(nbr);
+  switch (bs) {
+    case 9: k_cheb_step<9><<<g, 128, 0, st>>>(ptr, col, blocks, x_in, b, Dinv, d, x_out, nbr, c1, c2, divide); break;
+    case 16: k_cheb_step<16><<<g, 128, 0, st>>>(ptr, col, blocks, x_in, b, Dinv, d, x_out, nbr, c1, c2, divide); break;
+    case 1: k_cheb_step<1><<<g, 128, 0, st>>>(ptr, col, blocks, x_in, b, Dinv, d, x_out, nbr, c1, c2, divide); break;
+    default: bamg_set_error("cheb_step: unsupported block size %d", bs); return BAMG_ERR_UNSUPPORTED;
+  }
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// prolongation / restriction with the tentative prolongator: one bs x 16 block per
+// fine node, block column = aggregate (multigrid.py:234-236).
+
+// y_i (+)= P_i xc_agg(i)
+__global__ void k_prolong(const int* __restrict__ agg, const double* __restrict__ P, const double* __restrict__ xc,
+                          int nf, int bs, double* __restrict__ y, int accumulate) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)nf * bs; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / bs;
+    int r = (int)(t - i * bs);
+    const double* p = P + (i * bs + r) * 16;
+    const double* xa = xc + (int64_t)agg[i] * 16;
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) s = fma(p[c], xa[c], s);
+    y[t] = accumulate ? y[t] + s : s;
+  }
+}
+
+// bc_a[c] = sum_{i in a, ascending} sum_r P_i[r][c] r_i[r]
+__global__ void k_restrict(const int* __restrict__ agg_ptr, const int* __restrict__ members,
+                           const double* __restrict__ P, const double* __restrict__ r, int nagg, int bs,
+                           double* __restrict__ bc) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)nagg * 16; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = t >> 4;
+    int c = (int)(t & 15);
+    double s = 0.0;
+    for (int q = agg_ptr[a]; q < agg_ptr[a + 1]; ++q) {
+      int64_t i = members[q];
+      const double* p = P + i * bs * 16 + c;
+      const double* ri = r + i * bs;
+      for (int k = 0; k < bs; ++k) s = fma(p[k * 16], ri[k], s);
+    }
+    bc[t] = s;
+  }
+}
+
+extern "C" int bamg_prolong(bamg_ctx* ctx, const int32_t* agg, const double* P, const double* xc, int32_t nf,
+                            int32_t bs, double* y, int32_t accumulate, void* stream) {
+  (void)ctx;
+  if (nf <= 0) return 0;
+  k_prolong<<<grid_for((int64_t)nf * bs, 256), 256, 0, as_stream(stream)>>>(agg, P, xc, nf, bs, y, accumulate);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int bamg_restrict(bamg_ctx* ctx, const int32_t* agg_ptr, const int32_t* members, const double* P,
+                             const double* r, int32_t nagg, int32_t bs, double* bc, void* stream) {
+  (void)ctx;
+  if (nagg <= 0) return 0;
+  k_restrict<<<grid_for((int64_t)nagg * 16, 256), 256, 0, as_stream(stream)>>>(agg_ptr, members, P, r, nagg, bs, bc);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// batched block Cholesky + explicit inverse, bs <= 32 (blockmat.py:95-115):
+// warp per block, L in shared memory, inverse = L^-T L^-1.
+
+#define BCH_WARPS 4
+
+__global__ void __launch_bounds__(BCH_WARPS * 32)
+k_block_chol_inv(const double* __restrict__ M, int n, int bs, double* __restrict__ Lout, double* __restrict__ inv,
+                 int* __restrict__ bad_min) {
+  extern __shared__ double shm[];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* L = shm + (size_t)w * 2 * bs * bs;
+  double* Li = L + bs * bs;
+  int warp = blockIdx.x * BCH_WARPS + w;
+  int nwarps = gridDim.x * BCH_WARPS;
+  for (int blk = warp; blk < n; blk += nwarps) {
+    const double* m = M + (int64_t)blk * bs * bs;
+    for (int q = lane; q < bs * bs; q += 32) L[q] = m[q];
+    __syncwarp();
+    bool ok = true;
+    for (int j = 0; j < bs; ++j) {
+      // diagonal (lane 0), left-looking
+      double d = 0.0;
+      if (lane == 0) {
+        d = L[j * bs + j];
+        for (int k = 0; k < j; ++k) d -= L[j * bs + k] * L[j * bs + k];
+      }
+      d = __shfl_sync(FULL_MASK, d, 0);
+      if (!(d > 0.0)) {
+        ok = false;
+        break;
+      }
+      double ljj = sqrt(d);
+      int i = lane;
+      double v = 0.0;
+      if (i > j && i < bs) {
+        v = L[i * bs + j];
+        for (int k = 0; k < j; ++k) v -= L[i * bs + k] * L[j * bs + k];
+        v /= ljj;
+      }
+      __syncwarp();
+      if (i > j && i < bs) L[i * bs + j] = v;
+      if (lane == 0) L[j * bs + j] = ljj;
+      __syncwarp();
+    }
+    if (!ok) {
+      if (lane == 0) atomicMin(bad_min, blk);
+      __syncwarp();
+      continue;
+    }
+    // zero the strict upper triangle of L
+    for (int q = lane; q < bs * bs; q += 32) {
+      int r = q / bs, c = q - r * bs;
+      if (c > r) L[q] = 0.0;
+    }
+    __syncwarp();
+    // Li = L^-1: lane c computes column c by forward substitution
+    if (lane < bs) {
+      int c = lane;
+      for (int i = 0; i < bs; ++i) {
+        double v;
+        if (i < c) v = 0.0;
+        else if (i == c) v = 1.0 / L[c * bs + c];
+        else {
+          double s = 0.0;
+          for (int k = c; k < i; ++k) s += L[i * bs + k] * Li[k * bs + c];
+          v = -s / L[i * bs + i];
+        }
+        Li[i * bs + c] = v;
+      }
+    }
+    __syncwarp();
+    double* out = inv + (int64_t)blk * bs * bs;
+    for (int q = lane; q < bs * bs; q += 32) {
+      int i = q / bs, j = q - i * bs;
+      int k0 = i > j ? i : j;
+      double s = 0.0;
+      for (int k = k0; k < bs; ++k) s += Li[k * bs + i] * Li[k * bs + j];
+      out[q] = s;
+      if (Lout) Lout[(int64_t)blk * bs * bs + q] = L[q];
+    }
+    __syncwarp();
+  }
+}
+
+extern "C" int bamg_block_chol_inv(bamg_ctx* ctx, const double* M, int32_t n, int32_t bs, double* L, double* inv,
+                                   int32_t* bad_min_dev, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  int big = 0x7fffffff;
+  BAMG_CUDA_CHECK(cudaMemcpyAsync(bad_min_dev, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+  if (n <= 0) return 0;
+  if (bs > 32 || bs < 1) {
+    bamg_set_error("block_chol_inv: block size %d outside [1, 32]", bs);
+    return BAMG_ERR_UNSUPPORTED;
+  }
+  size_t sm = sizeof(double) * 2 * bs * bs * BCH_WARPS;
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_block_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_block_chol_inv<<<grid_for(n, BCH_WARPS, 16), BCH_WARPS * 32, sm, st>>>(M, n, bs, L, inv, bad_min_dev);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// y_b = M_b x_b (block-diagonal apply), bs arbitrary
+__global__ void k_blockdiag_apply(const double* __restrict__ M, const double* __restrict__ x, int n, int bs,
+                                  double* __restrict__ y) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * bs; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = t / bs;
+    int r = (int)(t - b * bs);
+    const double* m = M + (b * bs + r) * bs;
+    const double* xb = x + b * bs;
+    double s = 0.0;
+    for (int c = 0; c < bs; ++c) s = fma(m[c], xb[c], s);
+    y[t] = s;
+  }
+}
+
+extern "C" int bamg_blockdiag_apply(bamg_ctx* ctx, const double* M, const double* x, int32_t n, int32_t bs,
+                                    double* y, void* stream) {
+  (void)ctx;
+  if (n <= 0) return 0;
+  k_blockdiag_apply<<<grid_for((int64_t)n * bs, 256), 256, 0, as_stream(stream)>>>(M, x, n, bs, y);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// diagonal blocks of a square BSR (zero where absent), blockmat.py:270-282
+__global__ void k_diag_blocks(const int* __restrict__ ptr, const int* __restrict__ col,
+                              const double* __restrict__ blocks, int nbr, int bs, double* __restrict__ D) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)nbr * bs * bs; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / (bs * bs);
+    int q = (int)(t - i * bs * bs);
+    int b0 = ptr[i], n = ptr[i + 1] - b0;
+    int k = lower_bound_i32(col + b0, n, (int)i);
+    D[t] = (k < n && col[b0 + k] == i) ? blocks[(int64_t)(b0 + k) * bs * bs + q] : 0.0;
+  }
+}
+
+extern "C" int bamg_diag_blocks(bamg_ctx* ctx, const int32_t* ptr, const int32_t* col, const double* blocks,
+                                int32_t nbr, int32_t bs, double* D, void* stream) {
+  (void)ctx;
+  if (nbr <= 0) return 0;
+  k_diag_blocks<<<grid_for((int64_t)nbr * bs * bs, 256), 256, 0, as_stream(stream)>>>(ptr, col, blocks, nbr, bs, D);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// coarsest level: densify + symmetrise, single-CTA Cholesky, explicit inverse
+// (multigrid.py:431-440, 477-478)
+
+__global__ void k_densify_sym(const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ blocks,
+                              int nbr, int bs, double* __restrict__ Dn) {
+  int n = nbr * bs;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * n; t += (int64_t)gridDim.x * blockDim.x)
+    Dn[t] = 0.0;
+}
+
+__global__ void k_scatter_dense(const int* __restrict__ ptr, const int* __restrict__ col,
+                                const double* __restrict__ blocks, int nbr, int bs, double* __restrict__ Dn) {
+  int n = nbr * bs;
+  for (int i = blockIdx.x; i < nbr; i += gridDim.x)
+    for (int b = ptr[i]; b < ptr[i + 1]; ++b)
+      for (int q = threadIdx.x; q < bs * bs; q += blockDim.x) {
+        int r = q / bs, c = q - r * bs;
+        Dn[(int64_t)(i * bs + r) * n + col[b] * bs + c] = blocks[(int64_t)b * bs * bs + q];
+      }
+}
+
+__global__ void k_symmetrize(double* __restrict__ Dn, int n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * n; t += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(t / n), j = (int)(t - (int64_t)i * n);
+    if (j < i) continue;
+    double a = Dn[(int64_t)i * n + j], b = Dn[(int64_t)j * n + i];
+    double v = 0.5 * (a + b);
+    Dn[(int64_t)i * n + j] = v;
+    Dn[(int64_t)j * n + i] = v;
+  }
+}
+
+// In-place lower Cholesky of the n x n matrix in `a` (one CTA); flag[0] = 1 on failure.
+__global__ void __launch_bounds__(1024) k_dense_chol(double* a, int n, int* flag) {
+  __shared__ double piv;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (threadIdx.x == 0) {
+      double d = a[(int64_t)j * n + j];
+      if (!(d > 0.0)) bad = 1;
+      piv = sqrt(d);
+      a[(int64_t)j * n + j] = piv;
+    }
+    __syncthreads();
+    if (bad) break;
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) a[(int64_t)i * n + j] /= piv;
+    __syncthreads();
+    int m = n - j - 1;
+    for (int64_t t = threadIdx.x; t < (int64_t)m * m; t += blockDim.x) {
+      int ii = (int)(t / m), kk = (int)(t - (int64_t)ii * m);
+      if (kk > ii) continue;
+      int i = j + 1 + ii, k = j + 1 + kk;
+      a[(int64_t)i * n + k] -= a[(int64_t)i * n + j] * a[(int64_t)k * n + j];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) flag[0] = bad;
+}
+
+// Li = L^-1 (lower), thread per column
+__global__ void k_tri_inv(const double* __restrict__ L, int n, double* __restrict__ Li) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    for (int i = 0; i < n; ++i) {
+      double v;
+      if (i < c) v = 0.0;
+      else if (i == c) v = 1.0 / L[(int64_t)c * n + c];
+      else {
+        double s = 0.0;
+        for (int k = c; k < i; ++k) s += L[(int64_t)i * n + k] * Li[(int64_t)k * n + c];
+        v = -s / L[(int64_t)i * n + i];
+      }
+      Li[(int64_t)i * n + c] = v;
+    }
+  }
+}
+
+__global__ void k_ltl(const double* __restrict__ Li, int n, double* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * n; t += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(t / n), j = (int)(t - (int64_t)i * n);
+    int k0 = i > j ? i : j;
+    double s = 0.0;
+    for (int k = k0; k < n; ++k) s += Li[(int64_t)k * n + i] * Li[(int64_t)k * n + j];
+    out[t] = s;
+  }
+}
+
+// dense = sym(BSR); L = chol(dense) (in `work`), inv = L^-T L^-1.
+extern "C" int bamg_coarse_factor(bamg_ctx* ctx, const int32_t* ptr, const int32_t* col, const double* blocks,
+                                  int32_t nbr, int32_t bs, double* dense, double* work, double* inv,
+                                  int32_t* flag_dev, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  int n = nbr * bs;
+  if (n <= 0) return 0;
+  k_densify_sym<<<grid_for((int64_t)n * n, 256), 256, 0, st>>>(ptr, col, blocks, nbr, bs, dense);
+  k_scatter_dense<<<grid_for(nbr, 1, 8), 128, 0, st>>>(ptr, col, blocks, nbr, bs, dense);
+  k_symmetrize<<<grid_for((int64_t)n * n, 256), 256, 0, st>>>(dense, n);
+  BAMG_CUDA_CHECK(cudaMemcpyAsync(work, dense, sizeof(double) * n * (int64_t)n, cudaMemcpyDeviceToDevice, st));
+  k_dense_chol<<<1, 1024, 0, st>>>(work, n, flag_dev);
+  k_tri_inv<<<grid_for(n, 64), 64, 0, st>>>(work, n, dense);  // dense <- L^-1 (dense sym copy no longer needed)
+  k_ltl<<<grid_for((int64_t)n * n, 256), 256, 0, st>>>(dense, n, inv);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// y = M x for dense n x n (warp per row)
+__global__ void k_gemv(const double* __restrict__ M, const double* __restrict__ x, int n, double* __restrict__ y) {
+  int lane = threadIdx.x & 31;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = warp; i < n; i += nwarps) {
+    double s = 0.0;
+    for (int c = lane; c < n; c += 32) s = fma(M[(int64_t)i * n + c], x[c], s);
+    s = warp_sum(s);
+    if (lane == 0) y[i] = s;
+  }
+}
+
+extern "C" int bamg_dense_gemv(bamg_ctx* ctx, const double* M, const double* x, int32_t n, double* y, void* stream) {
+  (void)ctx;
+  if (n <= 0) return 0;
+  k_gemv<<<grid_for((int64_t)n * 32, 128, 8), 128, 0, as_stream(stream)>>>(M, x, n, y);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// PCG vector updates (solver.py:108-127): x += a p ; r -= a ap ; rr = <r, r>
+__global__ void __launch_bounds__(256)
+k_pcg_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p, const double* __restrict__ ap,
+             double a, int64_t n, double* partials, unsigned int* counter, double* rr_out) {
+  __shared__ double scratch[33];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] += a * p[i];
+    double ri = r[i] - a * ap[i];
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  s = block_sum(s, scratch);
+  grid_finish(partials, counter, s, scratch, rr_out);
+}
+
+extern "C" int bamg_pcg_update(bamg_ctx* ctx, double* x, double* r, const double* p, const double* ap, double alpha,
+                               int64_t n, double* rr_dev, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  int g = grid_for(n, 256, 4);
+  k_pcg_update<<<g, 256, 0, st>>>(x, r, p, ap, alpha, n, ctx->partials, ctx->counters + BAMG_CTR_PCG0, rr_dev);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// p = z + beta p
+__global__ void k_xpby(const double* __restrict__ z, double beta, double* __restrict__ p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = z[i] + beta * p[i];
+}
+
+extern "C" int bamg_xpby(bamg_ctx* ctx, const double* z, double beta, double* p, int64_t n, void* stream) {
+  (void)ctx;
+  if (n) k_xpby<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(z, beta, p, n);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}

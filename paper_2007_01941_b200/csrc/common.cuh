@@ -1,0 +1,105 @@
+// Shared device helpers for libbamg_b200 (sm_100a, fp64 block-sparse path).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/bamg_b200.h"
+
+#define BAMG_WARP 32
+#define FULL_MASK 0xffffffffu
+
+// Thread-local last-error text (bamg_last_error).
+void bamg_set_error(const char* fmt, ...);
+
+#define BAMG_CUDA_CHECK(expr)                                                     \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      bamg_set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,                   \
+                     cudaGetErrorString(_e));                                     \
+      return BAMG_ERR_CUDA;                                                       \
+    }                                                                             \
+  } while (0)
+
+#define BAMG_LAUNCH_CHECK() BAMG_CUDA_CHECK(cudaGetLastError())
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// grid size for grid-stride loops: a multiple of the SM count (148 on B200)
+int bamg_num_sms();
+static inline int grid_for(int64_t n, int threads, int per_sm = 8) {
+  int64_t want = ceil_div(n, threads);
+  int64_t cap = (int64_t)bamg_num_sms() * per_sm;
+  if (want < 1) want = 1;
+  return (int)(want < cap ? want : cap);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int warp_sum_int(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+  return v;
+}
+
+// Deterministic block-wide sum (fixed tree). `scratch` >= 32 doubles. All threads
+// receive the result.
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  double t = (threadIdx.x < nw) ? scratch[threadIdx.x] : 0.0;
+  if (wid == 0) t = warp_sum(t);
+  if (threadIdx.x == 0) scratch[0] = t;
+  __syncthreads();
+  double r = scratch[0];
+  __syncthreads();
+  return r;
+}
+
+// Last-block-done finisher for deterministic grid reductions: every block writes
+// `partial[blockIdx.x]`, the final block sums all partials in index order.
+// Returns true in the block that must write the final value (thread 0 holds it).
+__device__ __forceinline__ bool grid_finish(double* partials, unsigned int* counter,
+                                            double block_value, double* scratch,
+                                            double* out_total) {
+  __shared__ bool am_last;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = block_value;
+    __threadfence();
+    unsigned int t = atomicAdd(counter, 1u);
+    am_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return false;
+  __threadfence();
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
+    v += ((volatile double*)partials)[i];
+  v = block_sum(v, scratch);
+  if (threadIdx.x == 0) {
+    *out_total = v;
+    *counter = 0u;  // re-arm for the next launch
+  }
+  return true;
+}
+
+__device__ __forceinline__ int lower_bound_i32(const int* a, int n, int key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}

@@ -1,0 +1,744 @@
+// Multigrid setup (multigrid.py:83-237, 371-471; problem.py:332-352):
+// operator strength, greedy aggregation (bit-exact, single warp), gauge
+// near-nullspace K, per-aggregate Householder QR prolongation (economic + pivoted
+// branches), Galerkin P^T A P (symbolic + numeric, deterministic), symmetrise,
+// decoupled-dof patch.
+#include "common.cuh"
+#include "ctx.h"
+
+int radix_sort_pairs(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
+                     int64_t n, int key_bits, cudaStream_t st);
+int scan_exclusive_int(const int* in, int* out, int64_t n, int* total, cudaStream_t st);
+int segment_ptr(const int* ids, int64_t n, int nseg, int* ptr, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// operator strength (multigrid.py:83-98)
+
+__global__ void k_block_fro(const double* __restrict__ blocks, int64_t nnz, int bb, double* __restrict__ nrm) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nnz; b += (int64_t)gridDim.x * blockDim.x) {
+    const double* a = blocks + b * bb;
+    double s = 0.0;
+    for (int q = 0; q < bb; ++q) s += a[q] * a[q];
+    nrm[b] = sqrt(s);
+  }
+}
+
+__global__ void k_op_strength(const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ nrm,
+                              int n, const double* __restrict__ dnorm, int* __restrict__ G_ptr, int* __restrict__ G_col,
+                              double* __restrict__ G_val, int* __restrict__ zero_diag) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double di = dnorm[i];
+    if (di == 0.0) atomicAdd(zero_diag, 1);
+    int out = G_ptr[i];
+    for (int q = ptr[i]; q < ptr[i + 1]; ++q) {
+      int j = col[q];
+      if (j == i) continue;
+      double v = nrm[q] / sqrt(di * dnorm[j]);
+      G_col[out] = j;
+      G_val[out] = v < 1.0 ? v : 1.0;
+      ++out;
+    }
+  }
+}
+
+__global__ void k_diag_norm_and_count(const int* __restrict__ ptr, const int* __restrict__ col,
+                                      const double* __restrict__ nrm, int n, double* __restrict__ dnorm,
+                                      int* __restrict__ offcount) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double d = 0.0;
+    int c = 0;
+    for (int q = ptr[i]; q < ptr[i + 1]; ++q) {
+      if (col[q] == i) d = nrm[q];
+      else ++c;
+    }
+    dnorm[i] = d;
+    offcount[i] = c;
+  }
+}
+
+// G_ptr must hold n+1 ints. Sizes: call with G_col == null to get G_ptr + total.
+extern "C" int bamg_operator_strength(bamg_ctx* ctx, const int32_t* ptr, const int32_t* col, const double* blocks,
+                                      int32_t n, int64_t nnz, int32_t bs, double* nrm_work, double* dnorm_work,
+                                      int32_t* G_ptr, int32_t* G_col, double* G_val, int32_t* flags_dev,
+                                      void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (G_col == nullptr) {
+    BAMG_CUDA_CHECK(cudaMemsetAsync(flags_dev, 0, sizeof(int) * 2, st));
+    k_block_fro<<<grid_for(nnz, 256), 256, 0, st>>>(blocks, nnz, bs * bs, nrm_work);
+    k_diag_norm_and_count<<<grid_for(n, 128), 128, 0, st>>>(ptr, col, nrm_work, n, dnorm_work, G_ptr);
+    BAMG_LAUNCH_CHECK();
+    return scan_exclusive_int(G_ptr, G_ptr, n + 1, flags_dev + 1, st);  // G_ptr[n] is scratch -> total
+  }
+  k_op_strength<<<grid_for(n, 128), 128, 0, st>>>(ptr, col, nrm_work, n, dnorm_work, G_ptr, G_col, G_val, flags_dev);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// greedy aggregation (multigrid.py:127-176), one warp, sequential over nodes.
+// In-scan choice: among neighbours that are unaggregated or in an aggregate of
+// size < max_size, the first in (-G, aggregated?, index) order. Post-pass: the
+// (G, -index)-largest neighbour whose aggregate has size <= max_size.
+
+struct Cand {
+  double g;
+  int un;  // 1 if unaggregated
+  int j;
+};
+
+__device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
+  if (a.j < 0) return false;
+  if (b.j < 0) return true;
+  if (a.g != b.g) return a.g > b.g;
+  if (a.un != b.un) return a.un > b.un;
+  return a.j < b.j;
+}
+
+__device__ __forceinline__ Cand warp_best(Cand c) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Cand t;
+    t.g = __shfl_xor_sync(FULL_MASK, c.g, o);
+    t.un = __shfl_xor_sync(FULL_MASK, c.un, o);
+    t.j = __shfl_xor_sync(FULL_MASK, c.j, o);
+    if (better(t, c)) c = t;
+  }
+  return c;
+}
+
+__global__ void __launch_bounds__(32)
+k_aggregate(const int* __restrict__ G_ptr, const int* __restrict__ G_col, const double* __restrict__ G_val, int n,
+            int max_size, int* __restrict__ agg_g, int* __restrict__ size_g, int use_smem, int* __restrict__ n_agg_out) {
+  extern __shared__ int sh[];
+  int lane = threadIdx.x;
+  int* agg = use_smem ? sh : agg_g;
+  int* size = use_smem ? sh + n : size_g;
+  for (int i = lane; i < n; i += 32) {
+    agg[i] = -1;
+    size[i] = 0;
+  }
+  __syncwarp();
+  int nagg = 0;
+  for (int i = 0; i < n; ++i) {
+    if (agg[i] >= 0) continue;
+    Cand best{0.0, 0, -1};
+    for (int q = G_ptr[i] + lane; q < G_ptr[i + 1]; q += 32) {
+      int j = G_col[q];
+      int a = agg[j];
+      bool elig = (a < 0) || (size[a] < max_size);
+      if (elig) {
+        Cand c{G_val[q], a < 0 ? 1 : 0, j};
+        if (better(c, best)) best = c;
+      }
+    }
+    best = warp_best(best);
+    if (best.j >= 0) {
+      int aj = agg[best.j];  // every lane reads the pre-update value
+      __syncwarp();
+      if (lane == 0) {
+        if (aj < 0) {
+          agg[i] = nagg;
+          agg[best.j] = nagg;
+          size[nagg] = 2;
+        } else {
+          agg[i] = aj;
+          size[aj] += 1;
+        }
+      }
+      if (aj < 0) ++nagg;
+      __syncwarp();
+    }
+  }
+  // post-pass over leftovers in index order
+  for (int i = 0; i < n; ++i) {
+    __syncwarp();
+    if (agg[i] >= 0) continue;
+    Cand best{0.0, 0, -1};
+    for (int q = G_ptr[i] + lane; q < G_ptr[i + 1]; q += 32) {
+      int j = G_col[q];
+      int a = agg[j];
+      if (a >= 0 && size[a] <= max_size) {
+        Cand c{G_val[q], 0, j};
+        if (better(c, best)) best = c;
+      }
+    }
+    best = warp_best(best);
+    __syncwarp();
+    if (lane == 0) {
+      if (best.j >= 0) {
+        int a = agg[best.j];
+        agg[i] = a;
+        size[a] += 1;
+      } else {
+        agg[i] = nagg;
+        size[nagg] = 1;
+      }
+    }
+    if (best.j < 0) ++nagg;
+    __syncwarp();
+  }
+  __syncwarp();
+  if (use_smem)
+    for (int i = lane; i < n; i += 32) {
+      agg_g[i] = agg[i];
+      size_g[i] = size[i];
+    }
+  if (lane == 0) *n_agg_out = nagg;
+}
+
+extern "C" int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t* G_col, const double* G_val,
+                              int32_t n, int32_t max_size, int32_t* agg, int32_t* size_work, int32_t* n_agg_dev,
+                              void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (n <= 0) {
+    BAMG_CUDA_CHECK(cudaMemsetAsync(n_agg_dev, 0, sizeof(int), st));
+    return 0;
+  }
+  size_t sm = sizeof(int) * 2 * (size_t)n;
+  int use_smem = sm <= 200 * 1024;
+  if (!use_smem) sm = 0;
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_aggregate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_aggregate<<<1, 32, sm, st>>>(G_ptr, G_col, G_val, n, max_size, agg, size_work, use_smem, n_agg_dev);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// gauge near-nullspace (problem.py:332-352), (9 nc) x 16 row-major
+
+__global__ void k_gauge(const double* __restrict__ cams, int nc, double* __restrict__ K) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+    const double* c = cams + (int64_t)i * 9;
+    double aa[3] = {c[0], c[1], c[2]};
+    double a2 = aa[0] * aa[0] + aa[1] * aa[1] + aa[2] * aa[2];
+    double a = sqrt(a2);
+    bool small = a < 1e-4;
+    double s1, s2, d2;
+    if (small) {
+      s1 = 1.0 - a2 / 6.0;
+      s2 = 0.5 - a2 / 24.0;
+      d2 = 1.0 / 12.0 + a2 / 720.0;
+    } else {
+      double sn, cs;
+      sincos(a, &sn, &cs);
+      s1 = sn / a;
+      s2 = (1.0 - cs) / (a * a);
+      double sh, ch;
+      sincos(a / 2.0, &sh, &ch);
+      d2 = 1.0 / (a * a) - (ch / sh) / (2.0 * a);
+    }
+    double Kx[9] = {0.0, -aa[2], aa[1], aa[2], 0.0, -aa[0], -aa[1], aa[0], 0.0};
+    double K2[9];
+    for (int r = 0; r < 3; ++r)
+      for (int q = 0; q < 3; ++q) K2[r * 3 + q] = Kx[r * 3] * Kx[q] + Kx[r * 3 + 1] * Kx[3 + q] + Kx[r * 3 + 2] * Kx[6 + q];
+    double* out = K + (int64_t)i * 9 * 16;
+    for (int q = 0; q < 144; ++q) out[q] = 0.0;
+    for (int r = 0; r < 3; ++r)
+      for (int q = 0; q < 3; ++q) {
+        double I = (r == q) ? 1.0 : 0.0;
+        double R = I + s1 * Kx[r * 3 + q] + s2 * K2[r * 3 + q];
+        double Ji = I + 0.5 * Kx[r * 3 + q] + d2 * K2[r * 3 + q];
+        out[(3 + r) * 16 + q] = -R;
+        out[r * 16 + 3 + q] = -Ji;
+      }
+    for (int r = 0; r < 3; ++r) out[(3 + r) * 16 + 6] = c[3 + r];
+    for (int k = 0; k < 9; ++k) out[k * 16 + 7 + k] = 1.0;
+  }
+}
+
+extern "C" int bamg_gauge_nullspace(bamg_ctx* ctx, const double* cams, int32_t nc, double* K, void* stream) {
+  (void)ctx;
+  if (nc <= 0) return 0;
+  k_gauge<<<grid_for(nc, 128), 128, 0, as_stream(stream)>>>(cams, nc, K);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// members of each aggregate, ascending (multigrid.py:121-124): stable sort of node
+// ids by aggregate id.
+
+__global__ void k_iota_i(uint32_t* a, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = (uint32_t)i;
+}
+
+extern "C" int bamg_aggregate_members(bamg_ctx* ctx, const int32_t* agg, int32_t n, int32_t n_agg,
+                                      int32_t* agg_ptr, int32_t* members, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (n <= 0) return 0;
+  uint32_t *iota = nullptr, *skey = nullptr;
+  BAMG_CUDA_CHECK(cudaMallocAsync(&iota, 4 * (size_t)n, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&skey, 4 * (size_t)n, st));
+  k_iota_i<<<grid_for(n, 256), 256, 0, st>>>(iota, n);
+  int bits = 1;
+  while ((1ll << bits) < n_agg) ++bits;
+  int rc = radix_sort_pairs((const uint32_t*)agg, iota, skey, (uint32_t*)members, n, bits, st);
+  if (rc) return rc;
+  rc = segment_ptr((const int*)skey, n, n_agg, agg_ptr, st);
+  if (rc) return rc;
+  cudaFreeAsync(iota, st);
+  cudaFreeAsync(skey, st);
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// tentative prolongation by per-aggregate Householder QR (multigrid.py:179-237).
+// One warp per aggregate; local matrix (m x 16, m = members*bs) and Q in smem.
+// LAPACK dlarfg convention: beta = -sign(alpha) |(alpha, x)|, tau = (beta-alpha)/beta,
+// v = x / (alpha - beta); x == 0 gives tau = 0 (H = I).
+
+#define NS 16
+
+__device__ void householder_step(double* A, int m, int j, int lane, double* tau_out, int ncols_apply_from,
+                                 double* diag_out) {
+  // column j, rows j..m-1
+  double xs = 0.0;
+  for (int i = j + 1 + lane; i < m; i += 32) xs += A[i * NS + j] * A[i * NS + j];
+  xs = warp_sum(xs);
+  double alpha = A[j * NS + j];
+  double tau = 0.0, beta = alpha;
+  if (xs > 0.0) {
+    double xnorm = sqrt(xs);
+    beta = -copysign(hypot(alpha, xnorm), alpha);
+    tau = (beta - alpha) / beta;
+    double scal = 1.0 / (alpha - beta);
+    for (int i = j + 1 + lane; i < m; i += 32) A[i * NS + j] *= scal;
+  }
+  __syncwarp();
+  if (lane == 0) A[j * NS + j] = beta;
+  *tau_out = tau;
+  *diag_out = beta;
+  __syncwarp();
+  if (tau != 0.0) {
+    for (int c = ncols_apply_from; c < NS; ++c) {
+      double w = 0.0;
+      for (int i = j + 1 + lane; i < m; i += 32) w += A[i * NS + j] * A[i * NS + c];
+      w = warp_sum(w) + A[j * NS + c];
+      __syncwarp();
+      for (int i = j + 1 + lane; i < m; i += 32) A[i * NS + c] -= tau * w * A[i * NS + j];
+      if (lane == 0) A[j * NS + c] -= tau * w;
+      __syncwarp();
+    }
+  }
+}
+
+// Q[:, :keep] = H_0 ... H_{k-1} I[:, :keep] (reflectors stored below the diagonal of A)
+__device__ void form_q(const double* A, const double* tau, int m, int k, int keep, double* Q, int lane) {
+  for (int i = lane; i < m; i += 32)
+    for (int c = 0; c < NS; ++c) Q[i * NS + c] = (i == c && c < keep) ? 1.0 : 0.0;
+  __syncwarp();
+  for (int j = k - 1; j >= 0; --j) {
+    if (tau[j] == 0.0) continue;
+    for (int c = j; c < keep; ++c) {
+      double w = Q[j * NS + c];
+      double part = 0.0;
+      for (int i = j + 1 + lane; i < m; i += 32) part += A[i * NS + j] * Q[i * NS + c];
+      w += warp_sum(part);
+      __syncwarp();
+      for (int i = j + 1 + lane; i < m; i += 32) Q[i * NS + c] -= tau[j] * w * A[i * NS + j];
+      if (lane == 0) Q[j * NS + c] -= tau[j] * w;
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void k_prolong_qr(const int* __restrict__ agg_ptr, const int* __restrict__ members,
+                             const double* __restrict__ K, int n_agg, int bs, int m_max, double* __restrict__ Pblocks,
+                             double* __restrict__ Kc, int* __restrict__ info /* [n_agg][2]: pivoted, rank */,
+                             int* __restrict__ padded_cnt) {
+  extern __shared__ double sm[];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int wpb = blockDim.x >> 5;
+  double* A = sm + (size_t)w * (2 * m_max * NS + 2 * NS + NS);
+  double* Q = A + m_max * NS;
+  double* tau = Q + m_max * NS;
+  double* dg = tau + NS;
+  int* piv = (int*)(dg + NS);  // NS ints packed in the NS-double tail... use separate region
+  (void)piv;
+  for (int a = blockIdx.x * wpb + w; a < n_agg; a += gridDim.x * wpb) {
+    int b0 = agg_ptr[a], nm = agg_ptr[a + 1] - b0;
+    int m = nm * bs;
+    // load
+    for (int t = lane; t < m * NS; t += 32) {
+      int r = t / NS, c = t - r * NS;
+      int node = members[b0 + r / bs];
+      A[t] = K[((int64_t)node * bs + (r % bs)) * NS + c];
+    }
+    __syncwarp();
+    int keep = m < NS ? m : NS;
+    bool done = false;
+    if (m >= NS) {
+      // economic QR, no pivoting (scipy.linalg.qr mode="economic")
+      for (int j = 0; j < NS; ++j) {
+        double tj, dj;
+        householder_step(A, m, j, lane, &tj, j + 1, &dj);
+        if (lane == 0) {
+          tau[j] = tj;
+          dg[j] = dj;
+        }
+        __syncwarp();
+      }
+      double mn = 1e308, mx = 0.0;
+      for (int j = 0; j < NS; ++j) {
+        double v = fabs(dg[j]);
+        mn = fmin(mn, v);
+        mx = fmax(mx, v);
+      }
+      if (mn > 1e-10 * mx) {
+        form_q(A, tau, m, NS, NS, Q, lane);
+        // sign fix: s = sign(diag R); P = Q s; Kc = s R
+        for (int t = lane; t < m * NS; t += 32) {
+          int c = t % NS;
+          double s = dg[c] < 0.0 ? -1.0 : 1.0;
+          Q[t] *= s;
+        }
+        double* kc = Kc + (int64_t)a * NS * NS;
+        for (int t = lane; t < NS * NS; t += 32) {
+          int r = t / NS, c = t - r * NS;
+          double s = dg[r] < 0.0 ? -1.0 : 1.0;
+          kc[t] = (c >= r) ? s * A[r * NS + c] : 0.0;
+        }
+        if (lane == 0) {
+          info[2 * a] = 0;
+          info[2 * a + 1] = NS;
+          padded_cnt[a] = 0;
+        }
+        done = true;
+      } else {
+        // reload for the pivoted branch
+        __syncwarp();
+        for (int t = lane; t < m * NS; t += 32) {
+          int r = t / NS, c = t - r * NS;
+          int node = members[b0 + r / bs];
+          A[t] = K[((int64_t)node * bs + (r % bs)) * NS + c];
+        }
+        __syncwarp();
+      }
+    }
+    if (!done) {
+      // pivoted QR (scipy.linalg.qr pivoting=True, LAPACK geqp3): at step j pick the
+      // remaining column with the largest norm of rows j..m-1 (first on ties).
+      int perm[NS];
+      for (int c = 0; c < NS; ++c) perm[c] = c;
+      int k = m < NS ? m : NS;
+      for (int j = 0; j < k; ++j) {
+        int bestc = j;
+        double bestn = -1.0;
+        for (int c = j; c < NS; ++c) {
+          double s = 0.0;
+          for (int i = j + lane; i < m; i += 32) s += A[i * NS + c] * A[i * NS + c];
+          s = warp_sum(s);
+          if (s > bestn) {
+            bestn = s;
+            bestc = c;
+          }
+        }
+        if (bestc != j) {
+          for (int i = lane; i < m; i += 32) {
+            double t = A[i * NS + j];
+            A[i * NS + j] = A[i * NS + bestc];
+            A[i * NS + bestc] = t;
+          }
+          int t = perm[j];
+          perm[j] = perm[bestc];
+          perm[bestc] = t;
+        }
+        __syncwarp();
+        double tj, dj;
+        householder_step(A, m, j, lane, &tj, j + 1, &dj);
+        if (lane == 0) {
+          tau[j] = tj;
+          dg[j] = dj;
+        }
+        __syncwarp();
+      }
+      double d0 = fabs(dg[0]);
+      int rank = 0;
+      if (k > 0 && d0 > 0.0)
+        for (int j = 0; j < k; ++j)
+          if (fabs(dg[j]) > 1e-10 * d0) ++rank;
+      form_q(A, tau, m, k, keep, Q, lane);
+      double* kc = Kc + (int64_t)a * NS * NS;
+      for (int t = lane; t < NS * NS; t += 32) kc[t] = 0.0;
+      __syncwarp();
+      // r_unpiv[:rank, perm] = R[:rank, :]
+      for (int t = lane; t < rank * NS; t += 32) {
+        int r = t / NS, c = t - r * NS;
+        kc[r * NS + perm[c]] = (c >= r) ? A[r * NS + c] : 0.0;
+      }
+      if (lane == 0) {
+        info[2 * a] = 1;
+        info[2 * a + 1] = rank;
+        padded_cnt[a] = NS - keep;
+      }
+    }
+    __syncwarp();
+    // scatter P blocks
+    for (int t = lane; t < m * NS; t += 32) {
+      int r = t / NS, c = t - r * NS;
+      int node = members[b0 + r / bs];
+      Pblocks[((int64_t)node * bs + (r % bs)) * NS + c] = (c < keep) ? Q[t] : 0.0;
+    }
+    __syncwarp();
+  }
+}
+
+extern "C" int bamg_prolongation_qr(bamg_ctx* ctx, const int32_t* agg_ptr, const int32_t* members, const double* K,
+                                    int32_t n_agg, int32_t bs, int32_t max_members, double* Pblocks, double* Kc,
+                                    int32_t* info, int32_t* padded_cnt, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (n_agg <= 0) return 0;
+  int m_max = max_members * bs;
+  size_t per_warp = sizeof(double) * (2 * (size_t)m_max * NS + 3 * NS);
+  int wpb = (int)((200 * 1024) / per_warp);
+  if (wpb < 1) {
+    bamg_set_error("prolongation: aggregate of %d rows exceeds shared memory", m_max);
+    return BAMG_ERR_UNSUPPORTED;
+  }
+  if (wpb > 4) wpb = 4;
+  size_t sm = per_warp * wpb;
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_prolong_qr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int blocks = (int)ceil_div(n_agg, wpb);
+  int cap = bamg_num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  k_prolong_qr<<<blocks, 32 * wpb, sm, st>>>(agg_ptr, members, K, n_agg, bs, m_max, Pblocks, Kc, info, padded_cnt);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Galerkin A_c = sym(P^T A P) (multigrid.py:409, 444-455; blockmat.py:337-360).
+// Coarse pattern: row a = union over members i of agg(cols of row i) (bitmap).
+// Numeric: each fine block (i, j) maps to coarse block (agg i, agg j); fine blocks
+// are grouped per coarse block by a stable radix sort (row-major order kept inside),
+// then one warp per coarse block accumulates sum P_i^T (A_ij P_j) in registers.
+
+__global__ void k_coarse_rows(const int* __restrict__ agg_ptr, const int* __restrict__ members,
+                              const int* __restrict__ ptr, const int* __restrict__ col, const int* __restrict__ agg,
+                              int n_agg, int* __restrict__ counts, const int* __restrict__ Cptr, int* __restrict__ Ccol) {
+  extern __shared__ unsigned int bm[];
+  int words = (n_agg + 31) >> 5;
+  for (int a = blockIdx.x; a < n_agg; a += gridDim.x) {
+    for (int w = threadIdx.x; w < words; w += blockDim.x) bm[w] = 0u;
+    __syncthreads();
+    for (int q = agg_ptr[a]; q < agg_ptr[a + 1]; ++q) {
+      int i = members[q];
+      for (int b = ptr[i] + threadIdx.x; b < ptr[i + 1]; b += blockDim.x) {
+        int c = agg[col[b]];
+        atomicOr(&bm[c >> 5], 1u << (c & 31));
+      }
+    }
+    __syncthreads();
+    if (Ccol == nullptr) {
+      int c = 0;
+      for (int w = threadIdx.x; w < words; w += blockDim.x) c += __popc(bm[w]);
+      c = warp_sum_int(c);
+      __shared__ int red[32];
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int t = 0;
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+        counts[a] = t;
+      }
+    } else if (threadIdx.x < 32) {
+      int lane = threadIdx.x;
+      int out = Cptr[a];
+      for (int w0 = 0; w0 < words; w0 += 32) {
+        int w = w0 + lane;
+        unsigned v = (w < words) ? bm[w] : 0u;
+        int cnt = __popc(v);
+        int incl = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+          int t = __shfl_up_sync(FULL_MASK, incl, o);
+          if (lane >= o) incl += t;
+        }
+        int pos = out + incl - cnt;
+        while (v) {
+          int b = __ffs(v) - 1;
+          v &= v - 1;
+          Ccol[pos++] = w * 32 + b;
+        }
+        out += __shfl_sync(FULL_MASK, incl, 31);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+extern "C" int bamg_galerkin_pattern(bamg_ctx* ctx, const int32_t* agg_ptr, const int32_t* members,
+                                     const int32_t* ptr, const int32_t* col, const int32_t* agg, int32_t n_agg,
+                                     int32_t* Cptr_or_counts, int32_t* Ccol, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  size_t sm = sizeof(unsigned) * ((n_agg + 31) / 32);
+  if (sm > 200 * 1024) {
+    bamg_set_error("galerkin bitmap for %d aggregates exceeds shared memory", n_agg);
+    return BAMG_ERR_UNSUPPORTED;
+  }
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_coarse_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (Ccol == nullptr)
+    k_coarse_rows<<<grid_for(n_agg, 1, 16), 128, sm, st>>>(agg_ptr, members, ptr, col, agg, n_agg, Cptr_or_counts,
+                                                           nullptr, nullptr);
+  else
+    k_coarse_rows<<<grid_for(n_agg, 1, 16), 128, sm, st>>>(agg_ptr, members, ptr, col, agg, n_agg, nullptr,
+                                                           Cptr_or_counts, Ccol);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// coarse block index of each fine block
+__global__ void k_fine_to_coarse(const int* __restrict__ ptr, const int* __restrict__ col, const int* __restrict__ agg,
+                                 int n, const int* __restrict__ Cptr, const int* __restrict__ Ccol,
+                                 uint32_t* __restrict__ key) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int a = agg[i];
+    const int* cc = Ccol + Cptr[a];
+    int nn = Cptr[a + 1] - Cptr[a];
+    for (int b = ptr[i]; b < ptr[i + 1]; ++b) key[b] = (uint32_t)(Cptr[a] + lower_bound_i32(cc, nn, agg[col[b]]));
+  }
+}
+
+__global__ void k_row_of_block(const int* __restrict__ ptr, int n, int* __restrict__ row) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    for (int b = ptr[i]; b < ptr[i + 1]; ++b) row[b] = i;
+}
+
+extern "C" int bamg_galerkin_map(bamg_ctx* ctx, const int32_t* ptr, const int32_t* col, const int32_t* agg, int32_t n,
+                                 int64_t nnz_fine, const int32_t* Cptr, const int32_t* Ccol, int64_t nnz_coarse,
+                                 int32_t* fine_sorted, int32_t* cblk_ptr, int32_t* fine_row, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (nnz_fine <= 0) return 0;
+  uint32_t *key = nullptr, *iota = nullptr, *skey = nullptr;
+  BAMG_CUDA_CHECK(cudaMallocAsync(&key, 4 * nnz_fine, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&iota, 4 * nnz_fine, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&skey, 4 * nnz_fine, st));
+  k_fine_to_coarse<<<grid_for(n, 128), 128, 0, st>>>(ptr, col, agg, n, Cptr, Ccol, key);
+  k_iota_i<<<grid_for(nnz_fine, 256), 256, 0, st>>>(iota, (int)nnz_fine);
+  k_row_of_block<<<grid_for(n, 128), 128, 0, st>>>(ptr, n, fine_row);
+  BAMG_LAUNCH_CHECK();
+  int bits = 1;
+  while ((1ll << bits) < nnz_coarse) ++bits;
+  int rc = radix_sort_pairs(key, iota, skey, (uint32_t*)fine_sorted, nnz_fine, bits, st);
+  if (rc) return rc;
+  rc = segment_ptr((const int*)skey, nnz_fine, (int)nnz_coarse, cblk_ptr, st);
+  if (rc) return rc;
+  cudaFreeAsync(key, st);
+  cudaFreeAsync(iota, st);
+  cudaFreeAsync(skey, st);
+  return 0;
+}
+
+// Warp per coarse block; lane owns 8 entries (row lane/2, cols 8*(lane&1)..+7).
+// T = A_ij P_j (bs x 16) staged in shared memory per fine block.
+template <int BS>
+__global__ void __launch_bounds__(128)
+k_galerkin_numeric(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_sorted,
+                   const int* __restrict__ fine_row, const int* __restrict__ col, const double* __restrict__ blocks,
+                   const double* __restrict__ P, int64_t nnz_coarse, double* __restrict__ out) {
+  __shared__ double Ts[4][BS * NS];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int r = lane >> 1, c0 = (lane & 1) * 8;
+  double* T = Ts[w];
+  for (int64_t cb = warp; cb < nnz_coarse; cb += nwarps) {
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    for (int q = cblk_ptr[cb]; q < cblk_ptr[cb + 1]; ++q) {
+      int fb = fine_sorted[q];
+      int i = fine_row[fb], j = col[fb];
+      const double* a = blocks + (int64_t)fb * BS * BS;
+      const double* pj = P + (int64_t)j * BS * NS;
+      // T = A_ij P_j
+      for (int t = lane; t < BS * NS; t += 32) {
+        int rr = t / NS, cc = t - rr * NS;
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < BS; ++k) s = fma(a[rr * BS + k], pj[k * NS + cc], s);
+        T[t] = s;
+      }
+      __syncwarp();
+      const double* pi = P + (int64_t)i * BS * NS;
+#pragma unroll
+      for (int k = 0; k < BS; ++k) {
+        double pik = pi[k * NS + r];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = fma(pik, T[k * NS + c0 + q], acc[q]);
+      }
+      __syncwarp();
+    }
+    double* o = out + cb * NS * NS + r * NS + c0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = acc[q];
+  }
+}
+
+// out_ab = 0.5 (B_ab + B_ba^T), in place, thread per upper block
+__global__ void k_sym_blocks(const int* __restrict__ Cptr, const int* __restrict__ Ccol, int n, double* __restrict__ B) {
+  for (int a = blockIdx.x; a < n; a += gridDim.x) {
+    for (int q = Cptr[a]; q < Cptr[a + 1]; ++q) {
+      int b = Ccol[q];
+      if (b < a) continue;
+      int t = Cptr[b] + lower_bound_i32(Ccol + Cptr[b], Cptr[b + 1] - Cptr[b], a);
+      double* X = B + (int64_t)q * NS * NS;
+      double* Y = B + (int64_t)t * NS * NS;
+      __syncthreads();
+      if (b == a) {
+        for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+          int r = e / NS, c = e - r * NS;
+          if (c < r) continue;
+          double v = 0.5 * (X[r * NS + c] + X[c * NS + r]);
+          X[r * NS + c] = v;
+          X[c * NS + r] = v;
+        }
+      } else {
+        for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+          int r = e / NS, c = e - r * NS;
+          double v = 0.5 * (X[r * NS + c] + Y[c * NS + r]);
+          X[r * NS + c] = v;
+          Y[c * NS + r] = v;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// +1.0 on padded coarse dofs' diagonal entries (multigrid.py:458-471)
+__global__ void k_patch(const int* __restrict__ padded_cnt, const int* __restrict__ Cptr, const int* __restrict__ Ccol,
+                        int n_agg, double* __restrict__ B) {
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n_agg; a += gridDim.x * blockDim.x) {
+    int np = padded_cnt[a];
+    if (!np) continue;
+    int t = Cptr[a] + lower_bound_i32(Ccol + Cptr[a], Cptr[a + 1] - Cptr[a], a);
+    if (t >= Cptr[a + 1] || Ccol[t] != a) continue;
+    double* X = B + (int64_t)t * NS * NS;
+    for (int c = NS - np; c < NS; ++c) X[c * NS + c] += 1.0;
+  }
+}
+
+extern "C" int bamg_galerkin_numeric(bamg_ctx* ctx, int32_t bs, const int32_t* cblk_ptr, const int32_t* fine_sorted,
+                                     const int32_t* fine_row, const int32_t* col, const double* blocks,
+                                     const double* P, int32_t n_agg, const int32_t* Cptr, const int32_t* Ccol,
+                                     int64_t nnz_coarse, const int32_t* padded_cnt, double* out, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (nnz_coarse <= 0) return 0;
+  int g = grid_for(nnz_coarse * 32, 128, 16);
+  switch (bs) {
+    case 9: k_galerkin_numeric<9><<<g, 128, 0, st>>>(cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
+    case 16: k_galerkin_numeric<16><<<g, 128, 0, st>>>(cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
+    default: bamg_set_error("galerkin: unsupported block size %d", bs); return BAMG_ERR_UNSUPPORTED;
+  }
+  k_sym_blocks<<<grid_for(n_agg, 1, 16), 128, 0, st>>>(Cptr, Ccol, n_agg, out);
+  k_patch<<<grid_for(n_agg, 128), 128, 0, st>>>(padded_cnt, Cptr, Ccol, n_agg, out);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}

@@ -1,0 +1,840 @@
+// Observation structure, residual/Jacobian evaluation, normal blocks, damping,
+// reduced right-hand side, back-substitution.
+//
+// Device layout: observations are stored POINT-MAJOR, sorted by
+// (point, camera); `pt_ptr` delimits each point's segment. `cm_list` lists the
+// point-major positions in (camera, point) order -- exactly the block order of the
+// reference's W (`schur.py:114-116` via `blockmat.py:217-230`); `cam_ptr`
+// delimits each camera's run in it. Per-observation arrays (all fp64, AoS per
+// observation): F (2x9 row-major), E (2x3), res (2), w (1), H = E C^-1 (2x3).
+#include <math.h>
+
+#include "common.cuh"
+#include "ctx.h"
+
+int radix_sort_pairs(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
+                     int64_t n, int key_bits, cudaStream_t st);
+int scan_exclusive_int(const int* in, int* out, int64_t n, int* total, cudaStream_t st);
+int segment_ptr(const int* ids, int64_t n, int nseg, int* ptr, cudaStream_t st);
+
+static int bits_for(int64_t n) {
+  int b = 1;
+  while ((1ll << b) < n) ++b;
+  return b;
+}
+
+__global__ void k_iota(uint32_t* a, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = (uint32_t)i;
+}
+
+__global__ void k_take_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ idx, int64_t n,
+                           uint32_t* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
+// Builds the point-major permutation and the camera-major list (problem.py:84-86
+// keeps input order; only the device layout changes).
+extern "C" int bamg_obs_orders(bamg_ctx* ctx, const int32_t* cam_idx, const int32_t* pt_idx, int64_t k,
+                               int32_t nc, int32_t npt, int32_t* pm_perm, int32_t* obs_cam_pm,
+                               int32_t* obs_pt_pm, int32_t* pt_ptr, int32_t* cm_list, int32_t* cam_ptr,
+                               void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (k == 0) {
+    BAMG_CUDA_CHECK(cudaMemsetAsync(pt_ptr, 0, sizeof(int) * (npt + 1), st));
+    BAMG_CUDA_CHECK(cudaMemsetAsync(cam_ptr, 0, sizeof(int) * (nc + 1), st));
+    return 0;
+  }
+  uint32_t *iota = nullptr, *k1 = nullptr, *v1 = nullptr, *kk = nullptr, *cm_keys = nullptr;
+  BAMG_CUDA_CHECK(cudaMallocAsync(&iota, 4 * k, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&k1, 4 * k, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&v1, 4 * k, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&kk, 4 * k, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&cm_keys, 4 * k, st));
+  int g = grid_for(k, 256);
+  k_iota<<<g, 256, 0, st>>>(iota, k);
+  int rc;
+  // (a) stable by camera
+  rc = radix_sort_pairs((const uint32_t*)cam_idx, iota, k1, v1, k, bits_for(nc), st);
+  if (rc) return rc;
+  // (b) stable by point -> (point, camera) order
+  k_take_u32<<<g, 256, 0, st>>>((const uint32_t*)pt_idx, v1, k, kk);
+  rc = radix_sort_pairs(kk, v1, (uint32_t*)obs_pt_pm, (uint32_t*)pm_perm, k, bits_for(npt), st);
+  if (rc) return rc;
+  k_take_u32<<<g, 256, 0, st>>>((const uint32_t*)cam_idx, (const uint32_t*)pm_perm, k, (uint32_t*)obs_cam_pm);
+  // (c) point-major positions stably by camera -> (camera, point) order
+  rc = radix_sort_pairs((const uint32_t*)obs_cam_pm, iota, cm_keys, (uint32_t*)cm_list, k, bits_for(nc), st);
+  if (rc) return rc;
+  rc = segment_ptr(obs_pt_pm, k, npt, pt_ptr, st);
+  if (rc) return rc;
+  rc = segment_ptr((const int*)cm_keys, k, nc, cam_ptr, st);
+  if (rc) return rc;
+  BAMG_LAUNCH_CHECK();
+  cudaFreeAsync(iota, st);
+  cudaFreeAsync(k1, st);
+  cudaFreeAsync(v1, st);
+  cudaFreeAsync(kk, st);
+  cudaFreeAsync(cm_keys, st);
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// covisibility pattern (S pattern incl. diagonal) and visibility strength
+
+// Row i: OR a bitmap of cameras co-observing any point of camera i; the diagonal
+// is always present (A is block-diagonal, schur.py:136).
+__global__ void k_covis_rows(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list,
+                             const int* __restrict__ obs_pt_pm, const int* __restrict__ pt_ptr,
+                             const int* __restrict__ obs_cam_pm, int nc, int* __restrict__ counts,
+                             const int* __restrict__ S_ptr, int* __restrict__ S_col) {
+  extern __shared__ unsigned int bm[];
+  int words = (nc + 31) >> 5;
+  for (int i = blockIdx.x; i < nc; i += gridDim.x) {
+    for (int w = threadIdx.x; w < words; w += blockDim.x) bm[w] = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) atomicOr(&bm[i >> 5], 1u << (i & 31));
+    for (int q = cam_ptr[i] + threadIdx.x; q < cam_ptr[i + 1]; q += blockDim.x) {
+      int p = obs_pt_pm[cm_list[q]];
+      for (int o = pt_ptr[p]; o < pt_ptr[p + 1]; ++o) {
+        int j = obs_cam_pm[o];
+        atomicOr(&bm[j >> 5], 1u << (j & 31));
+      }
+    }
+    __syncthreads();
+    if (S_col == nullptr) {
+      int c = 0;
+      for (int w = threadIdx.x; w < words; w += blockDim.x) c += __popc(bm[w]);
+      c = warp_sum_int(c);
+      __shared__ int red[32];
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int t = 0;
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+        counts[i] = t;
+      }
+    } else {
+      // ordered fill: one warp walks the words, lanes compact set bits
+      if (threadIdx.x < 32) {
+        int lane = threadIdx.x;
+        int out = S_ptr[i];
+        for (int w0 = 0; w0 < words; w0 += 32) {
+          int w = w0 + lane;
+          unsigned v = (w < words) ? bm[w] : 0u;
+          int c = __popc(v);
+          int incl = c;
+          for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(FULL_MASK, incl, o);
+            if (lane >= o) incl += t;
+          }
+          int pos = out + incl - c;
+          while (v) {
+            int b = __ffs(v) - 1;
+            v &= v - 1;
+            S_col[pos++] = w * 32 + b;
+          }
+          out += __shfl_sync(FULL_MASK, incl, 31);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+extern "C" int bamg_covis_count(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
+                                const int32_t* obs_pt_pm, const int32_t* pt_ptr, const int32_t* obs_cam_pm,
+                                int32_t nc, int32_t* row_counts, void* stream) {
+  (void)ctx;
+  size_t sm = sizeof(unsigned) * ((nc + 31) / 32);
+  if (sm > 200 * 1024) {
+    bamg_set_error("covisibility bitmap for %d cameras exceeds shared memory", nc);
+    return BAMG_ERR_UNSUPPORTED;
+  }
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_covis_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_covis_rows<<<grid_for(nc, 1, 16), 256, sm, as_stream(stream)>>>(cam_ptr, cm_list, obs_pt_pm, pt_ptr,
+                                                                    obs_cam_pm, nc, row_counts, nullptr, nullptr);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int bamg_covis_fill(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
+                               const int32_t* obs_pt_pm, const int32_t* pt_ptr, const int32_t* obs_cam_pm,
+                               int32_t nc, const int32_t* S_ptr, int32_t* S_col, void* stream) {
+  (void)ctx;
+  size_t sm = sizeof(unsigned) * ((nc + 31) / 32);
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_covis_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_covis_rows<<<grid_for(nc, 1, 16), 256, sm, as_stream(stream)>>>(cam_ptr, cm_list, obs_pt_pm, pt_ptr,
+                                                                    obs_cam_pm, nc, nullptr, S_ptr, S_col);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// Shared-point counts per covisibility slot (diagonal = degree), exact integers.
+__global__ void k_shared_counts(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list,
+                                const int* __restrict__ obs_pt_pm, const int* __restrict__ pt_ptr,
+                                const int* __restrict__ obs_cam_pm, int nc, const int* __restrict__ S_ptr,
+                                const int* __restrict__ S_col, int* __restrict__ shared_cnt) {
+  extern __shared__ int sm_i[];
+  for (int i = blockIdx.x; i < nc; i += gridDim.x) {
+    int b = S_ptr[i], n = S_ptr[i + 1] - b;
+    int* cols = sm_i;
+    int* cnt = sm_i + n;
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+      cols[q] = S_col[b + q];
+      cnt[q] = 0;
+    }
+    __syncthreads();
+    for (int q = cam_ptr[i] + threadIdx.x; q < cam_ptr[i + 1]; q += blockDim.x) {
+      int p = obs_pt_pm[cm_list[q]];
+      for (int o = pt_ptr[p]; o < pt_ptr[p + 1]; ++o) {
+        int s = lower_bound_i32(cols, n, obs_cam_pm[o]);
+        atomicAdd(&cnt[s], 1);
+      }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < n; q += blockDim.x) shared_cnt[b + q] = cnt[q];
+    __syncthreads();
+  }
+}
+
+extern "C" int bamg_shared_counts(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
+                                  const int32_t* obs_pt_pm, const int32_t* pt_ptr, const int32_t* obs_cam_pm,
+                                  int32_t nc, const int32_t* S_ptr, const int32_t* S_col, int32_t max_row,
+                                  int32_t* shared_cnt, void* stream) {
+  (void)ctx;
+  size_t sm = sizeof(int) * 2 * (size_t)max_row;
+  if (sm > 200 * 1024) {
+    bamg_set_error("covisibility row of %d blocks exceeds shared memory", max_row);
+    return BAMG_ERR_UNSUPPORTED;
+  }
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_shared_counts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_shared_counts<<<grid_for(nc, 1, 16), 256, sm, as_stream(stream)>>>(cam_ptr, cm_list, obs_pt_pm, pt_ptr,
+                                                                       obs_cam_pm, nc, S_ptr, S_col, shared_cnt);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// Visibility strength (multigrid.py:52-80): G_ij = min(shared / sqrt(deg_i deg_j), 1)
+// for i != j, stored on the covisibility pattern minus the diagonal. Exact integer
+// counts + IEEE sqrt/div => bit-identical to the reference. Also counts the
+// int8-wrapped covisibility blocks of schur.py:151-159 (slots with shared % 256 != 0).
+__global__ void k_visibility_strength(const int* __restrict__ S_ptr, const int* __restrict__ S_col,
+                                      const int* __restrict__ shared_cnt, int nc, int* __restrict__ G_ptr,
+                                      int* __restrict__ G_col, double* __restrict__ G_val,
+                                      int* __restrict__ wrapped_count) {
+  int local = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+    int b = S_ptr[i], e = S_ptr[i + 1];
+    int out = b - i;  // every row holds exactly one (forced) diagonal slot
+    G_ptr[i] = out;
+    if (i == nc - 1) G_ptr[nc] = e - nc;
+    for (int q = b; q < e; ++q) {
+      int j = S_col[q];
+      int c = shared_cnt[q];
+      if ((c & 255) != 0) ++local;
+      if (j == i) continue;
+      G_col[out] = j;
+      G_val[out] = (double)c;  // finished by k_strength_scale
+      ++out;
+    }
+  }
+  local = warp_sum_int(local);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(wrapped_count, local);
+}
+
+__global__ void k_strength_scale(const int* __restrict__ G_ptr, const int* __restrict__ G_col,
+                                 const int* __restrict__ deg, int nc, double* __restrict__ G_val) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+    double di = (double)deg[i];
+    for (int q = G_ptr[i]; q < G_ptr[i + 1]; ++q) {
+      double scale = sqrt(di * (double)deg[G_col[q]]);
+      double v = G_val[q] / scale;
+      G_val[q] = v < 1.0 ? v : 1.0;
+    }
+  }
+}
+
+__global__ void k_degrees(const int* __restrict__ cam_ptr, int nc, int* __restrict__ deg, int* __restrict__ zero) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+    int d = cam_ptr[i + 1] - cam_ptr[i];
+    deg[i] = d;
+    if (d == 0) atomicAdd(zero, 1);
+  }
+}
+
+// Outputs: G (CSR without diagonal), degrees, flags[0] = #cameras with no points,
+// flags[1] = int8-wrapped covisibility block count. Host reads flags.
+extern "C" int bamg_visibility_strength(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* S_ptr,
+                                        const int32_t* S_col, const int32_t* shared_cnt, int32_t nc,
+                                        int32_t* deg, int32_t* G_ptr, int32_t* G_col, double* G_val,
+                                        int32_t* flags_dev, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  BAMG_CUDA_CHECK(cudaMemsetAsync(flags_dev, 0, 2 * sizeof(int), st));
+  int g = grid_for(nc, 128);
+  k_degrees<<<g, 128, 0, st>>>(cam_ptr, nc, deg, flags_dev);
+  k_visibility_strength<<<g, 128, 0, st>>>(S_ptr, S_col, shared_cnt, nc, G_ptr, G_col, G_val, flags_dev + 1);
+  k_strength_scale<<<g, 128, 0, st>>>(G_ptr, G_col, deg, nc, G_val);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// residuals and Jacobians (problem.py:202-219, 272-326; rotation.py:36-114)
+
+struct CamModel {
+  double R[9];   // rotation matrix (rotation.py:61-71)
+  double Jr[9];  // right Jacobian (rotation.py:74-88)
+  double s1, s2;
+};
+
+__device__ __forceinline__ void rot_coeffs(const double* aa, double& a2, double& s1, double& s2, double& c2,
+                                           bool& small) {
+  a2 = aa[0] * aa[0] + aa[1] * aa[1] + aa[2] * aa[2];
+  double a = sqrt(a2);
+  small = a < 1e-4;
+  if (small) {
+    s1 = 1.0 - a2 / 6.0;
+    s2 = 0.5 - a2 / 24.0;
+    c2 = 1.0 / 6.0 - a2 / 120.0;
+  } else {
+    double sn, cs;
+    sincos(a, &sn, &cs);
+    s1 = sn / a;
+    s2 = (1.0 - cs) / a2;
+    c2 = (a - sn) / (a2 * a);
+  }
+}
+
+__device__ __forceinline__ void hat(const double* v, double* K) {
+  K[0] = 0.0;   K[1] = -v[2]; K[2] = v[1];
+  K[3] = v[2];  K[4] = 0.0;   K[5] = -v[0];
+  K[6] = -v[1]; K[7] = v[0];  K[8] = 0.0;
+}
+
+__device__ __forceinline__ void mm3(const double* A, const double* B, double* C) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) C[i * 3 + j] = A[i * 3] * B[j] + A[i * 3 + 1] * B[3 + j] + A[i * 3 + 2] * B[6 + j];
+}
+
+struct ProjOut {
+  double pc[3], p[2], n2, dist, res[2], s;
+};
+
+__device__ __forceinline__ bool project_one(const double* __restrict__ cam, const double* __restrict__ X,
+                                            const double* __restrict__ pix, ProjOut& o) {
+  const double* aa = cam;
+  double a2, s1, s2, c2;
+  bool small;
+  rot_coeffs(aa, a2, s1, s2, c2, small);
+  // rotate(): X + s1 (aa x X) + s2 (aa x (aa x X))
+  double c1v[3] = {aa[1] * X[2] - aa[2] * X[1], aa[2] * X[0] - aa[0] * X[2], aa[0] * X[1] - aa[1] * X[0]};
+  double c2v[3] = {aa[1] * c1v[2] - aa[2] * c1v[1], aa[2] * c1v[0] - aa[0] * c1v[2], aa[0] * c1v[1] - aa[1] * c1v[0]};
+#pragma unroll
+  for (int d = 0; d < 3; ++d) o.pc[d] = (X[d] + s1 * c1v[d] + s2 * c2v[d]) + cam[3 + d];
+  double z = o.pc[2];
+  if (z >= -1e-12) return false;  // problem.py:211 (bad = z >= -eps)
+  o.p[0] = -o.pc[0] / z;
+  o.p[1] = -o.pc[1] / z;
+  o.n2 = o.p[0] * o.p[0] + o.p[1] * o.p[1];
+  double k1 = cam[7], k2 = cam[8], f = cam[6];
+  o.dist = 1.0 + k1 * o.n2 + k2 * o.n2 * o.n2;
+  double fd = f * o.dist;
+  o.res[0] = fd * o.p[0] - pix[0];
+  o.res[1] = fd * o.p[1] - pix[1];
+  o.s = o.res[0] * o.res[0] + o.res[1] * o.res[1];
+  return true;
+}
+
+__device__ __forceinline__ double loss_rho(double s, int huber) {
+  if (!huber) return s;
+  return s <= 1.0 ? s : 2.0 * sqrt(fmax(s, 1.0)) - 1.0;
+}
+
+__device__ __forceinline__ double loss_w(double s, int huber) {
+  if (!huber) return 1.0;
+  return s <= 1.0 ? 1.0 : pow(fmax(s, 1.0), -0.25);
+}
+
+#define EVAL_THREADS 256
+
+// One thread per observation (point-major). Writes F, E, res, w and a behind flag;
+// objective partials reduced deterministically (last block finishes).
+__global__ void __launch_bounds__(EVAL_THREADS)
+k_evaluate(const double* __restrict__ cams, const double* __restrict__ pts, const int* __restrict__ ocam,
+           const int* __restrict__ opt, const double* __restrict__ pix, int64_t k, int huber, int with_jac,
+           double* __restrict__ F, double* __restrict__ E, double* __restrict__ res, double* __restrict__ w,
+           unsigned char* __restrict__ behind, int* __restrict__ n_behind, double* partials,
+           unsigned int* counter, double* objective) {
+  __shared__ double scratch[33];
+  double acc = 0.0;
+  int nb = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < k; t += (int64_t)gridDim.x * blockDim.x) {
+    const double* cam = cams + (int64_t)ocam[t] * 9;
+    const double* X = pts + (int64_t)opt[t] * 3;
+    ProjOut o;
+    bool ok = project_one(cam, X, pix + 2 * t, o);
+    if (behind) behind[t] = ok ? 0 : 1;
+    if (!ok) {
+      ++nb;
+      continue;
+    }
+    acc += loss_rho(o.s, huber);
+    if (!with_jac) continue;
+    double wt = loss_w(o.s, huber);
+    double z = o.pc[2];
+    double f = cam[6], k1 = cam[7], k2 = cam[8];
+    // dp/dpc (2x3)
+    double iz = -1.0 / z;
+    double z2 = z * z;
+    double dp[6] = {iz, 0.0, o.pc[0] / z2, 0.0, iz, o.pc[1] / z2};
+    double coef = f * (2.0 * k1 + 4.0 * k2 * o.n2);
+    double fd = f * o.dist;
+    double M[4] = {fd + coef * o.p[0] * o.p[0], coef * o.p[0] * o.p[1], coef * o.p[1] * o.p[0],
+                   fd + coef * o.p[1] * o.p[1]};
+    double D[6];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) D[r * 3 + c] = M[r * 2] * dp[c] + M[r * 2 + 1] * dp[3 + c];
+    // R, Jr
+    const double* aa = cam;
+    double a2, s1, s2, c2;
+    bool small;
+    rot_coeffs(aa, a2, s1, s2, c2, small);
+    double K[9], K2[9];
+    hat(aa, K);
+    mm3(K, K, K2);
+    double R[9], Jr[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      double I = (q % 4 == 0) ? 1.0 : 0.0;
+      R[q] = I + s1 * K[q] + s2 * K2[q];
+      Jr[q] = I - s2 * K[q] + c2 * K2[q];
+    }
+    // rotate_jacobian = -R [X]x Jr
+    double HX[9], T1[9], RJ[9];
+    hat(X, HX);
+    mm3(R, HX, T1);
+    mm3(T1, Jr, RJ);
+    double* Fo = F + t * 18;
+    double* Eo = E + t * 6;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double v = -(D[r * 3] * RJ[c] + D[r * 3 + 1] * RJ[3 + c] + D[r * 3 + 2] * RJ[6 + c]);
+        Fo[r * 9 + c] = v * wt;
+        Fo[r * 9 + 3 + c] = D[r * 3 + c] * wt;
+        Eo[r * 3 + c] = (D[r * 3] * R[c] + D[r * 3 + 1] * R[3 + c] + D[r * 3 + 2] * R[6 + c]) * wt;
+      }
+      Fo[r * 9 + 6] = (o.dist * o.p[r]) * wt;
+      Fo[r * 9 + 7] = ((f * o.n2) * o.p[r]) * wt;
+      Fo[r * 9 + 8] = ((f * o.n2 * o.n2) * o.p[r]) * wt;
+    }
+    res[2 * t] = o.res[0] * wt;
+    res[2 * t + 1] = o.res[1] * wt;
+    w[t] = wt;
+  }
+  nb = warp_sum_int(nb);
+  if ((threadIdx.x & 31) == 0 && nb) atomicAdd(n_behind, nb);
+  acc = block_sum(acc, scratch);
+  grid_finish(partials, counter, acc, scratch, objective);
+}
+
+extern "C" int bamg_evaluate(bamg_ctx* ctx, const double* cams, const double* pts, const int32_t* obs_cam,
+                             const int32_t* obs_pt, const double* pixels, int64_t k, int32_t huber,
+                             int32_t with_jacobian, double* F, double* E, double* res, double* w,
+                             uint8_t* behind, double* objective_dev, int32_t* n_behind_dev, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  BAMG_CUDA_CHECK(cudaMemsetAsync(n_behind_dev, 0, sizeof(int), st));
+  int g = grid_for(k, EVAL_THREADS, 4);
+  k_evaluate<<<g, EVAL_THREADS, 0, st>>>(cams, pts, obs_cam, obs_pt, pixels, k, huber, with_jacobian, F, E, res,
+                                         w, behind, n_behind_dev, ctx->partials, ctx->counters + BAMG_CTR_OBJ,
+                                         objective_dev);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// normal-equation blocks (problem.py:255-269, schur.py:104-112)
+
+// Warp per camera: A_raw = sum F^T F (full 9x9), g = sum F^T r. Lanes stride the
+// camera's observations in (camera, point) order, then a fixed shuffle tree.
+__global__ void __launch_bounds__(128)
+k_cam_normal(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, const double* __restrict__ F,
+             const double* __restrict__ res, int nc, double* __restrict__ A_raw, double* __restrict__ g_cam) {
+  int lane = threadIdx.x & 31;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = warp; i < nc; i += nwarps) {
+    double a[45];
+    double g[9];
+#pragma unroll
+    for (int q = 0; q < 45; ++q) a[q] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) g[q] = 0.0;
+    for (int q = cam_ptr[i] + lane; q < cam_ptr[i + 1]; q += 32) {
+      int o = cm_list[q];
+      const double* f = F + (int64_t)o * 18;
+      double f0[9], f1[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) {
+        f0[c] = f[c];
+        f1[c] = f[9 + c];
+      }
+      double r0 = res[2 * o], r1 = res[2 * o + 1];
+      int t = 0;
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+#pragma unroll
+        for (int l = j; l < 9; ++l) a[t++] += f0[j] * f0[l] + f1[j] * f1[l];
+        g[j] += f0[j] * r0 + f1[j] * r1;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 45; ++q) a[q] = warp_sum(a[q]);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) g[q] = warp_sum(g[q]);
+    if (lane == 0) {
+      double* out = A_raw + (int64_t)i * 81;
+      int t = 0;
+#pragma unroll
+      for (int j = 0; j < 9; ++j)
+#pragma unroll
+        for (int l = j; l < 9; ++l) {
+          out[j * 9 + l] = a[t];
+          out[l * 9 + j] = a[t];
+          ++t;
+        }
+#pragma unroll
+      for (int j = 0; j < 9; ++j) g_cam[(int64_t)i * 9 + j] = g[j];
+    }
+  }
+}
+
+// Thread per point: C_raw = sum E^T E (3x3), g_pt = sum E^T r.
+__global__ void k_pt_normal(const int* __restrict__ pt_ptr, const double* __restrict__ E,
+                            const double* __restrict__ res, int npt, double* __restrict__ C_raw,
+                            double* __restrict__ g_pt) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npt; p += gridDim.x * blockDim.x) {
+    double c[6] = {0, 0, 0, 0, 0, 0}, g[3] = {0, 0, 0};
+    for (int o = pt_ptr[p]; o < pt_ptr[p + 1]; ++o) {
+      const double* e = E + (int64_t)o * 6;
+      double r0 = res[2 * o], r1 = res[2 * o + 1];
+      int t = 0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+#pragma unroll
+        for (int l = j; l < 3; ++l) c[t++] += e[j] * e[l] + e[3 + j] * e[3 + l];
+        g[j] += e[j] * r0 + e[3 + j] * r1;
+      }
+    }
+    double* out = C_raw + (int64_t)p * 9;
+    out[0] = c[0]; out[1] = c[1]; out[2] = c[2];
+    out[3] = c[1]; out[4] = c[3]; out[5] = c[4];
+    out[6] = c[2]; out[7] = c[4]; out[8] = c[5];
+    g_pt[3 * p] = g[0];
+    g_pt[3 * p + 1] = g[1];
+    g_pt[3 * p + 2] = g[2];
+  }
+}
+
+extern "C" int bamg_normal_blocks(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
+                                  const int32_t* pt_ptr, const double* F, const double* E, const double* res,
+                                  int32_t nc, int32_t npt, double* A_raw, double* g_cam, double* C_raw,
+                                  double* g_pt, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (nc > 0) {
+    k_cam_normal<<<grid_for((int64_t)nc * 32, 128, 8), 128, 0, st>>>(cam_ptr, cm_list, F, res, nc, A_raw, g_cam);
+    BAMG_LAUNCH_CHECK();
+  }
+  if (npt > 0) {
+    k_pt_normal<<<grid_for(npt, 128, 16), 128, 0, st>>>(pt_ptr, E, res, npt, C_raw, g_pt);
+    BAMG_LAUNCH_CHECK();
+  }
+  return 0;
+}
+
+// Damping (schur.py:38-47): clip(diag, 1e-6, 1e32) / radius.
+__global__ void k_damping(const double* __restrict__ raw, int n, int bs, double radius, double* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * bs; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = t / bs;
+    int j = (int)(t - b * bs);
+    double d = raw[b * bs * bs + j * (bs + 1)];
+    d = fmin(fmax(d, 1e-6), 1e32);
+    if (d != d) d = raw[b * bs * bs + j * (bs + 1)];
+    out[t] = d / radius;
+  }
+}
+
+extern "C" int bamg_damping(bamg_ctx* ctx, const double* A_raw, const double* C_raw, int32_t nc, int32_t npt,
+                            double radius, double* d_cam, double* d_pt, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (nc) k_damping<<<grid_for((int64_t)nc * 9, 256), 256, 0, st>>>(A_raw, nc, 9, radius, d_cam);
+  if (npt) k_damping<<<grid_for((int64_t)npt * 3, 256), 256, 0, st>>>(C_raw, npt, 3, radius, d_pt);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// A = A_raw + diag(d_cam)
+__global__ void k_add_diag(const double* __restrict__ raw, const double* __restrict__ d, int n, int bs,
+                           double* __restrict__ out) {
+  int64_t tot = (int64_t)n * bs * bs;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = t / (bs * bs);
+    int q = (int)(t - b * bs * bs);
+    int r = q / bs, c = q - r * bs;
+    out[t] = raw[t] + (r == c ? d[b * bs + r] : 0.0);
+  }
+}
+
+// 3x3 Cholesky + L^-T L^-1 (blockmat.py:95-115). Returns false if not PD.
+__device__ __forceinline__ bool chol_inv3(const double* C, double* Ci) {
+  double l00 = C[0];
+  if (!(l00 > 0.0)) return false;
+  l00 = sqrt(l00);
+  double l10 = C[3] / l00, l20 = C[6] / l00;
+  double d1 = C[4] - l10 * l10;
+  if (!(d1 > 0.0)) return false;
+  double l11 = sqrt(d1);
+  double l21 = (C[7] - l20 * l10) / l11;
+  double d2 = C[8] - l20 * l20 - l21 * l21;
+  if (!(d2 > 0.0)) return false;
+  double l22 = sqrt(d2);
+  // M = L^-1 (lower)
+  double m00 = 1.0 / l00, m11 = 1.0 / l11, m22 = 1.0 / l22;
+  double m10 = -l10 * m00 / l11;
+  double m21 = -l21 * m11 / l22;
+  double m20 = -(l20 * m00 + l21 * m10) / l22;
+  // Ci = M^T M
+  Ci[0] = m00 * m00 + m10 * m10 + m20 * m20;
+  Ci[1] = m10 * m11 + m20 * m21;
+  Ci[2] = m20 * m22;
+  Ci[4] = m11 * m11 + m21 * m21;
+  Ci[5] = m21 * m22;
+  Ci[8] = m22 * m22;
+  Ci[3] = Ci[1];
+  Ci[6] = Ci[2];
+  Ci[7] = Ci[5];
+  return true;
+}
+
+// Thread per point: C = C_raw + D_p, factor, C^-1, b_p = -g_p, Cb = C^-1 b_p,
+// then per observation H = E C^-1 (2x3) and q = E Cb (2).
+__global__ void k_build_points(const int* __restrict__ pt_ptr, const double* __restrict__ E,
+                               const double* __restrict__ C_raw, const double* __restrict__ d_pt,
+                               const double* __restrict__ g_pt, int npt, double* __restrict__ C,
+                               double* __restrict__ Cinv, double* __restrict__ Cb, double* __restrict__ H,
+                               double* __restrict__ qo, int* __restrict__ bad_min) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npt; p += gridDim.x * blockDim.x) {
+    double c[9], ci[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) c[q] = C_raw[(int64_t)p * 9 + q];
+    c[0] += d_pt[3 * p];
+    c[4] += d_pt[3 * p + 1];
+    c[8] += d_pt[3 * p + 2];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) C[(int64_t)p * 9 + q] = c[q];
+    if (!chol_inv3(c, ci)) {
+      atomicMin(bad_min, p);
+#pragma unroll
+      for (int q = 0; q < 9; ++q) ci[q] = 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) Cinv[(int64_t)p * 9 + q] = ci[q];
+    double b0 = -g_pt[3 * p], b1 = -g_pt[3 * p + 1], b2 = -g_pt[3 * p + 2];
+    double x0 = ci[0] * b0 + ci[1] * b1 + ci[2] * b2;
+    double x1 = ci[3] * b0 + ci[4] * b1 + ci[5] * b2;
+    double x2 = ci[6] * b0 + ci[7] * b1 + ci[8] * b2;
+    Cb[3 * p] = x0;
+    Cb[3 * p + 1] = x1;
+    Cb[3 * p + 2] = x2;
+    for (int o = pt_ptr[p]; o < pt_ptr[p + 1]; ++o) {
+      const double* e = E + (int64_t)o * 6;
+      double* h = H + (int64_t)o * 6;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc)
+          h[r * 3 + cc] = e[r * 3] * ci[cc] + e[r * 3 + 1] * ci[3 + cc] + e[r * 3 + 2] * ci[6 + cc];
+        qo[2 * (int64_t)o + r] = e[r * 3] * x0 + e[r * 3 + 1] * x1 + e[r * 3 + 2] * x2;
+      }
+    }
+  }
+}
+
+// Warp per camera: out_i = -g_i - sum_o F_o^T q_o   (schur.py:122 rhs), or with
+// `base` != null: out_i = A_i x_i - sum_o F_o^T q_o (implicit matvec, schur.py:84-86).
+__global__ void __launch_bounds__(128)
+k_cam_gather(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, const double* __restrict__ F,
+             const double* __restrict__ qo, const double* __restrict__ g_cam, const double* __restrict__ A,
+             const double* __restrict__ x, int nc, double* __restrict__ out) {
+  int lane = threadIdx.x & 31;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = warp; i < nc; i += nwarps) {
+    double s[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) s[j] = 0.0;
+    for (int q = cam_ptr[i] + lane; q < cam_ptr[i + 1]; q += 32) {
+      int o = cm_list[q];
+      const double* f = F + (int64_t)o * 18;
+      double q0 = qo[2 * (int64_t)o], q1 = qo[2 * (int64_t)o + 1];
+#pragma unroll
+      for (int j = 0; j < 9; ++j) s[j] += f[j] * q0 + f[9 + j] * q1;
+    }
+#pragma unroll
+    for (int j = 0; j < 9; ++j) s[j] = warp_sum(s[j]);
+    if (lane < 9) {
+      double v = 0.0;
+#pragma unroll
+      for (int j = 0; j < 9; ++j)
+        if (j == lane) v = s[j];
+      double b;
+      if (A) {
+        const double* a = A + (int64_t)i * 81 + lane * 9;
+        const double* xi = x + (int64_t)i * 9;
+        b = 0.0;
+#pragma unroll
+        for (int c = 0; c < 9; ++c) b += a[c] * xi[c];
+      } else {
+        b = -g_cam[(int64_t)i * 9 + lane];
+      }
+      out[(int64_t)i * 9 + lane] = b - v;
+    }
+  }
+}
+
+extern "C" int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
+                                 const int32_t* pt_ptr, const double* F, const double* E, const double* A_raw,
+                                 const double* C_raw, const double* g_cam, const double* g_pt,
+                                 const double* d_cam, const double* d_pt, int32_t nc, int32_t npt, double* A,
+                                 double* C, double* Cinv, double* Cb, double* H, double* qo, double* rhs,
+                                 int32_t* bad_min_dev, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  int big = 0x7fffffff;
+  BAMG_CUDA_CHECK(cudaMemcpyAsync(bad_min_dev, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+  if (nc) k_add_diag<<<grid_for((int64_t)nc * 81, 256), 256, 0, st>>>(A_raw, d_cam, nc, 9, A);
+  if (npt)
+    k_build_points<<<grid_for(npt, 128, 16), 128, 0, st>>>(pt_ptr, E, C_raw, d_pt, g_pt, npt, C, Cinv, Cb, H, qo,
+                                                          bad_min_dev);
+  if (nc)
+    k_cam_gather<<<grid_for((int64_t)nc * 32, 128, 8), 128, 0, st>>>(cam_ptr, cm_list, F, qo, g_cam, nullptr,
+                                                                     nullptr, nc, rhs);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// Per point: u_p = sum_o E_o^T (F_o x_cam(o)); v_p = Cinv u_p; q_o = E_o v_p.
+__global__ void k_point_wtx(const int* __restrict__ pt_ptr, const int* __restrict__ ocam,
+                            const double* __restrict__ F, const double* __restrict__ E,
+                            const double* __restrict__ Cinv, const double* __restrict__ x, const double* __restrict__ base,
+                            int npt, double* __restrict__ v_out, double* __restrict__ qo) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npt; p += gridDim.x * blockDim.x) {
+    double u[3] = {0, 0, 0};
+    for (int o = pt_ptr[p]; o < pt_ptr[p + 1]; ++o) {
+      const double* f = F + (int64_t)o * 18;
+      const double* e = E + (int64_t)o * 6;
+      const double* xc = x + (int64_t)ocam[o] * 9;
+      double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) {
+        double xv = xc[c];
+        t0 += f[c] * xv;
+        t1 += f[9 + c] * xv;
+      }
+#pragma unroll
+      for (int j = 0; j < 3; ++j) u[j] += e[j] * t0 + e[3 + j] * t1;
+    }
+    if (base) {
+      // back-substitution form: v = Cinv (base - u)  (schur.py:171-173)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) u[j] = base[3 * (int64_t)p + j] - u[j];
+    }
+    const double* ci = Cinv + (int64_t)p * 9;
+    double v0 = ci[0] * u[0] + ci[1] * u[1] + ci[2] * u[2];
+    double v1 = ci[3] * u[0] + ci[4] * u[1] + ci[5] * u[2];
+    double v2 = ci[6] * u[0] + ci[7] * u[1] + ci[8] * u[2];
+    if (v_out) {
+      v_out[3 * (int64_t)p] = v0;
+      v_out[3 * (int64_t)p + 1] = v1;
+      v_out[3 * (int64_t)p + 2] = v2;
+    }
+    if (qo) {
+      for (int o = pt_ptr[p]; o < pt_ptr[p + 1]; ++o) {
+        const double* e = E + (int64_t)o * 6;
+        qo[2 * (int64_t)o] = e[0] * v0 + e[1] * v1 + e[2] * v2;
+        qo[2 * (int64_t)o + 1] = e[3] * v0 + e[4] * v1 + e[5] * v2;
+      }
+    }
+  }
+}
+
+// Implicit Schur matvec y = A x - W C^-1 W^T x (schur.py:84-86). qo: k*2 scratch.
+extern "C" int bamg_implicit_matvec(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
+                                    const int32_t* pt_ptr, const int32_t* obs_cam_pm, const double* F,
+                                    const double* E, const double* A, const double* Cinv, const double* x,
+                                    int32_t nc, int32_t npt, double* qo, double* y, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (npt) k_point_wtx<<<grid_for(npt, 128, 16), 128, 0, st>>>(pt_ptr, obs_cam_pm, F, E, Cinv, x, nullptr, npt,
+                                                              nullptr, qo);
+  if (nc)
+    k_cam_gather<<<grid_for((int64_t)nc * 32, 128, 8), 128, 0, st>>>(cam_ptr, cm_list, F, qo, nullptr, A, x, nc, y);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// Back-substitution dp = C^-1 (b_p - W^T dc) (schur.py:171-173); b_p = -g_pt.
+__global__ void k_neg(const double* __restrict__ a, double* __restrict__ b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = -a[i];
+}
+
+extern "C" int bamg_back_substitute(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs_cam_pm,
+                                    const double* F, const double* E, const double* Cinv, const double* grad_pt,
+                                    const double* dc, int32_t npt, double* dp, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (npt) k_point_wtx<<<grid_for(npt, 128, 16), 128, 0, st>>>(pt_ptr, obs_cam_pm, F, E, Cinv, dc, grad_pt, npt, dp,
+                                                              nullptr);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int bamg_negate(bamg_ctx* ctx, const double* a, double* b, int64_t n, void* stream) {
+  (void)ctx;
+  if (n) k_neg<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(a, b, n);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// W blocks in the reference's BSR order (for API views): W_b = F_o^T E_o, o = cm_list[b].
+__global__ void k_materialize_W(const int* __restrict__ cm_list, const double* __restrict__ F,
+                                const double* __restrict__ E, int64_t k, double* __restrict__ W) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < k * 27; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = t / 27;
+    int q = (int)(t - b * 27);
+    int r = q / 3, c = q - r * 3;
+    int64_t o = cm_list[b];
+    const double* f = F + o * 18;
+    const double* e = E + o * 6;
+    W[t] = f[r] * e[c] + f[9 + r] * e[3 + c];
+  }
+}
+
+extern "C" int bamg_materialize_W(bamg_ctx* ctx, const int32_t* cm_list, const double* F, const double* E,
+                                  int64_t k, double* W, void* stream) {
+  (void)ctx;
+  if (k) k_materialize_W<<<grid_for(k * 27, 256), 256, 0, as_stream(stream)>>>(cm_list, F, E, k, W);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}

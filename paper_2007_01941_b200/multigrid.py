@@ -1,0 +1,460 @@
+"""Aggregation multigrid on the device (drop-in for `bamg.multigrid`, multigrid.py:1-505).
+
+Setup per level: strength (visibility counts at level 0, block-Frobenius cosine
+below), greedy aggregation (one warp, bit-exact scan order), per-aggregate
+Householder QR of the 16 near-nullspace columns, Galerkin P^T A P with the
+decoupled-dof patch, batched Jacobi inverses, 5-step D-Lanczos for the Chebyshev
+interval and a dense Cholesky of the coarsest operator. The V-cycle runs fused
+Chebyshev steps (SpMV + block-Jacobi + update in one kernel per step).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _lib
+from .blockmat import BlockDiagMatrix, BlockSparseMatrix, DenseTall
+from .problem import CAMERA_SIZE, BundleProblem, ObsStructure
+from .schur import SchurSystem
+
+NULLSPACE_DIM = 16
+_RANK_TOL = 1e-10
+_LANCZOS_SEED = 20210607
+_LANCZOS_STEPS = 5
+_CHEB_UPPER = 1.1
+_CHEB_LOWER = 0.3
+
+
+class StrengthMatrix:
+    """Symmetric nonnegative coupling strengths, CSR without diagonal (multigrid.py:33-49)."""
+
+    def __init__(self, indptr, indices, data, n):
+        self.indptr = D.i32(indptr)
+        self.indices = D.i32(indices)
+        self.data = D.f64(data)
+        self._n = int(n)
+        self._agg_cache = {}
+
+    @staticmethod
+    def from_scipy(g) -> "StrengthMatrix":
+        g = g.tocsr()
+        g.sort_indices()
+        if g.shape[0] != g.shape[1]:
+            raise ValueError("strength matrix must be square")
+        return StrengthMatrix(g.indptr, g.indices, g.data, g.shape[0])
+
+    @property
+    def n(self) -> int:
+        return self._n
+
+    def row(self, i: int):
+        lo, hi = int(self.indptr[i].item()), int(self.indptr[i + 1].item())
+        return self.indices[lo:hi].to(torch.int64), self.data[lo:hi]
+
+
+def _structure_of(problem_or_obs) -> ObsStructure:
+    if isinstance(problem_or_obs, BundleProblem):
+        return problem_or_obs.structure
+    cam_index, pt_index, nc, npt = problem_or_obs
+    ci = torch.as_tensor(cam_index, device=D.dev()).to(torch.int32).reshape(-1)
+    pi = torch.as_tensor(pt_index, device=D.dev()).to(torch.int32).reshape(-1)
+    return ObsStructure(ci, pi, int(nc), int(npt), D.zeros(ci.numel(), 2))
+
+
+def visibility_strength(problem_or_obs) -> StrengthMatrix:
+    """Cosine similarity of camera visibility sets (multigrid.py:52-80), bit-exact."""
+    st = _structure_of(problem_or_obs)
+    s = st.strength
+    if s["n_empty"]:
+        raise ValueError(f"{s['n_empty']} camera(s) observe no points; visibility strength undefined")
+    return StrengthMatrix(s["G_ptr"], s["G_col"], s["G_val"], st.nc)
+
+
+def operator_strength(op: BlockSparseMatrix) -> StrengthMatrix:
+    """Block-Frobenius cosine coupling of a square block operator (multigrid.py:83-98)."""
+    n, nnz, bs = op.n_block_rows, op.n_block_entries, op.row_block_size
+    nrm = D.empty(max(nnz, 1))
+    dn = D.empty(max(n, 1))
+    G_ptr = D.empty(n + 1, dtype=torch.int32)
+    flags = D.empty(2, dtype=torch.int32)
+    D.call("bamg_operator_strength", op._ptr, op._col, op.blocks, n, nnz, bs, nrm, dn, G_ptr, None, None, flags)
+    tot = int(G_ptr[n].item())
+    G_col = D.empty(max(tot, 1), dtype=torch.int32)
+    G_val = D.empty(max(tot, 1))
+    D.call("bamg_operator_strength", op._ptr, op._col, op.blocks, n, nnz, bs, nrm, dn, G_ptr, G_col, G_val, flags)
+    if int(flags[0].item()):
+        raise ValueError("operator has a structurally zero diagonal block")
+    return StrengthMatrix(G_ptr, G_col[:tot], G_val[:tot], n)
+
+
+class Aggregation:
+    """Partition of fine nodes into aggregates (multigrid.py:101-124)."""
+
+    def __init__(self, assignment, n_aggregates: int):
+        self._a32 = D.i32(assignment)
+        self.n_aggregates = int(n_aggregates)
+        self._members = None
+
+    @property
+    def assignment(self):
+        return self._a32.to(torch.int64)
+
+    def sizes(self):
+        return torch.bincount(self.assignment, minlength=self.n_aggregates)
+
+    def mean_size(self) -> float:
+        return self._a32.numel() / self.n_aggregates
+
+    def member_lists(self):
+        """(agg_ptr, members) device CSR; members ascending inside each aggregate."""
+        if self._members is None:
+            n, na = self._a32.numel(), self.n_aggregates
+            ptr = D.empty(na + 1, dtype=torch.int32)
+            mem = D.empty(max(n, 1), dtype=torch.int32)
+            D.call("bamg_aggregate_members", self._a32, n, na, ptr, mem)
+            self._members = (ptr, mem[:n])
+        return self._members
+
+    def members(self):
+        ptr, mem = self.member_lists()
+        p = D.host(ptr)
+        return [mem[p[a]:p[a + 1]].to(torch.int64) for a in range(self.n_aggregates)]
+
+
+def aggregate(strength: StrengthMatrix, max_size: int = 20) -> Aggregation:
+    """Greedy pairwise aggregation (multigrid.py:127-176), bit-exact scan order."""
+    n = strength.n
+    agg = D.empty(max(n, 1), dtype=torch.int32)
+    work = D.empty(max(n, 1), dtype=torch.int32)
+    na = D.empty(1, dtype=torch.int32)
+    D.call("bamg_aggregate", strength.indptr, strength.indices, strength.data, n, int(max_size), agg, work, na)
+    return Aggregation(agg[:n], int(na.item()))
+
+
+def _aggregate_cached(strength: StrengthMatrix, max_size: int) -> Aggregation:
+    # the level-0 graph is parameter independent (solver.py:221-230): same input,
+    # same deterministic result, so the scan runs once per strength object
+    if max_size not in strength._agg_cache:
+        strength._agg_cache[max_size] = aggregate(strength, max_size)
+    return strength._agg_cache[max_size]
+
+
+def build_prolongation(agg: Aggregation, K: DenseTall, fine_block_size: int):
+    """Per-aggregate orthonormal prolongation and coarse near-nullspace (multigrid.py:179-237).
+
+    Returns (P, K_coarse, padded_coarse_dofs); P carries the kernels'
+    prolong/restrict fast path. `P.qr_info` is (n_agg, 2): (pivoted branch?, rank).
+    """
+    bs = int(fine_block_size)
+    if K.cols != NULLSPACE_DIM:
+        raise ValueError(f"near-nullspace must have {NULLSPACE_DIM} columns, got {K.cols}")
+    n = agg._a32.numel()
+    if K.rows != n * bs:
+        raise ValueError(f"near-nullspace has {K.rows} rows, expected {n * bs}")
+    na = agg.n_aggregates
+    ptr, mem = agg.member_lists()
+    max_members = int((ptr[1:] - ptr[:-1]).max().item()) if na else 0
+    Pb = D.empty(max(n, 1), bs, NULLSPACE_DIM)
+    Kc = D.empty(max(na, 1) * NULLSPACE_DIM, NULLSPACE_DIM)
+    info = D.empty(max(na, 1), 2, dtype=torch.int32)
+    pad = D.empty(max(na, 1), dtype=torch.int32)
+    D.call("bamg_prolongation_qr", ptr, mem, K.data, na, bs, max_members, Pb, Kc, info, pad)
+    rows = torch.arange(n + 1, device=D.dev(), dtype=torch.int32)
+    P = BlockSparseMatrix(n, na, bs, NULLSPACE_DIM, rows, agg._a32, Pb[:n], _validate=False)
+    P._prolongator = (ptr, mem)
+    P.qr_info = info[:na]
+    P.padded_count = pad[:na]
+    cnt = pad[:na].to(torch.int64)
+    a_idx = torch.repeat_interleave(torch.arange(na, device=D.dev()), cnt)
+    start = torch.repeat_interleave(NULLSPACE_DIM - cnt, cnt)
+    off = torch.arange(int(cnt.sum().item()), device=D.dev()) - torch.repeat_interleave(torch.cumsum(cnt, 0) - cnt, cnt)
+    padded = a_idx * NULLSPACE_DIM + start + off
+    return P, DenseTall(Kc[: na * NULLSPACE_DIM]), padded
+
+
+def galerkin(P: BlockSparseMatrix, A: BlockSparseMatrix, agg: Aggregation) -> BlockSparseMatrix:
+    """sym(P^T A P) + decoupled-dof patch (multigrid.py:409-411, 444-471)."""
+    na, n = agg.n_aggregates, A.n_block_rows
+    ptr, mem = agg.member_lists()
+    counts = D.empty(na + 1, dtype=torch.int32)
+    D.call("bamg_galerkin_pattern", ptr, mem, A._ptr, A._col, agg._a32, na, counts, None)
+    D.call("bamg_scan_exclusive_i32", counts, counts, na + 1, None)
+    nnzc = int(counts[na].item())
+    Ccol = D.empty(max(nnzc, 1), dtype=torch.int32)
+    D.call("bamg_galerkin_pattern", ptr, mem, A._ptr, A._col, agg._a32, na, counts, Ccol)
+    nnzf = A.n_block_entries
+    fine_sorted = D.empty(max(nnzf, 1), dtype=torch.int32)
+    cblk_ptr = D.empty(nnzc + 1, dtype=torch.int32)
+    fine_row = D.empty(max(nnzf, 1), dtype=torch.int32)
+    D.call("bamg_galerkin_map", A._ptr, A._col, agg._a32, n, nnzf, counts, Ccol, nnzc, fine_sorted, cblk_ptr,
+           fine_row)
+    out = D.empty(max(nnzc, 1), NULLSPACE_DIM, NULLSPACE_DIM)
+    D.call("bamg_galerkin_numeric", A.row_block_size, cblk_ptr, fine_sorted, fine_row, A._col, A.blocks, P.blocks,
+           na, counts, Ccol, nnzc, P.padded_count, out)
+    return BlockSparseMatrix(na, na, NULLSPACE_DIM, NULLSPACE_DIM, counts, Ccol[:nnzc], out[:nnzc], _validate=False)
+
+
+# -- smoother -----------------------------------------------------------------------
+
+
+def _start_vector(n: int, seed: int) -> torch.Tensor:
+    # The seeded Lanczos start vector of multigrid.py:251-252 (numpy PCG64 normal
+    # stream). It is input data, generated once per (seed, n) on the host and
+    # uploaded; every operation on it runs on the device.
+    key = (int(n), int(seed))
+    if key not in _START_CACHE:
+        _START_CACHE[key] = D.f64(np.random.default_rng(seed).standard_normal(n))
+    return _START_CACHE[key]
+
+
+_START_CACHE: dict = {}
+
+
+def _axpby(a, x, b, y):
+    D.call("bamg_axpby", float(a), x, float(b), y, y.numel())
+    return y
+
+
+def estimate_lambda_max(matvec, jacobi: BlockDiagMatrix, n: int, steps: int = _LANCZOS_STEPS,
+                        seed: int = _LANCZOS_SEED) -> float:
+    """Largest eigenvalue of D^-1 A by D-inner-product Lanczos (multigrid.py:243-284)."""
+    v = _start_vector(n, seed)
+    jacobi.factor()
+    alphas, betas = [], []
+    q_prev = D.zeros(n)
+    dnorm = np.sqrt(D.dot(v, jacobi.matvec(v)))
+    q = D.empty(n)
+    _axpby(1.0 / dnorm, v, 0.0, q)  # q = v / dnorm
+    basis = [q]
+    beta_prev = 0.0
+    for _ in range(steps):
+        u = matvec(q)
+        alpha = D.dot(q, u)
+        z = jacobi.solve(u)
+        _axpby(-alpha, q, 1.0, z)
+        _axpby(-beta_prev, q_prev, 1.0, z)
+        for qb in basis:
+            c = D.dot(qb, jacobi.matvec(z))
+            _axpby(-c, qb, 1.0, z)
+        alphas.append(alpha)
+        beta2 = D.dot(z, jacobi.matvec(z))
+        if not np.isfinite(beta2):
+            raise FloatingPointError("Lanczos iteration produced a non-finite value")
+        if beta2 <= 0 or np.sqrt(beta2) < 1e-12 * abs(alpha):
+            break
+        beta = float(np.sqrt(beta2))
+        betas.append(beta)
+        qn = D.empty(n)
+        _axpby(1.0 / beta, z, 0.0, qn)
+        q_prev, q = q, qn
+        basis.append(q)
+        beta_prev = beta
+    if len(betas) >= len(alphas):
+        betas = betas[: len(alphas) - 1]
+    a = np.ascontiguousarray(alphas, dtype=np.float64)
+    b = np.ascontiguousarray(betas if betas else [0.0], dtype=np.float64)
+    return float(_lib.lib().bamg_tridiag_max_eig(a.ctypes.data, b.ctypes.data, len(a)))
+
+
+def _explicit_operator(matvec):
+    """The BSR operator behind a matvec callable, if the fused kernels can use it."""
+    owner = getattr(matvec, "__self__", None)
+    if isinstance(owner, BlockSparseMatrix):
+        op = owner
+    elif isinstance(owner, SchurSystem) and owner.mode == "explicit":
+        op = owner.ensure_explicit()
+    else:
+        return None
+    if getattr(matvec, "__func__", None) not in (BlockSparseMatrix.matvec, SchurSystem.matvec):
+        return None
+    if op._prolongator is not None or op.row_block_size != op.col_block_size or op.row_block_size not in (1, 9, 16):
+        return None
+    return op
+
+
+class ChebyshevSmoother:
+    """Fixed-interval Chebyshev iteration with block-Jacobi (multigrid.py:287-328)."""
+
+    def __init__(self, jacobi: BlockDiagMatrix, lambda_max: float, lower: float, upper: float, iterations: int = 2):
+        if not 0 < lower < upper:
+            raise ValueError(f"need 0 < lower < upper, got [{lower}, {upper}]")
+        self.jacobi = jacobi
+        self.lambda_max = lambda_max
+        self.lower = lower
+        self.upper = upper
+        self.iterations = iterations
+        self.jacobi.factor()
+
+    def apply(self, matvec, x, b):
+        theta = 0.5 * (self.upper + self.lower)
+        delta = 0.5 * (self.upper - self.lower)
+        sigma = theta / delta
+        rho = 1.0 / sigma
+        b = D.f64(b).reshape(-1)
+        op = _explicit_operator(matvec)
+        if op is not None:
+            return self._apply_fused(op, x, b, theta, delta, sigma, rho)
+        # generic operator: separate matvec / Jacobi / update kernels
+        if x is None:
+            r = b.clone()
+            x = D.zeros(b.numel())
+        else:
+            x = D.f64(x).reshape(-1).clone()
+            r = b.clone()
+            _axpby(-1.0, matvec(x), 1.0, r)
+        d = self.jacobi.solve(r)
+        _axpby(0.0, d, 1.0 / theta, d)
+        _axpby(1.0, d, 1.0, x)
+        for _ in range(self.iterations - 1):
+            r = b.clone()
+            _axpby(-1.0, matvec(x), 1.0, r)
+            rho_next = 1.0 / (2.0 * sigma - rho)
+            z = self.jacobi.solve(r)
+            _axpby(2.0 * rho_next / delta, z, rho_next * rho, d)
+            _axpby(1.0, d, 1.0, x)
+            rho = rho_next
+        return x
+
+    def _apply_fused(self, op, x, b, theta, delta, sigma, rho):
+        n, bs = op.n_block_rows, op.row_block_size
+        Dinv = self.jacobi.inverse_blocks()
+        d = D.empty(b.numel())
+        xo = D.empty(b.numel())
+        if x is None:
+            D.call("bamg_cheb_step", bs, op._ptr, op._col, None, None, b, Dinv, d, xo, n, 0.0, theta, 1)
+        else:
+            x = D.f64(x).reshape(-1)
+            D.call("bamg_cheb_step", bs, op._ptr, op._col, op.blocks, x, b, Dinv, d, xo, n, 0.0, theta, 1)
+        x = xo
+        spare = D.empty(b.numel())
+        for _ in range(self.iterations - 1):
+            rho_next = 1.0 / (2.0 * sigma - rho)
+            D.call("bamg_cheb_step", bs, op._ptr, op._col, op.blocks, x, b, Dinv, d, spare, n,
+                   rho_next * rho, 2.0 * rho_next / delta, 0)
+            x, spare = spare, x
+            rho = rho_next
+        return x
+
+
+def make_smoother(matvec, jacobi: BlockDiagMatrix, n: int, seed: int = _LANCZOS_SEED) -> ChebyshevSmoother:
+    lam = estimate_lambda_max(matvec, jacobi, n, seed=seed)
+    if not lam > 0:
+        raise ValueError(f"nonpositive spectral estimate {lam}")
+    return ChebyshevSmoother(jacobi, lam, _CHEB_LOWER * lam, _CHEB_UPPER * lam)
+
+
+# -- hierarchy ------------------------------------------------------------------------
+
+
+class MgLevel:
+    """One grid level (multigrid.py:342-355)."""
+
+    def __init__(self, index, matvec, scalar_dim, operator, explicit, nullspace=None):
+        self.index = index
+        self.matvec = matvec
+        self.scalar_dim = scalar_dim
+        self.operator = operator
+        self.explicit = explicit
+        self.smoother = None
+        self.P = None
+        self.aggregation = None
+        self.nullspace = nullspace
+        self.coarse_factor = None
+
+
+class MgHierarchy:
+    def __init__(self, levels):
+        self.levels = levels
+
+    @property
+    def n_levels(self) -> int:
+        return len(self.levels)
+
+    def apply(self, r):
+        """One V-cycle from a zero initial guess (multigrid.py:366-368)."""
+        return mgcycle(self, 0, None, D.f64(r).reshape(-1))
+
+
+def _coarse_factor(op: BlockSparseMatrix):
+    n = op.shape[0]
+    dense = D.empty(n, n)
+    work = D.empty(n, n)
+    inv = D.empty(n, n)
+    flag = D.empty(1, dtype=torch.int32)
+    D.call("bamg_coarse_factor", op._ptr, op._col, op.blocks, op.n_block_rows, op.row_block_size, dense, work,
+           inv, flag)
+    if int(flag.item()):
+        raise ValueError("coarsest-level operator is not positive definite "
+                         "(damping too small for the given geometry)")
+    return {"inv": inv, "n": n, "L": work}
+
+
+def build_hierarchy(sys: SchurSystem, nullspace: DenseTall, strength: StrengthMatrix, *, max_coarse_dim: int = 400,
+                    max_ratio: float = 0.7, max_aggregate: int = 20, seed: int = _LANCZOS_SEED) -> MgHierarchy:
+    """Coarsen the reduced camera system (multigrid.py:371-441)."""
+    s_explicit = sys.ensure_explicit()
+    level0 = MgLevel(0, sys.matvec, sys.n_cameras * CAMERA_SIZE, sys, s_explicit, nullspace)
+    levels = [level0]
+    K = nullspace
+    while levels[-1].scalar_dim > max_coarse_dim:
+        cur = levels[-1]
+        if cur.index == 0:
+            agg = _aggregate_cached(strength, max_aggregate)
+        else:
+            agg = aggregate(operator_strength(cur.explicit), max_size=max_aggregate)
+        ratio = (agg.n_aggregates * NULLSPACE_DIM) / cur.scalar_dim
+        if ratio > max_ratio:
+            break
+        bs = CAMERA_SIZE if cur.index == 0 else NULLSPACE_DIM
+        P, K_next, padded = build_prolongation(agg, K, bs)
+        a_next = galerkin(P, cur.explicit, agg)
+        cur.P = P
+        cur.aggregation = agg
+        levels.append(MgLevel(cur.index + 1, a_next.matvec, agg.n_aggregates * NULLSPACE_DIM, a_next, a_next,
+                              K_next))
+        K = K_next
+    for lvl in levels[:-1]:
+        jacobi = BlockDiagMatrix(lvl.explicit.diagonal_blocks())
+        lvl.smoother = make_smoother(lvl.matvec, jacobi, lvl.scalar_dim, seed=seed + lvl.index)
+    levels[-1].coarse_factor = _coarse_factor(levels[-1].explicit)
+    return MgHierarchy(levels)
+
+
+def mgcycle(h: MgHierarchy, level: int, x, b):
+    """One V-cycle at the given level (multigrid.py:474-483)."""
+    lvl = h.levels[level]
+    if lvl.coarse_factor is not None:
+        y = D.empty(lvl.coarse_factor["n"])
+        D.call("bamg_dense_gemv", lvl.coarse_factor["inv"], b, lvl.coarse_factor["n"], y)
+        return y
+    x = lvl.smoother.apply(lvl.matvec, x, b)
+    op = _explicit_operator(lvl.matvec)
+    r = D.empty(b.numel())
+    if op is not None:
+        D.call("bamg_bsr_residual", op.row_block_size, op._ptr, op._col, op.blocks, x, b, r, op.n_block_rows)
+    else:
+        r.copy_(b)
+        _axpby(-1.0, lvl.matvec(x), 1.0, r)
+    xc = mgcycle(h, level + 1, None, lvl.P.rmatvec(r))
+    D.call("bamg_prolong", lvl.P._col, lvl.P.blocks, xc, lvl.P.n_block_rows, lvl.P.row_block_size, x, 1)
+    return lvl.smoother.apply(lvl.matvec, x, b)
+
+
+def hierarchy_stats(h: MgHierarchy) -> str:
+    """Text summary, one line per level (multigrid.py:486-505)."""
+    lines = []
+    for lvl in h.levels:
+        nnz = lvl.explicit.nnz_scalar() if lvl.explicit is not None else 0
+        parts = [f"level={lvl.index}", f"scalar_dim={lvl.scalar_dim}",
+                 f"block_rows={lvl.explicit.n_block_rows if lvl.explicit else 0}", f"nnz_scalar={nnz}"]
+        if lvl.smoother is not None:
+            parts.append(f"lambda_max={lvl.smoother.lambda_max:.6g}")
+        if lvl.aggregation is not None:
+            parts.append(f"aggregates={lvl.aggregation.n_aggregates}")
+            parts.append(f"mean_aggregate_size={lvl.aggregation.mean_size():.3f}")
+        if lvl.coarse_factor is not None:
+            parts.append("direct_solve=1")
+        lines.append(" ".join(parts))
+    return "\n".join(lines)

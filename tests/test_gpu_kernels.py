@@ -1,0 +1,193 @@
+"""Kernel-level parity on the GPU: primitives, BSR SpMV, block Cholesky-inverse,
+aggregation known-answer cases, prolongation QR branches, Chebyshev analytic
+cases, PCG hand cases. Each compares against numpy / the CPU oracle."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from conftest import golden, relerr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2007_01941_b200 as P
+
+    return P
+
+
+def D():
+    from paper_2007_01941_b200 import _device
+
+    return _device
+
+
+def test_radix_sort_stable(P):
+    import torch
+
+    rng = np.random.default_rng(1)
+    for n, bits in [(1, 3), (1000, 5), (70000, 14), (300001, 23)]:
+        keys = rng.integers(0, 1 << bits, n).astype(np.uint32)
+        vals = np.arange(n, dtype=np.uint32)
+        kd = torch.as_tensor(keys.view(np.int32), device="cuda")
+        vd = torch.as_tensor(vals.view(np.int32), device="cuda")
+        ko = torch.empty_like(kd)
+        vo = torch.empty_like(vd)
+        D().call("bamg_sort_pairs_u32", kd, vd, ko, vo, n, bits)
+        order = np.argsort(keys, kind="stable")
+        np.testing.assert_array_equal(vo.cpu().numpy().view(np.uint32), order)
+        np.testing.assert_array_equal(ko.cpu().numpy().view(np.uint32), keys[order])
+
+
+def test_scan(P):
+    import torch
+
+    rng = np.random.default_rng(2)
+    for n in [1, 2047, 2048, 2049, 5_000_000]:
+        a = rng.integers(0, 7, n).astype(np.int32)
+        t = torch.as_tensor(a, device="cuda")
+        tot = torch.empty(1, dtype=torch.int32, device="cuda")
+        D().call("bamg_scan_exclusive_i32", t, t, n, tot)
+        ref = np.concatenate([[0], np.cumsum(a)[:-1]])
+        np.testing.assert_array_equal(t.cpu().numpy(), ref)
+        assert int(tot.item()) == int(a.sum())
+
+
+@pytest.mark.parametrize("bs", [9, 16])
+def test_bsr_spmv_and_fused_dot(P, bs):
+    rng = np.random.default_rng(bs)
+    nb = 300
+    m = sp.random(nb, nb, density=0.05, random_state=3, format="csr")
+    m = (m + sp.eye(nb)).tocsr()
+    m.sort_indices()
+    blocks = rng.normal(size=(m.nnz, bs, bs))
+    A = P.BlockSparseMatrix(nb, nb, bs, bs, m.indptr, m.indices, blocks)
+    x = rng.normal(size=nb * bs)
+    ref = sp.bsr_matrix((blocks, m.indices, m.indptr), shape=(nb * bs, nb * bs)) @ x
+    y = A.matvec(x)
+    assert np.max(np.abs(D().host(y) - ref)) <= 1e-12 * np.max(np.abs(ref))
+    out = D().empty(1)
+    y2 = D().empty(nb * bs)
+    xd = D().f64(x)
+    D().call("bamg_bsr_spmv", bs, A._ptr, A._col, A.blocks, xd, y2, nb, out)
+    assert abs(float(out.item()) - x @ ref) <= 1e-11 * abs(x @ ref)
+    # rerun: bit-identical (deterministic reductions)
+    out2 = D().empty(1)
+    D().call("bamg_bsr_spmv", bs, A._ptr, A._col, A.blocks, xd, y2, nb, out2)
+    assert float(out.item()) == float(out2.item())
+
+
+@pytest.mark.parametrize("bs", [1, 3, 9, 16])
+def test_block_cholesky_inverse(P, bs):
+    rng = np.random.default_rng(10 + bs)
+    raw = rng.normal(size=(50, bs, bs))
+    blocks = np.einsum("nij,nkj->nik", raw, raw) + bs * np.eye(bs)
+    M = P.BlockDiagMatrix(blocks).factor()
+    np.testing.assert_allclose(D().host(M.inverse_blocks()), np.linalg.inv(blocks), rtol=1e-10, atol=1e-12)
+    x = rng.normal(size=50 * bs)
+    want = np.einsum("nij,nj->ni", np.linalg.inv(blocks), x.reshape(50, bs)).ravel()
+    assert relerr(D().host(M.solve(x)), want) <= 1e-12
+    bad = blocks.copy()
+    bad[7] = -np.eye(bs)
+    bad[20] = -np.eye(bs)
+    with pytest.raises(P.IndefiniteBlockError) as e:
+        P.BlockDiagMatrix(bad).factor()
+    assert e.value.block_index == 7
+
+
+@pytest.mark.parametrize("name", ["chain", "star", "isolated", "random_ties", "clique30"])
+def test_aggregate_known_answers(P, name):
+    g = golden("aggregate_cases")
+    n = len(g[f"{name}_indptr"]) - 1
+    G = P.StrengthMatrix(g[f"{name}_indptr"], g[f"{name}_indices"], g[f"{name}_data"], n)
+    agg = P.aggregate(G)
+    np.testing.assert_array_equal(D().host(agg.assignment), g[f"{name}_assign"])
+
+
+def test_prolongation_branches(P):
+    from paper_2007_01941_b200.multigrid import Aggregation
+
+    rng = np.random.default_rng(72)
+    # full-rank (economic, sign-fixed) branch: equals numpy QR with positive diag R
+    assign = np.array([0, 0, 1, 1, 1, 2, 2])
+    K = rng.normal(size=(63, 16))
+    Pm, kc, padded = P.build_prolongation(Aggregation(assign, 3), P.DenseTall(K), 9)
+    pd, kcd = D().host(Pm.to_dense()), D().host(kc.data)
+    np.testing.assert_allclose(pd.T @ pd, np.eye(48), atol=1e-12)
+    np.testing.assert_allclose(pd @ kcd, K, atol=1e-12)
+    for a in range(3):
+        mem = np.flatnonzero(assign == a)
+        rows = (mem[:, None] * 9 + np.arange(9)).ravel()
+        qo, ro = np.linalg.qr(K[rows])
+        s = np.where(np.diag(ro) < 0, -1.0, 1.0)
+        np.testing.assert_allclose(pd[np.ix_(rows, np.arange(16 * a, 16 * a + 16))], qo * s, atol=1e-12)
+        np.testing.assert_allclose(kcd[16 * a:16 * a + 16], ro * s[:, None], atol=1e-12)
+    assert len(padded) == 0
+    # singletons pad (multigrid.py:228-230)
+    K2 = rng.normal(size=(18, 16))
+    Pm, kc, padded = P.build_prolongation(Aggregation(np.array([0, 1]), 2), P.DenseTall(K2), 9)
+    pd = D().host(Pm.to_dense())
+    np.testing.assert_allclose(pd @ D().host(kc.data), K2, atol=1e-12)
+    assert len(padded) == 14
+    kept = sorted(set(range(32)) - set(D().host(padded).tolist()))
+    np.testing.assert_allclose((pd.T @ pd)[np.ix_(kept, kept)], np.eye(18), atol=1e-12)
+    # rank-deficient completion
+    K3 = rng.normal(size=(27, 16))
+    K3[:, 5] = K3[:, 3]
+    Pm, kc, _ = P.build_prolongation(Aggregation(np.zeros(3, dtype=np.int64), 1), P.DenseTall(K3), 9)
+    pd = D().host(Pm.to_dense())
+    np.testing.assert_allclose(pd.T @ pd, np.eye(16), atol=1e-12)
+    np.testing.assert_allclose(pd @ D().host(kc.data), K3, atol=1e-12)
+    assert int(D().host(Pm.qr_info)[0, 0]) == 1 and int(D().host(Pm.qr_info)[0, 1]) == 15
+
+
+def test_pcg_hand_cases(P):
+    n = 12
+    b = np.arange(1.0, n + 1)
+    ident = P.BlockDiagMatrix(np.ones((n, 1, 1)))
+    x, rep = P.pcg(ident.matvec, ident.matvec, b, tau=1e-30)
+    np.testing.assert_allclose(D().host(x), b, rtol=1e-14)
+    assert rep.iterations == 1
+    rng = np.random.default_rng(4)
+    M = rng.normal(size=(n, n))
+    A = M @ M.T + n * np.eye(n)
+    Ad = P.BlockDiagMatrix(A[None])
+    x, rep = P.pcg(Ad.matvec, ident.matvec, b, tau=1e-30, max_iterations=200)
+    assert relerr(D().host(x), np.linalg.solve(A, b)) <= 1e-8
+    z, rep = P.pcg(Ad.matvec, ident.matvec, np.zeros(n), tau=0.1)
+    assert rep.iterations == 0 and rep.stop_reason == "residual_tol"
+    with pytest.raises(P.CgDivergence):
+        P.pcg(P.BlockDiagMatrix(-np.ones((n, 1, 1))).matvec, ident.matvec, b, tau=0.1)
+
+
+def test_chebyshev_matches_oracle(P):
+    from oracle import bamg_oracle as O
+
+    rng = np.random.default_rng(5)
+    nb, bs = 40, 9
+    m = sp.random(nb, nb, density=0.1, random_state=6, format="csr")
+    m = (m + m.T + sp.eye(nb)).tocsr()
+    m.sort_indices()
+    raw = rng.normal(size=(m.nnz, bs, bs)) * 0.05
+    A = sp.bsr_matrix((raw, m.indices, m.indptr), shape=(nb * bs, nb * bs)).toarray()
+    A = A + A.T + 4 * nb * np.eye(nb * bs) * 0.1
+    Ab = sp.bsr_matrix(A, blocksize=(bs, bs))
+    Ab.sort_indices()
+    Bd = P.BlockSparseMatrix(nb, nb, bs, bs, Ab.indptr, Ab.indices, Ab.data)
+    Dblk = np.stack([A[i * bs:(i + 1) * bs, i * bs:(i + 1) * bs] for i in range(nb)])
+    jac = P.BlockDiagMatrix(Dblk)
+    sm = P.ChebyshevSmoother(jac, 2.0, 0.6, 2.2)
+    ch = O.Cheb(np.linalg.inv(Dblk), 2.0, 0.6, 2.2)
+    b = rng.normal(size=nb * bs)
+    x0 = rng.normal(size=nb * bs)
+    mv = lambda v: A @ v  # noqa: E731
+    got = D().host(sm.apply(Bd.matvec, None, b))
+    assert relerr(got, ch.apply(mv, None, b)) <= 1e-12
+    got = D().host(sm.apply(Bd.matvec, x0, b))
+    assert relerr(got, ch.apply(mv, x0, b)) <= 1e-12
