@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""Benchmark: one LM linear solve of the config-4 scene on B200 (BASELINE.json).
+
+A "step" is one full LM linear solve at the scene's initial point, exactly the
+reference's timed region (solver.py:244-274: damping, A/C/W/rhs, explicit S,
+multigrid setup, PCG to relative residual 1e-6, back-substitution) plus the
+Jacobian evaluation that feeds it (north-star item 1). Inputs are resident in
+HBM when the timed region starts; `e2e` repeats the step through the public API
+from pinned host arrays (BundleProblem construction incl. the structure pass,
+H2D, solve, D2H of the update).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 4]
+
+With N > 1 (torchrun) every rank solves its own replica (the path has no data
+exchange); timing is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LM linear-solve time (s) to rel-res 1e-6"
+UNIT = "s"
+CFG = dict(preconditioner="multigrid", tau=1e-30, max_iterations=10, function_tolerance=0.0, gradient_tolerance=0.0,
+           parameter_tolerance=0.0, initial_radius=1e4, cg_max_iterations=20000, cg_residual_tolerance=1e-6)
+CPU_SAMPLE_CLUSTERS = 2  # bounded CPU sample of config 4: 2 of 40 clusters
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def scene_for(config: int, fraction_clusters: int | None = None):
+    from paper_2007_01941_b200 import scenes
+
+    cache = f"/tmp/bamg_scene_c{config}_{fraction_clusters or 'full'}_v1.npz"
+    if os.path.exists(cache):
+        d = np.load(cache)
+        return scenes.Scene(str(d["name"]), d["cams"], d["pts"], d["ci"], d["pi"], d["pix"])
+    t0 = time.time()
+    if config == 4 and fraction_clusters:
+        sc = scenes.large(n_clusters=fraction_clusters, n_points=int(4_500_000 * fraction_clusters / 40))
+    else:
+        sc = scenes.config(config)
+    log(f"[bench] generated config {config} ({sc.n_cameras} cams, {sc.n_points} pts, {sc.n_observations} obs) "
+        f"in {time.time() - t0:.1f}s")
+    try:
+        np.savez(cache, name=sc.name, cams=sc.camera_params, pts=sc.points, ci=sc.cam_index, pi=sc.pt_index,
+                 pix=sc.pixels)
+    except OSError:
+        pass
+    return sc
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.samples, self._stop = gpu, [], threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[2:]) if v.lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# -- GPU arm ---------------------------------------------------------------------
+
+
+def gpu_arm(args, rank, world):
+    import torch
+
+    import paper_2007_01941_b200 as P
+    from paper_2007_01941_b200 import _device as D
+    from paper_2007_01941_b200 import solver
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    sc = scene_for(args.config)
+    cfg = P.SolveConfig(**CFG)
+
+    def one_step(prob):
+        obj, jac = P.evaluate(prob)
+        return solver.linear_solve(prob, jac, cfg.initial_radius, cfg)
+
+    prob = P.BundleProblem(*sc.arrays())
+    strength = P.visibility_strength(prob)  # once per problem (solver.py:221-230)
+    _ = prob.structure.symbolic
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        out = one_step(prob)
+    torch.cuda.synchronize()
+    cg_its = out[2].iterations
+    n_levels = out[6].n_levels if out[6] is not None else 1
+
+    # timed region: K device-resident steps, CUDA events on the launching stream
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            out = one_step(prob)
+        ev1.record()
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    setup_s, solve_s = out[4], out[5]
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # kernel roofline: level-0 S SpMV (the operator streamed 5x per PCG iteration)
+    sys_ = out[3]
+    S = sys_.ensure_explicit()
+    nbr, nnzb = S.n_block_rows, S.n_block_entries
+    x = D.f64(np.random.default_rng(0).standard_normal(nbr * 9))
+    y = D.empty(nbr * 9)
+    reps = 50
+    for _ in range(5):
+        D.call("bamg_bsr_spmv", 9, S._ptr, S._col, S.blocks, x, y, nbr, None)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        D.call("bamg_bsr_spmv", 9, S._ptr, S._col, S.blocks, x, y, nbr, None)
+    e1.record()
+    torch.cuda.synchronize()
+    t_spmv = e0.elapsed_time(e1) / reps / 1e3
+    b_spmv = nnzb * (8 * 81 + 4) + 4 * (nbr + 1) + 8 * 9 * nbr + 8 * 9 * nbr
+    peak, peak_kind = measured_peak_hbm()
+    achieved = b_spmv / t_spmv / 1e9
+
+    # V-cycle bandwidth (whole preconditioner application, all levels)
+    h = out[6]
+    vcyc = None
+    if h is not None:
+        r = D.f64(np.random.default_rng(1).standard_normal(nbr * 9))
+        for _ in range(3):
+            h.apply(r)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(10):
+            h.apply(r)
+        e1.record()
+        torch.cuda.synchronize()
+        t_v = e0.elapsed_time(e1) / 10 / 1e3
+        bv = 0
+        for li, lvl in enumerate(h.levels[:-1]):
+            A = lvl.explicit
+            b = A.row_block_size
+            n = A.n_block_rows
+            bsp = A.n_block_entries * (8 * b * b + 4) + 4 * (n + 1) + 16 * b * n
+            bv += 4 * bsp + 4 * 8 * b * b * n + 2 * (8 * 16 * b * n + 4 * n) + 10 * 8 * b * n
+        nL = h.levels[-1].scalar_dim
+        bv += 8 * nL * nL
+        vcyc = {"achieved_gbs": bv / t_v / 1e9, "ms": t_v * 1e3, "bytes": bv, "frac": bv / t_v / 1e9 / peak}
+
+    # kernel launches of ONE step, counted by the CUDA profiler (CUPTI)
+    launches = None
+    try:
+        from torch.profiler import ProfilerActivity, profile
+
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            one_step(prob)
+            torch.cuda.synchronize()
+        launches = sum(1 for e in prof.events() if e.device_type.name == "CUDA" and e.name.startswith("k_"))
+    except Exception as e:  # pragma: no cover
+        log(f"[bench] profiler launch count unavailable: {e}")
+
+    # e2e: public API from pinned host arrays, H2D + structure + solve + D2H
+    import torch as T
+
+    host = [T.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in sc.arrays()]
+    h2d = sum(t.numel() * t.element_size() for t in host)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(max(1, args.steps)):
+        prob2 = P.BundleProblem(*host)
+        obj, jac = P.evaluate(prob2)
+        dc, dp, cg, *_ = solver.linear_solve(prob2, jac, cfg.initial_radius, cfg)
+        dc_h, dp_h = dc.cpu(), dp.cpu()
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_s = e0.elapsed_time(e1) / max(1, args.steps) / 1e3
+    d2h = (dc_h.numel() + dp_h.numel()) * 8
+
+    if rank != 0:
+        return
+    cpu = cpu_baseline(args) if world == 1 and not args.no_cpu else None
+    line = {
+        "metric": METRIC, "value": ms / 1e3, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY App. C config-4 generator, seed 0)",
+        "config": {"workload": f"config {args.config}: one LM linear solve (evaluate + damping + A/C/rhs + explicit S"
+                               " + MG setup + PCG(V-cycle) to rel-res 1e-6 + back-substitution)",
+                   "n_cameras": sc.n_cameras, "n_points": sc.n_points, "n_observations": sc.n_observations,
+                   "nnz_S_blocks": nnzb, "mg_levels": n_levels, "cg_iterations": cg_its,
+                   "l2": "inputs larger than L2 (S alone is %.2f GB)" % (nnzb * 648 / 1e9),
+                   "parallelism": f"replicas x{world}"},
+        "breakdown_s": {"setup": setup_s, "solve": solve_s},
+        "roofline": {"kernel": "k_bsr_spmv<9> (level-0 S SpMV)", "bound": "hbm", "achieved": achieved,
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "bytes_per_launch": b_spmv, "launch_ms": t_spmv * 1e3},
+        "vcycle": vcyc,
+        "e2e": {"value": e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches * args.steps if launches is not None else None,
+        "clocks": clk.summary(),
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+
+
+# -- CPU baseline / reference arm ------------------------------------------------
+
+
+def _oracle_solve(sc, threads=None):
+    from oracle import bamg_oracle as O
+
+    prob = O.Problem.of(sc)
+    t0 = time.perf_counter()
+    obj, jac = O.evaluate(prob)
+    t_eval = time.perf_counter() - t0
+    out = O.linear_solve(prob, radius=1e4, cg_residual_tolerance=1e-6)
+    return t_eval + out["setup"] + out["solve"], out
+
+
+def cpu_baseline(args):
+    """Oracle (numpy/scipy restatement of the reference) on a bounded sample of config 4."""
+    sc = scene_for(4, CPU_SAMPLE_CLUSTERS) if args.config == 4 else scene_for(args.config)
+    full_obs = 29e6 if args.config == 4 else sc.n_observations
+    t, out = _oracle_solve(sc)
+    scale = full_obs / sc.n_observations if args.config == 4 else 1.0
+    return {"value": t * scale, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"config-4 generator with {CPU_SAMPLE_CLUSTERS}/40 clusters ({sc.n_observations} obs, "
+                      f"{sc.n_cameras} cams): {t:.2f}s measured, scaled x{scale:.1f} by observation count "
+                      "(clusters are independent; scipy.sparse/numpy.add.at are single-threaded)",
+            "sample_seconds": t, "cg_iterations": out["cg"].iterations}
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+    sc = scene_for(4, CPU_SAMPLE_CLUSTERS) if args.config == 4 else scene_for(args.config)
+    scale = 29e6 / sc.n_observations if args.config == 4 else 1.0
+    for _ in range(max(0, min(args.warmup, 1))):
+        _oracle_solve(sc)
+    times = []
+    for _ in range(args.steps):
+        t, out = _oracle_solve(sc)
+        times.append(t)
+    v = float(np.mean(times)) * scale
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config {args.config} LM linear solve (CPU oracle port of the reference, "
+                                   f"bounded sample scaled by observation count)"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"{sc.n_observations} obs sample x{scale:.1f}"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200")
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    if world > 1 and args.impl != "reference":
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+    else:
+        gpu_arm(args, rank, world)
+    if world > 1 and args.impl != "reference":
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

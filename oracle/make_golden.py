@@ -132,6 +132,27 @@ def dump_problem(bamg, prob, tag, sample=None, extra=None, lm=True, store_inputs
         finally:
             solver.pcg = orig
         recs = rep.records
+        # the reference's own sensitivity: the same LM run on 1-ulp perturbed camera
+        # parameters (SURVEY TL;DR hazard 1: the pivoted-QR completion is set by
+        # roundoff), recorded as a per-step envelope of CG iteration counts
+        cgs = [[r.cg_iterations for r in recs]]
+        solver.pcg = functools.partial(orig, residual_tolerance=1e-6)
+        try:
+            for trial in range(1, 5):
+                rng = np.random.default_rng(trial)
+                cams = prob.camera_params.copy()
+                mask = rng.random(cams.shape) < 0.5
+                cams = np.where(mask, np.nextafter(cams, np.inf), cams)
+                pp = problem_of(bamg, type("S", (), dict(camera_params=cams, points=prob.points,
+                                                         cam_index=prob.cam_index, pt_index=prob.pt_index,
+                                                         pixels=prob.pixels))())
+                _, rp = solver.lm_solve(pp, cfg)
+                if len(rp.records) == len(recs):
+                    cgs.append([r.cg_iterations for r in rp.records])
+        finally:
+            solver.pcg = orig
+        cgs = np.array(cgs)
+        out["lm_cg_min"], out["lm_cg_max"] = cgs.min(0), cgs.max(0)
         out["lm_cg"] = np.array([r.cg_iterations for r in recs])
         out["lm_obj"] = np.array([r.objective for r in recs])
         out["lm_radius"] = np.array([r.radius for r in recs])
