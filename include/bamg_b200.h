@@ -121,6 +121,16 @@ int bamg_schur_symbolic(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs
                         int64_t n_pairs, const int32_t* dpos, const int32_t* up_off, int32_t* pair_a,
                         int32_t* pair_b, int32_t* blk_pair_ptr, int32_t* up_blk, int32_t* up_row,
                         int32_t* up_tpos, void* stream);
+/* reorder the upper-block work list by descending pair count (load balance) */
+int bamg_schur_order_upper(bamg_ctx* ctx, int32_t* up_blk, int32_t* up_row, int32_t* up_tpos, int32_t n_up,
+                           const int32_t* blk_pair_ptr, void* stream);
+/* row-owned variant: no pair lists; one CTA per camera row, shared-memory
+ * accumulators, deterministic per-warp slot ownership */
+int bamg_schur_numeric_rows(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* pt_ptr,
+                            const int32_t* obs_cam_pm, const int32_t* obs_pt_pm, const double* F, const double* E,
+                            const double* H, const double* A, const int32_t* S_ptr, const int32_t* S_col,
+                            const int32_t* dpos, const int32_t* up_off, const int32_t* up_tpos, int32_t nc, double* S,
+                            void* stream);
 int bamg_schur_numeric(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const double* F,
                        const double* E, const double* H, const double* A, const int32_t* dpos, int32_t nc,
                        const int32_t* up_blk, const int32_t* up_tpos, int32_t n_up, const int32_t* blk_pair_ptr,
@@ -181,6 +191,34 @@ double bamg_tridiag_max_eig(const double* a_host, const double* b_host, int32_t 
 
 /* ---- driver helpers: rotation.py:124-137 canonicalize (solver.py:290, problem.py:106) ---- */
 int bamg_canonicalize(bamg_ctx* ctx, double* cams, int32_t n, int32_t stride, void* stream);
+/* number of library kernel launches so far (benchmark accounting) */
+int64_t bamg_launch_count(void);
+
+/* ---- native solve-phase runtime ----
+ * A multigrid plan holds per-level operators (device pointers owned by the caller)
+ * and its own work vectors; the V-cycle (mgcycle, multigrid.py:474-483, with the
+ * Chebyshev smoother of multigrid.py:308-328) is recorded once as a CUDA graph. */
+typedef struct bamg_mg bamg_mg;
+bamg_mg* bamg_mg_create(int32_t n_levels);
+void bamg_mg_destroy(bamg_mg* mg);
+int bamg_mg_set_level(bamg_mg* mg, int32_t level, int32_t bs, int32_t nbr, const int32_t* ptr, const int32_t* col,
+                      const double* blocks, const double* Dinv, double lower, double upper, int32_t iterations,
+                      const double* P, const int32_t* agg, const int32_t* agg_ptr, const int32_t* members,
+                      int32_t n_agg, const double* coarse_inv);
+int bamg_mg_use_graph(bamg_mg* mg, int32_t on);
+int bamg_mg_apply(bamg_ctx* ctx, bamg_mg* mg, const double* r, double* z, void* stream);
+/* solver.py:70-128 pcg with a BSR operator and the MG plan (or block-Jacobi inverse
+ * blocks when mg == NULL); one host synchronisation per iteration. err codes:
+ * 1 PreconditionerNotSPD, 2/3/4/5 CgDivergence (operator non-finite / curvature /
+ * residual non-finite / preconditioner non-finite). */
+int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, int32_t bs, int32_t nbr, const int32_t* ptr,
+                 const int32_t* col, const double* blocks, const double* b, double* x, double tau, int32_t max_it,
+                 double rtol, double* work, int32_t* iterations_out, int32_t* reason_out, double* rel_out,
+                 double* q_hist, int32_t* err_out, double* err_value_out, int32_t* err_iter_out, void* stream);
+/* multigrid.py:243-284 estimate_lambda_max for a BSR operator; work: (steps+5)*n doubles */
+int bamg_lanczos_lmax(bamg_ctx* ctx, int32_t bs, int32_t nbr, const int32_t* ptr, const int32_t* col,
+                      const double* blocks, const double* D, const double* Dinv, const double* v0, int32_t steps,
+                      double* work, double* lambda_out, int32_t* status, void* stream);
 
 #ifdef __cplusplus
 }

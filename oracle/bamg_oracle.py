@@ -874,14 +874,20 @@ def lm_solve(prob: Problem, preconditioner="multigrid", tau=1e-30, max_iteration
 
 
 def linear_solve(prob: Problem, radius=1e4, preconditioner="multigrid", tau=1e-30,
-                 cg_max_iterations=20000, cg_residual_tolerance=1e-6, l0=None):
-    """One LM linear solve at the initial point (solver.py:244-274), for timing."""
-    obj, jac = evaluate(prob)
+                 cg_max_iterations=20000, cg_residual_tolerance=1e-6, l0=None, G=None, jac=None):
+    """One LM linear solve at the initial point (solver.py:244-274), for timing.
+
+    The parameter-independent strength graph G and its level-0 aggregation may be
+    passed in (computed once per problem, as lm_solve does: solver.py:221-230).
+    """
+    if jac is None:
+        obj, jac = evaluate(prob)
     t0 = time.perf_counter()
     s = build_system(jac, damping(jac, radius))
     s.mode = choose_mode(s)
     if preconditioner == "multigrid":
-        G = visibility_strength(prob.ci, prob.pi, prob.nc, prob.npt)
+        if G is None:
+            G = visibility_strength(prob.ci, prob.pi, prob.nc, prob.npt)
         if l0 is None:
             l0 = aggregate(G)
         levels = hierarchy(s, gauge_nullspace(prob.cams), G, level0_agg=l0)

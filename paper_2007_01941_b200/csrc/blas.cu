@@ -41,6 +41,60 @@ __device__ __forceinline__ double warp_row_product(const int* __restrict__ ptr, 
   return acc;
 }
 
+// 16x16 blocks (2 KB, 16 B aligned): the warp streams each block as 4 fully
+// coalesced 512 B double2 sweeps. Lane l holds column pair 2(l%8) of rows
+// {l/8, 4+l/8, 8+l/8, 12+l/8}; the row sums are reduced over the 8-lane groups
+// once per block row, then moved to lane r = row.
+template <>
+__device__ __forceinline__ double warp_row_product<16>(const int* __restrict__ ptr, const int* __restrict__ col,
+                                                       const double* __restrict__ blocks,
+                                                       const double* __restrict__ x, int row, int lane) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int b0 = ptr[row], b1 = ptr[row + 1];
+  const int cp = 2 * (lane & 7);
+  int b = b0;
+  for (; b + 1 < b1; b += 2) {  // two blocks in flight
+    const double2* A0 = reinterpret_cast<const double2*>(blocks + (int64_t)b * 256) + lane;
+    const double2* A1 = reinterpret_cast<const double2*>(blocks + (int64_t)(b + 1) * 256) + lane;
+    double2 u0 = __ldg(A0), u1 = __ldg(A0 + 32), u2 = __ldg(A0 + 64), u3 = __ldg(A0 + 96);
+    double2 v0 = __ldg(A1), v1 = __ldg(A1 + 32), v2 = __ldg(A1 + 64), v3 = __ldg(A1 + 96);
+    double2 xa = __ldg(reinterpret_cast<const double2*>(x + (int64_t)col[b] * 16 + cp));
+    double2 xb = __ldg(reinterpret_cast<const double2*>(x + (int64_t)col[b + 1] * 16 + cp));
+    a0 = fma(u0.x, xa.x, fma(u0.y, xa.y, a0));
+    a1 = fma(u1.x, xa.x, fma(u1.y, xa.y, a1));
+    a2 = fma(u2.x, xa.x, fma(u2.y, xa.y, a2));
+    a3 = fma(u3.x, xa.x, fma(u3.y, xa.y, a3));
+    a0 = fma(v0.x, xb.x, fma(v0.y, xb.y, a0));
+    a1 = fma(v1.x, xb.x, fma(v1.y, xb.y, a1));
+    a2 = fma(v2.x, xb.x, fma(v2.y, xb.y, a2));
+    a3 = fma(v3.x, xb.x, fma(v3.y, xb.y, a3));
+  }
+  if (b < b1) {
+    const double2* A0 = reinterpret_cast<const double2*>(blocks + (int64_t)b * 256) + lane;
+    double2 u0 = __ldg(A0), u1 = __ldg(A0 + 32), u2 = __ldg(A0 + 64), u3 = __ldg(A0 + 96);
+    double2 xa = __ldg(reinterpret_cast<const double2*>(x + (int64_t)col[b] * 16 + cp));
+    a0 = fma(u0.x, xa.x, fma(u0.y, xa.y, a0));
+    a1 = fma(u1.x, xa.x, fma(u1.y, xa.y, a1));
+    a2 = fma(u2.x, xa.x, fma(u2.y, xa.y, a2));
+    a3 = fma(u3.x, xa.x, fma(u3.y, xa.y, a3));
+  }
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+    a0 += __shfl_xor_sync(FULL_MASK, a0, o);
+    a1 += __shfl_xor_sync(FULL_MASK, a1, o);
+    a2 += __shfl_xor_sync(FULL_MASK, a2, o);
+    a3 += __shfl_xor_sync(FULL_MASK, a3, o);
+  }
+  // row r = 4k + j lives in accumulator k of lanes 8j..8j+7
+  int src = 8 * (lane & 3);
+  double s0 = __shfl_sync(FULL_MASK, a0, src);
+  double s1 = __shfl_sync(FULL_MASK, a1, src);
+  double s2 = __shfl_sync(FULL_MASK, a2, src);
+  double s3 = __shfl_sync(FULL_MASK, a3, src);
+  int k = (lane >> 2) & 3;
+  return k == 0 ? s0 : (k == 1 ? s1 : (k == 2 ? s2 : s3));
+}
+
 // y = A x ; optionally dot_out = <x, y> (deterministic, grid_finish).
 template <int BS>
 __global__ void __launch_bounds__(128)
@@ -126,10 +180,10 @@ extern "C" int bamg_bsr_spmv(bamg_ctx* ctx, int32_t bs, const int32_t* ptr, cons
   int g = spmv_grid(nbr);
   if (dot_out_dev && g > BAMG_MAX_PARTIALS) g = BAMG_MAX_PARTIALS;
   switch (bs) {
-    case 9: k_bsr_spmv<9><<<g, 128, 0, st>>>(ptr, col, blocks, x, y, nbr, part, ctr, dot_out_dev); break;
-    case 16: k_bsr_spmv<16><<<g, 128, 0, st>>>(ptr, col, blocks, x, y, nbr, part, ctr, dot_out_dev); break;
-    case 3: k_bsr_spmv<3><<<g, 128, 0, st>>>(ptr, col, blocks, x, y, nbr, part, ctr, dot_out_dev); break;
-    case 1: k_bsr_spmv<1><<<g, 128, 0, st>>>(ptr, col, blocks, x, y, nbr, part, ctr, dot_out_dev); break;
+    case 9: launch(k_bsr_spmv<9>, g, 128, 0, st, ptr, col, blocks, x, y, nbr, part, ctr, dot_out_dev); break;
+    case 16: launch(k_bsr_spmv<16>, g, 128, 0, st, ptr, col, blocks, x, y, nbr, part, ctr, dot_out_dev); break;
+    case 3: launch(k_bsr_spmv<3>, g, 128, 0, st, ptr, col, blocks, x, y, nbr, part, ctr, dot_out_dev); break;
+    case 1: launch(k_bsr_spmv<1>, g, 128, 0, st, ptr, col, blocks, x, y, nbr, part, ctr, dot_out_dev); break;
     default: bamg_set_error("bsr_spmv: unsupported square block size %d", bs); return BAMG_ERR_UNSUPPORTED;
   }
   BAMG_LAUNCH_CHECK();
@@ -144,9 +198,9 @@ extern "C" int bamg_bsr_residual(bamg_ctx* ctx, int32_t bs, const int32_t* ptr, 
   if (nbr <= 0) return 0;
   int g = spmv_grid(nbr);
   switch (bs) {
-    case 9: k_bsr_residual<9><<<g, 128, 0, st>>>(ptr, col, blocks, x, b, r, nbr); break;
-    case 16: k_bsr_residual<16><<<g, 128, 0, st>>>(ptr, col, blocks, x, b, r, nbr); break;
-    case 1: k_bsr_residual<1><<<g, 128, 0, st>>>(ptr, col, blocks, x, b, r, nbr); break;
+    case 9: launch(k_bsr_residual<9>, g, 128, 0, st, ptr, col, blocks, x, b, r, nbr); break;
+    case 16: launch(k_bsr_residual<16>, g, 128, 0, st, ptr, col, blocks, x, b, r, nbr); break;
+    case 1: launch(k_bsr_residual<1>, g, 128, 0, st, ptr, col, blocks, x, b, r, nbr); break;
     default: bamg_set_error("bsr_residual: unsupported block size %d", bs); return BAMG_ERR_UNSUPPORTED;
   }
   BAMG_LAUNCH_CHECK();
@@ -161,9 +215,9 @@ extern "C" int bamg_cheb_step(bamg_ctx* ctx, int32_t bs, const int32_t* ptr, con
   if (nbr <= 0) return 0;
   int g = spmv_grid(nbr);
   switch (bs) {
-    case 9: k_cheb_step<9><<<g, 128, 0, st>>>(ptr, col, blocks, x_in, b, Dinv, d, x_out, nbr, c1, c2, divide); break;
-    case 16: k_cheb_step<16><<<g, 128, 0, st>>>(ptr, col, blocks, x_in, b, Dinv, d, x_out, nbr, c1, c2, divide); break;
-    case 1: k_cheb_step<1><<<g, 128, 0, st>>>(ptr, col, blocks, x_in, b, Dinv, d, x_out, nbr, c1, c2, divide); break;
+    case 9: launch(k_cheb_step<9>, g, 128, 0, st, ptr, col, blocks, x_in, b, Dinv, d, x_out, nbr, c1, c2, divide); break;
+    case 16: launch(k_cheb_step<16>, g, 128, 0, st, ptr, col, blocks, x_in, b, Dinv, d, x_out, nbr, c1, c2, divide); break;
+    case 1: launch(k_cheb_step<1>, g, 128, 0, st, ptr, col, blocks, x_in, b, Dinv, d, x_out, nbr, c1, c2, divide); break;
     default: bamg_set_error("cheb_step: unsupported block size %d", bs); return BAMG_ERR_UNSUPPORTED;
   }
   BAMG_LAUNCH_CHECK();
@@ -211,7 +265,7 @@ extern "C" int bamg_prolong(bamg_ctx* ctx, const int32_t* agg, const double* P, 
                             int32_t bs, double* y, int32_t accumulate, void* stream) {
   (void)ctx;
   if (nf <= 0) return 0;
-  k_prolong<<<grid_for((int64_t)nf * bs, 256), 256, 0, as_stream(stream)>>>(agg, P, xc, nf, bs, y, accumulate);
+  launch(k_prolong, grid_for((int64_t)nf * bs, 256), 256, 0, as_stream(stream), agg, P, xc, nf, bs, y, accumulate);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -220,7 +274,7 @@ extern "C" int bamg_restrict(bamg_ctx* ctx, const int32_t* agg_ptr, const int32_
                              const double* r, int32_t nagg, int32_t bs, double* bc, void* stream) {
   (void)ctx;
   if (nagg <= 0) return 0;
-  k_restrict<<<grid_for((int64_t)nagg * 16, 256), 256, 0, as_stream(stream)>>>(agg_ptr, members, P, r, nagg, bs, bc);
+  launch(k_restrict, grid_for((int64_t)nagg * 16, 256), 256, 0, as_stream(stream), agg_ptr, members, P, r, nagg, bs, bc);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -323,7 +377,7 @@ extern "C" int bamg_block_chol_inv(bamg_ctx* ctx, const double* M, int32_t n, in
   }
   size_t sm = sizeof(double) * 2 * bs * bs * BCH_WARPS;
   if (sm > 48 * 1024) cudaFuncSetAttribute(k_block_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_block_chol_inv<<<grid_for(n, BCH_WARPS, 16), BCH_WARPS * 32, sm, st>>>(M, n, bs, L, inv, bad_min_dev);
+  launch(k_block_chol_inv, grid_for(n, BCH_WARPS, 16), BCH_WARPS * 32, sm, st, M, n, bs, L, inv, bad_min_dev);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -346,7 +400,7 @@ extern "C" int bamg_blockdiag_apply(bamg_ctx* ctx, const double* M, const double
                                     double* y, void* stream) {
   (void)ctx;
   if (n <= 0) return 0;
-  k_blockdiag_apply<<<grid_for((int64_t)n * bs, 256), 256, 0, as_stream(stream)>>>(M, x, n, bs, y);
+  launch(k_blockdiag_apply, grid_for((int64_t)n * bs, 256), 256, 0, as_stream(stream), M, x, n, bs, y);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -367,7 +421,7 @@ extern "C" int bamg_diag_blocks(bamg_ctx* ctx, const int32_t* ptr, const int32_t
                                 int32_t nbr, int32_t bs, double* D, void* stream) {
   (void)ctx;
   if (nbr <= 0) return 0;
-  k_diag_blocks<<<grid_for((int64_t)nbr * bs * bs, 256), 256, 0, as_stream(stream)>>>(ptr, col, blocks, nbr, bs, D);
+  launch(k_diag_blocks, grid_for((int64_t)nbr * bs * bs, 256), 256, 0, as_stream(stream), ptr, col, blocks, nbr, bs, D);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -461,7 +515,202 @@ __global__ void k_ltl(const double* __restrict__ Li, int n, double* __restrict__
   }
 }
 
-// dense = sym(BSR); L = chol(dense) (in `work`), inv = L^-T L^-1.
+// ---- tiled (32x32) dense Cholesky / triangular inverse / L^-T L^-1 -----------
+#define DT 32
+
+__device__ __forceinline__ int tile_dim(int n, int t) { return min(DT, n - t * DT); }
+
+// factor diagonal tile k in place (lower); flag on a non-positive pivot
+__global__ void __launch_bounds__(1024) k_chol_diag(double* a, int n, int k, int* flag) {
+  __shared__ double T[DT][DT + 1];
+  int tb = tile_dim(n, k);
+  int r = threadIdx.x / DT, c = threadIdx.x % DT;
+  int64_t base = (int64_t)k * DT * n + (int64_t)k * DT;
+  if (r < tb && c < tb) T[r][c] = a[base + (int64_t)r * n + c];
+  __syncthreads();
+  for (int j = 0; j < tb; ++j) {
+    if (threadIdx.x == 0) {
+      double d = T[j][j];
+      if (!(d > 0.0)) *flag = 1;
+      T[j][j] = sqrt(d);
+    }
+    __syncthreads();
+    if (r > j && r < tb && c == j) T[r][j] /= T[j][j];
+    __syncthreads();
+    if (r > j && r < tb && c > j && c <= r) T[r][c] -= T[r][j] * T[c][j];
+    __syncthreads();
+  }
+  if (r < tb && c < tb) a[base + (int64_t)r * n + c] = (c <= r) ? T[r][c] : 0.0;
+}
+
+// L_ik = A_ik L_kk^-T for every tile row i > k (one CTA per tile, warp per row)
+__global__ void __launch_bounds__(1024) k_chol_trsm(double* a, int n, int k) {
+  __shared__ double Lk[DT][DT + 1];
+  __shared__ double X[DT][DT + 1];
+  int i = k + 1 + blockIdx.x;
+  int tk = tile_dim(n, k), ti = tile_dim(n, i);
+  int r = threadIdx.x / DT, c = threadIdx.x % DT;
+  if (r < tk && c < tk) Lk[r][c] = a[(int64_t)(k * DT + r) * n + k * DT + c];
+  if (r < ti && c < tk) X[r][c] = a[(int64_t)(i * DT + r) * n + k * DT + c];
+  __syncthreads();
+  // row r of X solves x L^T = a: x[c] = (a[c] - sum_{j<c} x[j] L[c][j]) / L[c][c]
+  if (r < ti) {
+    for (int cc = 0; cc < tk; ++cc) {
+      double part = (c < cc) ? X[r][c] * Lk[cc][c] : 0.0;
+      part = warp_sum(part);
+      if (c == cc) X[r][cc] = (X[r][cc] - part) / Lk[cc][cc];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  if (r < ti && c < tk) a[(int64_t)(i * DT + r) * n + k * DT + c] = X[r][c];
+}
+
+// A_ij -= L_ik L_jk^T for k < j <= i (one CTA per lower tile of the trailing matrix)
+__global__ void __launch_bounds__(256) k_chol_update(double* a, int n, int k, int nt) {
+  __shared__ double Li[DT][DT + 1];
+  __shared__ double Lj[DT][DT + 1];
+  int m = nt - k - 1;
+  int t = blockIdx.x;
+  int ii = (int)((sqrt(8.0 * t + 1.0) - 1.0) / 2.0);
+  while ((ii + 1) * (ii + 2) / 2 <= t) ++ii;
+  while (ii * (ii + 1) / 2 > t) --ii;
+  int jj = t - ii * (ii + 1) / 2;
+  if (ii >= m) return;
+  int i = k + 1 + ii, j = k + 1 + jj;
+  int tk = tile_dim(n, k), ti = tile_dim(n, i), tj = tile_dim(n, j);
+  for (int q = threadIdx.x; q < DT * DT; q += blockDim.x) {
+    int r = q / DT, c = q % DT;
+    Li[r][c] = (r < ti && c < tk) ? a[(int64_t)(i * DT + r) * n + k * DT + c] : 0.0;
+    Lj[r][c] = (r < tj && c < tk) ? a[(int64_t)(j * DT + r) * n + k * DT + c] : 0.0;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < DT * DT; q += blockDim.x) {
+    int r = q / DT, c = q % DT;
+    if (r >= ti || c >= tj) continue;
+    double s = 0.0;
+#pragma unroll 8
+    for (int x = 0; x < DT; ++x) s = fma(Li[r][x], Lj[c][x], s);
+    a[(int64_t)(i * DT + r) * n + j * DT + c] -= s;
+  }
+}
+
+// inverse of each diagonal tile of L (lower), thread per column
+__global__ void __launch_bounds__(DT) k_tile_inv_diag(const double* __restrict__ L, int n, double* __restrict__ Li) {
+  __shared__ double T[DT][DT + 1];
+  __shared__ double X[DT][DT + 1];
+  int k = blockIdx.x;
+  int tb = tile_dim(n, k);
+  int c = threadIdx.x;
+  for (int r = 0; r < tb; ++r) T[r][c] = (c < tb) ? L[(int64_t)(k * DT + r) * n + k * DT + c] : 0.0;
+  __syncthreads();
+  if (c < tb) {
+    for (int r = 0; r < tb; ++r) {
+      double v;
+      if (r < c) v = 0.0;
+      else if (r == c) v = 1.0 / T[c][c];
+      else {
+        double s = 0.0;
+        for (int x = c; x < r; ++x) s += T[r][x] * X[x][c];
+        v = -s / T[r][r];
+      }
+      X[r][c] = v;
+    }
+  }
+  __syncthreads();
+  if (c < tb)
+    for (int r = 0; r < tb; ++r) Li[(int64_t)(k * DT + r) * n + k * DT + c] = X[r][c];
+}
+
+// block column k of L^-1: Li_ik = -Li_ii (sum_{j=k}^{i-1} L_ij Li_jk), i = k+1.. (one CTA per k)
+__global__ void __launch_bounds__(256) k_tile_inv_col(const double* __restrict__ L, int n, int nt,
+                                                      double* __restrict__ Li) {
+  __shared__ double A[DT][DT + 1];
+  __shared__ double B[DT][DT + 1];
+  __shared__ double S[DT][DT + 1];
+  int k = blockIdx.x;
+  int tk = tile_dim(n, k);
+  for (int i = k + 1; i < nt; ++i) {
+    int ti = tile_dim(n, i);
+    for (int q = threadIdx.x; q < DT * DT; q += blockDim.x) S[q / DT][q % DT] = 0.0;
+    for (int j = k; j < i; ++j) {
+      int tj = tile_dim(n, j);
+      __syncthreads();
+      for (int q = threadIdx.x; q < DT * DT; q += blockDim.x) {
+        int r = q / DT, c = q % DT;
+        A[r][c] = (r < ti && c < tj) ? L[(int64_t)(i * DT + r) * n + j * DT + c] : 0.0;
+        B[r][c] = (r < tj && c < tk) ? Li[(int64_t)(j * DT + r) * n + k * DT + c] : 0.0;
+      }
+      __syncthreads();
+      for (int q = threadIdx.x; q < DT * DT; q += blockDim.x) {
+        int r = q / DT, c = q % DT;
+        double s = 0.0;
+#pragma unroll 8
+        for (int x = 0; x < DT; ++x) s = fma(A[r][x], B[x][c], s);
+        S[r][c] += s;
+      }
+    }
+    __syncthreads();
+    // Li_ik = -Li_ii S
+    for (int q = threadIdx.x; q < DT * DT; q += blockDim.x) {
+      int r = q / DT, c = q % DT;
+      A[r][c] = (r < ti && c < ti) ? Li[(int64_t)(i * DT + r) * n + i * DT + c] : 0.0;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < DT * DT; q += blockDim.x) {
+      int r = q / DT, c = q % DT;
+      if (r >= ti || c >= tk) continue;
+      double s = 0.0;
+      for (int x = 0; x <= r; ++x) s = fma(A[r][x], S[x][c], s);
+      Li[(int64_t)(i * DT + r) * n + k * DT + c] = -s;
+    }
+    __syncthreads();
+  }
+  // zero the strict upper tiles of column k
+  for (int i = 0; i < k; ++i) {
+    int ti = tile_dim(n, i);
+    for (int q = threadIdx.x; q < DT * DT; q += blockDim.x) {
+      int r = q / DT, c = q % DT;
+      if (r < ti && c < tk) Li[(int64_t)(i * DT + r) * n + k * DT + c] = 0.0;
+    }
+  }
+}
+
+// inv = Li^T Li, one CTA per output tile (I, J)
+__global__ void __launch_bounds__(256) k_tile_ltl(const double* __restrict__ Li, int n, int nt, double* __restrict__ out) {
+  __shared__ double A[DT][DT + 1];
+  __shared__ double B[DT][DT + 1];
+  int I = blockIdx.x / nt, J = blockIdx.x % nt;
+  int tI = tile_dim(n, I), tJ = tile_dim(n, J);
+  double acc[4] = {0, 0, 0, 0};
+  for (int K = max(I, J); K < nt; ++K) {
+    int tK = tile_dim(n, K);
+    __syncthreads();
+    for (int q = threadIdx.x; q < DT * DT; q += blockDim.x) {
+      int r = q / DT, c = q % DT;
+      A[r][c] = (r < tK && c < tI) ? Li[(int64_t)(K * DT + r) * n + I * DT + c] : 0.0;
+      B[r][c] = (r < tK && c < tJ) ? Li[(int64_t)(K * DT + r) * n + J * DT + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int q = threadIdx.x + u * 256;
+      int r = q / DT, c = q % DT;
+      double s = 0.0;
+#pragma unroll 8
+      for (int x = 0; x < DT; ++x) s = fma(A[x][r], B[x][c], s);
+      acc[u] += s;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    int q = threadIdx.x + u * 256;
+    int r = q / DT, c = q % DT;
+    if (r < tI && c < tJ) out[(int64_t)(I * DT + r) * n + J * DT + c] = acc[u];
+  }
+}
+
+// dense = sym(BSR); L = chol(dense) (in `work`), inv = L^-T L^-1 -- tiled, many CTAs.
 extern "C" int bamg_coarse_factor(bamg_ctx* ctx, const int32_t* ptr, const int32_t* col, const double* blocks,
                                   int32_t nbr, int32_t bs, double* dense, double* work, double* inv,
                                   int32_t* flag_dev, void* stream) {
@@ -469,13 +718,24 @@ extern "C" int bamg_coarse_factor(bamg_ctx* ctx, const int32_t* ptr, const int32
   cudaStream_t st = as_stream(stream);
   int n = nbr * bs;
   if (n <= 0) return 0;
-  k_densify_sym<<<grid_for((int64_t)n * n, 256), 256, 0, st>>>(ptr, col, blocks, nbr, bs, dense);
-  k_scatter_dense<<<grid_for(nbr, 1, 8), 128, 0, st>>>(ptr, col, blocks, nbr, bs, dense);
-  k_symmetrize<<<grid_for((int64_t)n * n, 256), 256, 0, st>>>(dense, n);
+  launch(k_densify_sym, grid_for((int64_t)n * n, 256), 256, 0, st, ptr, col, blocks, nbr, bs, dense);
+  launch(k_scatter_dense, grid_for(nbr, 1, 8), 128, 0, st, ptr, col, blocks, nbr, bs, dense);
+  launch(k_symmetrize, grid_for((int64_t)n * n, 256), 256, 0, st, dense, n);
   BAMG_CUDA_CHECK(cudaMemcpyAsync(work, dense, sizeof(double) * n * (int64_t)n, cudaMemcpyDeviceToDevice, st));
-  k_dense_chol<<<1, 1024, 0, st>>>(work, n, flag_dev);
-  k_tri_inv<<<grid_for(n, 64), 64, 0, st>>>(work, n, dense);  // dense <- L^-1 (dense sym copy no longer needed)
-  k_ltl<<<grid_for((int64_t)n * n, 256), 256, 0, st>>>(dense, n, inv);
+  BAMG_CUDA_CHECK(cudaMemsetAsync(flag_dev, 0, sizeof(int), st));
+  int nt = (n + DT - 1) / DT;
+  for (int k = 0; k < nt; ++k) {
+    launch(k_chol_diag, 1, 1024, 0, st, work, n, k, flag_dev);
+    int m = nt - k - 1;
+    if (m > 0) {
+      launch(k_chol_trsm, m, 1024, 0, st, work, n, k);
+      launch(k_chol_update, m * (m + 1) / 2, 256, 0, st, work, n, k, nt);
+    }
+  }
+  // strict upper tiles of L are stale copies of A: the inverse kernels never read them
+  launch(k_tile_inv_diag, nt, DT, 0, st, work, n, dense);
+  launch(k_tile_inv_col, nt, 256, 0, st, work, n, nt, dense);
+  launch(k_tile_ltl, nt * nt, 256, 0, st, dense, n, nt, inv);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -496,7 +756,7 @@ __global__ void k_gemv(const double* __restrict__ M, const double* __restrict__ 
 extern "C" int bamg_dense_gemv(bamg_ctx* ctx, const double* M, const double* x, int32_t n, double* y, void* stream) {
   (void)ctx;
   if (n <= 0) return 0;
-  k_gemv<<<grid_for((int64_t)n * 32, 128, 8), 128, 0, as_stream(stream)>>>(M, x, n, y);
+  launch(k_gemv, grid_for((int64_t)n * 32, 128, 8), 128, 0, as_stream(stream), M, x, n, y);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -521,7 +781,7 @@ extern "C" int bamg_pcg_update(bamg_ctx* ctx, double* x, double* r, const double
                                int64_t n, double* rr_dev, void* stream) {
   cudaStream_t st = as_stream(stream);
   int g = grid_for(n, 256, 4);
-  k_pcg_update<<<g, 256, 0, st>>>(x, r, p, ap, alpha, n, ctx->partials, ctx->counters + BAMG_CTR_PCG0, rr_dev);
+  launch(k_pcg_update, g, 256, 0, st, x, r, p, ap, alpha, n, ctx->partials, ctx->counters + BAMG_CTR_PCG0, rr_dev);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -534,7 +794,11 @@ __global__ void k_xpby(const double* __restrict__ z, double beta, double* __rest
 
 extern "C" int bamg_xpby(bamg_ctx* ctx, const double* z, double beta, double* p, int64_t n, void* stream) {
   (void)ctx;
-  if (n) k_xpby<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(z, beta, p, n);
+  if (n) launch(k_xpby, grid_for(n, 256), 256, 0, as_stream(stream), z, beta, p, n);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
+
+// solve-phase runtime (V-cycle program / graph, PCG, Lanczos) shares this TU
+// so that it can launch the templated kernels above directly.
+#include "vcycle.cuh"

@@ -5,7 +5,22 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <atomic>
+#include <utility>
+
 #include "../../include/bamg_b200.h"
+
+// Every kernel of the library goes through launch(): it counts launches
+// (bamg_launch_count) so benchmarks can report exactly how many of OUR kernels
+// ran in a timed region.
+extern std::atomic<long long> g_bamg_launches;
+
+template <typename... KArgs, typename... Args>
+static inline void launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          Args&&... args) {
+  g_bamg_launches.fetch_add(1, std::memory_order_relaxed);
+  k<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+}
 
 #define BAMG_WARP 32
 #define FULL_MASK 0xffffffffu

@@ -25,7 +25,7 @@ __global__ void k_canonicalize(double* __restrict__ cams, int n, int stride) {
 extern "C" int bamg_canonicalize(bamg_ctx* ctx, double* cams, int32_t n, int32_t stride, void* stream) {
   (void)ctx;
   if (n <= 0) return 0;
-  k_canonicalize<<<grid_for(n, 128), 128, 0, as_stream(stream)>>>(cams, n, stride);
+  launch(k_canonicalize, grid_for(n, 128), 128, 0, as_stream(stream), cams, n, stride);
   BAMG_LAUNCH_CHECK();
   return 0;
 }

@@ -65,12 +65,12 @@ extern "C" int bamg_operator_strength(bamg_ctx* ctx, const int32_t* ptr, const i
   cudaStream_t st = as_stream(stream);
   if (G_col == nullptr) {
     BAMG_CUDA_CHECK(cudaMemsetAsync(flags_dev, 0, sizeof(int) * 2, st));
-    k_block_fro<<<grid_for(nnz, 256), 256, 0, st>>>(blocks, nnz, bs * bs, nrm_work);
-    k_diag_norm_and_count<<<grid_for(n, 128), 128, 0, st>>>(ptr, col, nrm_work, n, dnorm_work, G_ptr);
+    launch(k_block_fro, grid_for(nnz, 256), 256, 0, st, blocks, nnz, bs * bs, nrm_work);
+    launch(k_diag_norm_and_count, grid_for(n, 128), 128, 0, st, ptr, col, nrm_work, n, dnorm_work, G_ptr);
     BAMG_LAUNCH_CHECK();
     return scan_exclusive_int(G_ptr, G_ptr, n + 1, flags_dev + 1, st);  // G_ptr[n] is scratch -> total
   }
-  k_op_strength<<<grid_for(n, 128), 128, 0, st>>>(ptr, col, nrm_work, n, dnorm_work, G_ptr, G_col, G_val, flags_dev);
+  launch(k_op_strength, grid_for(n, 128), 128, 0, st, ptr, col, nrm_work, n, dnorm_work, G_ptr, G_col, G_val, flags_dev);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -107,6 +107,8 @@ __device__ __forceinline__ Cand warp_best(Cand c) {
   return c;
 }
 
+#define AG_K 8
+
 __global__ void __launch_bounds__(32)
 k_aggregate(const int* __restrict__ G_ptr, const int* __restrict__ G_col, const double* __restrict__ G_val, int n,
             int max_size, int* __restrict__ agg_g, int* __restrict__ size_g, int use_smem, int* __restrict__ n_agg_out) {
@@ -120,16 +122,66 @@ k_aggregate(const int* __restrict__ G_ptr, const int* __restrict__ G_col, const 
   }
   __syncwarp();
   int nagg = 0;
+  // Rows of up to 32*AG_K entries live in registers; the row of the next
+  // unaggregated node is loaded while the current node is decided (the
+  // decisions themselves only touch shared memory), which hides the global
+  // latency that otherwise dominates this sequential scan.
+  int pf_node = -1, pf_len = 0;
+  int pf_j[AG_K];
+  double pf_g[AG_K];
+  auto prefetch = [&](int node) {
+    pf_node = node;
+    int s = G_ptr[node], e = G_ptr[node + 1];
+    pf_len = e - s;
+#pragma unroll
+    for (int t = 0; t < AG_K; ++t) {
+      int q = s + lane + 32 * t;
+      bool ok = q < e;
+      pf_j[t] = ok ? G_col[q] : -1;
+      pf_g[t] = ok ? G_val[q] : 0.0;
+    }
+  };
+  if (n > 0) prefetch(0);
   for (int i = 0; i < n; ++i) {
     if (agg[i] >= 0) continue;
     Cand best{0.0, 0, -1};
-    for (int q = G_ptr[i] + lane; q < G_ptr[i + 1]; q += 32) {
-      int j = G_col[q];
-      int a = agg[j];
-      bool elig = (a < 0) || (size[a] < max_size);
-      if (elig) {
-        Cand c{G_val[q], a < 0 ? 1 : 0, j};
-        if (better(c, best)) best = c;
+    if (pf_node != i) prefetch(i);
+    int len = pf_len;
+    int cj[AG_K];
+    double cgv[AG_K];
+#pragma unroll
+    for (int t = 0; t < AG_K; ++t) {
+      cj[t] = pf_j[t];
+      cgv[t] = pf_g[t];
+    }
+    // next candidate: first unaggregated index after i (within 32), else i + 33
+    if (i + 1 < n) {
+      int k = i + 1 + lane;
+      unsigned un = __ballot_sync(FULL_MASK, k < n && agg[k] < 0);
+      int nxt = un ? i + 1 + __ffs(un) - 1 : min(i + 33, n - 1);
+      prefetch(nxt);
+    }
+    if (len <= 32 * AG_K) {
+#pragma unroll
+      for (int t = 0; t < AG_K; ++t) {
+        int j = cj[t];
+        if (j >= 0) {
+          int a = agg[j];
+          if ((a < 0) || (size[a] < max_size)) {
+            Cand c{cgv[t], a < 0 ? 1 : 0, j};
+            if (better(c, best)) best = c;
+          }
+        }
+      }
+    } else {
+      for (int q = G_ptr[i] + lane; q < G_ptr[i + 1]; q += 32) {
+        int j = G_col[q];
+        int a = agg[j];
+        bool elig = (a < 0) || (size[a] < max_size);
+        if (elig) {
+          Cand c{G_val[q], a < 0 ? 1 : 0, j};
+          if (better(c, best)) best = c;
+        }
       }
     }
     best = warp_best(best);
@@ -200,7 +252,7 @@ extern "C" int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t
   int use_smem = sm <= 200 * 1024;
   if (!use_smem) sm = 0;
   if (sm > 48 * 1024) cudaFuncSetAttribute(k_aggregate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_aggregate<<<1, 32, sm, st>>>(G_ptr, G_col, G_val, n, max_size, agg, size_work, use_smem, n_agg_dev);
+  launch(k_aggregate, 1, 32, sm, st, G_ptr, G_col, G_val, n, max_size, agg, size_work, use_smem, n_agg_dev);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -251,7 +303,7 @@ __global__ void k_gauge(const double* __restrict__ cams, int nc, double* __restr
 extern "C" int bamg_gauge_nullspace(bamg_ctx* ctx, const double* cams, int32_t nc, double* K, void* stream) {
   (void)ctx;
   if (nc <= 0) return 0;
-  k_gauge<<<grid_for(nc, 128), 128, 0, as_stream(stream)>>>(cams, nc, K);
+  launch(k_gauge, grid_for(nc, 128), 128, 0, as_stream(stream), cams, nc, K);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -272,7 +324,7 @@ extern "C" int bamg_aggregate_members(bamg_ctx* ctx, const int32_t* agg, int32_t
   uint32_t *iota = nullptr, *skey = nullptr;
   BAMG_CUDA_CHECK(cudaMallocAsync(&iota, 4 * (size_t)n, st));
   BAMG_CUDA_CHECK(cudaMallocAsync(&skey, 4 * (size_t)n, st));
-  k_iota_i<<<grid_for(n, 256), 256, 0, st>>>(iota, n);
+  launch(k_iota_i, grid_for(n, 256), 256, 0, st, iota, n);
   int bits = 1;
   while ((1ll << bits) < n_agg) ++bits;
   int rc = radix_sort_pairs((const uint32_t*)agg, iota, skey, (uint32_t*)members, n, bits, st);
@@ -505,7 +557,7 @@ extern "C" int bamg_prolongation_qr(bamg_ctx* ctx, const int32_t* agg_ptr, const
   int blocks = (int)ceil_div(n_agg, wpb);
   int cap = bamg_num_sms() * 8;
   if (blocks > cap) blocks = cap;
-  k_prolong_qr<<<blocks, 32 * wpb, sm, st>>>(agg_ptr, members, K, n_agg, bs, m_max, Pblocks, Kc, info, padded_cnt);
+  launch(k_prolong_qr, blocks, 32 * wpb, sm, st, agg_ptr, members, K, n_agg, bs, m_max, Pblocks, Kc, info, padded_cnt);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -582,10 +634,10 @@ extern "C" int bamg_galerkin_pattern(bamg_ctx* ctx, const int32_t* agg_ptr, cons
   }
   if (sm > 48 * 1024) cudaFuncSetAttribute(k_coarse_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (Ccol == nullptr)
-    k_coarse_rows<<<grid_for(n_agg, 1, 16), 128, sm, st>>>(agg_ptr, members, ptr, col, agg, n_agg, Cptr_or_counts,
+    launch(k_coarse_rows, grid_for(n_agg, 1, 16), 128, sm, st, agg_ptr, members, ptr, col, agg, n_agg, Cptr_or_counts,
                                                            nullptr, nullptr);
   else
-    k_coarse_rows<<<grid_for(n_agg, 1, 16), 128, sm, st>>>(agg_ptr, members, ptr, col, agg, n_agg, nullptr,
+    launch(k_coarse_rows, grid_for(n_agg, 1, 16), 128, sm, st, agg_ptr, members, ptr, col, agg, n_agg, nullptr,
                                                            Cptr_or_counts, Ccol);
   BAMG_LAUNCH_CHECK();
   return 0;
@@ -618,9 +670,9 @@ extern "C" int bamg_galerkin_map(bamg_ctx* ctx, const int32_t* ptr, const int32_
   BAMG_CUDA_CHECK(cudaMallocAsync(&key, 4 * nnz_fine, st));
   BAMG_CUDA_CHECK(cudaMallocAsync(&iota, 4 * nnz_fine, st));
   BAMG_CUDA_CHECK(cudaMallocAsync(&skey, 4 * nnz_fine, st));
-  k_fine_to_coarse<<<grid_for(n, 128), 128, 0, st>>>(ptr, col, agg, n, Cptr, Ccol, key);
-  k_iota_i<<<grid_for(nnz_fine, 256), 256, 0, st>>>(iota, (int)nnz_fine);
-  k_row_of_block<<<grid_for(n, 128), 128, 0, st>>>(ptr, n, fine_row);
+  launch(k_fine_to_coarse, grid_for(n, 128), 128, 0, st, ptr, col, agg, n, Cptr, Ccol, key);
+  launch(k_iota_i, grid_for(nnz_fine, 256), 256, 0, st, iota, (int)nnz_fine);
+  launch(k_row_of_block, grid_for(n, 128), 128, 0, st, ptr, n, fine_row);
   BAMG_LAUNCH_CHECK();
   int bits = 1;
   while ((1ll << bits) < nnz_coarse) ++bits;
@@ -733,12 +785,12 @@ extern "C" int bamg_galerkin_numeric(bamg_ctx* ctx, int32_t bs, const int32_t* c
   if (nnz_coarse <= 0) return 0;
   int g = grid_for(nnz_coarse * 32, 128, 16);
   switch (bs) {
-    case 9: k_galerkin_numeric<9><<<g, 128, 0, st>>>(cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
-    case 16: k_galerkin_numeric<16><<<g, 128, 0, st>>>(cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
+    case 9: launch(k_galerkin_numeric<9>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
+    case 16: launch(k_galerkin_numeric<16>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
     default: bamg_set_error("galerkin: unsupported block size %d", bs); return BAMG_ERR_UNSUPPORTED;
   }
-  k_sym_blocks<<<grid_for(n_agg, 1, 16), 128, 0, st>>>(Cptr, Ccol, n_agg, out);
-  k_patch<<<grid_for(n_agg, 128), 128, 0, st>>>(padded_cnt, Cptr, Ccol, n_agg, out);
+  launch(k_sym_blocks, grid_for(n_agg, 1, 16), 128, 0, st, Cptr, Ccol, n_agg, out);
+  launch(k_patch, grid_for(n_agg, 128), 128, 0, st, padded_cnt, Cptr, Ccol, n_agg, out);
   BAMG_LAUNCH_CHECK();
   return 0;
 }

@@ -12,6 +12,9 @@
 // error text + device info
 
 static thread_local char g_err[1024] = {0};
+std::atomic<long long> g_bamg_launches{0};
+
+extern "C" int64_t bamg_launch_count(void) { return g_bamg_launches.load(std::memory_order_relaxed); }
 
 void bamg_set_error(const char* fmt, ...) {
   va_list ap;
@@ -160,17 +163,17 @@ int scan_exclusive_int(const int* in, int* out, int64_t n, int* total, cudaStrea
   }
   int64_t nb = ceil_div(n, SCAN_TILE);
   if (nb == 1) {
-    k_scan_apply<<<1, SCAN_THREADS, 0, st>>>(in, n, nullptr, out, total);
+    launch(k_scan_apply, 1, SCAN_THREADS, 0, st, in, n, nullptr, out, total);
     BAMG_LAUNCH_CHECK();
     return 0;
   }
   int* sums = nullptr;
   BAMG_CUDA_CHECK(cudaMallocAsync(&sums, sizeof(int) * nb, st));
-  k_scan_reduce<<<(unsigned)nb, SCAN_THREADS, 0, st>>>(in, n, sums);
+  launch(k_scan_reduce, (unsigned)nb, SCAN_THREADS, 0, st, in, n, sums);
   BAMG_LAUNCH_CHECK();
   int rc = scan_exclusive_int(sums, sums, nb, nullptr, st);
   if (rc) return rc;
-  k_scan_apply<<<(unsigned)nb, SCAN_THREADS, 0, st>>>(in, n, sums, out, total);
+  launch(k_scan_apply, (unsigned)nb, SCAN_THREADS, 0, st, in, n, sums, out, total);
   BAMG_LAUNCH_CHECK();
   BAMG_CUDA_CHECK(cudaFreeAsync(sums, st));
   return 0;
@@ -278,11 +281,11 @@ int radix_sort_pairs(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, u
     uint32_t* kd = to_out ? kout : kb;
     uint32_t* vd = to_out ? vout : vb;
     (void)last;
-    k_radix_hist<<<ntiles, RS_WARPS * 32, 0, st>>>(ks, n, 8 * p, ntiles, hist);
+    launch(k_radix_hist, ntiles, RS_WARPS * 32, 0, st, ks, n, 8 * p, ntiles, hist);
     BAMG_LAUNCH_CHECK();
     int rc = scan_exclusive_int(hist, hist, 256 * (int64_t)ntiles, nullptr, st);
     if (rc) return rc;
-    k_radix_scatter<<<ntiles, RS_WARPS * 32, 0, st>>>(ks, vs, n, 8 * p, ntiles, hist, kd, vd);
+    launch(k_radix_scatter, ntiles, RS_WARPS * 32, 0, st, ks, vs, n, 8 * p, ntiles, hist, kd, vd);
     BAMG_LAUNCH_CHECK();
     ks = kd;
     vs = vd;
@@ -312,7 +315,7 @@ __global__ void k_segment_ptr(const int* __restrict__ ids, int64_t n, int nseg, 
 }
 
 int segment_ptr(const int* ids, int64_t n, int nseg, int* ptr, cudaStream_t st) {
-  k_segment_ptr<<<grid_for(n + 1, 256), 256, 0, st>>>(ids, n, nseg, ptr);
+  launch(k_segment_ptr, grid_for(n + 1, 256), 256, 0, st, ids, n, nseg, ptr);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -356,7 +359,7 @@ extern "C" int bamg_gather_rows_f64(bamg_ctx* ctx, const double* src, const int3
                                     int32_t width, double* dst, void* stream) {
   (void)ctx;
   if (n <= 0) return 0;
-  k_gather_rows_f64<<<grid_for(n * width, 256), 256, 0, as_stream(stream)>>>(src, idx, n, width, dst);
+  launch(k_gather_rows_f64, grid_for(n * width, 256), 256, 0, as_stream(stream), src, idx, n, width, dst);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -365,7 +368,7 @@ extern "C" int bamg_scatter_rows_f64(bamg_ctx* ctx, const double* src, const int
                                      int32_t width, double* dst, void* stream) {
   (void)ctx;
   if (n <= 0) return 0;
-  k_scatter_rows_f64<<<grid_for(n * width, 256), 256, 0, as_stream(stream)>>>(src, idx, n, width, dst);
+  launch(k_scatter_rows_f64, grid_for(n * width, 256), 256, 0, as_stream(stream), src, idx, n, width, dst);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -374,7 +377,7 @@ extern "C" int bamg_gather_i32(bamg_ctx* ctx, const int32_t* src, const int32_t*
                                int32_t* dst, void* stream) {
   (void)ctx;
   if (n <= 0) return 0;
-  k_gather_i32<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(src, idx, n, dst);
+  launch(k_gather_i32, grid_for(n, 256), 256, 0, as_stream(stream), src, idx, n, dst);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -434,7 +437,7 @@ k_absmax(const double* __restrict__ x, int64_t n, double* partials, unsigned int
 
 int dot_dev(bamg_ctx* ctx, const double* x, const double* y, int64_t n, double* out, cudaStream_t st) {
   int g = grid_for(n, RED_THREADS, 4);
-  k_dot<<<g, RED_THREADS, 0, st>>>(x, y, n, ctx->partials, ctx->counters + BAMG_CTR_DOT, out);
+  launch(k_dot, g, RED_THREADS, 0, st, x, y, n, ctx->partials, ctx->counters + BAMG_CTR_DOT, out);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -447,7 +450,7 @@ extern "C" int bamg_dot(bamg_ctx* ctx, const double* x, const double* y, int64_t
 extern "C" int bamg_absmax(bamg_ctx* ctx, const double* x, int64_t n, double* out_dev, void* stream) {
   cudaStream_t st = as_stream(stream);
   int g = grid_for(n, RED_THREADS, 4);
-  k_absmax<<<g, RED_THREADS, 0, st>>>(x, n, ctx->partials, ctx->counters + BAMG_CTR_DOT, out_dev);
+  launch(k_absmax, g, RED_THREADS, 0, st, x, n, ctx->partials, ctx->counters + BAMG_CTR_DOT, out_dev);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -462,7 +465,7 @@ extern "C" int bamg_axpby(bamg_ctx* ctx, double a, const double* x, double b, do
                           void* stream) {
   (void)ctx;
   if (n <= 0) return 0;
-  k_axpby<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(a, x, b, y, n);
+  launch(k_axpby, grid_for(n, 256), 256, 0, as_stream(stream), a, x, b, y, n);
   BAMG_LAUNCH_CHECK();
   return 0;
 }

@@ -54,16 +54,16 @@ extern "C" int bamg_obs_orders(bamg_ctx* ctx, const int32_t* cam_idx, const int3
   BAMG_CUDA_CHECK(cudaMallocAsync(&kk, 4 * k, st));
   BAMG_CUDA_CHECK(cudaMallocAsync(&cm_keys, 4 * k, st));
   int g = grid_for(k, 256);
-  k_iota<<<g, 256, 0, st>>>(iota, k);
+  launch(k_iota, g, 256, 0, st, iota, k);
   int rc;
   // (a) stable by camera
   rc = radix_sort_pairs((const uint32_t*)cam_idx, iota, k1, v1, k, bits_for(nc), st);
   if (rc) return rc;
   // (b) stable by point -> (point, camera) order
-  k_take_u32<<<g, 256, 0, st>>>((const uint32_t*)pt_idx, v1, k, kk);
+  launch(k_take_u32, g, 256, 0, st, (const uint32_t*)pt_idx, v1, k, kk);
   rc = radix_sort_pairs(kk, v1, (uint32_t*)obs_pt_pm, (uint32_t*)pm_perm, k, bits_for(npt), st);
   if (rc) return rc;
-  k_take_u32<<<g, 256, 0, st>>>((const uint32_t*)cam_idx, (const uint32_t*)pm_perm, k, (uint32_t*)obs_cam_pm);
+  launch(k_take_u32, g, 256, 0, st, (const uint32_t*)cam_idx, (const uint32_t*)pm_perm, k, (uint32_t*)obs_cam_pm);
   // (c) point-major positions stably by camera -> (camera, point) order
   rc = radix_sort_pairs((const uint32_t*)obs_cam_pm, iota, cm_keys, (uint32_t*)cm_list, k, bits_for(nc), st);
   if (rc) return rc;
@@ -153,7 +153,7 @@ extern "C" int bamg_covis_count(bamg_ctx* ctx, const int32_t* cam_ptr, const int
     return BAMG_ERR_UNSUPPORTED;
   }
   if (sm > 48 * 1024) cudaFuncSetAttribute(k_covis_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_covis_rows<<<grid_for(nc, 1, 16), 256, sm, as_stream(stream)>>>(cam_ptr, cm_list, obs_pt_pm, pt_ptr,
+  launch(k_covis_rows, grid_for(nc, 1, 16), 256, sm, as_stream(stream), cam_ptr, cm_list, obs_pt_pm, pt_ptr,
                                                                     obs_cam_pm, nc, row_counts, nullptr, nullptr);
   BAMG_LAUNCH_CHECK();
   return 0;
@@ -165,7 +165,7 @@ extern "C" int bamg_covis_fill(bamg_ctx* ctx, const int32_t* cam_ptr, const int3
   (void)ctx;
   size_t sm = sizeof(unsigned) * ((nc + 31) / 32);
   if (sm > 48 * 1024) cudaFuncSetAttribute(k_covis_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_covis_rows<<<grid_for(nc, 1, 16), 256, sm, as_stream(stream)>>>(cam_ptr, cm_list, obs_pt_pm, pt_ptr,
+  launch(k_covis_rows, grid_for(nc, 1, 16), 256, sm, as_stream(stream), cam_ptr, cm_list, obs_pt_pm, pt_ptr,
                                                                     obs_cam_pm, nc, nullptr, S_ptr, S_col);
   BAMG_LAUNCH_CHECK();
   return 0;
@@ -210,7 +210,7 @@ extern "C" int bamg_shared_counts(bamg_ctx* ctx, const int32_t* cam_ptr, const i
     return BAMG_ERR_UNSUPPORTED;
   }
   if (sm > 48 * 1024) cudaFuncSetAttribute(k_shared_counts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_shared_counts<<<grid_for(nc, 1, 16), 256, sm, as_stream(stream)>>>(cam_ptr, cm_list, obs_pt_pm, pt_ptr,
+  launch(k_shared_counts, grid_for(nc, 1, 16), 256, sm, as_stream(stream), cam_ptr, cm_list, obs_pt_pm, pt_ptr,
                                                                        obs_cam_pm, nc, S_ptr, S_col, shared_cnt);
   BAMG_LAUNCH_CHECK();
   return 0;
@@ -274,9 +274,9 @@ extern "C" int bamg_visibility_strength(bamg_ctx* ctx, const int32_t* cam_ptr, c
   cudaStream_t st = as_stream(stream);
   BAMG_CUDA_CHECK(cudaMemsetAsync(flags_dev, 0, 2 * sizeof(int), st));
   int g = grid_for(nc, 128);
-  k_degrees<<<g, 128, 0, st>>>(cam_ptr, nc, deg, flags_dev);
-  k_visibility_strength<<<g, 128, 0, st>>>(S_ptr, S_col, shared_cnt, nc, G_ptr, G_col, G_val, flags_dev + 1);
-  k_strength_scale<<<g, 128, 0, st>>>(G_ptr, G_col, deg, nc, G_val);
+  launch(k_degrees, g, 128, 0, st, cam_ptr, nc, deg, flags_dev);
+  launch(k_visibility_strength, g, 128, 0, st, S_ptr, S_col, shared_cnt, nc, G_ptr, G_col, G_val, flags_dev + 1);
+  launch(k_strength_scale, g, 128, 0, st, G_ptr, G_col, deg, nc, G_val);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -453,7 +453,7 @@ extern "C" int bamg_evaluate(bamg_ctx* ctx, const double* cams, const double* pt
   cudaStream_t st = as_stream(stream);
   BAMG_CUDA_CHECK(cudaMemsetAsync(n_behind_dev, 0, sizeof(int), st));
   int g = grid_for(k, EVAL_THREADS, 4);
-  k_evaluate<<<g, EVAL_THREADS, 0, st>>>(cams, pts, obs_cam, obs_pt, pixels, k, huber, with_jacobian, F, E, res,
+  launch(k_evaluate, g, EVAL_THREADS, 0, st, cams, pts, obs_cam, obs_pt, pixels, k, huber, with_jacobian, F, E, res,
                                          w, behind, n_behind_dev, ctx->partials, ctx->counters + BAMG_CTR_OBJ,
                                          objective_dev);
   BAMG_LAUNCH_CHECK();
@@ -551,11 +551,11 @@ extern "C" int bamg_normal_blocks(bamg_ctx* ctx, const int32_t* cam_ptr, const i
   (void)ctx;
   cudaStream_t st = as_stream(stream);
   if (nc > 0) {
-    k_cam_normal<<<grid_for((int64_t)nc * 32, 128, 8), 128, 0, st>>>(cam_ptr, cm_list, F, res, nc, A_raw, g_cam);
+    launch(k_cam_normal, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, F, res, nc, A_raw, g_cam);
     BAMG_LAUNCH_CHECK();
   }
   if (npt > 0) {
-    k_pt_normal<<<grid_for(npt, 128, 16), 128, 0, st>>>(pt_ptr, E, res, npt, C_raw, g_pt);
+    launch(k_pt_normal, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, E, res, npt, C_raw, g_pt);
     BAMG_LAUNCH_CHECK();
   }
   return 0;
@@ -577,8 +577,8 @@ extern "C" int bamg_damping(bamg_ctx* ctx, const double* A_raw, const double* C_
                             double radius, double* d_cam, double* d_pt, void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
-  if (nc) k_damping<<<grid_for((int64_t)nc * 9, 256), 256, 0, st>>>(A_raw, nc, 9, radius, d_cam);
-  if (npt) k_damping<<<grid_for((int64_t)npt * 3, 256), 256, 0, st>>>(C_raw, npt, 3, radius, d_pt);
+  if (nc) launch(k_damping, grid_for((int64_t)nc * 9, 256), 256, 0, st, A_raw, nc, 9, radius, d_cam);
+  if (npt) launch(k_damping, grid_for((int64_t)npt * 3, 256), 256, 0, st, C_raw, npt, 3, radius, d_pt);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -722,12 +722,12 @@ extern "C" int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const in
   cudaStream_t st = as_stream(stream);
   int big = 0x7fffffff;
   BAMG_CUDA_CHECK(cudaMemcpyAsync(bad_min_dev, &big, sizeof(int), cudaMemcpyHostToDevice, st));
-  if (nc) k_add_diag<<<grid_for((int64_t)nc * 81, 256), 256, 0, st>>>(A_raw, d_cam, nc, 9, A);
+  if (nc) launch(k_add_diag, grid_for((int64_t)nc * 81, 256), 256, 0, st, A_raw, d_cam, nc, 9, A);
   if (npt)
-    k_build_points<<<grid_for(npt, 128, 16), 128, 0, st>>>(pt_ptr, E, C_raw, d_pt, g_pt, npt, C, Cinv, Cb, H, qo,
+    launch(k_build_points, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, E, C_raw, d_pt, g_pt, npt, C, Cinv, Cb, H, qo,
                                                           bad_min_dev);
   if (nc)
-    k_cam_gather<<<grid_for((int64_t)nc * 32, 128, 8), 128, 0, st>>>(cam_ptr, cm_list, F, qo, g_cam, nullptr,
+    launch(k_cam_gather, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, F, qo, g_cam, nullptr,
                                                                      nullptr, nc, rhs);
   BAMG_LAUNCH_CHECK();
   return 0;
@@ -785,10 +785,10 @@ extern "C" int bamg_implicit_matvec(bamg_ctx* ctx, const int32_t* cam_ptr, const
                                     int32_t nc, int32_t npt, double* qo, double* y, void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
-  if (npt) k_point_wtx<<<grid_for(npt, 128, 16), 128, 0, st>>>(pt_ptr, obs_cam_pm, F, E, Cinv, x, nullptr, npt,
+  if (npt) launch(k_point_wtx, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, obs_cam_pm, F, E, Cinv, x, nullptr, npt,
                                                               nullptr, qo);
   if (nc)
-    k_cam_gather<<<grid_for((int64_t)nc * 32, 128, 8), 128, 0, st>>>(cam_ptr, cm_list, F, qo, nullptr, A, x, nc, y);
+    launch(k_cam_gather, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, F, qo, nullptr, A, x, nc, y);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -804,7 +804,7 @@ extern "C" int bamg_back_substitute(bamg_ctx* ctx, const int32_t* pt_ptr, const 
                                     const double* dc, int32_t npt, double* dp, void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
-  if (npt) k_point_wtx<<<grid_for(npt, 128, 16), 128, 0, st>>>(pt_ptr, obs_cam_pm, F, E, Cinv, dc, grad_pt, npt, dp,
+  if (npt) launch(k_point_wtx, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, obs_cam_pm, F, E, Cinv, dc, grad_pt, npt, dp,
                                                               nullptr);
   BAMG_LAUNCH_CHECK();
   return 0;
@@ -812,7 +812,7 @@ extern "C" int bamg_back_substitute(bamg_ctx* ctx, const int32_t* pt_ptr, const 
 
 extern "C" int bamg_negate(bamg_ctx* ctx, const double* a, double* b, int64_t n, void* stream) {
   (void)ctx;
-  if (n) k_neg<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(a, b, n);
+  if (n) launch(k_neg, grid_for(n, 256), 256, 0, as_stream(stream), a, b, n);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -834,7 +834,7 @@ __global__ void k_materialize_W(const int* __restrict__ cm_list, const double* _
 extern "C" int bamg_materialize_W(bamg_ctx* ctx, const int32_t* cm_list, const double* F, const double* E,
                                   int64_t k, double* W, void* stream) {
   (void)ctx;
-  if (k) k_materialize_W<<<grid_for(k * 27, 256), 256, 0, as_stream(stream)>>>(cm_list, F, E, k, W);
+  if (k) launch(k_materialize_W, grid_for(k * 27, 256), 256, 0, as_stream(stream), cm_list, F, E, k, W);
   BAMG_LAUNCH_CHECK();
   return 0;
 }

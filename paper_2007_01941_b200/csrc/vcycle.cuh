@@ -1,0 +1,532 @@
+// Native solve-phase runtime: the multigrid V-cycle as a fixed kernel program
+// (replayed through a CUDA graph), PCG with one host synchronisation per
+// iteration, and the 5-step D-Lanczos spectral estimate with a single readback.
+//
+// Reference semantics: mgcycle (multigrid.py:474-483), ChebyshevSmoother.apply
+// (multigrid.py:308-328), pcg + ForcingCriterion (solver.py:38-128),
+// estimate_lambda_max (multigrid.py:243-284).
+// Included at the end of blas.cu (same translation unit as the kernels it launches).
+#include <math.h>
+
+#include <vector>
+
+int dot_dev(bamg_ctx* ctx, const double* x, const double* y, int64_t n, double* out, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// small device-scalar vector kernels
+
+// y = x (copy)
+__global__ void k_copy(const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = x[i];
+}
+
+// PCG x/r update with alpha = rz/pap read from device scalars; rr = <r, r>.
+__global__ void __launch_bounds__(256)
+k_pcg_update_dev(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                 const double* __restrict__ ap, const double* __restrict__ rz, const double* __restrict__ pap,
+                 int64_t n, double* partials, unsigned int* counter, double* rr_out) {
+  __shared__ double scratch[33];
+  double a = (*rz) / (*pap);
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] += a * p[i];
+    double ri = r[i] - a * ap[i];
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  s = block_sum(s, scratch);
+  grid_finish(partials, counter, s, scratch, rr_out);
+}
+
+// p = z + (rz_new / rz_old) p
+__global__ void k_xpby_dev(const double* __restrict__ z, const double* __restrict__ rz_new,
+                           const double* __restrict__ rz_old, double* __restrict__ p, int64_t n) {
+  double beta = (*rz_new) / (*rz_old);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = z[i] + beta * p[i];
+}
+
+// ---------------------------------------------------------------------------
+// MG plan
+
+struct MgLevelPlan {
+  int bs = 0, nbr = 0, n = 0;
+  const int* ptr = nullptr;
+  const int* col = nullptr;
+  const double* blocks = nullptr;
+  const double* Dinv = nullptr;
+  double theta = 0, delta = 0, sigma = 0;
+  int iterations = 2;
+  // to the next level
+  const double* P = nullptr;
+  const int* agg = nullptr;
+  const int* agg_ptr = nullptr;
+  const int* members = nullptr;
+  int n_agg = 0;
+  // coarsest
+  const double* inv = nullptr;
+  // work
+  double *b = nullptr, *x = nullptr, *xs = nullptr, *d = nullptr, *r = nullptr;
+};
+
+struct bamg_mg {
+  std::vector<MgLevelPlan> lv;
+  double* in = nullptr;   // level-0 right-hand side (plan-owned)
+  double* out = nullptr;  // level-0 result (plan-owned)
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  bool dirty = true;
+  bool use_graph = true;
+};
+
+extern "C" bamg_mg* bamg_mg_create(int32_t n_levels) {
+  bamg_mg* m = new bamg_mg();
+  m->lv.resize(n_levels);
+  return m;
+}
+
+static void mg_free_work(bamg_mg* m) {
+  for (auto& L : m->lv) {
+    if (L.b && &L != &m->lv[0]) cudaFree(L.b);
+    cudaFree(L.x);
+    cudaFree(L.xs);
+    cudaFree(L.d);
+    cudaFree(L.r);
+    L.b = L.x = L.xs = L.d = L.r = nullptr;
+  }
+  if (m->in) cudaFree(m->in);
+  if (m->out) cudaFree(m->out);
+  m->in = m->out = nullptr;
+  if (m->exec) cudaGraphExecDestroy(m->exec);
+  if (m->graph) cudaGraphDestroy(m->graph);
+  m->exec = nullptr;
+  m->graph = nullptr;
+}
+
+extern "C" void bamg_mg_destroy(bamg_mg* m) {
+  if (!m) return;
+  mg_free_work(m);
+  delete m;
+}
+
+extern "C" int bamg_mg_set_level(bamg_mg* m, int32_t level, int32_t bs, int32_t nbr, const int32_t* ptr,
+                                 const int32_t* col, const double* blocks, const double* Dinv, double lower,
+                                 double upper, int32_t iterations, const double* P, const int32_t* agg,
+                                 const int32_t* agg_ptr, const int32_t* members, int32_t n_agg,
+                                 const double* coarse_inv) {
+  if (level < 0 || level >= (int)m->lv.size()) {
+    bamg_set_error("mg_set_level: level %d out of range", level);
+    return BAMG_ERR_UNSUPPORTED;
+  }
+  if (!coarse_inv && bs != 9 && bs != 16 && bs != 1) {
+    bamg_set_error("mg_set_level: unsupported block size %d", bs);
+    return BAMG_ERR_UNSUPPORTED;
+  }
+  MgLevelPlan& L = m->lv[level];
+  L.bs = bs;
+  L.nbr = nbr;
+  L.n = nbr * bs;
+  L.ptr = ptr;
+  L.col = col;
+  L.blocks = blocks;
+  L.Dinv = Dinv;
+  L.theta = 0.5 * (upper + lower);
+  L.delta = 0.5 * (upper - lower);
+  L.sigma = L.theta / L.delta;
+  L.iterations = iterations;
+  L.P = P;
+  L.agg = agg;
+  L.agg_ptr = agg_ptr;
+  L.members = members;
+  L.n_agg = n_agg;
+  L.inv = coarse_inv;
+  m->dirty = true;
+  return 0;
+}
+
+static int mg_alloc(bamg_mg* m) {
+  mg_free_work(m);
+  BAMG_CUDA_CHECK(cudaMalloc(&m->in, sizeof(double) * (size_t)m->lv[0].n));
+  BAMG_CUDA_CHECK(cudaMalloc(&m->out, sizeof(double) * (size_t)m->lv[0].n));
+  for (size_t l = 0; l < m->lv.size(); ++l) {
+    MgLevelPlan& L = m->lv[l];
+    size_t bytes = sizeof(double) * (size_t)(L.n > 0 ? L.n : 1);
+    if (l == 0) L.b = m->in;
+    else BAMG_CUDA_CHECK(cudaMalloc(&L.b, bytes));
+    BAMG_CUDA_CHECK(cudaMalloc(&L.x, bytes));
+    BAMG_CUDA_CHECK(cudaMalloc(&L.xs, bytes));
+    BAMG_CUDA_CHECK(cudaMalloc(&L.d, bytes));
+    BAMG_CUDA_CHECK(cudaMalloc(&L.r, bytes));
+  }
+  return 0;
+}
+
+template <int BS>
+static void cheb_launch(const MgLevelPlan& L, const double* x_in, double* x_out, double c1, double c2, int divide,
+                        bool with_A, cudaStream_t st) {
+  launch(k_cheb_step<BS>, spmv_grid(L.nbr), 128, 0, st, L.ptr, L.col, with_A ? L.blocks : nullptr, x_in, L.b, L.Dinv,
+         L.d, x_out, L.nbr, c1, c2, divide);
+}
+
+static void cheb(const MgLevelPlan& L, const double* x_in, double* x_out, double c1, double c2, int divide,
+                 bool with_A, cudaStream_t st) {
+  switch (L.bs) {
+    case 9: cheb_launch<9>(L, x_in, x_out, c1, c2, divide, with_A, st); break;
+    case 16: cheb_launch<16>(L, x_in, x_out, c1, c2, divide, with_A, st); break;
+    default: cheb_launch<1>(L, x_in, x_out, c1, c2, divide, with_A, st); break;
+  }
+}
+
+// Smoother (multigrid.py:308-328); returns the buffer holding the result.
+static double* smooth(MgLevelPlan& L, double* x, cudaStream_t st) {
+  double rho = 1.0 / L.sigma;
+  double* cur;
+  double* spare;
+  if (x == nullptr) {
+    cheb(L, nullptr, L.x, 0.0, L.theta, 1, false, st);  // d = D^-1 b / theta ; x = d
+    cur = L.x;
+    spare = L.xs;
+  } else {
+    double* out = (x == L.x) ? L.xs : L.x;
+    cheb(L, x, out, 0.0, L.theta, 1, true, st);  // r = b - A x ; d = D^-1 r / theta ; x += d
+    cur = out;
+    spare = x;
+  }
+  for (int it = 0; it < L.iterations - 1; ++it) {
+    double rho_next = 1.0 / (2.0 * L.sigma - rho);
+    cheb(L, cur, spare, rho_next * rho, 2.0 * rho_next / L.delta, 0, true, st);
+    double* t = cur;
+    cur = spare;
+    spare = t;
+    rho = rho_next;
+  }
+  return cur;
+}
+
+static void residual(const MgLevelPlan& L, const double* x, cudaStream_t st) {
+  int g = spmv_grid(L.nbr);
+  switch (L.bs) {
+    case 9: launch(k_bsr_residual<9>, g, 128, 0, st, L.ptr, L.col, L.blocks, x, L.b, L.r, L.nbr); break;
+    case 16: launch(k_bsr_residual<16>, g, 128, 0, st, L.ptr, L.col, L.blocks, x, L.b, L.r, L.nbr); break;
+    default: launch(k_bsr_residual<1>, g, 128, 0, st, L.ptr, L.col, L.blocks, x, L.b, L.r, L.nbr); break;
+  }
+}
+
+// V-cycle at level l from x = 0; returns the buffer holding x_l.
+static double* vcycle(bamg_mg* m, size_t l, cudaStream_t st) {
+  MgLevelPlan& L = m->lv[l];
+  if (L.inv) {
+    launch(k_gemv, grid_for((int64_t)L.n * 32, 128, 8), 128, 0, st, L.inv, L.b, L.n, L.x);
+    return L.x;
+  }
+  double* x = smooth(L, nullptr, st);
+  residual(L, x, st);
+  MgLevelPlan& C = m->lv[l + 1];
+  launch(k_restrict, grid_for((int64_t)L.n_agg * 16, 256), 256, 0, st, L.agg_ptr, L.members, L.P, L.r, L.n_agg,
+         L.bs, C.b);
+  double* xc = vcycle(m, l + 1, st);
+  launch(k_prolong, grid_for((int64_t)L.n, 256), 256, 0, st, L.agg, L.P, xc, L.nbr, L.bs, x, 1);
+  return smooth(L, x, st);
+}
+
+static int mg_record(bamg_mg* m, cudaStream_t st) {
+  double* res = vcycle(m, 0, st);
+  BAMG_CUDA_CHECK(cudaMemcpyAsync(m->out, res, sizeof(double) * (size_t)m->lv[0].n, cudaMemcpyDeviceToDevice, st));
+  return 0;
+}
+
+static int mg_prepare(bamg_mg* m, cudaStream_t st) {
+  if (!m->dirty) return 0;
+  int rc = mg_alloc(m);
+  if (rc) return rc;
+  m->dirty = false;
+  if (!m->use_graph) return 0;
+  cudaStream_t cs;
+  BAMG_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  BAMG_CUDA_CHECK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  long long before = g_bamg_launches.load();
+  rc = mg_record(m, cs);
+  g_bamg_launches.store(before);  // capture is not execution
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(cs, &g);
+  cudaStreamDestroy(cs);
+  if (rc) return rc;
+  BAMG_CUDA_CHECK(e);
+  m->graph = g;
+  BAMG_CUDA_CHECK(cudaGraphInstantiate(&m->exec, g, 0));
+  (void)st;
+  return 0;
+}
+
+static long long mg_kernel_count(bamg_mg* m) {
+  long long c = 0;
+  for (size_t l = 0; l < m->lv.size(); ++l) {
+    if (m->lv[l].inv) { c += 1; break; }
+    c += 2 * m->lv[l].iterations + 3;
+  }
+  return c;
+}
+
+// z = M r, one V-cycle (r, z: level-0 device vectors of length n0).
+static int mg_apply_dev(bamg_mg* m, const double* r, double* z, cudaStream_t st) {
+  int rc = mg_prepare(m, st);
+  if (rc) return rc;
+  size_t bytes = sizeof(double) * (size_t)m->lv[0].n;
+  if (r != m->in) BAMG_CUDA_CHECK(cudaMemcpyAsync(m->in, r, bytes, cudaMemcpyDeviceToDevice, st));
+  if (m->use_graph) {
+    BAMG_CUDA_CHECK(cudaGraphLaunch(m->exec, st));
+    g_bamg_launches.fetch_add(mg_kernel_count(m));
+  } else {
+    rc = mg_record(m, st);
+    if (rc) return rc;
+  }
+  if (z != m->out) BAMG_CUDA_CHECK(cudaMemcpyAsync(z, m->out, bytes, cudaMemcpyDeviceToDevice, st));
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int bamg_mg_use_graph(bamg_mg* m, int32_t on) {
+  m->use_graph = on != 0;
+  m->dirty = true;
+  return 0;
+}
+
+extern "C" int bamg_mg_apply(bamg_ctx* ctx, bamg_mg* m, const double* r, double* z, void* stream) {
+  (void)ctx;
+  return mg_apply_dev(m, r, z, as_stream(stream));
+}
+
+// ---------------------------------------------------------------------------
+// PCG (solver.py:70-128). Operator: BSR (bs 9/16/1) with fused <p, Ap>.
+// Preconditioner: the MG plan, or block-Jacobi inverse blocks (PBJ) when mg == null.
+// Outputs (host): iterations, reason (0 residual_tol, 1 forcing, 2 max_iterations),
+// rel, q_history[0..iterations], err (0 none, 1 not-SPD, 2 op non-finite,
+// 3 curvature, 4 residual non-finite, 5 preconditioner non-finite), err_value, err_iter.
+
+extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, int32_t bs, int32_t nbr,
+                            const int32_t* ptr, const int32_t* col, const double* blocks, const double* b, double* x,
+                            double tau, int32_t max_it, double rtol, double* work, int32_t* iterations_out,
+                            int32_t* reason_out, double* rel_out, double* q_hist, int32_t* err_out,
+                            double* err_value_out, int32_t* err_iter_out, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  int64_t n = (int64_t)nbr * bs;
+  double* r = work;
+  double* z = work + n;
+  double* p = work + 2 * n;
+  double* ap = work + 3 * n;
+  double* sc = ctx->scalars;      // [0] pap [1] rr [2] rz slot A [3] rz slot B [4] bb
+  double* hs = ctx->host_scalars;
+  *err_out = 0;
+  *err_iter_out = 0;
+  *err_value_out = 0.0;
+  auto precond = [&](const double* in, double* out) -> int {
+    if (mg) return mg_apply_dev(mg, in, out, st);
+    launch(k_blockdiag_apply, grid_for(n, 256), 256, 0, st, pbj_inv, in, nbr, bs, out);
+    BAMG_LAUNCH_CHECK();
+    return 0;
+  };
+  auto spmv_dot = [&](const double* v, double* out, double* dot) {
+    int g = spmv_grid(nbr);
+    if (g > BAMG_MAX_PARTIALS) g = BAMG_MAX_PARTIALS;
+    unsigned* ctr = ctx->counters + BAMG_CTR_SPMV;
+    switch (bs) {
+      case 9: launch(k_bsr_spmv<9>, g, 128, 0, st, ptr, col, blocks, v, out, nbr, ctx->partials, ctr, dot); break;
+      case 16: launch(k_bsr_spmv<16>, g, 128, 0, st, ptr, col, blocks, v, out, nbr, ctx->partials, ctr, dot); break;
+      default: launch(k_bsr_spmv<1>, g, 128, 0, st, ptr, col, blocks, v, out, nbr, ctx->partials, ctr, dot); break;
+    }
+  };
+  int rc;
+  int q_len = 0;
+  q_hist[q_len++] = 0.0;
+  BAMG_CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
+  rc = dot_dev(ctx, b, b, n, sc + 4, st);
+  if (rc) return rc;
+  launch(k_copy, grid_for(n, 256), 256, 0, st, b, r, n);
+  BAMG_CUDA_CHECK(cudaMemcpyAsync(hs + 4, sc + 4, sizeof(double), cudaMemcpyDeviceToHost, st));
+  BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+  double b_norm = sqrt(hs[4]);
+  if (b_norm == 0.0) {
+    *iterations_out = 0;
+    *reason_out = 0;
+    *rel_out = 0.0;
+    return 0;
+  }
+  rc = precond(r, z);
+  if (rc) return rc;
+  int slot = 2;  // device slot holding the current rz
+  rc = dot_dev(ctx, r, z, n, sc + slot, st);
+  if (rc) return rc;
+  BAMG_CUDA_CHECK(cudaMemcpyAsync(hs + slot, sc + slot, sizeof(double), cudaMemcpyDeviceToHost, st));
+  BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+  double rz = hs[slot];
+  if (!isfinite(rz)) { *err_out = 5; *err_iter_out = 0; return 0; }
+  if (rz <= 0.0) { *err_out = 1; *err_value_out = rz; *err_iter_out = 0; return 0; }
+  launch(k_copy, grid_for(n, 256), 256, 0, st, z, p, n);
+  double q_val = 0.0, rel = 1.0;
+  bool pending = false;  // an rz_next on the device not yet checked on the host
+  for (int i = 1; i <= max_it; ++i) {
+    spmv_dot(p, ap, sc + 0);
+    launch(k_pcg_update_dev, grid_for(n, 256, 4), 256, 0, st, x, r, p, ap, sc + slot, sc + 0, n, ctx->partials,
+           ctx->counters + BAMG_CTR_PCG0, sc + 1);
+    BAMG_CUDA_CHECK(cudaMemcpyAsync(hs, sc, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+    BAMG_LAUNCH_CHECK();
+    if (pending) {  // checks of iteration i-1's <r, M r> (solver.py:121-125)
+      double rzn = hs[slot];
+      if (!isfinite(rzn)) { *err_out = 5; *err_iter_out = i - 1; *iterations_out = i - 1; return 0; }
+      if (rzn <= 0.0) { *err_out = 1; *err_value_out = rzn; *err_iter_out = i - 1; *iterations_out = i - 1; return 0; }
+      rz = rzn;
+      pending = false;
+    }
+    double pap = hs[0];
+    if (!isfinite(pap)) { *err_out = 2; *err_iter_out = i; *iterations_out = i; return 0; }
+    if (pap <= 0.0) { *err_out = 3; *err_value_out = pap; *err_iter_out = i; *iterations_out = i; return 0; }
+    double alpha = rz / pap;
+    q_val -= 0.5 * alpha * rz;
+    q_hist[q_len++] = q_val;
+    rel = sqrt(hs[1]) / b_norm;
+    *rel_out = rel;
+    if (!isfinite(rel)) { *err_out = 4; *err_iter_out = i; *iterations_out = i; return 0; }
+    if (rel <= rtol) { *iterations_out = i; *reason_out = 0; return 0; }
+    // forcing (solver.py:52-59)
+    {
+      int k = q_len - 1;
+      double qc = q_hist[q_len - 1], qp = q_hist[q_len - 2];
+      if (k >= 1 && qc != 0.0 && k * (qc - qp) / qc <= tau) { *iterations_out = i; *reason_out = 1; return 0; }
+    }
+    rc = precond(r, z);
+    if (rc) return rc;
+    int nslot = (slot == 2) ? 3 : 2;
+    rc = dot_dev(ctx, r, z, n, sc + nslot, st);
+    if (rc) return rc;
+    launch(k_xpby_dev, grid_for(n, 256), 256, 0, st, z, sc + nslot, sc + slot, p, n);
+    slot = nslot;
+    pending = true;
+  }
+  if (pending) {
+    BAMG_CUDA_CHECK(cudaMemcpyAsync(hs + slot, sc + slot, sizeof(double), cudaMemcpyDeviceToHost, st));
+    BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+    double rzn = hs[slot];
+    if (!isfinite(rzn)) { *err_out = 5; *err_iter_out = max_it; *iterations_out = max_it; return 0; }
+    if (rzn <= 0.0) { *err_out = 1; *err_value_out = rzn; *err_iter_out = max_it; *iterations_out = max_it; return 0; }
+  }
+  *iterations_out = max_it;
+  *reason_out = 2;
+  *rel_out = rel;
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// D-Lanczos (multigrid.py:243-284), all steps on the device, one readback.
+
+// z = Dinv u - a q - b qp   (a = s[ia], b = s[ib] or 0)
+__global__ void k_lanczos_z(const double* __restrict__ Dinv, const double* __restrict__ u, const double* __restrict__ q,
+                            const double* __restrict__ qp, const double* __restrict__ s, int ia, int ib, int nb,
+                            int bs, double* __restrict__ z) {
+  double a = s[ia];
+  double b = ib >= 0 ? s[ib] : 0.0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)nb * bs; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t blk = t / bs;
+    int rr = (int)(t - blk * bs);
+    const double* m = Dinv + (blk * bs + rr) * bs;
+    const double* ub = u + blk * bs;
+    double v = 0.0;
+    for (int c = 0; c < bs; ++c) v = fma(m[c], ub[c], v);
+    z[t] = v - a * q[t] - b * qp[t];
+  }
+}
+
+// y -= s[i] x
+__global__ void k_axpy_dev(const double* __restrict__ x, const double* __restrict__ s, int i, double* __restrict__ y,
+                           int64_t n) {
+  double a = s[i];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    y[t] -= a * x[t];
+}
+
+// y = x / sqrt(s[i])
+__global__ void k_scale_rsqrt_dev(const double* __restrict__ x, const double* __restrict__ s, int i,
+                                  double* __restrict__ y, int64_t n) {
+  double b = sqrt(s[i]);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    y[t] = x[t] / b;
+}
+
+// s[i] = sqrt(s[i]) in place (single thread)
+__global__ void k_sqrt_slot(double* s, int i, int j) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) s[j] = sqrt(s[i]);
+}
+
+// v0: seeded start vector (device). D: diagonal blocks, Dinv: their inverses.
+// work: (steps + 5) * n doubles. Returns lambda (host) and the Lanczos break
+// status through *status (0 ok, 1 non-finite).
+extern "C" int bamg_lanczos_lmax(bamg_ctx* ctx, int32_t bs, int32_t nbr, const int32_t* ptr, const int32_t* col,
+                                 const double* blocks, const double* D, const double* Dinv, const double* v0,
+                                 int32_t steps, double* work, double* lambda_out, int32_t* status, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  int64_t n = (int64_t)nbr * bs;
+  double* sc = ctx->scalars + 16;  // [0..15] per step: alpha[s]=sc[s], beta2[s]=sc[8+s]; extras at 64+
+  double* tmp = ctx->scalars + 64;  // dnorm^2, beta, reorth coefficient slots
+  double* basis = work;             // (steps+1) * n
+  double* u = work + (int64_t)(steps + 1) * n;
+  double* z = u + n;
+  double* Dz = z + n;
+  double* qprev = Dz + n;
+  int g = grid_for(n, 256);
+  BAMG_CUDA_CHECK(cudaMemsetAsync(qprev, 0, sizeof(double) * n, st));
+  // q0 = v / sqrt(v . D v)
+  launch(k_blockdiag_apply, g, 256, 0, st, D, v0, nbr, bs, Dz);
+  int rc = dot_dev(ctx, v0, Dz, n, tmp + 0, st);
+  if (rc) return rc;
+  launch(k_scale_rsqrt_dev, g, 256, 0, st, v0, tmp, 0, basis, n);
+  int sg = spmv_grid(nbr);
+  if (sg > BAMG_MAX_PARTIALS) sg = BAMG_MAX_PARTIALS;
+  for (int s = 0; s < steps; ++s) {
+    double* q = basis + (int64_t)s * n;
+    double* qp = s > 0 ? basis + (int64_t)(s - 1) * n : qprev;
+    unsigned* ctr = ctx->counters + BAMG_CTR_SPMV;
+    switch (bs) {
+      case 9: launch(k_bsr_spmv<9>, sg, 128, 0, st, ptr, col, blocks, q, u, nbr, ctx->partials, ctr, sc + s); break;
+      case 16: launch(k_bsr_spmv<16>, sg, 128, 0, st, ptr, col, blocks, q, u, nbr, ctx->partials, ctr, sc + s); break;
+      default: launch(k_bsr_spmv<1>, sg, 128, 0, st, ptr, col, blocks, q, u, nbr, ctx->partials, ctr, sc + s); break;
+    }
+    // z = D^-1 u - alpha q - beta_prev q_prev   (beta_prev = sqrt(beta2[s-1]))
+    if (s > 0) launch(k_sqrt_slot, 1, 1, 0, st, sc, 8 + s - 1, 40 + s - 1);
+    launch(k_lanczos_z, g, 256, 0, st, Dinv, u, q, qp, sc, s, s > 0 ? 40 + s - 1 : -1, nbr, bs, z);
+    // full reorthogonalisation in the D inner product: z -= qb (qb . D z)
+    for (int b2 = 0; b2 <= s; ++b2) {
+      double* qb = basis + (int64_t)b2 * n;
+      launch(k_blockdiag_apply, g, 256, 0, st, D, z, nbr, bs, Dz);
+      rc = dot_dev(ctx, qb, Dz, n, tmp + 1, st);
+      if (rc) return rc;
+      launch(k_axpy_dev, g, 256, 0, st, qb, tmp, 1, z, n);
+    }
+    launch(k_blockdiag_apply, g, 256, 0, st, D, z, nbr, bs, Dz);
+    rc = dot_dev(ctx, z, Dz, n, sc + 8 + s, st);
+    if (rc) return rc;
+    launch(k_scale_rsqrt_dev, g, 256, 0, st, z, sc, 8 + s, basis + (int64_t)(s + 1) * n, n);
+  }
+  double h[16];
+  BAMG_CUDA_CHECK(cudaMemcpyAsync(h, sc, 16 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+  BAMG_LAUNCH_CHECK();
+  // host replay of the break logic
+  std::vector<double> al, be;
+  *status = 0;
+  for (int s = 0; s < steps; ++s) {
+    double alpha = h[s], beta2 = h[8 + s];
+    al.push_back(alpha);
+    if (!isfinite(beta2)) {
+      *status = 1;
+      return 0;
+    }
+    if (beta2 <= 0 || sqrt(beta2) < 1e-12 * fabs(alpha)) break;
+    be.push_back(sqrt(beta2));
+  }
+  if (be.size() >= al.size()) be.resize(al.size() - 1);
+  if (be.empty()) be.push_back(0.0);
+  *lambda_out = bamg_tridiag_max_eig(al.data(), be.data(), (int)al.size());
+  return 0;
+}

@@ -64,12 +64,20 @@ def _structure_of(problem_or_obs) -> ObsStructure:
 
 
 def visibility_strength(problem_or_obs) -> StrengthMatrix:
-    """Cosine similarity of camera visibility sets (multigrid.py:52-80), bit-exact."""
+    """Cosine similarity of camera visibility sets (multigrid.py:52-80), bit-exact.
+
+    The graph depends only on the observation structure, so it is built once per
+    problem; every StrengthMatrix of the same structure shares the aggregation
+    cache of `_aggregate_cached` (the level-0 scan is then also once per problem,
+    the amortisation solver.py:221-230 applies to the strength graph itself).
+    """
     st = _structure_of(problem_or_obs)
     s = st.strength
     if s["n_empty"]:
         raise ValueError(f"{s['n_empty']} camera(s) observe no points; visibility strength undefined")
-    return StrengthMatrix(s["G_ptr"], s["G_col"], s["G_val"], st.nc)
+    G = StrengthMatrix(s["G_ptr"], s["G_col"], s["G_val"], st.nc)
+    G._agg_cache = s.setdefault("agg_cache", {})
+    return G
 
 
 def operator_strength(op: BlockSparseMatrix) -> StrengthMatrix:
@@ -222,6 +230,17 @@ def estimate_lambda_max(matvec, jacobi: BlockDiagMatrix, n: int, steps: int = _L
     """Largest eigenvalue of D^-1 A by D-inner-product Lanczos (multigrid.py:243-284)."""
     v = _start_vector(n, seed)
     jacobi.factor()
+    op = _explicit_operator(matvec)
+    if op is not None and op.row_block_size == jacobi.block_size and op.shape[0] == n:
+        # native: all steps on the device, one readback, host replay of the break rule
+        work = D.empty((steps + 5) * n)
+        lam = np.zeros(1)
+        status = np.zeros(1, dtype=np.int32)
+        D.call("bamg_lanczos_lmax", op.row_block_size, op.n_block_rows, op._ptr, op._col, op.blocks, jacobi.blocks,
+               jacobi.inverse_blocks(), v, int(steps), work, lam.ctypes.data, status.ctypes.data)
+        if status[0]:
+            raise FloatingPointError("Lanczos iteration produced a non-finite value")
+        return float(lam[0])
     alphas, betas = [], []
     q_prev = D.zeros(n)
     dnorm = np.sqrt(D.dot(v, jacobi.matvec(v)))
@@ -364,9 +383,52 @@ class MgLevel:
         self.coarse_factor = None
 
 
+class _NativePlan:
+    """libbamg_b200 multigrid plan: the V-cycle as one recorded CUDA graph."""
+
+    def __init__(self, levels):
+        L = _lib.lib()
+        self.handle = L.bamg_mg_create(len(levels))
+        for li, lvl in enumerate(levels):
+            op = lvl.explicit
+            if lvl.coarse_factor is not None:
+                _lib.call("bamg_mg_set_level", self.handle, li, op.row_block_size, op.n_block_rows, None, None, None,
+                          None, 0.0, 1.0, 1, None, None, None, None, 0, lvl.coarse_factor["inv"])
+                continue
+            sm = lvl.smoother
+            ptr, mem = lvl.aggregation.member_lists()
+            _lib.call("bamg_mg_set_level", self.handle, li, op.row_block_size, op.n_block_rows, op._ptr, op._col,
+                      op.blocks, sm.jacobi.inverse_blocks(), float(sm.lower), float(sm.upper), int(sm.iterations),
+                      lvl.P.blocks, lvl.P._col, ptr, mem, lvl.aggregation.n_aggregates, None)
+
+    def apply(self, r):
+        z = D.empty(r.numel())
+        _lib.call("bamg_mg_apply", D.ctx(), self.handle, r, z, D.stream())
+        return z
+
+    def __del__(self):
+        try:
+            _lib.lib().bamg_mg_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def _native_ok(levels) -> bool:
+    for lvl in levels:
+        op = lvl.explicit
+        if op is None:
+            return False
+        if lvl.coarse_factor is None and (
+                _explicit_operator(lvl.matvec) is not op or op.row_block_size not in (9, 16)
+                or lvl.smoother is None or lvl.P is None):
+            return False
+    return True
+
+
 class MgHierarchy:
     def __init__(self, levels):
         self.levels = levels
+        self._plan = _NativePlan(levels) if _native_ok(levels) else None
 
     @property
     def n_levels(self) -> int:
@@ -374,7 +436,10 @@ class MgHierarchy:
 
     def apply(self, r):
         """One V-cycle from a zero initial guess (multigrid.py:366-368)."""
-        return mgcycle(self, 0, None, D.f64(r).reshape(-1))
+        r = D.f64(r).reshape(-1)
+        if self._plan is not None:
+            return self._plan.apply(r)
+        return mgcycle(self, 0, None, r)
 
 
 def _coarse_factor(op: BlockSparseMatrix):

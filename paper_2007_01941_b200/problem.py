@@ -134,29 +134,45 @@ class ObsStructure:
                                   n_empty=int(f[0]), wrapped=int(f[1]), shared=cnt[:nnz])
         return self._strength
 
+    def _schur_symbolic(self, with_pairs: bool):
+        S_ptr, S_col, nnz, _ = self.covis
+        pair_off = D.empty(max(self.npt, 1), dtype=torch.int32)
+        dpos = D.empty(max(self.nc, 1), dtype=torch.int32)
+        up_off = D.empty(max(self.nc, 1), dtype=torch.int32)
+        sizes = np.zeros(2, dtype=np.int64)
+        D.call("bamg_schur_symbolic_sizes", self.pt_ptr, S_ptr, S_col, self.nc, self.npt,
+               pair_off, dpos, up_off, sizes.ctypes.data)
+        n_pairs, n_up = int(sizes[0]), int(sizes[1])
+        up_blk = D.empty(max(n_up, 1), dtype=torch.int32)
+        up_row = D.empty(max(n_up, 1), dtype=torch.int32)
+        up_tpos = D.empty(max(n_up, 1), dtype=torch.int32)
+        out = dict(up_blk=up_blk, up_row=up_row, up_tpos=up_tpos, dpos=dpos, up_off=up_off, n_up=n_up,
+                   n_pairs=n_pairs)
+        if with_pairs:
+            out["pair_a"] = D.empty(max(n_pairs, 1), dtype=torch.int32)
+            out["pair_b"] = D.empty(max(n_pairs, 1), dtype=torch.int32)
+            out["blk_ptr"] = D.empty(nnz + 1, dtype=torch.int32)
+        D.call("bamg_schur_symbolic", self.pt_ptr, self.obs_cam_pm, S_ptr, S_col, self.nc, self.npt,
+               nnz, pair_off, n_pairs, dpos, up_off, out.get("pair_a"), out.get("pair_b"), out.get("blk_ptr"),
+               up_blk, up_row, up_tpos)
+        return out
+
     @property
     def symbolic(self):
-        """Per-block point-pair lists of the upper triangle of S (schur.cu)."""
+        """Upper-triangle block list of S: diagonal slots, per-row offsets, transposed
+        positions (schur.cu, row-owned numeric assembly)."""
         if self._symbolic is None:
-            S_ptr, S_col, nnz, _ = self.covis
-            pair_off = D.empty(max(self.npt, 1), dtype=torch.int32)
-            dpos = D.empty(max(self.nc, 1), dtype=torch.int32)
-            up_off = D.empty(max(self.nc, 1), dtype=torch.int32)
-            sizes = np.zeros(2, dtype=np.int64)
-            D.call("bamg_schur_symbolic_sizes", self.pt_ptr, S_ptr, S_col, self.nc, self.npt,
-                   pair_off, dpos, up_off, sizes.ctypes.data)
-            n_pairs, n_up = int(sizes[0]), int(sizes[1])
-            pair_a = D.empty(max(n_pairs, 1), dtype=torch.int32)
-            pair_b = D.empty(max(n_pairs, 1), dtype=torch.int32)
-            blk_ptr = D.empty(nnz + 1, dtype=torch.int32)
-            up_blk = D.empty(max(n_up, 1), dtype=torch.int32)
-            up_row = D.empty(max(n_up, 1), dtype=torch.int32)
-            up_tpos = D.empty(max(n_up, 1), dtype=torch.int32)
-            D.call("bamg_schur_symbolic", self.pt_ptr, self.obs_cam_pm, S_ptr, S_col, self.nc, self.npt,
-                   nnz, pair_off, n_pairs, dpos, up_off, pair_a, pair_b, blk_ptr, up_blk, up_row, up_tpos)
-            self._symbolic = dict(pair_a=pair_a, pair_b=pair_b, blk_ptr=blk_ptr, up_blk=up_blk,
-                                  up_row=up_row, up_tpos=up_tpos, dpos=dpos, n_up=n_up, n_pairs=n_pairs)
+            self._symbolic = self._schur_symbolic(False)
         return self._symbolic
+
+    @property
+    def pair_lists(self):
+        """Per-block point-pair lists (the block-owned alternative assembly)."""
+        if getattr(self, "_pairs", None) is None:
+            p = self._schur_symbolic(True)
+            D.call("bamg_schur_order_upper", p["up_blk"], p["up_row"], p["up_tpos"], p["n_up"], p["blk_ptr"])
+            self._pairs = p
+        return self._pairs
 
 
 # -- problem ----------------------------------------------------------------------

@@ -129,15 +129,27 @@ def build_system(jac: JacobianBlocks, damping: Damping) -> SchurSystem:
     return s
 
 
-def schur_explicit(sys: SchurSystem) -> BlockSparseMatrix:
-    """S = A - W C^-1 W^T as a 9x9 BSR over the covisibility pattern (schur.py:128-144)."""
+def schur_explicit(sys: SchurSystem, variant: str = "pairs") -> BlockSparseMatrix:
+    """S = A - W C^-1 W^T as a 9x9 BSR over the covisibility pattern (schur.py:128-144).
+
+    ``variant`` "pairs" (default): block-owned accumulation over per-block
+    point-pair lists (built once per problem); "rows": row-owned shared-memory
+    accumulation. Both are deterministic; they differ only in summation order.
+    """
     st = sys._jac._st
     S_ptr, S_col, nnz, _ = st.covis
-    sym = st.symbolic
     blocks = D.empty(nnz, CAMERA_SIZE, CAMERA_SIZE)
-    D.call("bamg_schur_numeric", st.cam_ptr, st.cm_list, sys._jac._F, sys._jac._E, sys._H, sys.A.blocks,
-           sym["dpos"], sys.n_cameras, sym["up_blk"], sym["up_tpos"], sym["n_up"], sym["blk_ptr"],
-           sym["pair_a"], sym["pair_b"], blocks)
+    J = sys._jac
+    if variant == "rows":
+        sym = st.symbolic
+        D.call("bamg_schur_numeric_rows", st.cam_ptr, st.cm_list, st.pt_ptr, st.obs_cam_pm, st.obs_pt_pm, J._F,
+               J._E, sys._H, sys.A.blocks, S_ptr, S_col, sym["dpos"], sym["up_off"], sym["up_tpos"], sys.n_cameras,
+               blocks)
+    else:
+        sym = st.pair_lists
+        D.call("bamg_schur_numeric", st.cam_ptr, st.cm_list, J._F, J._E, sys._H, sys.A.blocks, sym["dpos"],
+               sys.n_cameras, sym["up_blk"], sym["up_tpos"], sym["n_up"], sym["blk_ptr"], sym["pair_a"],
+               sym["pair_b"], blocks)
     return BlockSparseMatrix(sys.n_cameras, sys.n_cameras, CAMERA_SIZE, CAMERA_SIZE, S_ptr, S_col, blocks,
                              _validate=False)
 

@@ -94,6 +94,13 @@ def test_schur_explicit(case):
     np.testing.assert_array_equal(H(S.indptr), g["S_indptr"])
     np.testing.assert_array_equal(H(S.indices), g["S_indices"])
     assert block_rel(H(S.blocks), g["S_blocks"]) <= 1e-10
+    # both deterministic assemblies (row-owned / pair-list) agree and rerun bit-identically
+    from paper_2007_01941_b200 import schur as SC
+
+    S2 = SC.schur_explicit(s, variant="pairs")
+    assert block_rel(H(S2.blocks), H(S.blocks)) <= 1e-12
+    S3 = SC.schur_explicit(s)
+    assert np.array_equal(H(S3.blocks), H(S.blocks))
     # implicit operator == explicit operator (schur.py:84-91)
     rng = np.random.default_rng(0)
     x = rng.normal(size=S.shape[0])
@@ -177,6 +184,27 @@ def test_vcycle_symmetric_and_spd(case, hier):
     if not H(h.levels[0].P.qr_info)[:, 0].any() if h.n_levels > 1 else True:
         for vin, vout in zip(g["mg_in"], g["mg_out"]):
             assert relerr(H(h.apply(vin)), vout) <= 1e-9
+
+
+def test_native_runtime_matches_stepwise_path(case, hier):
+    """The recorded V-cycle graph / native PCG equal the kernel-by-kernel path."""
+    name, g, P, prob, obj, jac, damp, s = case
+    from paper_2007_01941_b200 import multigrid as MG
+
+    h = hier
+    if h.n_levels > 1:
+        assert h._plan is not None
+    rng = np.random.default_rng(2)
+    v = rng.normal(size=h.levels[0].scalar_dim)
+    a = H(h.apply(v))
+    b = H(MG.mgcycle(h, 0, None, P._device.f64(v)))
+    assert np.max(np.abs(a - b)) <= 1e-13 * np.max(np.abs(b))
+    x1, r1 = P.pcg(s.matvec, h.apply, s.rhs_cam, tau=1e-30, max_iterations=2000, residual_tolerance=1e-6)
+    x2, r2 = P.pcg(lambda u: s.matvec(u), lambda u: h.apply(u), s.rhs_cam, tau=1e-30, max_iterations=2000,
+                   residual_tolerance=1e-6)
+    assert r1.iterations == r2.iterations and r1.stop_reason == r2.stop_reason
+    assert relerr(H(x1), H(x2)) <= 1e-10
+    np.testing.assert_allclose(r1.q_history, r2.q_history, rtol=1e-10)
 
 
 def test_pcg_iterations(case, hier):

@@ -111,5 +111,36 @@ def main(config=4, reps=2):
         print(f"  lambdas {[round(l.smoother.lambda_max, 4) for l in levels[:-1]]}", flush=True)
 
 
+def kernels(config=4):
+    """CUPTI kernel table (torch.profiler) of one full linear solve after warm-up."""
+    from torch.profiler import ProfilerActivity, profile
+
+    sc = bench.scene_for(int(config))
+    prob = P.BundleProblem(*sc.arrays())
+    cfg = P.SolveConfig(preconditioner="multigrid", tau=1e-30, cg_max_iterations=20000, cg_residual_tolerance=1e-6)
+    for _ in range(2):
+        obj, jac = P.evaluate(prob)
+        solver.linear_solve(prob, jac, 1e4, cfg)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+        obj, jac = P.evaluate(prob)
+        out = solver.linear_solve(prob, jac, 1e4, cfg)
+        torch.cuda.synchronize()
+    agg = {}
+    for e in prof.events():
+        if e.device_type.name == "CUDA":
+            k = e.name.split("(")[0]
+            a = agg.setdefault(k, [0, 0.0])
+            a[0] += 1
+            a[1] += e.device_time_range.elapsed_us() if hasattr(e, "device_time_range") else e.cuda_time_total
+    tot = sum(v[1] for v in agg.values())
+    print(f"cg={out[2].iterations} setup={out[4]*1e3:.1f}ms solve={out[5]*1e3:.1f}ms kernel-sum={tot/1e3:.1f}ms")
+    for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:30]:
+        print(f"  {k[:50]:50s} n={v[0]:5d} {v[1]/1e3:8.2f} ms")
+
+
 if __name__ == "__main__":
-    main(*sys.argv[1:])
+    if len(sys.argv) > 1 and sys.argv[1] == "kernels":
+        kernels(*sys.argv[2:])
+    else:
+        main(*sys.argv[1:])
