@@ -91,6 +91,24 @@ def dot_dev(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor):
     call("bamg_dot", x, y, x.numel(), out)
 
 
+# optional phase timing (BAMG_PHASES=1): sync-timed, diagnostics only
+PHASES: dict = {}
+_PHASE_ON = bool(int(__import__("os").environ.get("BAMG_PHASES", "0")))
+_last = [0.0]
+
+
+def phase(name: str) -> None:
+    if not _PHASE_ON:
+        return
+    import time
+
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    if name != "start":
+        PHASES[name] = PHASES.get(name, 0.0) + t - _last[0]
+    _last[0] = t
+
+
 def absmax(x: torch.Tensor) -> float:
     if x.numel() == 0:
         return 0.0

@@ -52,6 +52,17 @@ extern "C" bamg_ctx* bamg_ctx_create(void) {
   if (cudaMalloc(&c->flags, sizeof(int) * BAMG_NUM_FLAGS) != cudaSuccess) goto fail;
   if (cudaMallocHost(&c->host_scalars, sizeof(double) * BAMG_NUM_SCALARS) != cudaSuccess) goto fail;
   if (cudaMallocHost(&c->host_flags, sizeof(int) * BAMG_NUM_FLAGS) != cudaSuccess) goto fail;
+  {
+    // stream-ordered scratch (sort keys, pair lists, plan vectors) comes from the
+    // device's default pool; keep its memory mapped across synchronisations so
+    // repeated solves do not pay page-mapping costs on every allocation
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   cudaMemset(c->counters, 0, sizeof(unsigned int) * BAMG_NUM_COUNTERS);
   cudaMemset(c->scalars, 0, sizeof(double) * BAMG_NUM_SCALARS);
   cudaMemset(c->flags, 0, sizeof(int) * BAMG_NUM_FLAGS);

@@ -72,12 +72,14 @@ struct MgLevelPlan {
 
 struct bamg_mg {
   std::vector<MgLevelPlan> lv;
-  double* in = nullptr;   // level-0 right-hand side (plan-owned)
-  double* out = nullptr;  // level-0 result (plan-owned)
+  double* in = nullptr;     // level-0 right-hand side (plan-owned)
+  double* out = nullptr;    // level-0 result (plan-owned)
+  double* arena = nullptr;  // every work vector, one stream-ordered allocation
+  cudaStream_t arena_stream = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
   bool dirty = true;
-  bool use_graph = true;
+  bool use_graph = false;
 };
 
 extern "C" bamg_mg* bamg_mg_create(int32_t n_levels) {
@@ -87,16 +89,9 @@ extern "C" bamg_mg* bamg_mg_create(int32_t n_levels) {
 }
 
 static void mg_free_work(bamg_mg* m) {
-  for (auto& L : m->lv) {
-    if (L.b && &L != &m->lv[0]) cudaFree(L.b);
-    cudaFree(L.x);
-    cudaFree(L.xs);
-    cudaFree(L.d);
-    cudaFree(L.r);
-    L.b = L.x = L.xs = L.d = L.r = nullptr;
-  }
-  if (m->in) cudaFree(m->in);
-  if (m->out) cudaFree(m->out);
+  if (m->arena) cudaFreeAsync(m->arena, m->arena_stream);
+  m->arena = nullptr;
+  for (auto& L : m->lv) L.b = L.x = L.xs = L.d = L.r = nullptr;
   m->in = m->out = nullptr;
   if (m->exec) cudaGraphExecDestroy(m->exec);
   if (m->graph) cudaGraphDestroy(m->graph);
@@ -145,19 +140,26 @@ extern "C" int bamg_mg_set_level(bamg_mg* m, int32_t level, int32_t bs, int32_t 
   return 0;
 }
 
-static int mg_alloc(bamg_mg* m) {
+static int mg_alloc(bamg_mg* m, cudaStream_t st) {
   mg_free_work(m);
-  BAMG_CUDA_CHECK(cudaMalloc(&m->in, sizeof(double) * (size_t)m->lv[0].n));
-  BAMG_CUDA_CHECK(cudaMalloc(&m->out, sizeof(double) * (size_t)m->lv[0].n));
+  size_t total = 2 * (size_t)m->lv[0].n;
+  for (auto& L : m->lv) total += 5 * (size_t)(L.n > 0 ? L.n : 1);
+  BAMG_CUDA_CHECK(cudaMallocAsync(&m->arena, sizeof(double) * total, st));
+  m->arena_stream = st;
+  double* p = m->arena;
+  m->in = p;
+  p += m->lv[0].n;
+  m->out = p;
+  p += m->lv[0].n;
   for (size_t l = 0; l < m->lv.size(); ++l) {
     MgLevelPlan& L = m->lv[l];
-    size_t bytes = sizeof(double) * (size_t)(L.n > 0 ? L.n : 1);
+    size_t n = (size_t)(L.n > 0 ? L.n : 1);
     if (l == 0) L.b = m->in;
-    else BAMG_CUDA_CHECK(cudaMalloc(&L.b, bytes));
-    BAMG_CUDA_CHECK(cudaMalloc(&L.x, bytes));
-    BAMG_CUDA_CHECK(cudaMalloc(&L.xs, bytes));
-    BAMG_CUDA_CHECK(cudaMalloc(&L.d, bytes));
-    BAMG_CUDA_CHECK(cudaMalloc(&L.r, bytes));
+    else { L.b = p; p += n; }
+    L.x = p; p += n;
+    L.xs = p; p += n;
+    L.d = p; p += n;
+    L.r = p; p += n;
   }
   return 0;
 }
@@ -238,7 +240,7 @@ static int mg_record(bamg_mg* m, cudaStream_t st) {
 
 static int mg_prepare(bamg_mg* m, cudaStream_t st) {
   if (!m->dirty) return 0;
-  int rc = mg_alloc(m);
+  int rc = mg_alloc(m, st);
   if (rc) return rc;
   m->dirty = false;
   if (!m->use_graph) return 0;

@@ -463,18 +463,22 @@ def build_hierarchy(sys: SchurSystem, nullspace: DenseTall, strength: StrengthMa
     level0 = MgLevel(0, sys.matvec, sys.n_cameras * CAMERA_SIZE, sys, s_explicit, nullspace)
     levels = [level0]
     K = nullspace
+    D.phase("start")
     while levels[-1].scalar_dim > max_coarse_dim:
         cur = levels[-1]
         if cur.index == 0:
             agg = _aggregate_cached(strength, max_aggregate)
         else:
             agg = aggregate(operator_strength(cur.explicit), max_size=max_aggregate)
+        D.phase("mg.aggregate")
         ratio = (agg.n_aggregates * NULLSPACE_DIM) / cur.scalar_dim
         if ratio > max_ratio:
             break
         bs = CAMERA_SIZE if cur.index == 0 else NULLSPACE_DIM
         P, K_next, padded = build_prolongation(agg, K, bs)
+        D.phase("mg.prolong")
         a_next = galerkin(P, cur.explicit, agg)
+        D.phase("mg.galerkin")
         cur.P = P
         cur.aggregation = agg
         levels.append(MgLevel(cur.index + 1, a_next.matvec, agg.n_aggregates * NULLSPACE_DIM, a_next, a_next,
@@ -483,8 +487,12 @@ def build_hierarchy(sys: SchurSystem, nullspace: DenseTall, strength: StrengthMa
     for lvl in levels[:-1]:
         jacobi = BlockDiagMatrix(lvl.explicit.diagonal_blocks())
         lvl.smoother = make_smoother(lvl.matvec, jacobi, lvl.scalar_dim, seed=seed + lvl.index)
+    D.phase("mg.smoothers")
     levels[-1].coarse_factor = _coarse_factor(levels[-1].explicit)
-    return MgHierarchy(levels)
+    D.phase("mg.coarse")
+    h = MgHierarchy(levels)
+    D.phase("mg.plan")
+    return h
 
 
 def mgcycle(h: MgHierarchy, level: int, x, b):
