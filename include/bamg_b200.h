@@ -83,34 +83,37 @@ int bamg_visibility_strength(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_
                              double* G_val, int32_t* flags_dev, void* stream);
 
 /* ---- residuals / Jacobians: problem.py:202-219 (_project_arrays), 272-326 (evaluate) ---- */
+/* J: (k, 32) observation records [F 2x9 | E 2x3 | H 2x3 | r 2] (H filled by build_system) */
 int bamg_evaluate(bamg_ctx* ctx, const double* cams, const double* pts, const int32_t* obs_cam,
                   const int32_t* obs_pt, const double* pixels, int64_t k, int32_t huber, int32_t with_jacobian,
-                  double* F, double* E, double* res, double* w, uint8_t* behind, double* objective_dev,
-                  int32_t* n_behind_dev, void* stream);
+                  double* J, double* w, uint8_t* behind, double* objective_dev, int32_t* n_behind_dev,
+                  void* stream);
 
 /* ---- normal blocks / damping / reduced system: problem.py:255-269, schur.py:38-47, 99-125 ---- */
 int bamg_normal_blocks(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* pt_ptr,
-                       const double* F, const double* E, const double* res, int32_t nc, int32_t npt,
-                       double* A_raw, double* g_cam, double* C_raw, double* g_pt, void* stream);
+                       const double* J, int32_t nc, int32_t npt, double* A_raw, double* g_cam, double* C_raw,
+                       double* g_pt, void* stream);
 int bamg_damping(bamg_ctx* ctx, const double* A_raw, const double* C_raw, int32_t nc, int32_t npt, double radius,
                  double* d_cam, double* d_pt, void* stream);
-int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* pt_ptr,
-                      const double* F, const double* E, const double* A_raw, const double* C_raw,
-                      const double* g_cam, const double* g_pt, const double* d_cam, const double* d_pt,
-                      int32_t nc, int32_t npt, double* A, double* C, double* Cinv, double* Cb, double* H,
-                      double* qo, double* rhs, int32_t* bad_min_dev, void* stream);
+int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* obs_pt_pm,
+                      double* J, int64_t k, const double* A_raw, const double* C_raw, const double* g_cam,
+                      const double* g_pt, const double* d_cam, const double* d_pt, int32_t nc, int32_t npt,
+                      double* A, double* C, double* Cinv, double* Cb, double* qo, double* rhs,
+                      int32_t* bad_min_dev, void* stream);
+/* recompute the H slots of J (and q) from a system's C^-1 / C^-1 b */
+int bamg_obs_H(bamg_ctx* ctx, const int32_t* obs_pt_pm, const double* Cinv, const double* Cb, int64_t k, double* J,
+               double* qo, void* stream);
 /* schur.py:84-86 implicit_matvec */
 int bamg_implicit_matvec(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* pt_ptr,
-                         const int32_t* obs_cam_pm, const double* F, const double* E, const double* A,
-                         const double* Cinv, const double* x, int32_t nc, int32_t npt, double* qo, double* y,
-                         void* stream);
+                         const int32_t* obs_cam_pm, const double* J, const double* A, const double* Cinv,
+                         const double* x, int32_t nc, int32_t npt, double* qo, double* y, void* stream);
 /* schur.py:171-173 back_substitute */
-int bamg_back_substitute(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs_cam_pm, const double* F,
-                         const double* E, const double* Cinv, const double* grad_pt, const double* dc,
-                         int32_t npt, double* dp, void* stream);
+int bamg_back_substitute(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs_cam_pm, const double* J,
+                         const double* Cinv, const double* grad_pt, const double* dc, int32_t npt, double* dp,
+                         void* stream);
 /* schur.py:114-116 W blocks in reference BSR order (API view) */
-int bamg_materialize_W(bamg_ctx* ctx, const int32_t* cm_list, const double* F, const double* E, int64_t k,
-                       double* W, void* stream);
+int bamg_materialize_W(bamg_ctx* ctx, const int32_t* cm_list, const double* J, int64_t k, double* W,
+                       void* stream);
 
 /* ---- explicit S: schur.py:128-144 (+ blockmat.py:308-353) ---- */
 int bamg_schur_symbolic_sizes(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* S_ptr, const int32_t* S_col,
@@ -127,14 +130,13 @@ int bamg_schur_order_upper(bamg_ctx* ctx, int32_t* up_blk, int32_t* up_row, int3
 /* row-owned variant: no pair lists; one CTA per camera row, shared-memory
  * accumulators, deterministic per-warp slot ownership */
 int bamg_schur_numeric_rows(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* pt_ptr,
-                            const int32_t* obs_cam_pm, const int32_t* obs_pt_pm, const double* F, const double* E,
-                            const double* H, const double* A, const int32_t* S_ptr, const int32_t* S_col,
-                            const int32_t* dpos, const int32_t* up_off, const int32_t* up_tpos, int32_t nc, double* S,
-                            void* stream);
-int bamg_schur_numeric(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const double* F,
-                       const double* E, const double* H, const double* A, const int32_t* dpos, int32_t nc,
-                       const int32_t* up_blk, const int32_t* up_tpos, int32_t n_up, const int32_t* blk_pair_ptr,
-                       const int32_t* pair_a, const int32_t* pair_b, double* S, void* stream);
+                            const int32_t* obs_cam_pm, const int32_t* obs_pt_pm, const double* J, const double* A,
+                            const int32_t* S_ptr, const int32_t* S_col, const int32_t* dpos, const int32_t* up_off,
+                            const int32_t* up_tpos, int32_t nc, double* S, void* stream);
+int bamg_schur_numeric(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const double* J,
+                       const double* A, const int32_t* dpos, int32_t nc, const int32_t* up_blk, const int32_t* up_tpos,
+                       int32_t n_up, const int32_t* blk_pair_ptr, const int32_t* pair_a, const int32_t* pair_b,
+                       double* S, void* stream);
 
 /* ---- BSR kernels: blockmat.py:295-299 (matvec), 91-129 (block-diagonal), 270-282 ---- */
 int bamg_bsr_spmv(bamg_ctx* ctx, int32_t bs, const int32_t* ptr, const int32_t* col, const double* blocks,

@@ -118,3 +118,45 @@ __device__ __forceinline__ int lower_bound_i32(const int* a, int n, int key) {
   }
   return lo;
 }
+
+// Observation record layout (256 B, 16 B aligned):
+//   [ 0,18) F (2x9)   [18,24) E (2x3)   [24,30) H = E C^-1 (2x3)   [30,32) residual
+#define REC 32
+#define RF 0
+#define RE 18
+#define RH 24
+#define RR 30
+
+// ---------------------------------------------------------------------------
+// warp-cooperative record gather: 32 observations (one per lane) -> shared memory.
+// Fetches the double2 pieces [a0, a0+NA) then [b0, b0+NB) of each record, then
+// (if `extra` != null) one double2 per observation from a separate (k,2) array;
+// slot (l, i) of `buf` (stride ST doubles, odd) receives fetched piece i of lane l.
+template <int NA, int NB, int NX, int ST>
+__device__ __forceinline__ void gather_records(const double* __restrict__ J, int o_lane, bool valid, int a0, int b0,
+                                               const double* __restrict__ extra, double* buf, int lane) {
+  constexpr int NP = NA + NB + NX;
+  double2 v[NP];
+  // all NP loads are issued before any shared-memory store (no serialised latency)
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    int idx = k * 32 + lane;
+    int l = idx / NP, i = idx - l * NP;
+    int o = __shfl_sync(FULL_MASK, o_lane, l);
+    int vv = __shfl_sync(FULL_MASK, (int)valid, l);
+    const double2* src;
+    if (i < NA) src = reinterpret_cast<const double2*>(J + (int64_t)o * REC) + a0 + i;
+    else if (i < NA + NB) src = reinterpret_cast<const double2*>(J + (int64_t)o * REC) + b0 + i - NA;
+    else src = reinterpret_cast<const double2*>(extra + (int64_t)o * 2);
+    v[k] = vv ? __ldg(src) : make_double2(0.0, 0.0);
+  }
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    int idx = k * 32 + lane;
+    int l = idx / NP, i = idx - l * NP;
+    buf[l * ST + 2 * i] = v[k].x;
+    buf[l * ST + 2 * i + 1] = v[k].y;
+  }
+  __syncwarp();
+}
+

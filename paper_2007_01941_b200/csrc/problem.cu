@@ -360,85 +360,111 @@ __device__ __forceinline__ double loss_w(double s, int huber) {
   return s <= 1.0 ? 1.0 : pow(fmax(s, 1.0), -0.25);
 }
 
-#define EVAL_THREADS 256
+// ---------------------------------------------------------------------------
+// Observation records. Everything the assembly reads per observation lives in one
+// 256 B record (two full cache lines, 16 B aligned):
+//   [ 0,18) F (2x9)   [18,24) E (2x3)   [24,30) H = E C^-1 (2x3)   [30,32) residual
+// Kernels that visit observations in camera order gather whole records with
+// warp-cooperative double2 loads staged through shared memory, so every load
+// instruction touches a few cache lines instead of 32.
+#define EVAL_THREADS 128
+#define EVAL_STRIDE 33  // odd smem stride: conflict-free per-thread record writes
 
-// One thread per observation (point-major). Writes F, E, res, w and a behind flag;
-// objective partials reduced deterministically (last block finishes).
+// One thread per observation (point-major); the CTA's records are staged in shared
+// memory and written back as contiguous double2 stores (H slots untouched). The
+// objective is reduced deterministically (last block finishes).
 __global__ void __launch_bounds__(EVAL_THREADS)
 k_evaluate(const double* __restrict__ cams, const double* __restrict__ pts, const int* __restrict__ ocam,
            const int* __restrict__ opt, const double* __restrict__ pix, int64_t k, int huber, int with_jac,
-           double* __restrict__ F, double* __restrict__ E, double* __restrict__ res, double* __restrict__ w,
-           unsigned char* __restrict__ behind, int* __restrict__ n_behind, double* partials,
-           unsigned int* counter, double* objective) {
+           double* __restrict__ J, double* __restrict__ w, unsigned char* __restrict__ behind,
+           int* __restrict__ n_behind, double* partials, unsigned int* counter, double* objective) {
   __shared__ double scratch[33];
+  __shared__ double rec[EVAL_THREADS * EVAL_STRIDE];
   double acc = 0.0;
   int nb = 0;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < k; t += (int64_t)gridDim.x * blockDim.x) {
-    const double* cam = cams + (int64_t)ocam[t] * 9;
-    const double* X = pts + (int64_t)opt[t] * 3;
-    ProjOut o;
-    bool ok = project_one(cam, X, pix + 2 * t, o);
-    if (behind) behind[t] = ok ? 0 : 1;
-    if (!ok) {
-      ++nb;
-      continue;
-    }
-    acc += loss_rho(o.s, huber);
-    if (!with_jac) continue;
-    double wt = loss_w(o.s, huber);
-    double z = o.pc[2];
-    double f = cam[6], k1 = cam[7], k2 = cam[8];
-    // dp/dpc (2x3)
-    double iz = -1.0 / z;
-    double z2 = z * z;
-    double dp[6] = {iz, 0.0, o.pc[0] / z2, 0.0, iz, o.pc[1] / z2};
-    double coef = f * (2.0 * k1 + 4.0 * k2 * o.n2);
-    double fd = f * o.dist;
-    double M[4] = {fd + coef * o.p[0] * o.p[0], coef * o.p[0] * o.p[1], coef * o.p[1] * o.p[0],
-                   fd + coef * o.p[1] * o.p[1]};
-    double D[6];
+  double* my = rec + threadIdx.x * EVAL_STRIDE;
+  for (int64_t base = (int64_t)blockIdx.x * EVAL_THREADS; base < k; base += (int64_t)gridDim.x * EVAL_THREADS) {
+    int64_t t = base + threadIdx.x;
+    if (t < k) {
+      const double* cam = cams + (int64_t)ocam[t] * 9;
+      const double* X = pts + (int64_t)opt[t] * 3;
+      ProjOut o;
+      bool ok = project_one(cam, X, pix + 2 * t, o);
+      if (behind) behind[t] = ok ? 0 : 1;
+      if (!ok) {
+        ++nb;
+        if (with_jac) {
+          for (int q = 0; q < REC; ++q) my[q] = 0.0;
+          w[t] = 0.0;
+        }
+      } else {
+        acc += loss_rho(o.s, huber);
+        if (with_jac) {
+          double wt = loss_w(o.s, huber);
+          double z = o.pc[2];
+          double f = cam[6], k1 = cam[7], k2 = cam[8];
+          double iz = -1.0 / z;
+          double z2 = z * z;
+          double dp[6] = {iz, 0.0, o.pc[0] / z2, 0.0, iz, o.pc[1] / z2};
+          double coef = f * (2.0 * k1 + 4.0 * k2 * o.n2);
+          double fd = f * o.dist;
+          double M[4] = {fd + coef * o.p[0] * o.p[0], coef * o.p[0] * o.p[1], coef * o.p[1] * o.p[0],
+                         fd + coef * o.p[1] * o.p[1]};
+          double Dm[6];
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+          for (int r = 0; r < 2; ++r)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) D[r * 3 + c] = M[r * 2] * dp[c] + M[r * 2 + 1] * dp[3 + c];
-    // R, Jr
-    const double* aa = cam;
-    double a2, s1, s2, c2;
-    bool small;
-    rot_coeffs(aa, a2, s1, s2, c2, small);
-    double K[9], K2[9];
-    hat(aa, K);
-    mm3(K, K, K2);
-    double R[9], Jr[9];
+            for (int c = 0; c < 3; ++c) Dm[r * 3 + c] = M[r * 2] * dp[c] + M[r * 2 + 1] * dp[3 + c];
+          const double* aa = cam;
+          double a2, s1, s2, c2;
+          bool small;
+          rot_coeffs(aa, a2, s1, s2, c2, small);
+          double K[9], K2[9];
+          hat(aa, K);
+          mm3(K, K, K2);
+          double R[9], Jr[9];
 #pragma unroll
-    for (int q = 0; q < 9; ++q) {
-      double I = (q % 4 == 0) ? 1.0 : 0.0;
-      R[q] = I + s1 * K[q] + s2 * K2[q];
-      Jr[q] = I - s2 * K[q] + c2 * K2[q];
-    }
-    // rotate_jacobian = -R [X]x Jr
-    double HX[9], T1[9], RJ[9];
-    hat(X, HX);
-    mm3(R, HX, T1);
-    mm3(T1, Jr, RJ);
-    double* Fo = F + t * 18;
-    double* Eo = E + t * 6;
+          for (int q = 0; q < 9; ++q) {
+            double I = (q % 4 == 0) ? 1.0 : 0.0;
+            R[q] = I + s1 * K[q] + s2 * K2[q];
+            Jr[q] = I - s2 * K[q] + c2 * K2[q];
+          }
+          double HX[9], T1[9], RJ[9];
+          hat(X, HX);
+          mm3(R, HX, T1);
+          mm3(T1, Jr, RJ);
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+          for (int r = 0; r < 2; ++r) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double v = -(D[r * 3] * RJ[c] + D[r * 3 + 1] * RJ[3 + c] + D[r * 3 + 2] * RJ[6 + c]);
-        Fo[r * 9 + c] = v * wt;
-        Fo[r * 9 + 3 + c] = D[r * 3 + c] * wt;
-        Eo[r * 3 + c] = (D[r * 3] * R[c] + D[r * 3 + 1] * R[3 + c] + D[r * 3 + 2] * R[6 + c]) * wt;
+            for (int c = 0; c < 3; ++c) {
+              double v = -(Dm[r * 3] * RJ[c] + Dm[r * 3 + 1] * RJ[3 + c] + Dm[r * 3 + 2] * RJ[6 + c]);
+              my[RF + r * 9 + c] = v * wt;
+              my[RF + r * 9 + 3 + c] = Dm[r * 3 + c] * wt;
+              my[RE + r * 3 + c] = (Dm[r * 3] * R[c] + Dm[r * 3 + 1] * R[3 + c] + Dm[r * 3 + 2] * R[6 + c]) * wt;
+            }
+            my[RF + r * 9 + 6] = (o.dist * o.p[r]) * wt;
+            my[RF + r * 9 + 7] = ((f * o.n2) * o.p[r]) * wt;
+            my[RF + r * 9 + 8] = ((f * o.n2 * o.n2) * o.p[r]) * wt;
+          }
+          my[RR] = o.res[0] * wt;
+          my[RR + 1] = o.res[1] * wt;
+          w[t] = wt;
+        }
       }
-      Fo[r * 9 + 6] = (o.dist * o.p[r]) * wt;
-      Fo[r * 9 + 7] = ((f * o.n2) * o.p[r]) * wt;
-      Fo[r * 9 + 8] = ((f * o.n2 * o.n2) * o.p[r]) * wt;
     }
-    res[2 * t] = o.res[0] * wt;
-    res[2 * t + 1] = o.res[1] * wt;
-    w[t] = wt;
+    if (with_jac) {
+      __syncthreads();
+      // coalesced write-back of the CTA's records (16 double2 each, skip H = 12..14)
+      int nrec = (int)min((int64_t)EVAL_THREADS, k - base);
+      double2* dst = reinterpret_cast<double2*>(J + base * REC);
+      for (int g = threadIdx.x; g < nrec * 16; g += EVAL_THREADS) {
+        int rr = g >> 4, pc = g & 15;
+        if (pc >= 12 && pc < 15) continue;
+        const double* s = rec + rr * EVAL_STRIDE + 2 * pc;
+        dst[g] = make_double2(s[0], s[1]);
+      }
+      __syncthreads();
+    }
   }
   nb = warp_sum_int(nb);
   if ((threadIdx.x & 31) == 0 && nb) atomicAdd(n_behind, nb);
@@ -448,14 +474,13 @@ k_evaluate(const double* __restrict__ cams, const double* __restrict__ pts, cons
 
 extern "C" int bamg_evaluate(bamg_ctx* ctx, const double* cams, const double* pts, const int32_t* obs_cam,
                              const int32_t* obs_pt, const double* pixels, int64_t k, int32_t huber,
-                             int32_t with_jacobian, double* F, double* E, double* res, double* w,
-                             uint8_t* behind, double* objective_dev, int32_t* n_behind_dev, void* stream) {
+                             int32_t with_jacobian, double* J, double* w, uint8_t* behind, double* objective_dev,
+                             int32_t* n_behind_dev, void* stream) {
   cudaStream_t st = as_stream(stream);
   BAMG_CUDA_CHECK(cudaMemsetAsync(n_behind_dev, 0, sizeof(int), st));
-  int g = grid_for(k, EVAL_THREADS, 4);
-  launch(k_evaluate, g, EVAL_THREADS, 0, st, cams, pts, obs_cam, obs_pt, pixels, k, huber, with_jacobian, F, E, res,
-                                         w, behind, n_behind_dev, ctx->partials, ctx->counters + BAMG_CTR_OBJ,
-                                         objective_dev);
+  int g = grid_for(k, EVAL_THREADS, 8);
+  launch(k_evaluate, g, EVAL_THREADS, 0, st, cams, pts, obs_cam, obs_pt, pixels, k, huber, with_jacobian, J, w,
+         behind, n_behind_dev, ctx->partials, ctx->counters + BAMG_CTR_OBJ, objective_dev);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -463,12 +488,15 @@ extern "C" int bamg_evaluate(bamg_ctx* ctx, const double* cams, const double* pt
 // ---------------------------------------------------------------------------
 // normal-equation blocks (problem.py:255-269, schur.py:104-112)
 
-// Warp per camera: A_raw = sum F^T F (full 9x9), g = sum F^T r. Lanes stride the
-// camera's observations in (camera, point) order, then a fixed shuffle tree.
+#define CN_ST 21  // 9 F pieces + residual piece = 20 doubles, odd stride
+
+// Warp per camera: A_raw = sum F^T F (full 9x9), g = sum F^T r.
 __global__ void __launch_bounds__(128)
-k_cam_normal(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, const double* __restrict__ F,
-             const double* __restrict__ res, int nc, double* __restrict__ A_raw, double* __restrict__ g_cam) {
+k_cam_normal(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, const double* __restrict__ J, int nc,
+             double* __restrict__ A_raw, double* __restrict__ g_cam) {
+  __shared__ double sbuf[4][32 * CN_ST];
   int lane = threadIdx.x & 31;
+  double* buf = sbuf[threadIdx.x >> 5];
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int i = warp; i < nc; i += nwarps) {
@@ -478,23 +506,24 @@ k_cam_normal(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
     for (int q = 0; q < 45; ++q) a[q] = 0.0;
 #pragma unroll
     for (int q = 0; q < 9; ++q) g[q] = 0.0;
-    for (int q = cam_ptr[i] + lane; q < cam_ptr[i + 1]; q += 32) {
-      int o = cm_list[q];
-      const double* f = F + (int64_t)o * 18;
-      double f0[9], f1[9];
+    for (int base = cam_ptr[i]; base < cam_ptr[i + 1]; base += 32) {
+      int q = base + lane;
+      bool valid = q < cam_ptr[i + 1];
+      int o = valid ? cm_list[q] : 0;
+      gather_records<9, 1, 0, CN_ST>(J, o, valid, 0, RR / 2, nullptr, buf, lane);
+      const double* f = buf + lane * CN_ST;
+      if (valid) {
+        double r0 = f[18], r1 = f[19];
+        int t = 0;
 #pragma unroll
-      for (int c = 0; c < 9; ++c) {
-        f0[c] = f[c];
-        f1[c] = f[9 + c];
+        for (int j = 0; j < 9; ++j) {
+          double f0j = f[j], f1j = f[9 + j];
+#pragma unroll
+          for (int l = j; l < 9; ++l) a[t++] += f0j * f[l] + f1j * f[9 + l];
+          g[j] += f0j * r0 + f1j * r1;
+        }
       }
-      double r0 = res[2 * o], r1 = res[2 * o + 1];
-      int t = 0;
-#pragma unroll
-      for (int j = 0; j < 9; ++j) {
-#pragma unroll
-        for (int l = j; l < 9; ++l) a[t++] += f0[j] * f0[l] + f1[j] * f1[l];
-        g[j] += f0[j] * r0 + f1[j] * r1;
-      }
+      __syncwarp();
     }
 #pragma unroll
     for (int q = 0; q < 45; ++q) a[q] = warp_sum(a[q]);
@@ -518,20 +547,21 @@ k_cam_normal(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
 }
 
 // Thread per point: C_raw = sum E^T E (3x3), g_pt = sum E^T r.
-__global__ void k_pt_normal(const int* __restrict__ pt_ptr, const double* __restrict__ E,
-                            const double* __restrict__ res, int npt, double* __restrict__ C_raw,
-                            double* __restrict__ g_pt) {
+__global__ void k_pt_normal(const int* __restrict__ pt_ptr, const double* __restrict__ J, int npt,
+                            double* __restrict__ C_raw, double* __restrict__ g_pt) {
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npt; p += gridDim.x * blockDim.x) {
     double c[6] = {0, 0, 0, 0, 0, 0}, g[3] = {0, 0, 0};
     for (int o = pt_ptr[p]; o < pt_ptr[p + 1]; ++o) {
-      const double* e = E + (int64_t)o * 6;
-      double r0 = res[2 * o], r1 = res[2 * o + 1];
+      const double2* rp = reinterpret_cast<const double2*>(J + (int64_t)o * REC);
+      double2 e01 = __ldg(rp + RE / 2), e23 = __ldg(rp + RE / 2 + 1), e45 = __ldg(rp + RE / 2 + 2);
+      double2 rr = __ldg(rp + RR / 2);
+      double e[6] = {e01.x, e01.y, e23.x, e23.y, e45.x, e45.y};
       int t = 0;
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
 #pragma unroll
         for (int l = j; l < 3; ++l) c[t++] += e[j] * e[l] + e[3 + j] * e[3 + l];
-        g[j] += e[j] * r0 + e[3 + j] * r1;
+        g[j] += e[j] * rr.x + e[3 + j] * rr.y;
       }
     }
     double* out = C_raw + (int64_t)p * 9;
@@ -545,17 +575,16 @@ __global__ void k_pt_normal(const int* __restrict__ pt_ptr, const double* __rest
 }
 
 extern "C" int bamg_normal_blocks(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
-                                  const int32_t* pt_ptr, const double* F, const double* E, const double* res,
-                                  int32_t nc, int32_t npt, double* A_raw, double* g_cam, double* C_raw,
-                                  double* g_pt, void* stream) {
+                                  const int32_t* pt_ptr, const double* J, int32_t nc, int32_t npt, double* A_raw,
+                                  double* g_cam, double* C_raw, double* g_pt, void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
   if (nc > 0) {
-    launch(k_cam_normal, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, F, res, nc, A_raw, g_cam);
+    launch(k_cam_normal, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, J, nc, A_raw, g_cam);
     BAMG_LAUNCH_CHECK();
   }
   if (npt > 0) {
-    launch(k_pt_normal, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, E, res, npt, C_raw, g_pt);
+    launch(k_pt_normal, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, J, npt, C_raw, g_pt);
     BAMG_LAUNCH_CHECK();
   }
   return 0;
@@ -608,12 +637,10 @@ __device__ __forceinline__ bool chol_inv3(const double* C, double* Ci) {
   double d2 = C[8] - l20 * l20 - l21 * l21;
   if (!(d2 > 0.0)) return false;
   double l22 = sqrt(d2);
-  // M = L^-1 (lower)
   double m00 = 1.0 / l00, m11 = 1.0 / l11, m22 = 1.0 / l22;
   double m10 = -l10 * m00 / l11;
   double m21 = -l21 * m11 / l22;
   double m20 = -(l20 * m00 + l21 * m10) / l22;
-  // Ci = M^T M
   Ci[0] = m00 * m00 + m10 * m10 + m20 * m20;
   Ci[1] = m10 * m11 + m20 * m21;
   Ci[2] = m20 * m22;
@@ -626,13 +653,10 @@ __device__ __forceinline__ bool chol_inv3(const double* C, double* Ci) {
   return true;
 }
 
-// Thread per point: C = C_raw + D_p, factor, C^-1, b_p = -g_p, Cb = C^-1 b_p,
-// then per observation H = E C^-1 (2x3) and q = E Cb (2).
-__global__ void k_build_points(const int* __restrict__ pt_ptr, const double* __restrict__ E,
-                               const double* __restrict__ C_raw, const double* __restrict__ d_pt,
-                               const double* __restrict__ g_pt, int npt, double* __restrict__ C,
-                               double* __restrict__ Cinv, double* __restrict__ Cb, double* __restrict__ H,
-                               double* __restrict__ qo, int* __restrict__ bad_min) {
+// Thread per point: C = C_raw + D_p, factor, C^-1, b_p = -g_p, Cb = C^-1 b_p.
+__global__ void k_points_factor(const double* __restrict__ C_raw, const double* __restrict__ d_pt,
+                                const double* __restrict__ g_pt, int npt, double* __restrict__ C,
+                                double* __restrict__ Cinv, double* __restrict__ Cb, int* __restrict__ bad_min) {
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npt; p += gridDim.x * blockDim.x) {
     double c[9], ci[9];
 #pragma unroll
@@ -650,45 +674,63 @@ __global__ void k_build_points(const int* __restrict__ pt_ptr, const double* __r
 #pragma unroll
     for (int q = 0; q < 9; ++q) Cinv[(int64_t)p * 9 + q] = ci[q];
     double b0 = -g_pt[3 * p], b1 = -g_pt[3 * p + 1], b2 = -g_pt[3 * p + 2];
-    double x0 = ci[0] * b0 + ci[1] * b1 + ci[2] * b2;
-    double x1 = ci[3] * b0 + ci[4] * b1 + ci[5] * b2;
-    double x2 = ci[6] * b0 + ci[7] * b1 + ci[8] * b2;
-    Cb[3 * p] = x0;
-    Cb[3 * p + 1] = x1;
-    Cb[3 * p + 2] = x2;
-    for (int o = pt_ptr[p]; o < pt_ptr[p + 1]; ++o) {
-      const double* e = E + (int64_t)o * 6;
-      double* h = H + (int64_t)o * 6;
+    Cb[3 * p] = ci[0] * b0 + ci[1] * b1 + ci[2] * b2;
+    Cb[3 * p + 1] = ci[3] * b0 + ci[4] * b1 + ci[5] * b2;
+    Cb[3 * p + 2] = ci[6] * b0 + ci[7] * b1 + ci[8] * b2;
+  }
+}
+
+// Thread per observation: H = E C_p^-1 (into the record) and q = E C_p^-1 b_p.
+__global__ void k_obs_H(const int* __restrict__ opt, const double* __restrict__ Cinv, const double* __restrict__ Cb,
+                        int64_t k, double* __restrict__ J, double* __restrict__ qo) {
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < k; o += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p = opt[o];
+    double2* rp = reinterpret_cast<double2*>(J + o * REC);
+    double2 e01 = rp[RE / 2], e23 = rp[RE / 2 + 1], e45 = rp[RE / 2 + 2];
+    double e[6] = {e01.x, e01.y, e23.x, e23.y, e45.x, e45.y};
+    const double* ci = Cinv + p * 9;
+    double x0 = Cb[3 * p], x1 = Cb[3 * p + 1], x2 = Cb[3 * p + 2];
+    double h[6];
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < 2; ++r)
 #pragma unroll
-        for (int cc = 0; cc < 3; ++cc)
-          h[r * 3 + cc] = e[r * 3] * ci[cc] + e[r * 3 + 1] * ci[3 + cc] + e[r * 3 + 2] * ci[6 + cc];
-        qo[2 * (int64_t)o + r] = e[r * 3] * x0 + e[r * 3 + 1] * x1 + e[r * 3 + 2] * x2;
-      }
-    }
+      for (int cc = 0; cc < 3; ++cc)
+        h[r * 3 + cc] = e[r * 3] * ci[cc] + e[r * 3 + 1] * ci[3 + cc] + e[r * 3 + 2] * ci[6 + cc];
+    rp[RH / 2] = make_double2(h[0], h[1]);
+    rp[RH / 2 + 1] = make_double2(h[2], h[3]);
+    rp[RH / 2 + 2] = make_double2(h[4], h[5]);
+    reinterpret_cast<double2*>(qo)[o] =
+        make_double2(e[0] * x0 + e[1] * x1 + e[2] * x2, e[3] * x0 + e[4] * x1 + e[5] * x2);
   }
 }
 
 // Warp per camera: out_i = -g_i - sum_o F_o^T q_o   (schur.py:122 rhs), or with
-// `base` != null: out_i = A_i x_i - sum_o F_o^T q_o (implicit matvec, schur.py:84-86).
+// A != null: out_i = A_i x_i - sum_o F_o^T q_o (implicit matvec, schur.py:84-86).
 __global__ void __launch_bounds__(128)
-k_cam_gather(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, const double* __restrict__ F,
+k_cam_gather(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, const double* __restrict__ J,
              const double* __restrict__ qo, const double* __restrict__ g_cam, const double* __restrict__ A,
              const double* __restrict__ x, int nc, double* __restrict__ out) {
+  __shared__ double sbuf[4][32 * CN_ST];
   int lane = threadIdx.x & 31;
+  double* buf = sbuf[threadIdx.x >> 5];
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int i = warp; i < nc; i += nwarps) {
     double s[9];
 #pragma unroll
     for (int j = 0; j < 9; ++j) s[j] = 0.0;
-    for (int q = cam_ptr[i] + lane; q < cam_ptr[i + 1]; q += 32) {
-      int o = cm_list[q];
-      const double* f = F + (int64_t)o * 18;
-      double q0 = qo[2 * (int64_t)o], q1 = qo[2 * (int64_t)o + 1];
+    for (int base = cam_ptr[i]; base < cam_ptr[i + 1]; base += 32) {
+      int q = base + lane;
+      bool valid = q < cam_ptr[i + 1];
+      int o = valid ? cm_list[q] : 0;
+      gather_records<9, 0, 1, CN_ST>(J, o, valid, 0, 0, qo, buf, lane);
+      const double* f = buf + lane * CN_ST;
+      if (valid) {
+        double q0 = f[18], q1 = f[19];
 #pragma unroll
-      for (int j = 0; j < 9; ++j) s[j] += f[j] * q0 + f[9 + j] * q1;
+        for (int j = 0; j < 9; ++j) s[j] += f[j] * q0 + f[9 + j] * q1;
+      }
+      __syncwarp();
     }
 #pragma unroll
     for (int j = 0; j < 9; ++j) s[j] = warp_sum(s[j]);
@@ -713,49 +755,60 @@ k_cam_gather(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
 }
 
 extern "C" int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
-                                 const int32_t* pt_ptr, const double* F, const double* E, const double* A_raw,
-                                 const double* C_raw, const double* g_cam, const double* g_pt,
-                                 const double* d_cam, const double* d_pt, int32_t nc, int32_t npt, double* A,
-                                 double* C, double* Cinv, double* Cb, double* H, double* qo, double* rhs,
-                                 int32_t* bad_min_dev, void* stream) {
+                                 const int32_t* obs_pt_pm, double* J, int64_t k, const double* A_raw,
+                                 const double* C_raw, const double* g_cam, const double* g_pt, const double* d_cam,
+                                 const double* d_pt, int32_t nc, int32_t npt, double* A, double* C, double* Cinv,
+                                 double* Cb, double* qo, double* rhs, int32_t* bad_min_dev, void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
   int big = 0x7fffffff;
   BAMG_CUDA_CHECK(cudaMemcpyAsync(bad_min_dev, &big, sizeof(int), cudaMemcpyHostToDevice, st));
   if (nc) launch(k_add_diag, grid_for((int64_t)nc * 81, 256), 256, 0, st, A_raw, d_cam, nc, 9, A);
   if (npt)
-    launch(k_build_points, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, E, C_raw, d_pt, g_pt, npt, C, Cinv, Cb, H, qo,
-                                                          bad_min_dev);
+    launch(k_points_factor, grid_for(npt, 128, 16), 128, 0, st, C_raw, d_pt, g_pt, npt, C, Cinv, Cb, bad_min_dev);
+  if (k) launch(k_obs_H, grid_for(k, 256, 8), 256, 0, st, obs_pt_pm, Cinv, Cb, k, J, qo);
   if (nc)
-    launch(k_cam_gather, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, F, qo, g_cam, nullptr,
-                                                                     nullptr, nc, rhs);
+    launch(k_cam_gather, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, J, qo, g_cam, nullptr,
+           nullptr, nc, rhs);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
 
-// Per point: u_p = sum_o E_o^T (F_o x_cam(o)); v_p = Cinv u_p; q_o = E_o v_p.
-__global__ void k_point_wtx(const int* __restrict__ pt_ptr, const int* __restrict__ ocam,
-                            const double* __restrict__ F, const double* __restrict__ E,
+// H of every observation from a system's C^-1 (restores H after another system
+// built from the same Jacobian overwrote it).
+extern "C" int bamg_obs_H(bamg_ctx* ctx, const int32_t* obs_pt_pm, const double* Cinv, const double* Cb, int64_t k,
+                          double* J, double* qo, void* stream) {
+  (void)ctx;
+  if (k) launch(k_obs_H, grid_for(k, 256, 8), 256, 0, as_stream(stream), obs_pt_pm, Cinv, Cb, k, J, qo);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// Per point: u_p = sum_o E_o^T (F_o x_cam(o)); v_p = Cinv u_p (or Cinv (base - u_p));
+// q_o = E_o v_p.
+__global__ void k_point_wtx(const int* __restrict__ pt_ptr, const int* __restrict__ ocam, const double* __restrict__ J,
                             const double* __restrict__ Cinv, const double* __restrict__ x, const double* __restrict__ base,
                             int npt, double* __restrict__ v_out, double* __restrict__ qo) {
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npt; p += gridDim.x * blockDim.x) {
     double u[3] = {0, 0, 0};
     for (int o = pt_ptr[p]; o < pt_ptr[p + 1]; ++o) {
-      const double* f = F + (int64_t)o * 18;
-      const double* e = E + (int64_t)o * 6;
+      const double2* rp = reinterpret_cast<const double2*>(J + (int64_t)o * REC);
       const double* xc = x + (int64_t)ocam[o] * 9;
       double t0 = 0.0, t1 = 0.0;
 #pragma unroll
       for (int c = 0; c < 9; ++c) {
-        double xv = xc[c];
-        t0 += f[c] * xv;
-        t1 += f[9 + c] * xv;
+        double2 fc = __ldg(rp + c);  // fields 2c, 2c+1 of the flattened F (rows 0 and 1)
+        int e0 = 2 * c, e1 = 2 * c + 1;
+        // flattened index e -> (row e / 9, col e % 9)
+        if (e0 < 9) t0 += fc.x * xc[e0]; else t1 += fc.x * xc[e0 - 9];
+        if (e1 < 9) t0 += fc.y * xc[e1]; else t1 += fc.y * xc[e1 - 9];
       }
+      double2 e01 = __ldg(rp + RE / 2), e23 = __ldg(rp + RE / 2 + 1), e45 = __ldg(rp + RE / 2 + 2);
+      double e[6] = {e01.x, e01.y, e23.x, e23.y, e45.x, e45.y};
 #pragma unroll
       for (int j = 0; j < 3; ++j) u[j] += e[j] * t0 + e[3 + j] * t1;
     }
     if (base) {
-      // back-substitution form: v = Cinv (base - u)  (schur.py:171-173)
 #pragma unroll
       for (int j = 0; j < 3; ++j) u[j] = base[3 * (int64_t)p + j] - u[j];
     }
@@ -770,7 +823,7 @@ __global__ void k_point_wtx(const int* __restrict__ pt_ptr, const int* __restric
     }
     if (qo) {
       for (int o = pt_ptr[p]; o < pt_ptr[p + 1]; ++o) {
-        const double* e = E + (int64_t)o * 6;
+        const double* e = J + (int64_t)o * REC + RE;
         qo[2 * (int64_t)o] = e[0] * v0 + e[1] * v1 + e[2] * v2;
         qo[2 * (int64_t)o + 1] = e[3] * v0 + e[4] * v1 + e[5] * v2;
       }
@@ -780,15 +833,15 @@ __global__ void k_point_wtx(const int* __restrict__ pt_ptr, const int* __restric
 
 // Implicit Schur matvec y = A x - W C^-1 W^T x (schur.py:84-86). qo: k*2 scratch.
 extern "C" int bamg_implicit_matvec(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
-                                    const int32_t* pt_ptr, const int32_t* obs_cam_pm, const double* F,
-                                    const double* E, const double* A, const double* Cinv, const double* x,
-                                    int32_t nc, int32_t npt, double* qo, double* y, void* stream) {
+                                    const int32_t* pt_ptr, const int32_t* obs_cam_pm, const double* J,
+                                    const double* A, const double* Cinv, const double* x, int32_t nc, int32_t npt,
+                                    double* qo, double* y, void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
-  if (npt) launch(k_point_wtx, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, obs_cam_pm, F, E, Cinv, x, nullptr, npt,
-                                                              nullptr, qo);
+  if (npt) launch(k_point_wtx, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, obs_cam_pm, J, Cinv, x, nullptr, npt,
+                  nullptr, qo);
   if (nc)
-    launch(k_cam_gather, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, F, qo, nullptr, A, x, nc, y);
+    launch(k_cam_gather, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, J, qo, nullptr, A, x, nc, y);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -799,13 +852,13 @@ __global__ void k_neg(const double* __restrict__ a, double* __restrict__ b, int6
     b[i] = -a[i];
 }
 
-extern "C" int bamg_back_substitute(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs_cam_pm,
-                                    const double* F, const double* E, const double* Cinv, const double* grad_pt,
-                                    const double* dc, int32_t npt, double* dp, void* stream) {
+extern "C" int bamg_back_substitute(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs_cam_pm, const double* J,
+                                    const double* Cinv, const double* grad_pt, const double* dc, int32_t npt,
+                                    double* dp, void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
-  if (npt) launch(k_point_wtx, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, obs_cam_pm, F, E, Cinv, dc, grad_pt, npt, dp,
-                                                              nullptr);
+  if (npt) launch(k_point_wtx, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, obs_cam_pm, J, Cinv, dc, grad_pt, npt, dp,
+                  nullptr);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -818,23 +871,21 @@ extern "C" int bamg_negate(bamg_ctx* ctx, const double* a, double* b, int64_t n,
 }
 
 // W blocks in the reference's BSR order (for API views): W_b = F_o^T E_o, o = cm_list[b].
-__global__ void k_materialize_W(const int* __restrict__ cm_list, const double* __restrict__ F,
-                                const double* __restrict__ E, int64_t k, double* __restrict__ W) {
+__global__ void k_materialize_W(const int* __restrict__ cm_list, const double* __restrict__ J, int64_t k,
+                                double* __restrict__ W) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < k * 27; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t b = t / 27;
     int q = (int)(t - b * 27);
     int r = q / 3, c = q - r * 3;
-    int64_t o = cm_list[b];
-    const double* f = F + o * 18;
-    const double* e = E + o * 6;
-    W[t] = f[r] * e[c] + f[9 + r] * e[3 + c];
+    const double* rec = J + (int64_t)cm_list[b] * REC;
+    W[t] = rec[RF + r] * rec[RE + c] + rec[RF + 9 + r] * rec[RE + 3 + c];
   }
 }
 
-extern "C" int bamg_materialize_W(bamg_ctx* ctx, const int32_t* cm_list, const double* F, const double* E,
-                                  int64_t k, double* W, void* stream) {
+extern "C" int bamg_materialize_W(bamg_ctx* ctx, const int32_t* cm_list, const double* J, int64_t k, double* W,
+                                  void* stream) {
   (void)ctx;
-  if (k) launch(k_materialize_W, grid_for(k * 27, 256), 256, 0, as_stream(stream), cm_list, F, E, k, W);
+  if (k) launch(k_materialize_W, grid_for(k * 27, 256), 256, 0, as_stream(stream), cm_list, J, k, W);
   BAMG_LAUNCH_CHECK();
   return 0;
 }

@@ -218,40 +218,43 @@ extern "C" int bamg_schur_order_upper(bamg_ctx* ctx, int32_t* up_blk, int32_t* u
 }
 
 // Diagonal blocks: warp per camera, S_ii = A_i - sum_o F_o^T (H_o E_o^T) F_o.
+// Records (F, E, H = pieces 0..14) are gathered 32 at a time into shared memory.
+#define SD_ST 31
 __global__ void __launch_bounds__(128)
-k_schur_diag(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, const double* __restrict__ F,
-             const double* __restrict__ E, const double* __restrict__ H, const double* __restrict__ A,
-             const int* __restrict__ dpos, int nc, double* __restrict__ S) {
+k_schur_diag(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, const double* __restrict__ J,
+             const double* __restrict__ A, const int* __restrict__ dpos, int nc, double* __restrict__ S) {
+  __shared__ double sbuf[4][32 * SD_ST];
   int lane = threadIdx.x & 31;
+  double* buf = sbuf[threadIdx.x >> 5];
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int i = warp; i < nc; i += nwarps) {
     double acc[45];
 #pragma unroll
     for (int q = 0; q < 45; ++q) acc[q] = 0.0;
-    for (int q = cam_ptr[i] + lane; q < cam_ptr[i + 1]; q += 32) {
-      int64_t o = cm_list[q];
-      const double* f = F + o * 18;
-      const double* h = H + o * 6;
-      const double* e = E + o * 6;
-      double g00 = h[0] * e[0] + h[1] * e[1] + h[2] * e[2];
-      double g01 = h[0] * e[3] + h[1] * e[4] + h[2] * e[5];
-      double g10 = h[3] * e[0] + h[4] * e[1] + h[5] * e[2];
-      double g11 = h[3] * e[3] + h[4] * e[4] + h[5] * e[5];
-      double f0[9], f1[9];
+    for (int base = cam_ptr[i]; base < cam_ptr[i + 1]; base += 32) {
+      int q = base + lane;
+      bool valid = q < cam_ptr[i + 1];
+      int o = valid ? cm_list[q] : 0;
+      gather_records<15, 0, 0, SD_ST>(J, o, valid, 0, 0, nullptr, buf, lane);
+      const double* f = buf + lane * SD_ST;
+      if (valid) {
+        const double* e = f + RE;
+        const double* h = f + RH;
+        double g00 = h[0] * e[0] + h[1] * e[1] + h[2] * e[2];
+        double g01 = h[0] * e[3] + h[1] * e[4] + h[2] * e[5];
+        double g10 = h[3] * e[0] + h[4] * e[1] + h[5] * e[2];
+        double g11 = h[3] * e[3] + h[4] * e[4] + h[5] * e[5];
+        int t = 0;
 #pragma unroll
-      for (int c = 0; c < 9; ++c) {
-        f0[c] = f[c];
-        f1[c] = f[9 + c];
+        for (int j = 0; j < 9; ++j) {
+          double a0 = f[j] * g00 + f[9 + j] * g10;
+          double a1 = f[j] * g01 + f[9 + j] * g11;
+#pragma unroll
+          for (int l = j; l < 9; ++l) acc[t++] += a0 * f[l] + a1 * f[9 + l];
+        }
       }
-      int t = 0;
-#pragma unroll
-      for (int j = 0; j < 9; ++j) {
-        double a0 = f0[j] * g00 + f1[j] * g10;
-        double a1 = f0[j] * g01 + f1[j] * g11;
-#pragma unroll
-        for (int l = j; l < 9; ++l) acc[t++] += a0 * f0[l] + a1 * f1[l];
-      }
+      __syncwarp();
     }
 #pragma unroll
     for (int q = 0; q < 45; ++q) acc[q] = warp_sum(acc[q]);
@@ -271,13 +274,18 @@ k_schur_diag(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
   }
 }
 
-#define OFF_GROUPS 10  // blocks per warp (3 lanes each, lanes 30/31 idle)
+// Upper off-diagonal blocks from the per-block pair lists: 10 blocks per warp,
+// 3 lanes per block (each lane owns three columns of the 9x9 block in registers).
+// The a-side (F, H) and b-side (F, E) of a pair sit in one 256 B record each.
+// (A variant that staged the ten pairs' records through shared memory with
+// cooperative loads measured 2x slower at c4: the extra synchronisation
+// serialised the per-pair index -> record latency chain.)
+#define OFF_GROUPS 10
 
 __global__ void __launch_bounds__(128)
 k_schur_offdiag(const int* __restrict__ up_blk, const int* __restrict__ up_tpos, int n_up,
                 const int* __restrict__ blk_pair_ptr, const int* __restrict__ pair_a, const int* __restrict__ pair_b,
-                const double* __restrict__ F, const double* __restrict__ E, const double* __restrict__ H,
-                double* __restrict__ S) {
+                const double* __restrict__ J, double* __restrict__ S) {
   int lane = threadIdx.x & 31;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -291,12 +299,18 @@ k_schur_offdiag(const int* __restrict__ up_blk, const int* __restrict__ up_tpos,
 #pragma unroll
     for (int q = 0; q < 27; ++q) acc[q] = 0.0;
     int c0 = 3 * c3;
-    for (int q = blk_pair_ptr[blk]; q < blk_pair_ptr[blk + 1]; ++q) {
-      int64_t oa = pair_a[q], ob = pair_b[q];
-      const double* fa = F + oa * 18;
-      const double* ha = H + oa * 6;
-      const double* eb = E + ob * 6;
-      const double* fb = F + ob * 18;
+    int q = blk_pair_ptr[blk], qe = blk_pair_ptr[blk + 1];
+    int na = q < qe ? pair_a[q] : 0, nb = q < qe ? pair_b[q] : 0;
+    for (; q < qe; ++q) {
+      int64_t oa = na, ob = nb;
+      if (q + 1 < qe) {  // next pair's indices in flight during this pair's math
+        na = pair_a[q + 1];
+        nb = pair_b[q + 1];
+      }
+      const double* fa = J + oa * REC + RF;
+      const double* ha = J + oa * REC + RH;
+      const double* eb = J + ob * REC + RE;
+      const double* fb = J + ob * REC + RF;
       double g00 = ha[0] * eb[0] + ha[1] * eb[1] + ha[2] * eb[2];
       double g01 = ha[0] * eb[3] + ha[1] * eb[4] + ha[2] * eb[5];
       double g10 = ha[3] * eb[0] + ha[4] * eb[1] + ha[5] * eb[2];
@@ -353,10 +367,10 @@ struct SrTerm {
 
 __device__ __forceinline__ SrTerm sr_load(const SrEntry& en, const double* __restrict__ F, const double* __restrict__ E,
                                           const double* __restrict__ H, int r9, int cg) {
-  const double* fa = F + (int64_t)en.a * 18;
-  const double* ha = H + (int64_t)en.a * 6;
-  const double* eb = E + (int64_t)en.b * 6;
-  const double* fb = F + (int64_t)en.b * 18 + 3 * cg;
+  const double* fa = F + (int64_t)en.a * REC;
+  const double* ha = H + (int64_t)en.a * REC;
+  const double* eb = E + (int64_t)en.b * REC;
+  const double* fb = F + (int64_t)en.b * REC + 3 * cg;
   double g00 = ha[0] * eb[0] + ha[1] * eb[1] + ha[2] * eb[2];
   double g01 = ha[0] * eb[3] + ha[1] * eb[4] + ha[2] * eb[5];
   double g10 = ha[3] * eb[0] + ha[4] * eb[1] + ha[5] * eb[2];
@@ -519,13 +533,12 @@ k_schur_rows(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
 
 extern "C" int bamg_schur_numeric_rows(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
                                        const int32_t* pt_ptr, const int32_t* obs_cam_pm, const int32_t* obs_pt_pm,
-                                       const double* F, const double* E, const double* H, const double* A,
-                                       const int32_t* S_ptr, const int32_t* S_col, const int32_t* dpos,
-                                       const int32_t* up_off, const int32_t* up_tpos, int32_t nc, double* S,
-                                       void* stream) {
+                                       const double* J, const double* A, const int32_t* S_ptr, const int32_t* S_col,
+                                       const int32_t* dpos, const int32_t* up_off, const int32_t* up_tpos, int32_t nc,
+                                       double* S, void* stream) {
   cudaStream_t st = as_stream(stream);
   if (nc <= 0) return 0;
-  launch(k_schur_diag, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, F, E, H, A, dpos, nc, S);
+  launch(k_schur_diag, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, J, A, dpos, nc, S);
   const size_t budget = 200 * 1024;
   size_t fixed = sizeof(SrEntry) * SR_WARPS * SR_QCAP;
   int use_map = (nc <= 40000) ? 1 : 0;
@@ -541,25 +554,23 @@ extern "C" int bamg_schur_numeric_rows(bamg_ctx* ctx, const int32_t* cam_ptr, co
   unsigned* ctr = ctx->counters + BAMG_CTR_MISC;
   BAMG_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(unsigned), st));
   int blocks = bamg_num_sms() * (sm <= 100 * 1024 ? 2 : 1);
-  launch(k_schur_rows, blocks, SR_WARPS * 32, sm, st, cam_ptr, cm_list, pt_ptr, obs_cam_pm, obs_pt_pm, F, E, H,
-         S_ptr, S_col, dpos, up_tpos, up_off, nc, use_map, win_cap, ctr, S);
+  launch(k_schur_rows, blocks, SR_WARPS * 32, sm, st, cam_ptr, cm_list, pt_ptr, obs_cam_pm, obs_pt_pm, J + RF,
+         J + RE, J + RH, S_ptr, S_col, dpos, up_tpos, up_off, nc, use_map, win_cap, ctr, S);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
 
-extern "C" int bamg_schur_numeric(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
-                                  const double* F, const double* E, const double* H, const double* A,
-                                  const int32_t* dpos, int32_t nc, const int32_t* up_blk, const int32_t* up_tpos,
-                                  int32_t n_up, const int32_t* blk_pair_ptr, const int32_t* pair_a,
-                                  const int32_t* pair_b, double* S, void* stream) {
+extern "C" int bamg_schur_numeric(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const double* J,
+                                  const double* A, const int32_t* dpos, int32_t nc, const int32_t* up_blk,
+                                  const int32_t* up_tpos, int32_t n_up, const int32_t* blk_pair_ptr,
+                                  const int32_t* pair_a, const int32_t* pair_b, double* S, void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
-  if (nc)
-    launch(k_schur_diag, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, F, E, H, A, dpos, nc, S);
+  if (nc) launch(k_schur_diag, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, J, A, dpos, nc, S);
   if (n_up) {
     int64_t warps = ceil_div(n_up, OFF_GROUPS);
     launch(k_schur_offdiag, grid_for(warps * 32, 128, 8), 128, 0, st, up_blk, up_tpos, n_up, blk_pair_ptr, pair_a,
-                                                                  pair_b, F, E, H, S);
+           pair_b, J, S);
   }
   BAMG_LAUNCH_CHECK();
   return 0;

@@ -48,10 +48,158 @@ __global__ void k_xpby_dev(const double* __restrict__ z, const double* __restric
 }
 
 // ---------------------------------------------------------------------------
+// Chunked 16x16 SpMV for the coarse levels. Coarse rows are long (30-80 blocks)
+// and few (1-4 K), so a warp per row leaves the SMs latency-bound. Instead every
+// warp takes a chunk of <= CH consecutive blocks of ONE row and writes a 16-entry
+// partial; a second kernel sums a row's partials in chunk order (deterministic)
+// and applies the residual or the fused Chebyshev update.
+
+__device__ __forceinline__ double warp_blocks16(const int* __restrict__ col, const double* __restrict__ blocks,
+                                                const double* __restrict__ x, int b, int b1, int lane) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const int cp = 2 * (lane & 7);
+  for (; b + 1 < b1; b += 2) {
+    const double2* A0 = reinterpret_cast<const double2*>(blocks + (int64_t)b * 256) + lane;
+    const double2* A1 = reinterpret_cast<const double2*>(blocks + (int64_t)(b + 1) * 256) + lane;
+    double2 u0 = __ldg(A0), u1 = __ldg(A0 + 32), u2 = __ldg(A0 + 64), u3 = __ldg(A0 + 96);
+    double2 v0 = __ldg(A1), v1 = __ldg(A1 + 32), v2 = __ldg(A1 + 64), v3 = __ldg(A1 + 96);
+    double2 xa = __ldg(reinterpret_cast<const double2*>(x + (int64_t)col[b] * 16 + cp));
+    double2 xb = __ldg(reinterpret_cast<const double2*>(x + (int64_t)col[b + 1] * 16 + cp));
+    a0 = fma(u0.x, xa.x, fma(u0.y, xa.y, a0));
+    a1 = fma(u1.x, xa.x, fma(u1.y, xa.y, a1));
+    a2 = fma(u2.x, xa.x, fma(u2.y, xa.y, a2));
+    a3 = fma(u3.x, xa.x, fma(u3.y, xa.y, a3));
+    a0 = fma(v0.x, xb.x, fma(v0.y, xb.y, a0));
+    a1 = fma(v1.x, xb.x, fma(v1.y, xb.y, a1));
+    a2 = fma(v2.x, xb.x, fma(v2.y, xb.y, a2));
+    a3 = fma(v3.x, xb.x, fma(v3.y, xb.y, a3));
+  }
+  if (b < b1) {
+    const double2* A0 = reinterpret_cast<const double2*>(blocks + (int64_t)b * 256) + lane;
+    double2 u0 = __ldg(A0), u1 = __ldg(A0 + 32), u2 = __ldg(A0 + 64), u3 = __ldg(A0 + 96);
+    double2 xa = __ldg(reinterpret_cast<const double2*>(x + (int64_t)col[b] * 16 + cp));
+    a0 = fma(u0.x, xa.x, fma(u0.y, xa.y, a0));
+    a1 = fma(u1.x, xa.x, fma(u1.y, xa.y, a1));
+    a2 = fma(u2.x, xa.x, fma(u2.y, xa.y, a2));
+    a3 = fma(u3.x, xa.x, fma(u3.y, xa.y, a3));
+  }
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+    a0 += __shfl_xor_sync(FULL_MASK, a0, o);
+    a1 += __shfl_xor_sync(FULL_MASK, a1, o);
+    a2 += __shfl_xor_sync(FULL_MASK, a2, o);
+    a3 += __shfl_xor_sync(FULL_MASK, a3, o);
+  }
+  int src = 8 * (lane & 3);
+  double s0 = __shfl_sync(FULL_MASK, a0, src);
+  double s1 = __shfl_sync(FULL_MASK, a1, src);
+  double s2 = __shfl_sync(FULL_MASK, a2, src);
+  double s3 = __shfl_sync(FULL_MASK, a3, src);
+  int k = (lane >> 2) & 3;
+  return k == 0 ? s0 : (k == 1 ? s1 : (k == 2 ? s2 : s3));
+}
+
+__global__ void __launch_bounds__(128)
+k_spmv16_chunks(const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ blocks,
+                const double* __restrict__ x, const int* __restrict__ cbeg, const int* __restrict__ crow, int nch,
+                int CH, double* __restrict__ partial) {
+  int lane = threadIdx.x & 31;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int c = warp; c < nch; c += nwarps) {
+    int b0 = cbeg[c];
+    int b1 = min(b0 + CH, ptr[crow[c] + 1]);
+    double v = warp_blocks16(col, blocks, x, b0, b1, lane);
+    if (lane < 16) partial[(int64_t)c * 16 + lane] = v;
+  }
+}
+
+// Row finish: ax = sum of the row's partials (chunk order); then
+//   mode 0: r = b - ax
+//   mode 1: fused Chebyshev step (as k_cheb_step): r = b - ax; z = D^-1 r;
+//           d = divide ? z / c2 : c1 d + c2 z; x_out = x_in + d
+__global__ void __launch_bounds__(128)
+k_rows16_finish(const int* __restrict__ cptr, const double* __restrict__ partial, int nbr, int mode,
+                const double* __restrict__ b, const double* __restrict__ Dinv, double* __restrict__ d,
+                const double* __restrict__ x_in, double* __restrict__ out, double c1, double c2, int divide) {
+  int lane = threadIdx.x & 31;
+  int half = lane >> 4, r = lane & 15;
+  int row0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2;
+  int stride = ((gridDim.x * blockDim.x) >> 5) * 2;
+  for (int base = row0; base < nbr; base += stride) {
+    int row = base + half;
+    bool ok = row < nbr;
+    double ax = 0.0;
+    if (ok)
+      for (int c = cptr[row]; c < cptr[row + 1]; ++c) ax += partial[(int64_t)c * 16 + r];
+    int64_t e = (int64_t)row * 16 + r;
+    double rr = ok ? b[e] - ax : 0.0;
+    if (mode == 0) {
+      if (ok) out[e] = rr;
+      continue;
+    }
+    double z = 0.0;
+    const double* Di = Dinv + ((int64_t)(ok ? row : 0) * 16 + r) * 16;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      double rc = __shfl_sync(FULL_MASK, rr, c, 16);
+      if (ok) z = fma(Di[c], rc, z);
+    }
+    if (ok) {
+      double dn = divide ? z / c2 : c1 * d[e] + c2 * z;
+      d[e] = dn;
+      out[e] = x_in[e] + dn;
+    }
+  }
+}
+
+// warp per aggregate restriction: bc_a = sum_{i in a} P_i^T r_i
+__global__ void __launch_bounds__(128)
+k_restrict_warp(const int* __restrict__ agg_ptr, const int* __restrict__ members, const double* __restrict__ P,
+                const double* __restrict__ r, int nagg, int bs, double* __restrict__ bc) {
+  int lane = threadIdx.x & 31;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  int c = lane & 15, h = lane >> 4;
+  for (int a = warp; a < nagg; a += nwarps) {
+    int q0 = agg_ptr[a], m = agg_ptr[a + 1] - q0;
+    double s = 0.0;
+    for (int t = h; t < m * bs; t += 2) {
+      int q = t / bs, k = t - q * bs;
+      int64_t node = members[q0 + q];
+      s = fma(P[(node * bs + k) * 16 + c], r[node * bs + k], s);
+    }
+    s += __shfl_down_sync(FULL_MASK, s, 16);
+    if (lane < 16) bc[(int64_t)a * 16 + c] = s;
+  }
+}
+
+// chunk metadata: counts per row, then fill
+__global__ void k_chunk_counts(const int* __restrict__ ptr, int nbr, int CH, int* __restrict__ cnt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nbr; i += gridDim.x * blockDim.x) {
+    int len = ptr[i + 1] - ptr[i];
+    cnt[i] = (len + CH - 1) / CH;
+  }
+}
+
+__global__ void k_chunk_fill(const int* __restrict__ ptr, const int* __restrict__ cptr, int nbr, int CH,
+                             int* __restrict__ cbeg, int* __restrict__ crow) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nbr; i += gridDim.x * blockDim.x)
+    for (int c = cptr[i]; c < cptr[i + 1]; ++c) {
+      cbeg[c] = ptr[i] + (c - cptr[i]) * CH;
+      crow[c] = i;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // MG plan
 
 struct MgLevelPlan {
   int bs = 0, nbr = 0, n = 0;
+  // chunked 16x16 SpMV (coarse levels)
+  int CH = 0, nch = 0;
+  int *cptr = nullptr, *cbeg = nullptr, *crow = nullptr;
+  double* partial = nullptr;
   const int* ptr = nullptr;
   const int* col = nullptr;
   const double* blocks = nullptr;
@@ -80,6 +228,7 @@ struct bamg_mg {
   cudaGraph_t graph = nullptr;
   bool dirty = true;
   bool use_graph = false;
+  long long graph_kernels = 0;
 };
 
 extern "C" bamg_mg* bamg_mg_create(int32_t n_levels) {
@@ -140,11 +289,81 @@ extern "C" int bamg_mg_set_level(bamg_mg* m, int32_t level, int32_t bs, int32_t 
   return 0;
 }
 
+int scan_exclusive_int(const int* in, int* out, int64_t n, int* total, cudaStream_t st);
+
 static int mg_alloc(bamg_mg* m, cudaStream_t st) {
   mg_free_work(m);
+  // chunk plan of the 16x16 smoothing levels: CH blocks per warp, enough chunks
+  // to cover the SMs several times over
+  std::vector<int> nnzb(m->lv.size(), 0);
+  for (size_t l = 0; l < m->lv.size(); ++l) {
+    MgLevelPlan& L = m->lv[l];
+    L.CH = 0;
+    L.nch = 0;
+    if (L.inv || L.bs != 16 || !L.ptr) continue;
+    BAMG_CUDA_CHECK(cudaMemcpyAsync(&nnzb[l], L.ptr + L.nbr, sizeof(int), cudaMemcpyDeviceToHost, st));
+  }
+  BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
   size_t total = 2 * (size_t)m->lv[0].n;
-  for (auto& L : m->lv) total += 5 * (size_t)(L.n > 0 ? L.n : 1);
+  size_t itotal = 0;
+  for (size_t l = 0; l < m->lv.size(); ++l) {
+    MgLevelPlan& L = m->lv[l];
+    total += 5 * (size_t)(L.n > 0 ? L.n : 1);
+    if (L.inv || L.bs != 16 || !L.ptr) continue;
+    int CH = nnzb[l] / 8192;
+    L.CH = CH < 1 ? 1 : (CH > 8 ? 8 : CH);
+    itotal += (size_t)L.nbr + 1;
+  }
+  // chunk counts need a scan before the arrays can be sized: count on the device
+  int* counts = nullptr;
+  if (itotal) BAMG_CUDA_CHECK(cudaMallocAsync(&counts, sizeof(int) * itotal, st));
+  {
+    size_t off = 0;
+    std::vector<int> nch(m->lv.size(), 0);
+    for (size_t l = 0; l < m->lv.size(); ++l) {
+      MgLevelPlan& L = m->lv[l];
+      if (!L.CH) continue;
+      launch(k_chunk_counts, grid_for(L.nbr, 256), 256, 0, st, L.ptr, L.nbr, L.CH, counts + off);
+      int rc = scan_exclusive_int(counts + off, counts + off, L.nbr + 1, nullptr, st);
+      if (rc) return rc;
+      BAMG_CUDA_CHECK(cudaMemcpyAsync(&nch[l], counts + off + L.nbr, sizeof(int), cudaMemcpyDeviceToHost, st));
+      off += (size_t)L.nbr + 1;
+    }
+    BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (size_t l = 0; l < m->lv.size(); ++l) {
+      m->lv[l].nch = nch[l];
+      if (m->lv[l].CH) {
+        itotal += 2 * (size_t)nch[l];
+        total += 16 * (size_t)nch[l];
+      }
+    }
+  }
+  total += (itotal + 1) / 2 + 1;  // ints live at the end of the arena
   BAMG_CUDA_CHECK(cudaMallocAsync(&m->arena, sizeof(double) * total, st));
+  {
+    double* pd = m->arena + 2 * (size_t)m->lv[0].n;
+    for (auto& L : m->lv) pd += 5 * (size_t)(L.n > 0 ? L.n : 1);
+    for (auto& L : m->lv)
+      if (L.CH) {
+        L.partial = pd;
+        pd += 16 * (size_t)L.nch;
+      }
+    int* pi = reinterpret_cast<int*>(pd);
+    size_t off = 0;
+    for (auto& L : m->lv) {
+      if (!L.CH) continue;
+      L.cptr = pi;
+      pi += L.nbr + 1;
+      BAMG_CUDA_CHECK(cudaMemcpyAsync(L.cptr, counts + off, sizeof(int) * (L.nbr + 1), cudaMemcpyDeviceToDevice, st));
+      off += (size_t)L.nbr + 1;
+      L.cbeg = pi;
+      pi += L.nch;
+      L.crow = pi;
+      pi += L.nch;
+      launch(k_chunk_fill, grid_for(L.nbr, 256), 256, 0, st, L.ptr, L.cptr, L.nbr, L.CH, L.cbeg, L.crow);
+    }
+  }
+  if (counts) BAMG_CUDA_CHECK(cudaFreeAsync(counts, st));
   m->arena_stream = st;
   double* p = m->arena;
   m->in = p;
@@ -171,8 +390,21 @@ static void cheb_launch(const MgLevelPlan& L, const double* x_in, double* x_out,
          L.d, x_out, L.nbr, c1, c2, divide);
 }
 
+static void chunk_spmv(const MgLevelPlan& L, const double* x, cudaStream_t st) {
+  launch(k_spmv16_chunks, grid_for((int64_t)L.nch * 32, 128, 16), 128, 0, st, L.ptr, L.col, L.blocks, x, L.cbeg,
+         L.crow, L.nch, L.CH, L.partial);
+}
+
+static int finish_grid(int nbr) { return grid_for((int64_t)((nbr + 1) / 2) * 32, 128, 16); }
+
 static void cheb(const MgLevelPlan& L, const double* x_in, double* x_out, double c1, double c2, int divide,
                  bool with_A, cudaStream_t st) {
+  if (with_A && L.CH) {
+    chunk_spmv(L, x_in, st);
+    launch(k_rows16_finish, finish_grid(L.nbr), 128, 0, st, L.cptr, L.partial, L.nbr, 1, L.b, L.Dinv, L.d, x_in,
+           x_out, c1, c2, divide);
+    return;
+  }
   switch (L.bs) {
     case 9: cheb_launch<9>(L, x_in, x_out, c1, c2, divide, with_A, st); break;
     case 16: cheb_launch<16>(L, x_in, x_out, c1, c2, divide, with_A, st); break;
@@ -207,6 +439,12 @@ static double* smooth(MgLevelPlan& L, double* x, cudaStream_t st) {
 }
 
 static void residual(const MgLevelPlan& L, const double* x, cudaStream_t st) {
+  if (L.CH) {
+    chunk_spmv(L, x, st);
+    launch(k_rows16_finish, finish_grid(L.nbr), 128, 0, st, L.cptr, L.partial, L.nbr, 0, L.b, nullptr, nullptr,
+           nullptr, L.r, 0.0, 0.0, 0);
+    return;
+  }
   int g = spmv_grid(L.nbr);
   switch (L.bs) {
     case 9: launch(k_bsr_residual<9>, g, 128, 0, st, L.ptr, L.col, L.blocks, x, L.b, L.r, L.nbr); break;
@@ -225,8 +463,8 @@ static double* vcycle(bamg_mg* m, size_t l, cudaStream_t st) {
   double* x = smooth(L, nullptr, st);
   residual(L, x, st);
   MgLevelPlan& C = m->lv[l + 1];
-  launch(k_restrict, grid_for((int64_t)L.n_agg * 16, 256), 256, 0, st, L.agg_ptr, L.members, L.P, L.r, L.n_agg,
-         L.bs, C.b);
+  launch(k_restrict_warp, grid_for((int64_t)L.n_agg * 32, 128, 16), 128, 0, st, L.agg_ptr, L.members, L.P, L.r,
+         L.n_agg, L.bs, C.b);
   double* xc = vcycle(m, l + 1, st);
   launch(k_prolong, grid_for((int64_t)L.n, 256), 256, 0, st, L.agg, L.P, xc, L.nbr, L.bs, x, 1);
   return smooth(L, x, st);
@@ -249,6 +487,7 @@ static int mg_prepare(bamg_mg* m, cudaStream_t st) {
   BAMG_CUDA_CHECK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   long long before = g_bamg_launches.load();
   rc = mg_record(m, cs);
+  m->graph_kernels = g_bamg_launches.load() - before;
   g_bamg_launches.store(before);  // capture is not execution
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(cs, &g);
@@ -261,15 +500,6 @@ static int mg_prepare(bamg_mg* m, cudaStream_t st) {
   return 0;
 }
 
-static long long mg_kernel_count(bamg_mg* m) {
-  long long c = 0;
-  for (size_t l = 0; l < m->lv.size(); ++l) {
-    if (m->lv[l].inv) { c += 1; break; }
-    c += 2 * m->lv[l].iterations + 3;
-  }
-  return c;
-}
-
 // z = M r, one V-cycle (r, z: level-0 device vectors of length n0).
 static int mg_apply_dev(bamg_mg* m, const double* r, double* z, cudaStream_t st) {
   int rc = mg_prepare(m, st);
@@ -278,7 +508,7 @@ static int mg_apply_dev(bamg_mg* m, const double* r, double* z, cudaStream_t st)
   if (r != m->in) BAMG_CUDA_CHECK(cudaMemcpyAsync(m->in, r, bytes, cudaMemcpyDeviceToDevice, st));
   if (m->use_graph) {
     BAMG_CUDA_CHECK(cudaGraphLaunch(m->exec, st));
-    g_bamg_launches.fetch_add(mg_kernel_count(m));
+    g_bamg_launches.fetch_add(m->graph_kernels);
   } else {
     rc = mg_record(m, st);
     if (rc) return rc;

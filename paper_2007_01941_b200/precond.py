@@ -31,7 +31,8 @@ def _schur_diagonal_blocks(sys: SchurSystem):
     nc = sys.n_cameras
     out = D.empty(nc, CAMERA_SIZE, CAMERA_SIZE)
     dpos = torch.arange(nc, device=D.dev(), dtype=torch.int32)
-    D.call("bamg_schur_numeric", st.cam_ptr, st.cm_list, sys._jac._F, sys._jac._E, sys._H, sys.A.blocks, dpos, nc,
+    sys._own_H()
+    D.call("bamg_schur_numeric", st.cam_ptr, st.cm_list, sys._jac._J, sys.A.blocks, dpos, nc,
            None, None, 0, None, None, None, out)
     return out
 

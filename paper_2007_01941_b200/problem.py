@@ -285,31 +285,36 @@ class BundleProblem:
 class JacobianBlocks:
     """Loss-weighted residuals and Jacobian blocks (problem.py:237-269).
 
-    Device storage is point-major; ``camera``/``point``/``residual``/``weight``
-    give caller-order tensors (k,2,9)/(k,2,3)/(k,2)/(k,). The per-camera and
-    per-point reductions (J^T J blocks, gradient, diagonal) are computed once by
-    one deterministic kernel pass and shared by `gradient`, `normal_diagonal`,
+    Device storage is point-major, one 256-byte record per observation
+    ``_J[o] = [F (2x9) | E (2x3) | H (2x3) | r (2)]`` (H = E C^-1 is written by
+    `build_system`); ``camera``/``point``/``residual``/``weight`` give
+    caller-order tensors (k,2,9)/(k,2,3)/(k,2)/(k,). The per-camera and per-point
+    reductions (J^T J blocks, gradient, diagonal) are computed once by one
+    deterministic kernel pass and shared by `gradient`, `normal_diagonal`,
     `Damping.from_jacobian` and `build_system`.
     """
 
-    def __init__(self, st: ObsStructure, F, E, res, w, n_cameras, n_points, cam_index, pt_index):
+    REC = 32
+
+    def __init__(self, st: ObsStructure, J, w, n_cameras, n_points, cam_index, pt_index):
         self._st = st
-        self._F, self._E, self._res, self._w = F, E, res, w
+        self._J, self._w = J, w
         self.n_cameras, self.n_points = n_cameras, n_points
         self.cam_index, self.pt_index = cam_index, pt_index
         self._normal = None
+        self._h_owner = None  # SchurSystem whose C^-1 produced the H slots of _J
 
     @property
     def camera(self):
-        return self._st.to_input_order(self._F).reshape(-1, 2, CAMERA_SIZE)
+        return self._st.to_input_order(self._J[:, 0:18].contiguous()).reshape(-1, 2, CAMERA_SIZE)
 
     @property
     def point(self):
-        return self._st.to_input_order(self._E).reshape(-1, 2, POINT_SIZE)
+        return self._st.to_input_order(self._J[:, 18:24].contiguous()).reshape(-1, 2, POINT_SIZE)
 
     @property
     def residual(self):
-        return self._st.to_input_order(self._res).reshape(-1, 2)
+        return self._st.to_input_order(self._J[:, 30:32].contiguous()).reshape(-1, 2)
 
     @property
     def weight(self):
@@ -324,8 +329,7 @@ class JacobianBlocks:
             C = D.empty(npt, 3, 3)
             gp = D.empty(npt, 3)
             st = self._st
-            D.call("bamg_normal_blocks", st.cam_ptr, st.cm_list, st.pt_ptr, self._F, self._E, self._res,
-                   nc, npt, A, gc, C, gp)
+            D.call("bamg_normal_blocks", st.cam_ptr, st.cm_list, st.pt_ptr, self._J, nc, npt, A, gc, C, gp)
             self._normal = (A, gc, C, gp)
         return self._normal
 
@@ -360,12 +364,12 @@ def evaluate(problem: BundleProblem, camera_params=None, points=None, with_jacob
     nb = D.empty(1, dtype=torch.int32)
     behind = D.empty(max(k, 1), dtype=torch.uint8)
     if with_jacobian:
-        F, E, res, w = D.empty(k, 18), D.empty(k, 6), D.empty(k, 2), D.empty(k)
+        J, w = D.empty(max(k, 1), JacobianBlocks.REC)[:k], D.empty(k)
     else:
-        F = E = res = w = None
+        J = w = None
     if k:
         D.call("bamg_evaluate", cams, pts, st.obs_cam_pm, st.obs_pt_pm, st.pix_pm, k, huber,
-               1 if with_jacobian else 0, F, E, res, w, behind, obj, nb)
+               1 if with_jacobian else 0, J, w, behind, obj, nb)
         n_behind = int(nb.item())
     else:
         obj.zero_()
@@ -377,8 +381,7 @@ def evaluate(problem: BundleProblem, camera_params=None, points=None, with_jacob
     objective = float(obj.item())
     if not with_jacobian:
         return objective, None
-    return objective, JacobianBlocks(st, F, E, res, w, problem.n_cameras, problem.n_points,
-                                     problem._ci, problem._pi)
+    return objective, JacobianBlocks(st, J, w, problem.n_cameras, problem.n_points, problem._ci, problem._pi)
 
 
 def gauge_nullspace(problem: BundleProblem, camera_params=None) -> DenseTall:

@@ -10,6 +10,8 @@ the reference-shaped BSR view on demand.
 
 from __future__ import annotations
 
+import weakref
+
 import torch
 
 from . import _device as D
@@ -46,7 +48,7 @@ class Damping:
 class SchurSystem:
     """Block factors after point elimination (schur.py:58-96)."""
 
-    def __init__(self, A, C, rhs_cam, grad_pt, jac, H, Cb, mode="implicit"):
+    def __init__(self, A, C, rhs_cam, grad_pt, jac, Cb, mode="implicit"):
         self.A = A
         self.C = C
         self.rhs_cam = rhs_cam
@@ -54,7 +56,6 @@ class SchurSystem:
         self.mode = mode
         self.S_explicit = None
         self._jac = jac
-        self._H = H
         self._Cb = Cb
         self._W = None
         self._qo = None
@@ -75,7 +76,7 @@ class SchurSystem:
             k = st.k
             blocks = D.empty(k, CAMERA_SIZE, POINT_SIZE)
             if k:
-                D.call("bamg_materialize_W", st.cm_list, self._jac._F, self._jac._E, k, blocks)
+                D.call("bamg_materialize_W", st.cm_list, self._jac._J, k, blocks)
             cols = st.obs_pt_pm[st.cm_list.to(torch.int64)]
             self._W = BlockSparseMatrix(self.n_cameras, self.n_points, CAMERA_SIZE, POINT_SIZE, st.cam_ptr, cols,
                                         blocks)
@@ -88,14 +89,25 @@ class SchurSystem:
         if self._qo is None:
             self._qo = D.empty(max(st.k, 1), 2)
         y = D.empty(self.n_cameras * CAMERA_SIZE)
-        D.call("bamg_implicit_matvec", st.cam_ptr, st.cm_list, st.pt_ptr, st.obs_cam_pm, self._jac._F,
-               self._jac._E, self.A.blocks, self.C._inv, x, self.n_cameras, self.n_points, self._qo, y)
+        D.call("bamg_implicit_matvec", st.cam_ptr, st.cm_list, st.pt_ptr, st.obs_cam_pm, self._jac._J,
+               self.A.blocks, self.C._inv, x, self.n_cameras, self.n_points, self._qo, y)
         return y
 
     def matvec(self, x):
         if self.mode == "explicit":
             return self.ensure_explicit().matvec(x)
         return self.implicit_matvec(x)
+
+    def _own_H(self):
+        """Make the Jacobian's H slots (E C^-1) those of THIS system: another system
+        built from the same Jacobian (e.g. a rejected LM trial re-damped) overwrites them."""
+        owner = self._jac._h_owner() if self._jac._h_owner is not None else None
+        if owner is not self:
+            st = self._jac._st
+            if self._qo is None:
+                self._qo = D.empty(max(st.k, 1), 2)
+            D.call("bamg_obs_H", st.obs_pt_pm, self.C._inv, self._Cb, st.k, self._jac._J, self._qo)
+            self._jac._h_owner = weakref.ref(self)
 
     def ensure_explicit(self) -> BlockSparseMatrix:
         if self.S_explicit is None:
@@ -112,20 +124,20 @@ def build_system(jac: JacobianBlocks, damping: Damping) -> SchurSystem:
     C = D.empty(npt, 3, 3)
     Cinv = D.empty(npt, 3, 3)
     Cb = D.empty(npt, 3)
-    H = D.empty(max(st.k, 1), 6)
     qo = D.empty(max(st.k, 1), 2)
     rhs = D.empty(nc * CAMERA_SIZE)
     bad = D.empty(1, dtype=torch.int32)
-    D.call("bamg_build_system", st.cam_ptr, st.cm_list, st.pt_ptr, jac._F, jac._E, A_raw, C_raw, gc, gp,
-           damping.cam_diag, damping.pt_diag, nc, npt, A, C, Cinv, Cb, H, qo, rhs, bad)
+    D.call("bamg_build_system", st.cam_ptr, st.cm_list, st.obs_pt_pm, jac._J, st.k, A_raw, C_raw, gc, gp,
+           damping.cam_diag, damping.pt_diag, nc, npt, A, C, Cinv, Cb, qo, rhs, bad)
     b = int(bad.item())
     if b != 0x7FFFFFFF:
         raise IndefiniteBlockError(b)
     grad_pt = D.empty(npt * POINT_SIZE)
     D.call("bamg_negate", gp, grad_pt, npt * POINT_SIZE)
     Cm = BlockDiagMatrix(C, _inv=Cinv)
-    s = SchurSystem(BlockDiagMatrix(A), Cm, rhs, grad_pt, jac, H, Cb)
+    s = SchurSystem(BlockDiagMatrix(A), Cm, rhs, grad_pt, jac, Cb)
     s._qo = qo
+    jac._h_owner = weakref.ref(s)  # weak: no jac <-> system reference cycle
     return s
 
 
@@ -140,14 +152,14 @@ def schur_explicit(sys: SchurSystem, variant: str = "pairs") -> BlockSparseMatri
     S_ptr, S_col, nnz, _ = st.covis
     blocks = D.empty(nnz, CAMERA_SIZE, CAMERA_SIZE)
     J = sys._jac
+    sys._own_H()
     if variant == "rows":
         sym = st.symbolic
-        D.call("bamg_schur_numeric_rows", st.cam_ptr, st.cm_list, st.pt_ptr, st.obs_cam_pm, st.obs_pt_pm, J._F,
-               J._E, sys._H, sys.A.blocks, S_ptr, S_col, sym["dpos"], sym["up_off"], sym["up_tpos"], sys.n_cameras,
-               blocks)
+        D.call("bamg_schur_numeric_rows", st.cam_ptr, st.cm_list, st.pt_ptr, st.obs_cam_pm, st.obs_pt_pm, J._J,
+               sys.A.blocks, S_ptr, S_col, sym["dpos"], sym["up_off"], sym["up_tpos"], sys.n_cameras, blocks)
     else:
         sym = st.pair_lists
-        D.call("bamg_schur_numeric", st.cam_ptr, st.cm_list, J._F, J._E, sys._H, sys.A.blocks, sym["dpos"],
+        D.call("bamg_schur_numeric", st.cam_ptr, st.cm_list, J._J, sys.A.blocks, sym["dpos"],
                sys.n_cameras, sym["up_blk"], sym["up_tpos"], sym["n_up"], sym["blk_ptr"], sym["pair_a"],
                sym["pair_b"], blocks)
     return BlockSparseMatrix(sys.n_cameras, sys.n_cameras, CAMERA_SIZE, CAMERA_SIZE, S_ptr, S_col, blocks,
@@ -174,7 +186,7 @@ def back_substitute(sys: SchurSystem, delta_cam):
     st = sys._jac._st
     dc = D.f64(delta_cam).reshape(-1)
     dp = D.empty(sys.n_points * POINT_SIZE)
-    D.call("bamg_back_substitute", st.pt_ptr, st.obs_cam_pm, sys._jac._F, sys._jac._E, sys.C._inv, sys.grad_pt,
+    D.call("bamg_back_substitute", st.pt_ptr, st.obs_cam_pm, sys._jac._J, sys.C._inv, sys.grad_pt,
            dc, sys.n_points, dp)
     return dp
 
