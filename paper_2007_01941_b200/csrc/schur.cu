@@ -168,10 +168,10 @@ __global__ void k_up_keys(const int* __restrict__ up_blk, const int* __restrict_
   }
 }
 
-__global__ void k_row_keys(const uint32_t* __restrict__ perm, const int* __restrict__ up_row, int n,
-                           uint32_t* __restrict__ key) {
+__global__ void k_band_keys(const uint32_t* __restrict__ perm, const int* __restrict__ up_row, int n, int band,
+                            uint32_t* __restrict__ key) {
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x)
-    key[u] = (uint32_t)up_row[perm[u]];
+    key[u] = (uint32_t)(up_row[perm[u]] / band);
 }
 
 __global__ void k_permute3(const uint32_t* __restrict__ perm, int n, int* __restrict__ a, int* __restrict__ b,
@@ -204,6 +204,16 @@ extern "C" int bamg_schur_order_upper(bamg_ctx* ctx, int32_t* up_blk, int32_t* u
   launch(k_up_keys, grid_for(n_up, 256), 256, 0, st, up_blk, blk_pair_ptr, n_up, ck, io);
   int rc = radix_sort_pairs(ck, io, sk, pv, n_up, 24, st);
   if (rc) return rc;
+  // optional row bands (BAMG_SCHUR_BAND rows): blocks of nearby camera rows run
+  // together so their observation records stay in L2; count order inside a band
+  int band = 0;
+  if (const char* e = getenv("BAMG_SCHUR_BAND")) band = atoi(e);
+  if (band > 0) {
+    launch(k_band_keys, grid_for(n_up, 256), 256, 0, st, pv, up_row, n_up, band, ck);
+    rc = radix_sort_pairs(ck, pv, sk, io, n_up, 31, st);
+    if (rc) return rc;
+    std::swap(pv, io);
+  }
   launch(k_permute3, grid_for(n_up, 256), 256, 0, st, pv, n_up, up_blk, up_row, up_tpos, tmp);
   launch(k_copy_i32, grid_for(n_up, 256), 256, 0, st, tmp, up_blk, n_up);
   launch(k_copy_i32, grid_for(n_up, 256), 256, 0, st, tmp + n_up, up_row, n_up);

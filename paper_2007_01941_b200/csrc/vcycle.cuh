@@ -153,10 +153,13 @@ k_rows16_finish(const int* __restrict__ cptr, const double* __restrict__ partial
   }
 }
 
-// warp per aggregate restriction: bc_a = sum_{i in a} P_i^T r_i
+// warp per aggregate restriction: bc_a = sum_{i in a} P_i^T r_i. The member ids
+// are loaded once (one per lane) and broadcast, so the P / r loads of all members
+// are independent; lane (c, h) accumulates column c over rows k = h (mod 2).
+template <int BS>
 __global__ void __launch_bounds__(128)
 k_restrict_warp(const int* __restrict__ agg_ptr, const int* __restrict__ members, const double* __restrict__ P,
-                const double* __restrict__ r, int nagg, int bs, double* __restrict__ bc) {
+                const double* __restrict__ r, int nagg, double* __restrict__ bc) {
   int lane = threadIdx.x & 31;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -164,10 +167,18 @@ k_restrict_warp(const int* __restrict__ agg_ptr, const int* __restrict__ members
   for (int a = warp; a < nagg; a += nwarps) {
     int q0 = agg_ptr[a], m = agg_ptr[a + 1] - q0;
     double s = 0.0;
-    for (int t = h; t < m * bs; t += 2) {
-      int q = t / bs, k = t - q * bs;
-      int64_t node = members[q0 + q];
-      s = fma(P[(node * bs + k) * 16 + c], r[node * bs + k], s);
+    for (int qb = 0; qb < m; qb += 32) {
+      int mine = (qb + lane < m) ? members[q0 + qb + lane] : 0;
+      int mm = min(32, m - qb);
+#pragma unroll 4
+      for (int q = 0; q < mm; ++q) {
+        int64_t node = __shfl_sync(FULL_MASK, mine, q);
+        const double* pr = P + node * BS * 16 + c;
+        const double* rr = r + node * BS;
+#pragma unroll
+        for (int k = 0; k < BS; k += 2)
+          if (k + h < BS) s = fma(pr[(k + h) * 16], rr[k + h], s);
+      }
     }
     s += __shfl_down_sync(FULL_MASK, s, 16);
     if (lane < 16) bc[(int64_t)a * 16 + c] = s;
@@ -463,8 +474,12 @@ static double* vcycle(bamg_mg* m, size_t l, cudaStream_t st) {
   double* x = smooth(L, nullptr, st);
   residual(L, x, st);
   MgLevelPlan& C = m->lv[l + 1];
-  launch(k_restrict_warp, grid_for((int64_t)L.n_agg * 32, 128, 16), 128, 0, st, L.agg_ptr, L.members, L.P, L.r,
-         L.n_agg, L.bs, C.b);
+  if (L.bs == 9)
+    launch(k_restrict_warp<9>, grid_for((int64_t)L.n_agg * 32, 128, 16), 128, 0, st, L.agg_ptr, L.members, L.P, L.r,
+           L.n_agg, C.b);
+  else
+    launch(k_restrict_warp<16>, grid_for((int64_t)L.n_agg * 32, 128, 16), 128, 0, st, L.agg_ptr, L.members, L.P,
+           L.r, L.n_agg, C.b);
   double* xc = vcycle(m, l + 1, st);
   launch(k_prolong, grid_for((int64_t)L.n, 256), 256, 0, st, L.agg, L.P, xc, L.nbr, L.bs, x, 1);
   return smooth(L, x, st);
