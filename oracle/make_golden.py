@@ -185,6 +185,24 @@ def main():
                      max_coarse=40, sample=(4 if nc > 12 else None))
         print(f"small_{seed} done", flush=True)
 
+    # robust loss (problem.py:179-196): large pixel noise puts many residuals in
+    # the Huber region
+    sc = scenes.random_problem(1005, n_cameras=12, n_points=60, pixel_noise=3.0)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        prob = bamg.BundleProblem(sc.camera_params, sc.points, sc.cam_index, sc.pt_index, sc.pixels,
+                                  loss="huber")
+    dump_problem(bamg, prob, "huber_1005", store_inputs=True, max_coarse=40,
+                 extra={"loss": np.array("huber")})
+    print("huber_1005 done", flush=True)
+
+    # dense covisibility with few points: choose_mode picks the implicit operator
+    # (schur.py:162-168), so the level-0 smoother runs on A x - W C^-1 W^T x
+    sc = scenes.random_problem(1006, n_cameras=50, n_points=15)
+    prob = problem_of(bamg, sc)
+    dump_problem(bamg, prob, "implicit_1006", store_inputs=True, max_coarse=40)
+    print("implicit_1006 done", flush=True)
+
     # unit known-answer cases (reference tests' hand cases, re-derived by running
     # the reference on the same small inputs)
     from bamg import multigrid as mg

@@ -296,13 +296,38 @@ class JacobianBlocks:
 
     REC = 32
 
-    def __init__(self, st: ObsStructure, J, w, n_cameras, n_points, cam_index, pt_index):
+    def __init__(self, camera, point, residual, weight, cam_index, pt_index, n_cameras, n_points):
+        """Reference constructor (problem.py:237-253): caller-order blocks, e.g. a
+        fabricated Jacobian; packed here into the device record layout."""
+        ci = torch.as_tensor(cam_index, device=D.dev()).to(torch.int64).reshape(-1)
+        pi = torch.as_tensor(pt_index, device=D.dev()).to(torch.int64).reshape(-1)
+        k = ci.numel()
+        st = ObsStructure(ci.to(torch.int32), pi.to(torch.int32), int(n_cameras), int(n_points), D.zeros(k, 2))
+        J = D.zeros(max(k, 1), self.REC)[:k]
+        if k:
+            for a, lo, hi in ((camera, 0, 18), (point, 18, 24), (residual, 30, 32)):
+                src = D.f64(a).reshape(k, hi - lo)
+                tmp = D.empty(k, hi - lo)
+                D.call("bamg_gather_rows_f64", src, st.pm_perm, k, hi - lo, tmp)
+                J[:, lo:hi] = tmp
+        w = D.empty(k)
+        if k:
+            D.call("bamg_gather_rows_f64", D.f64(weight).reshape(k, 1), st.pm_perm, k, 1, w.reshape(k, 1))
+        self._init(st, J, w, int(n_cameras), int(n_points), ci, pi)
+
+    @classmethod
+    def _from_records(cls, st, J, w, n_cameras, n_points, cam_index, pt_index):
+        obj = cls.__new__(cls)
+        obj._init(st, J, w, n_cameras, n_points, cam_index, pt_index)
+        return obj
+
+    def _init(self, st: ObsStructure, J, w, n_cameras, n_points, cam_index, pt_index):
         self._st = st
         self._J, self._w = J, w
         self.n_cameras, self.n_points = n_cameras, n_points
         self.cam_index, self.pt_index = cam_index, pt_index
         self._normal = None
-        self._h_owner = None  # SchurSystem whose C^-1 produced the H slots of _J
+        self._h_owner = None  # weakref to the SchurSystem whose C^-1 produced the H slots
 
     @property
     def camera(self):
@@ -381,7 +406,8 @@ def evaluate(problem: BundleProblem, camera_params=None, points=None, with_jacob
     objective = float(obj.item())
     if not with_jacobian:
         return objective, None
-    return objective, JacobianBlocks(st, J, w, problem.n_cameras, problem.n_points, problem._ci, problem._pi)
+    return objective, JacobianBlocks._from_records(st, J, w, problem.n_cameras, problem.n_points, problem._ci,
+                                                   problem._pi)
 
 
 def gauge_nullspace(problem: BundleProblem, camera_params=None) -> DenseTall:
