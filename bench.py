@@ -37,6 +37,28 @@ CFG = dict(preconditioner="multigrid", tau=1e-30, max_iterations=10, function_to
 CPU_SAMPLE_CLUSTERS = 2  # bounded CPU sample of config 4: 2 of 40 clusters
 
 
+def max_over_ranks(value: float, world: int) -> float:
+    """Max of a per-rank timing over the process group (NCCL on GPUs, gloo on CPU)."""
+    if world <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def workload_config(args, world):
+    """The `config` object shared by both arms (same workload, metric, unit)."""
+    return {"workload": f"config {args.config} (SURVEY App. C generator, seed 0): one LM linear solve = evaluate +"
+                        " damping + A/C/rhs + explicit S + MG setup + PCG(V-cycle) to rel-res 1e-6 +"
+                        " back-substitution, at the initial point, radius 1e4",
+            "l2": "inputs larger than L2 (config 4: S alone is 1.4 GB, observation records 6.4 GB)",
+            "parallelism": f"replicas x{world}"}
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -55,9 +77,11 @@ def scene_for(config: int, fraction_clusters: int | None = None):
         sc = scenes.config(config)
     log(f"[bench] generated config {config} ({sc.n_cameras} cams, {sc.n_points} pts, {sc.n_observations} obs) "
         f"in {time.time() - t0:.1f}s")
-    try:
-        np.savez(cache, name=sc.name, cams=sc.camera_params, pts=sc.points, ci=sc.cam_index, pi=sc.pt_index,
+    try:  # atomic publish: concurrent ranks may generate the same scene
+        tmp = f"{cache}.{os.getpid()}.npz"
+        np.savez(tmp, name=sc.name, cams=sc.camera_params, pts=sc.points, ci=sc.cam_index, pi=sc.pt_index,
                  pix=sc.pixels)
+        os.replace(tmp, cache)
     except OSError:
         pass
     return sc
@@ -168,10 +192,7 @@ def gpu_arm(args, rank, world):
         launches_timed = _lib.lib().bamg_launch_count() - lc0
     ms = ev0.elapsed_time(ev1) / args.steps
     setup_s, solve_s = out[4], out[5]
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, world)
 
     # kernel roofline: level-0 S SpMV (the operator streamed 5x per PCG iteration)
     sys_ = out[3]
@@ -243,12 +264,10 @@ def gpu_arm(args, rank, world):
         "metric": METRIC, "value": ms / 1e3, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY App. C config-4 generator, seed 0)",
-        "config": {"workload": f"config {args.config}: one LM linear solve (evaluate + damping + A/C/rhs + explicit S"
-                               " + MG setup + PCG(V-cycle) to rel-res 1e-6 + back-substitution)",
-                   "n_cameras": sc.n_cameras, "n_points": sc.n_points, "n_observations": sc.n_observations,
-                   "nnz_S_blocks": nnzb, "mg_levels": n_levels, "cg_iterations": cg_its,
-                   "l2": "inputs larger than L2 (S alone is %.2f GB)" % (nnzb * 648 / 1e9),
-                   "parallelism": f"replicas x{world}"},
+        "config": workload_config(args, world),
+        "solve_stats": {"n_cameras": sc.n_cameras, "n_points": sc.n_points, "n_observations": sc.n_observations,
+                        "nnz_S_blocks": nnzb, "mg_levels": n_levels, "cg_iterations": cg_its,
+                        "S_gb": nnzb * 648 / 1e9},
         "breakdown_s": {"setup": setup_s, "solve": solve_s},
         "roofline": {"kernel": "k_bsr_spmv<9> (level-0 S SpMV)", "bound": "hbm", "achieved": achieved,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
@@ -317,8 +336,7 @@ def reference_arm(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"config {args.config} LM linear solve (CPU oracle port of the reference, "
-                                   f"bounded sample scaled by observation count)"},
+            "config": workload_config(args, world),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                              "sample": f"{sc.n_observations} obs sample x{scale:.1f}"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
