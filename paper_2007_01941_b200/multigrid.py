@@ -383,12 +383,17 @@ class MgLevel:
         self.coarse_factor = None
 
 
+_GRAPH = __import__("os").environ.get("BAMG_MG_GRAPH", "1") == "1"
+
+
 class _NativePlan:
     """libbamg_b200 multigrid plan: the V-cycle as one recorded CUDA graph."""
 
     def __init__(self, levels):
         L = _lib.lib()
         self.handle = L.bamg_mg_create(len(levels))
+        if _GRAPH:
+            _lib.call("bamg_mg_use_graph", self.handle, 1)
         for li, lvl in enumerate(levels):
             op = lvl.explicit
             if lvl.coarse_factor is not None:
