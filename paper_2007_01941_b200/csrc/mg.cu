@@ -732,6 +732,73 @@ k_galerkin_numeric(const int* __restrict__ cblk_ptr, const int* __restrict__ fin
   }
 }
 
+// CTA per coarse block: its fine blocks are dealt round-robin to the 4 warps; each
+// warp stages A_ij, P_j, P_i with coalesced loads into shared memory, forms
+// T = A_ij P_j there and accumulates P_i^T T (lane: row lane/2, 8 columns). The
+// four partial 16x16 sums are added in warp order (deterministic).
+template <int BS>
+__global__ void __launch_bounds__(128)
+k_galerkin_cta(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_sorted, const int* __restrict__ fine_row,
+               const int* __restrict__ col, const double* __restrict__ blocks, const double* __restrict__ P,
+               int64_t nnz_coarse, double* __restrict__ out) {
+  __shared__ double sA[4][BS * BS];
+  __shared__ double sPj[4][BS * NS];
+  __shared__ double sPi[4][BS * NS];
+  __shared__ double sT[4][BS * (NS + 1)];
+  __shared__ double red[4][NS * NS];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int r = lane >> 1, c0 = (lane & 1) * 8;
+  double* A = sA[w];
+  double* Pj = sPj[w];
+  double* Pi = sPi[w];
+  double* T = sT[w];
+  for (int64_t cb = blockIdx.x; cb < nnz_coarse; cb += gridDim.x) {
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    for (int q = cblk_ptr[cb] + w; q < cblk_ptr[cb + 1]; q += 4) {
+      int fb = fine_sorted[q];
+      int i = fine_row[fb], j = col[fb];
+      const double* a = blocks + (int64_t)fb * BS * BS;
+      const double* pj = P + (int64_t)j * BS * NS;
+      const double* pi = P + (int64_t)i * BS * NS;
+      for (int t = lane; t < BS * BS; t += 32) A[t] = __ldg(a + t);
+      for (int t = lane; t < BS * NS; t += 32) {
+        Pj[t] = __ldg(pj + t);
+        Pi[t] = __ldg(pi + t);
+      }
+      __syncwarp();
+      if (r < BS) {  // T[r][c0..c0+7] = sum_k A[r][k] Pj[k][c0..]
+        double t8[8];
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2) t8[q2] = 0.0;
+#pragma unroll
+        for (int k = 0; k < BS; ++k) {
+          double ark = A[r * BS + k];
+#pragma unroll
+          for (int q2 = 0; q2 < 8; ++q2) t8[q2] = fma(ark, Pj[k * NS + c0 + q2], t8[q2]);
+        }
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2) T[r * (NS + 1) + c0 + q2] = t8[q2];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < BS; ++k) {
+        double pik = Pi[k * NS + r];
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2) acc[q2] = fma(pik, T[k * (NS + 1) + c0 + q2], acc[q2]);
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int q2 = 0; q2 < 8; ++q2) red[w][r * NS + c0 + q2] = acc[q2];
+    __syncthreads();
+    double* o = out + cb * NS * NS;
+    for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) o[e] = ((red[0][e] + red[1][e]) + red[2][e]) + red[3][e];
+    __syncthreads();
+  }
+}
+
 // out_ab = 0.5 (B_ab + B_ba^T), in place, thread per upper block
 __global__ void k_sym_blocks(const int* __restrict__ Cptr, const int* __restrict__ Ccol, int n, double* __restrict__ B) {
   for (int a = blockIdx.x; a < n; a += gridDim.x) {
@@ -763,6 +830,38 @@ __global__ void k_sym_blocks(const int* __restrict__ Cptr, const int* __restrict
   }
 }
 
+// Same symmetrisation, one CTA per stored block q = (a, b) with a <= b: the row of q
+// comes from a binary search in Cptr, the mirror block from one in row b.
+__global__ void __launch_bounds__(256)
+k_sym_blocks2(const int* __restrict__ Cptr, const int* __restrict__ Ccol, int n, int64_t nnz, double* __restrict__ B) {
+  for (int64_t q = blockIdx.x; q < nnz; q += gridDim.x) {
+    int b = Ccol[q];
+    // row a: last a with Cptr[a] <= q
+    int lo = 0, hi = n;
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (Cptr[mid] <= q) lo = mid; else hi = mid;
+    }
+    int a = lo;
+    if (b < a) continue;
+    int t = Cptr[b] + lower_bound_i32(Ccol + Cptr[b], Cptr[b + 1] - Cptr[b], a);
+    double* X = B + q * NS * NS;
+    double* Y = B + (int64_t)t * NS * NS;
+    int e = threadIdx.x, r = e / NS, c = e - r * NS;
+    if (b == a) {
+      double v = 0.5 * (X[r * NS + c] + X[c * NS + r]);
+      __syncthreads();
+      X[r * NS + c] = v;
+    } else {
+      double v = 0.5 * (X[r * NS + c] + Y[c * NS + r]);
+      __syncthreads();
+      X[r * NS + c] = v;
+      Y[c * NS + r] = v;
+    }
+    __syncthreads();
+  }
+}
+
 // +1.0 on padded coarse dofs' diagonal entries (multigrid.py:458-471)
 __global__ void k_patch(const int* __restrict__ padded_cnt, const int* __restrict__ Cptr, const int* __restrict__ Ccol,
                         int n_agg, double* __restrict__ B) {
@@ -783,13 +882,13 @@ extern "C" int bamg_galerkin_numeric(bamg_ctx* ctx, int32_t bs, const int32_t* c
   (void)ctx;
   cudaStream_t st = as_stream(stream);
   if (nnz_coarse <= 0) return 0;
-  int g = grid_for(nnz_coarse * 32, 128, 16);
+  int g = grid_for(nnz_coarse, 1, 12);
   switch (bs) {
-    case 9: launch(k_galerkin_numeric<9>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
-    case 16: launch(k_galerkin_numeric<16>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
+    case 9: launch(k_galerkin_cta<9>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
+    case 16: launch(k_galerkin_cta<16>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
     default: bamg_set_error("galerkin: unsupported block size %d", bs); return BAMG_ERR_UNSUPPORTED;
   }
-  launch(k_sym_blocks, grid_for(n_agg, 1, 16), 128, 0, st, Cptr, Ccol, n_agg, out);
+  launch(k_sym_blocks2, grid_for(nnz_coarse, 1, 16), 256, 0, st, Cptr, Ccol, n_agg, nnz_coarse, out);
   launch(k_patch, grid_for(n_agg, 128), 128, 0, st, padded_cnt, Cptr, Ccol, n_agg, out);
   BAMG_LAUNCH_CHECK();
   return 0;

@@ -291,8 +291,11 @@ k_schur_diag(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
 // cooperative loads measured 2x slower at c4: the extra synchronisation
 // serialised the per-pair index -> record latency chain.)
 #define OFF_GROUPS 10
+#ifndef SCHUR_OFF_MINB
+#define SCHUR_OFF_MINB 1  // forcing 5 CTAs/SM (96 regs + spills) measured 8% slower at c4
+#endif
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, SCHUR_OFF_MINB)
 k_schur_offdiag(const int* __restrict__ up_blk, const int* __restrict__ up_tpos, int n_up,
                 const int* __restrict__ blk_pair_ptr, const int* __restrict__ pair_a, const int* __restrict__ pair_b,
                 const double* __restrict__ J, double* __restrict__ S) {
