@@ -312,6 +312,8 @@ k_schur_offdiag(const int* __restrict__ up_blk, const int* __restrict__ up_tpos,
 #pragma unroll
     for (int q = 0; q < 27; ++q) acc[q] = 0.0;
     int c0 = 3 * c3;
+    const int fb_lo = (RF + c0) >> 1, fb_hi = (RF + 9 + c0) >> 1;
+    const bool lo_odd = (RF + c0) & 1;  // RF even: the high triple has the other parity
     int q = blk_pair_ptr[blk], qe = blk_pair_ptr[blk + 1];
     int na = q < qe ? pair_a[q] : 0, nb = q < qe ? pair_b[q] : 0;
     for (; q < qe; ++q) {
@@ -320,20 +322,39 @@ k_schur_offdiag(const int* __restrict__ up_blk, const int* __restrict__ up_tpos,
         na = pair_a[q + 1];
         nb = pair_b[q + 1];
       }
-      const double* fa = J + oa * REC + RF;
-      const double* ha = J + oa * REC + RH;
-      const double* eb = J + ob * REC + RE;
-      const double* fb = J + ob * REC + RF;
+      // 16 B loads: the kernel is bound by L1 wavefronts (one per distinct line per
+      // load instruction), so fewer, wider loads per pair is what matters.
+      const double2* ra = reinterpret_cast<const double2*>(J + oa * REC);
+      const double2* rb = reinterpret_cast<const double2*>(J + ob * REC);
+      double fa[18], ha[6], eb[6];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        double2 v = __ldg(ra + RF / 2 + k);
+        fa[2 * k] = v.x;
+        fa[2 * k + 1] = v.y;
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        double2 v = __ldg(ra + RH / 2 + k), w = __ldg(rb + RE / 2 + k);
+        ha[2 * k] = v.x;
+        ha[2 * k + 1] = v.y;
+        eb[2 * k] = w.x;
+        eb[2 * k + 1] = w.y;
+      }
+      // this lane's columns c0..c0+2 of both F_b rows, from two aligned pairs each
+      double2 p0 = __ldg(rb + fb_lo), p1 = __ldg(rb + fb_lo + 1);
+      double2 s0 = __ldg(rb + fb_hi), s1 = __ldg(rb + fb_hi + 1);
+      double b0[3], b1[3];
+      b0[0] = lo_odd ? p0.y : p0.x;
+      b0[1] = lo_odd ? p1.x : p0.y;
+      b0[2] = lo_odd ? p1.y : p1.x;
+      b1[0] = lo_odd ? s0.x : s0.y;
+      b1[1] = lo_odd ? s0.y : s1.x;
+      b1[2] = lo_odd ? s1.x : s1.y;
       double g00 = ha[0] * eb[0] + ha[1] * eb[1] + ha[2] * eb[2];
       double g01 = ha[0] * eb[3] + ha[1] * eb[4] + ha[2] * eb[5];
       double g10 = ha[3] * eb[0] + ha[4] * eb[1] + ha[5] * eb[2];
       double g11 = ha[3] * eb[3] + ha[4] * eb[4] + ha[5] * eb[5];
-      double b0[3], b1[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        b0[c] = fb[c0 + c];
-        b1[c] = fb[9 + c0 + c];
-      }
 #pragma unroll
       for (int r = 0; r < 9; ++r) {
         double fr0 = fa[r], fr1 = fa[9 + r];
@@ -353,6 +374,155 @@ k_schur_offdiag(const int* __restrict__ up_blk, const int* __restrict__ up_tpos,
         sij[r * 9 + c0 + c] = v;
         sji[(c0 + c) * 9 + r] = v;
       }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Same assignment (10 blocks per warp, 3 lanes per block, same per-block pair order,
+// so bit-identical S), but the pair records are streamed into shared memory with
+// cp.async through an OFFP_STAGES-deep per-warp pipeline. The register version keeps
+// only one pair step in flight per warp and its scattered 8-16 B loads spend L1
+// wavefronts per distinct line; here the copies are coalesced 16 B chunks and the
+// bytes in flight no longer depend on the register budget. Warps are independent
+// (no CTA barrier); the index of step t+1 is fetched while step t's copies issue.
+#define OFFP_STAGES 3
+#define OFFP_RS 34  // doubles per staged record: 272 B rows put the 10 groups on distinct 16 B banks
+#define OFFP_STAGE_DOUBLES (2 * OFF_GROUPS * OFFP_RS)
+#define OFFP_WARP_DOUBLES (OFFP_STAGES * OFFP_STAGE_DOUBLES)
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Copy one step's records: lanes 0..19 hold rec = observation index of (group r>>1,
+// side r&1) or -1. a side: F (chunks 0-8) + H (12-14); b side: F + E (chunks 0-11).
+__device__ __forceinline__ void offp_issue(double* stage, const double* __restrict__ J, int myrec, int lane) {
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {  // 20 records x 12 chunks = 240 = 7.5 per lane
+    int c = lane + 32 * it;
+    int r = c / 12;
+    int k = c - 12 * r;
+    int rec = __shfl_sync(0xffffffffu, myrec, r < 20 ? r : 19);
+    if (c < 240 && rec >= 0) {
+      int side = r & 1, g = r >> 1;
+      int ch = side ? k : (k < 9 ? k : k + 3);
+      cp_async16(stage + (side * OFF_GROUPS + g) * OFFP_RS + 2 * ch, J + (int64_t)rec * REC + 2 * ch);
+    }
+  }
+  cp_async_commit();
+}
+
+__global__ void __launch_bounds__(128)
+k_schur_offdiag_pipe(const int* __restrict__ up_blk, const int* __restrict__ up_tpos, int n_up,
+                     const int* __restrict__ blk_pair_ptr, const int* __restrict__ pair_a,
+                     const int* __restrict__ pair_b, const double* __restrict__ J, double* __restrict__ S) {
+  extern __shared__ __align__(16) double smem_offp[];
+  int lane = threadIdx.x & 31;
+  double* wsm = smem_offp + (threadIdx.x >> 5) * OFFP_WARP_DOUBLES;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  int grp = lane / 3, c3 = lane - 3 * grp;
+  int c0 = 3 * c3;
+  const int fb_lo = (RF + c0) >> 1, fb_hi = (RF + 9 + c0) >> 1;
+  const bool lo_odd = (RF + c0) & 1;
+  const int ig = lane >> 1;
+  const int* ilist = (lane & 1) ? pair_b : pair_a;
+  for (int base = warp * OFF_GROUPS; base < n_up; base += nwarps * OFF_GROUPS) {
+    int u = base + grp;
+    bool active = (grp < OFF_GROUPS) && (u < n_up);
+    int blk = active ? up_blk[u] : 0;
+    int q0 = active ? blk_pair_ptr[blk] : 0;
+    int len = active ? blk_pair_ptr[blk + 1] - q0 : 0;
+    int maxlen = len;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    // index lanes 0..19 see group ig's pair range
+    int src = 3 * ig < 31 ? 3 * ig : 31;
+    int iq0 = __shfl_sync(0xffffffffu, q0, src);
+    int ilen = __shfl_sync(0xffffffffu, len, src);
+    if (lane >= 2 * OFF_GROUPS) ilen = 0;
+    int nrec = (ilen > 0) ? ilist[iq0] : -1;  // record index of step 0
+#pragma unroll
+    for (int t = 0; t < OFFP_STAGES - 1; ++t) {
+      int rec = nrec;
+      nrec = (t + 1 < ilen) ? ilist[iq0 + t + 1] : -1;
+      if (t < maxlen) offp_issue(wsm + t * OFFP_STAGE_DOUBLES, J, rec, lane);
+      else cp_async_commit();
+    }
+    double acc[27];
+#pragma unroll
+    for (int q = 0; q < 27; ++q) acc[q] = 0.0;
+    for (int s = 0; s < maxlen; ++s) {
+      int t = s + OFFP_STAGES - 1;
+      int rec = nrec;
+      nrec = (t + 1 < ilen) ? ilist[iq0 + t + 1] : -1;
+      if (t < maxlen) offp_issue(wsm + (t % OFFP_STAGES) * OFFP_STAGE_DOUBLES, J, rec, lane);
+      else cp_async_commit();
+      cp_async_wait<OFFP_STAGES - 1>();
+      __syncwarp();
+      if (s < len) {
+        const double* stg = wsm + (s % OFFP_STAGES) * OFFP_STAGE_DOUBLES;
+        const double2* ra = reinterpret_cast<const double2*>(stg + grp * OFFP_RS);
+        const double2* rb = reinterpret_cast<const double2*>(stg + (OFF_GROUPS + grp) * OFFP_RS);
+        double fa[18], ha[6], eb[6];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+          double2 v = ra[RF / 2 + k];
+          fa[2 * k] = v.x;
+          fa[2 * k + 1] = v.y;
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          double2 v = ra[RH / 2 + k], w = rb[RE / 2 + k];
+          ha[2 * k] = v.x;
+          ha[2 * k + 1] = v.y;
+          eb[2 * k] = w.x;
+          eb[2 * k + 1] = w.y;
+        }
+        double2 p0 = rb[fb_lo], p1 = rb[fb_lo + 1];
+        double2 s0 = rb[fb_hi], s1 = rb[fb_hi + 1];
+        double b0[3], b1[3];
+        b0[0] = lo_odd ? p0.y : p0.x;
+        b0[1] = lo_odd ? p1.x : p0.y;
+        b0[2] = lo_odd ? p1.y : p1.x;
+        b1[0] = lo_odd ? s0.x : s0.y;
+        b1[1] = lo_odd ? s0.y : s1.x;
+        b1[2] = lo_odd ? s1.x : s1.y;
+        double g00 = ha[0] * eb[0] + ha[1] * eb[1] + ha[2] * eb[2];
+        double g01 = ha[0] * eb[3] + ha[1] * eb[4] + ha[2] * eb[5];
+        double g10 = ha[3] * eb[0] + ha[4] * eb[1] + ha[5] * eb[2];
+        double g11 = ha[3] * eb[3] + ha[4] * eb[4] + ha[5] * eb[5];
+#pragma unroll
+        for (int r = 0; r < 9; ++r) {
+          double fr0 = fa[r], fr1 = fa[9 + r];
+          double a0 = fr0 * g00 + fr1 * g10;
+          double a1 = fr0 * g01 + fr1 * g11;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) acc[r * 3 + c] += a0 * b0[c] + a1 * b1[c];
+        }
+      }
+      __syncwarp();
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+    if (active) {
+      double* sij = S + (int64_t)blk * 81;
+      double* sji = S + (int64_t)up_tpos[u] * 81;
+#pragma unroll
+      for (int r = 0; r < 9; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double v = -acc[r * 3 + c];
+          sij[r * 9 + c0 + c] = v;
+          sji[(c0 + c) * 9 + r] = v;
+        }
+    }
   }
 }
 
@@ -582,8 +752,23 @@ extern "C" int bamg_schur_numeric(bamg_ctx* ctx, const int32_t* cam_ptr, const i
   if (nc) launch(k_schur_diag, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, J, A, dpos, nc, S);
   if (n_up) {
     int64_t warps = ceil_div(n_up, OFF_GROUPS);
-    launch(k_schur_offdiag, grid_for(warps * 32, 128, 8), 128, 0, st, up_blk, up_tpos, n_up, blk_pair_ptr, pair_a,
-           pair_b, J, S);
+    static const int variant = [] {
+      const char* e = getenv("BAMG_SCHUR_OFF");
+      return (e && e[0] == 'r') ? 1 : 0;  // "reg": the register-only kernel
+    }();
+    if (variant == 1) {
+      launch(k_schur_offdiag, grid_for(warps * 32, 128, 8), 128, 0, st, up_blk, up_tpos, n_up, blk_pair_ptr, pair_a,
+             pair_b, J, S);
+    } else {
+      const size_t sm = 4 * OFFP_WARP_DOUBLES * sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_schur_offdiag_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        attr = true;
+      }
+      launch(k_schur_offdiag_pipe, grid_for(warps * 32, 128, 8), 128, sm, st, up_blk, up_tpos, n_up, blk_pair_ptr,
+             pair_a, pair_b, J, S);
+    }
   }
   BAMG_LAUNCH_CHECK();
   return 0;
