@@ -207,6 +207,25 @@ int bamg_mg_set_level(bamg_mg* mg, int32_t level, int32_t bs, int32_t nbr, const
                       const double* blocks, const double* Dinv, double lower, double upper, int32_t iterations,
                       const double* P, const int32_t* agg, const int32_t* agg_ptr, const int32_t* members,
                       int32_t n_agg, const double* coarse_inv);
+/* Symmetric half-storage view of the explicit S (9x9 blocks): the solve phase
+ * streams only the upper blocks (positions dpos[i]..ptr[i+1]-1) and forms the lower
+ * half from their transposes (S_ji == S_ij^T exactly, schur.py:143-144). Built from
+ * the upper-block list of the Schur symbolic phase; owns its mirror map and the
+ * transposed-product buffer (9 nnzb doubles). Replaces bsr_matvec on S inside
+ * SchurSystem.matvec / the V-cycle (blockmat.py:295-299). */
+typedef struct bamg_symop bamg_symop;
+bamg_symop* bamg_symop_create(int32_t nbr, const int32_t* ptr, const int32_t* col, const int32_t* dpos,
+                              const int32_t* up_blk, const int32_t* up_tpos, int32_t n_up, int64_t nnzb, void* stream);
+void bamg_symop_destroy(bamg_symop* sym);
+int bamg_symop_spmv(bamg_ctx* ctx, const bamg_symop* sym, const double* blocks, const double* x, double* y,
+                    double* dot_out_dev, void* stream);
+/* r = b - S x, and the fused Chebyshev step of bamg_cheb_step, through the half-storage view */
+int bamg_symop_residual(bamg_ctx* ctx, const bamg_symop* sym, const double* blocks, const double* x,
+                        const double* b, double* r, void* stream);
+int bamg_symop_cheb_step(bamg_ctx* ctx, const bamg_symop* sym, const double* blocks, const double* x_in,
+                         const double* b, const double* Dinv, double* d, double* x_out, double c1, double c2,
+                         int32_t divide, void* stream);
+int bamg_mg_set_symmetric(bamg_mg* mg, int32_t level, const bamg_symop* sym);
 int bamg_mg_use_graph(bamg_mg* mg, int32_t on);
 int bamg_mg_apply(bamg_ctx* ctx, bamg_mg* mg, const double* r, double* z, void* stream);
 /* solver.py:70-128 pcg with a BSR operator and the MG plan (or block-Jacobi inverse
@@ -216,11 +235,12 @@ int bamg_mg_apply(bamg_ctx* ctx, bamg_mg* mg, const double* r, double* z, void* 
 int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, int32_t bs, int32_t nbr, const int32_t* ptr,
                  const int32_t* col, const double* blocks, const double* b, double* x, double tau, int32_t max_it,
                  double rtol, double* work, int32_t* iterations_out, int32_t* reason_out, double* rel_out,
-                 double* q_hist, int32_t* err_out, double* err_value_out, int32_t* err_iter_out, void* stream);
+                 double* q_hist, int32_t* err_out, double* err_value_out, int32_t* err_iter_out,
+                 const bamg_symop* sym, void* stream);
 /* multigrid.py:243-284 estimate_lambda_max for a BSR operator; work: (steps+5)*n doubles */
 int bamg_lanczos_lmax(bamg_ctx* ctx, int32_t bs, int32_t nbr, const int32_t* ptr, const int32_t* col,
                       const double* blocks, const double* D, const double* Dinv, const double* v0, int32_t steps,
-                      double* work, double* lambda_out, int32_t* status, void* stream);
+                      double* work, double* lambda_out, int32_t* status, const bamg_symop* sym, void* stream);
 
 #ifdef __cplusplus
 }

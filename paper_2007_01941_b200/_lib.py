@@ -14,7 +14,7 @@ import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libbamg_b200.so")
+LIB_PATH = os.environ.get("BAMG_LIB") or os.path.join(HERE, "libbamg_b200.so")  # BAMG_LIB: A/B variant builds
 HEADER = os.path.join(ROOT, "include", "bamg_b200.h")
 
 BAMG_ERR_INDEFINITE = 1

@@ -117,6 +117,38 @@ class BlockDiagMatrix:
         return BlockSparseMatrix(n, n, self.block_size, self.block_size, ptr, idx, self.blocks.clone())
 
 
+class SymmetricPattern:
+    """Half-storage view of an exactly symmetric 9x9 block pattern (`bamg_symop`).
+
+    The explicit S is stored in full, but its solve-phase products stream only the
+    upper blocks and rebuild the lower half from their transposes. Built once per
+    observation structure from the Schur symbolic phase's upper-block list (diagonal
+    slots, block positions, mirror positions); shared by every S of that structure.
+    """
+
+    def __init__(self, ptr, col, dpos, up_blk, up_tpos, n_up: int, nbr: int):
+        from . import _lib
+
+        self._keep = (ptr, col, dpos)
+        self.nbr = int(nbr)
+        self.handle = _lib.lib().bamg_symop_create(
+            self.nbr, ptr.data_ptr(), col.data_ptr(), dpos.data_ptr(), up_blk.data_ptr(), up_tpos.data_ptr(),
+            int(n_up), int(col.numel()), D.stream())
+        if not self.handle:
+            raise _lib.NativeError(f"bamg_symop_create: {_lib.last_error()}")
+
+    def matches(self, m: "BlockSparseMatrix") -> bool:
+        return m._ptr is self._keep[0] and m._col is self._keep[1]
+
+    def __del__(self):
+        try:
+            from . import _lib
+
+            _lib.lib().bamg_symop_destroy(self.handle)
+        except Exception:
+            pass
+
+
 class BlockSparseMatrix:
     """Block-CSR matrix with uniform dense blocks (blockmat.py:152-335)."""
 
@@ -131,6 +163,7 @@ class BlockSparseMatrix:
         self.blocks = D.f64(blocks)
         self._prolongator = None  # (agg_ptr, members) when this is a tentative P
         self._T = None
+        self._symop = None  # SymmetricPattern when the blocks are exactly symmetric (explicit S)
         if _validate:
             if self._ptr.shape != (self.n_block_rows + 1,):
                 raise ValueError(f"indptr has length {self._ptr.shape[0]}, expected {self.n_block_rows + 1}")
@@ -186,6 +219,10 @@ class BlockSparseMatrix:
             D.call("bamg_prolong", self._col, self.blocks, x, self.n_block_rows, self.row_block_size, y, 0)
             return y
         bs = self.row_block_size
+        if self._symop is not None:
+            y = D.empty(self.shape[0])
+            D.call("bamg_symop_spmv", self._symop.handle, self.blocks, x, y, None)
+            return y
         if bs == self.col_block_size and bs in (1, 3, 9, 16):
             y = D.empty(self.shape[0])
             D.call("bamg_bsr_spmv", bs, self._ptr, self._col, self.blocks, x, y, self.n_block_rows, None)

@@ -39,16 +39,22 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines: list[str] | None = None,
+          out: str | None = None) -> str:
+    """Compile + link. `defines` / `out`: an A/B variant (extra -D flags) built into
+    its own object directory and library path (dev tool; the product is LIB)."""
+    defines = list(defines or [])
+    lib_path = out or LIB
+    obj_dir = OBJ if not defines else os.path.join(CSRC, "_obj_" + "_".join(d.lstrip("-D") for d in defines))
+    os.makedirs(obj_dir, exist_ok=True)
     headers = [os.path.join(CSRC, h) for h in HEADERS]
     objs, jobs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJ, src.replace(".cu", ".o"))
+        o = os.path.join(obj_dir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            cmd = [nvcc(), *ARCH, *FLAGS, "-c", s, "-o", o]
+            cmd = [nvcc(), *ARCH, *FLAGS, *defines, "-c", s, "-o", o]
             jobs.append((src, cmd))
 
     def run(job):
@@ -63,13 +69,15 @@ def build(verbose: bool = False, force: bool = False) -> str:
             for src, log in ex.map(run, jobs):
                 if verbose:
                     print(f"[build] {src}\n{log}", file=sys.stderr)
-    if force or jobs or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
+    if force or jobs or _stale(lib_path, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", lib_path, *objs]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"link failed:\n{p.stderr}")
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    defs = [a for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[len("--out="):] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, defines=defs, out=outs[0] if outs else None))

@@ -48,6 +48,266 @@ __global__ void k_xpby_dev(const double* __restrict__ z, const double* __restric
 }
 
 // ---------------------------------------------------------------------------
+// Symmetric half-storage 9x9 SpMV for S. S is stored in full (the setup phase
+// reads whole rows), but S_ji == S_ij^T bit for bit (schur.cu writes both from one
+// value), so the solve phase streams only the upper blocks U_ij (j >= i): positions
+// dpos[i]..ptr[i+1]-1 of each row. Two deterministic passes, no atomics:
+//   pass 1 (warp per chunk of row i): y_i^up = sum_{j>=i} U_ij x_j, and for j > i the
+//          mirror product t = U_ij^T x_i, stored at the block's own (upper) position
+//          so the writes are coalesced;
+//   pass 2 (warp per row j): y_j = sum_{lower p of row j, column order} T_tpos[p] + y_j^up,
+//          followed by the consumer's epilogue (plain / residual / Chebyshev step).
+// Bytes per product: (nnz+n)/2 blocks + 2 x 72 B per off-diagonal pair instead of
+// nnz blocks -- 0.6x of the full-storage stream.
+int scan_exclusive_int(const int* in, int* out, int64_t n, int* total, cudaStream_t st);
+extern "C" void bamg_symop_destroy(bamg_symop* S);
+
+struct bamg_symop {
+  int nbr = 0;
+  int64_t nnzb = 0;
+  const int* ptr = nullptr;
+  const int* col = nullptr;
+  const int* dpos = nullptr;
+  int* tpos = nullptr;     // per full position: mirror position
+  double* T = nullptr;     // nnzb x 9, upper off-diagonal positions used
+  // pass-1 work units: chunks of <= SYM_CH upper blocks of one row (rows' upper
+  // parts range from 0 to 2x the mean length, so a warp per row is imbalanced)
+  int nch = 0;
+  int* ucptr = nullptr;    // nbr + 1: chunk range of each row
+  int* cbeg = nullptr;     // nch: first upper position
+  int* crow = nullptr;     // nch: row
+  double* yup = nullptr;   // nch x 9 partial row products
+  cudaStream_t alloc_stream = nullptr;
+};
+
+#ifndef SYM_CH
+#define SYM_CH 24
+#endif
+#ifndef SYM_MINB
+#define SYM_MINB 1
+#endif
+
+__global__ void k_sym_chunk_counts(const int* __restrict__ ptr, const int* __restrict__ dpos, int nbr,
+                                   int* __restrict__ cnt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nbr; i += gridDim.x * blockDim.x)
+    cnt[i] = (ptr[i + 1] - dpos[i] + SYM_CH - 1) / SYM_CH;
+}
+
+__global__ void k_sym_chunk_fill(const int* __restrict__ dpos, const int* __restrict__ ucptr, int nbr,
+                                 int* __restrict__ cbeg, int* __restrict__ crow) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nbr; i += gridDim.x * blockDim.x)
+    for (int c = ucptr[i]; c < ucptr[i + 1]; ++c) {
+      cbeg[c] = dpos[i] + (c - ucptr[i]) * SYM_CH;
+      crow[c] = i;
+    }
+}
+
+__global__ void k_sym_mirror(const int* __restrict__ up_blk, const int* __restrict__ up_tpos, int n_up,
+                             int* __restrict__ tpos) {
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n_up; u += gridDim.x * blockDim.x) {
+    tpos[up_blk[u]] = up_tpos[u];
+    tpos[up_tpos[u]] = up_blk[u];
+  }
+}
+
+// pass 1: warp per chunk (<= SYM_CH upper blocks of row i); lane (g, c) =
+// (lane / 9, lane % 9) walks blocks cbeg+g, +3, ... and reads column c of U (the 27
+// lanes cover three consecutive blocks per step). Writes the chunk's partial row
+// product to yup[chunk].
+__global__ void __launch_bounds__(128, SYM_MINB)
+k_sym9_upper(const int* __restrict__ ptr, const int* __restrict__ col, const int* __restrict__ dpos,
+             const int* __restrict__ tpos, const int* __restrict__ cbeg, const int* __restrict__ crow, int nch,
+             const double* __restrict__ blocks, const double* __restrict__ x, double* __restrict__ T,
+             double* __restrict__ yup) {
+  __shared__ double red[4][27 * 9];
+  int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  int g = lane / 9, c = lane - 9 * g;
+  for (int ch = warp; ch < nch; ch += nwarps) {
+    int row = crow[ch];
+    double xi[9], acc[9];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) {
+      xi[r] = __ldg(x + (int64_t)row * 9 + r);
+      acc[r] = 0.0;
+    }
+    if (g < 3) {
+      int bd = dpos[row], b0 = cbeg[ch], be = min(b0 + SYM_CH, ptr[row + 1]);
+#pragma unroll 2
+      for (int b = b0 + g; b < be; b += 3) {
+        double xjc = __ldg(x + (int64_t)col[b] * 9 + c);
+        const double* U = blocks + (int64_t)b * 81 + c;
+        double t = 0.0;
+#pragma unroll
+        for (int r = 0; r < 9; ++r) {
+          double v = __ldg(U + 9 * r);
+          acc[r] = fma(v, xjc, acc[r]);
+          t = fma(v, xi[r], t);
+        }
+        if (b != bd) T[(int64_t)b * 9 + c] = t;  // coalesced: T lives at the upper position
+      }
+#pragma unroll
+      for (int r = 0; r < 9; ++r) red[wib][lane * 9 + r] = acc[r];
+    }
+    __syncwarp();
+    if (lane < 9) {
+      double s = 0.0;
+      for (int k = 0; k < 27; ++k) s += red[wib][k * 9 + lane];
+      yup[(int64_t)ch * 9 + lane] = s;
+    }
+    __syncwarp();
+  }
+}
+
+// pass 2 + epilogue. mode 0: out = ax (dot_out: <x_in, ax>, deterministic);
+// mode 1: out = b - ax; mode 2: the fused Chebyshev step of k_cheb_step.
+__global__ void __launch_bounds__(128)
+k_sym9_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const int* __restrict__ tpos,
+              const double* __restrict__ T,
+              const int* __restrict__ ucptr, const double* __restrict__ yup, int nbr, int mode, const double* __restrict__ b,
+              const double* __restrict__ Dinv, double* __restrict__ d, const double* __restrict__ x_in,
+              double* __restrict__ out, double c1, double c2, int divide, double* partials, unsigned int* counter,
+              double* dot_out) {
+  __shared__ double scratch[33];
+  int lane = threadIdx.x & 31;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  int g = lane / 9, c = lane - 9 * g;
+  double dsum = 0.0;
+  for (int row = warp; row < nbr; row += nwarps) {
+    double s = 0.0;
+    if (g < 3) {
+      int p1 = dpos[row];
+#pragma unroll 4
+      for (int p = ptr[row] + g; p < p1; p += 3) s += __ldg(T + (int64_t)__ldg(tpos + p) * 9 + c);
+    }
+    double s1 = __shfl_down_sync(FULL_MASK, s, 9);
+    double s2 = __shfl_down_sync(FULL_MASK, s, 18);
+    int64_t e = (int64_t)row * 9 + (lane < 9 ? lane : 0);
+    double up = 0.0;
+    if (lane < 9)
+      for (int k = ucptr[row]; k < ucptr[row + 1]; ++k) up += yup[(int64_t)k * 9 + lane];
+    double ax = (lane < 9) ? (s + s1) + s2 + up : 0.0;
+    if (mode == 0) {
+      if (lane < 9) {
+        out[e] = ax;
+        if (dot_out) dsum = fma(x_in[e], ax, dsum);
+      }
+      continue;
+    }
+    double rr = (lane < 9) ? b[e] - ax : 0.0;
+    if (mode == 1) {
+      if (lane < 9) out[e] = rr;
+      continue;
+    }
+    double z = 0.0;
+    const double* Di = Dinv + (int64_t)row * 81 + (lane < 9 ? lane : 0) * 9;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      double rk = __shfl_sync(FULL_MASK, rr, k);
+      if (lane < 9) z = fma(Di[k], rk, z);
+    }
+    if (lane < 9) {
+      double dn = divide ? z / c2 : c1 * d[e] + c2 * z;
+      d[e] = dn;
+      out[e] = x_in[e] + dn;
+    }
+  }
+  if (dot_out) {
+    dsum = block_sum(dsum, scratch);
+    grid_finish(partials, counter, dsum, scratch, dot_out);
+  }
+}
+
+static int sym_grid(int nbr) { return grid_for((int64_t)nbr * 32, 128, 16); }
+
+// y = S x through the symmetric operator, with the chosen epilogue.
+static void sym9_apply(bamg_ctx* ctx, const bamg_symop* S, const double* blocks, const double* x, int mode,
+                       const double* b, const double* Dinv, double* d, double* out, double c1, double c2, int divide,
+                       double* dot_out, cudaStream_t st) {
+  launch(k_sym9_upper, sym_grid(S->nch), 128, 0, st, S->ptr, S->col, S->dpos, (const int*)S->tpos,
+         (const int*)S->cbeg, (const int*)S->crow, S->nch, blocks, x, S->T, S->yup);
+  int g = sym_grid(S->nbr);
+  if (dot_out && g > BAMG_MAX_PARTIALS) g = BAMG_MAX_PARTIALS;
+  launch(k_sym9_finish, g, 128, 0, st, S->ptr, S->dpos, (const int*)S->tpos, (const double*)S->T, (const int*)S->ucptr,
+         (const double*)S->yup, S->nbr, mode, b,
+         Dinv, d, x, out, c1, c2, divide, ctx ? ctx->partials : nullptr,
+         ctx ? ctx->counters + BAMG_CTR_SPMV : nullptr, dot_out);
+}
+
+extern "C" bamg_symop* bamg_symop_create(int32_t nbr, const int32_t* ptr, const int32_t* col, const int32_t* dpos,
+                                         const int32_t* up_blk, const int32_t* up_tpos, int32_t n_up, int64_t nnzb,
+                                         void* stream) {
+  cudaStream_t st = as_stream(stream);
+  bamg_symop* S = new bamg_symop();
+  S->nbr = nbr;
+  S->nnzb = nnzb;
+  S->ptr = ptr;
+  S->col = col;
+  S->dpos = dpos;
+  S->alloc_stream = st;
+  size_t nn = (size_t)(nnzb > 0 ? nnzb : 1);
+  auto fail = [&](const char* what) -> bamg_symop* {
+    bamg_set_error("symop_create: %s", what);
+    bamg_symop_destroy(S);
+    return nullptr;
+  };
+  if (cudaMallocAsync(&S->tpos, sizeof(int) * nn, st) != cudaSuccess ||
+      cudaMallocAsync(&S->T, sizeof(double) * 9 * nn, st) != cudaSuccess ||
+      cudaMallocAsync(&S->ucptr, sizeof(int) * ((size_t)nbr + 1), st) != cudaSuccess)
+    return fail("allocation failed");
+  if (n_up > 0) launch(k_sym_mirror, grid_for(n_up, 256), 256, 0, st, up_blk, up_tpos, n_up, S->tpos);
+  if (nbr > 0) {
+    launch(k_sym_chunk_counts, grid_for(nbr, 256), 256, 0, st, ptr, dpos, nbr, S->ucptr);
+    if (scan_exclusive_int(S->ucptr, S->ucptr, (int64_t)nbr + 1, nullptr, st)) return fail("chunk scan failed");
+    if (cudaMemcpyAsync(&S->nch, S->ucptr + nbr, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return fail("chunk count readback failed");
+  }
+  size_t nc = (size_t)(S->nch > 0 ? S->nch : 1);
+  if (cudaMallocAsync(&S->cbeg, sizeof(int) * nc, st) != cudaSuccess ||
+      cudaMallocAsync(&S->crow, sizeof(int) * nc, st) != cudaSuccess ||
+      cudaMallocAsync(&S->yup, sizeof(double) * 9 * nc, st) != cudaSuccess)
+    return fail("allocation failed");
+  if (nbr > 0) launch(k_sym_chunk_fill, grid_for(nbr, 256), 256, 0, st, dpos, (const int*)S->ucptr, nbr, S->cbeg, S->crow);
+  return S;
+}
+
+extern "C" void bamg_symop_destroy(bamg_symop* S) {
+  if (!S) return;
+  void* bufs[] = {S->tpos, S->T, S->ucptr, S->cbeg, S->crow, S->yup};
+  for (void* b : bufs)
+    if (b) cudaFreeAsync(b, S->alloc_stream);
+  delete S;
+}
+
+extern "C" int bamg_symop_spmv(bamg_ctx* ctx, const bamg_symop* S, const double* blocks, const double* x, double* y,
+                               double* dot_out_dev, void* stream) {
+  if (!S || S->nbr <= 0) return 0;
+  sym9_apply(ctx, S, blocks, x, 0, nullptr, nullptr, nullptr, y, 0.0, 0.0, 0, dot_out_dev, as_stream(stream));
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int bamg_symop_residual(bamg_ctx* ctx, const bamg_symop* S, const double* blocks, const double* x,
+                                   const double* b, double* r, void* stream) {
+  if (!S || S->nbr <= 0) return 0;
+  sym9_apply(ctx, S, blocks, x, 1, b, nullptr, nullptr, r, 0.0, 0.0, 0, nullptr, as_stream(stream));
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int bamg_symop_cheb_step(bamg_ctx* ctx, const bamg_symop* S, const double* blocks, const double* x_in,
+                                    const double* b, const double* Dinv, double* d, double* x_out, double c1,
+                                    double c2, int32_t divide, void* stream) {
+  if (!S || S->nbr <= 0) return 0;
+  sym9_apply(ctx, S, blocks, x_in, 2, b, Dinv, d, x_out, c1, c2, divide, nullptr, as_stream(stream));
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
 // Chunked 16x16 SpMV for the coarse levels. Coarse rows are long (30-80 blocks)
 // and few (1-4 K), so a warp per row leaves the SMs latency-bound. Instead every
 // warp takes a chunk of <= CH consecutive blocks of ONE row and writes a 16-entry
@@ -225,6 +485,8 @@ struct MgLevelPlan {
   int n_agg = 0;
   // coarsest
   const double* inv = nullptr;
+  // symmetric half-storage operator (bs 9), when set
+  const bamg_symop* sym = nullptr;
   // work
   double *b = nullptr, *x = nullptr, *xs = nullptr, *d = nullptr, *r = nullptr;
 };
@@ -410,6 +672,10 @@ static int finish_grid(int nbr) { return grid_for((int64_t)((nbr + 1) / 2) * 32,
 
 static void cheb(const MgLevelPlan& L, const double* x_in, double* x_out, double c1, double c2, int divide,
                  bool with_A, cudaStream_t st) {
+  if (with_A && L.sym) {
+    sym9_apply(nullptr, L.sym, L.blocks, x_in, 2, L.b, L.Dinv, L.d, x_out, c1, c2, divide, nullptr, st);
+    return;
+  }
   if (with_A && L.CH) {
     chunk_spmv(L, x_in, st);
     launch(k_rows16_finish, finish_grid(L.nbr), 128, 0, st, L.cptr, L.partial, L.nbr, 1, L.b, L.Dinv, L.d, x_in,
@@ -450,6 +716,10 @@ static double* smooth(MgLevelPlan& L, double* x, cudaStream_t st) {
 }
 
 static void residual(const MgLevelPlan& L, const double* x, cudaStream_t st) {
+  if (L.sym) {
+    sym9_apply(nullptr, L.sym, L.blocks, x, 1, L.b, nullptr, nullptr, L.r, 0.0, 0.0, 0, nullptr, st);
+    return;
+  }
   if (L.CH) {
     chunk_spmv(L, x, st);
     launch(k_rows16_finish, finish_grid(L.nbr), 128, 0, st, L.cptr, L.partial, L.nbr, 0, L.b, nullptr, nullptr,
@@ -533,6 +803,16 @@ static int mg_apply_dev(bamg_mg* m, const double* r, double* z, cudaStream_t st)
   return 0;
 }
 
+extern "C" int bamg_mg_set_symmetric(bamg_mg* m, int32_t level, const bamg_symop* sym) {
+  if (level < 0 || level >= (int)m->lv.size() || (sym && m->lv[level].bs != 9)) {
+    bamg_set_error("mg_set_symmetric: level %d is not a 9x9 level", level);
+    return BAMG_ERR_UNSUPPORTED;
+  }
+  m->lv[level].sym = sym;
+  m->dirty = true;
+  return 0;
+}
+
 extern "C" int bamg_mg_use_graph(bamg_mg* m, int32_t on) {
   m->use_graph = on != 0;
   m->dirty = true;
@@ -555,9 +835,14 @@ extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, i
                             const int32_t* ptr, const int32_t* col, const double* blocks, const double* b, double* x,
                             double tau, int32_t max_it, double rtol, double* work, int32_t* iterations_out,
                             int32_t* reason_out, double* rel_out, double* q_hist, int32_t* err_out,
-                            double* err_value_out, int32_t* err_iter_out, void* stream) {
+                            double* err_value_out, int32_t* err_iter_out, const bamg_symop* sym,
+                            void* stream) {
   cudaStream_t st = as_stream(stream);
   int64_t n = (int64_t)nbr * bs;
+  if (sym && bs != 9) {
+    bamg_set_error("pcg_run: the symmetric operator is 9x9 only");
+    return BAMG_ERR_UNSUPPORTED;
+  }
   double* r = work;
   double* z = work + n;
   double* p = work + 2 * n;
@@ -574,6 +859,10 @@ extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, i
     return 0;
   };
   auto spmv_dot = [&](const double* v, double* out, double* dot) {
+    if (sym) {
+      sym9_apply(ctx, sym, blocks, v, 0, nullptr, nullptr, nullptr, out, 0.0, 0.0, 0, dot, st);
+      return;
+    }
     int g = spmv_grid(nbr);
     if (g > BAMG_MAX_PARTIALS) g = BAMG_MAX_PARTIALS;
     unsigned* ctr = ctx->counters + BAMG_CTR_SPMV;
@@ -711,7 +1000,8 @@ __global__ void k_sqrt_slot(double* s, int i, int j) {
 // status through *status (0 ok, 1 non-finite).
 extern "C" int bamg_lanczos_lmax(bamg_ctx* ctx, int32_t bs, int32_t nbr, const int32_t* ptr, const int32_t* col,
                                  const double* blocks, const double* D, const double* Dinv, const double* v0,
-                                 int32_t steps, double* work, double* lambda_out, int32_t* status, void* stream) {
+                                 int32_t steps, double* work, double* lambda_out, int32_t* status,
+                                 const bamg_symop* sym, void* stream) {
   cudaStream_t st = as_stream(stream);
   int64_t n = (int64_t)nbr * bs;
   double* sc = ctx->scalars + 16;  // [0..15] per step: alpha[s]=sc[s], beta2[s]=sc[8+s]; extras at 64+
@@ -734,7 +1024,8 @@ extern "C" int bamg_lanczos_lmax(bamg_ctx* ctx, int32_t bs, int32_t nbr, const i
     double* q = basis + (int64_t)s * n;
     double* qp = s > 0 ? basis + (int64_t)(s - 1) * n : qprev;
     unsigned* ctr = ctx->counters + BAMG_CTR_SPMV;
-    switch (bs) {
+    if (sym && bs == 9) sym9_apply(ctx, sym, blocks, q, 0, nullptr, nullptr, nullptr, u, 0.0, 0.0, 0, sc + s, st);
+    else switch (bs) {
       case 9: launch(k_bsr_spmv<9>, sg, 128, 0, st, ptr, col, blocks, q, u, nbr, ctx->partials, ctr, sc + s); break;
       case 16: launch(k_bsr_spmv<16>, sg, 128, 0, st, ptr, col, blocks, q, u, nbr, ctx->partials, ctr, sc + s); break;
       default: launch(k_bsr_spmv<1>, sg, 128, 0, st, ptr, col, blocks, q, u, nbr, ctx->partials, ctr, sc + s); break;

@@ -237,7 +237,8 @@ def estimate_lambda_max(matvec, jacobi: BlockDiagMatrix, n: int, steps: int = _L
         lam = np.zeros(1)
         status = np.zeros(1, dtype=np.int32)
         D.call("bamg_lanczos_lmax", op.row_block_size, op.n_block_rows, op._ptr, op._col, op.blocks, jacobi.blocks,
-               jacobi.inverse_blocks(), v, int(steps), work, lam.ctypes.data, status.ctypes.data)
+               jacobi.inverse_blocks(), v, int(steps), work, lam.ctypes.data, status.ctypes.data,
+               op._symop.handle if op._symop is not None else None)
         if status[0]:
             raise FloatingPointError("Lanczos iteration produced a non-finite value")
         return float(lam[0])
@@ -341,17 +342,23 @@ class ChebyshevSmoother:
         Dinv = self.jacobi.inverse_blocks()
         d = D.empty(b.numel())
         xo = D.empty(b.numel())
+        sym = op._symop
+
+        def step(x_in, out, c1, c2, divide):
+            if sym is not None:
+                D.call("bamg_symop_cheb_step", sym.handle, op.blocks, x_in, b, Dinv, d, out, c1, c2, divide)
+            else:
+                D.call("bamg_cheb_step", bs, op._ptr, op._col, op.blocks, x_in, b, Dinv, d, out, n, c1, c2, divide)
+
         if x is None:
             D.call("bamg_cheb_step", bs, op._ptr, op._col, None, None, b, Dinv, d, xo, n, 0.0, theta, 1)
         else:
-            x = D.f64(x).reshape(-1)
-            D.call("bamg_cheb_step", bs, op._ptr, op._col, op.blocks, x, b, Dinv, d, xo, n, 0.0, theta, 1)
+            step(D.f64(x).reshape(-1), xo, 0.0, theta, 1)
         x = xo
         spare = D.empty(b.numel())
         for _ in range(self.iterations - 1):
             rho_next = 1.0 / (2.0 * sigma - rho)
-            D.call("bamg_cheb_step", bs, op._ptr, op._col, op.blocks, x, b, Dinv, d, spare, n,
-                   rho_next * rho, 2.0 * rho_next / delta, 0)
+            step(x, spare, rho_next * rho, 2.0 * rho_next / delta, 0)
             x, spare = spare, x
             rho = rho_next
         return x
@@ -405,6 +412,8 @@ class _NativePlan:
             _lib.call("bamg_mg_set_level", self.handle, li, op.row_block_size, op.n_block_rows, op._ptr, op._col,
                       op.blocks, sm.jacobi.inverse_blocks(), float(sm.lower), float(sm.upper), int(sm.iterations),
                       lvl.P.blocks, lvl.P._col, ptr, mem, lvl.aggregation.n_aggregates, None)
+            if op._symop is not None:
+                _lib.call("bamg_mg_set_symmetric", self.handle, li, op._symop.handle)
 
     def apply(self, r):
         z = D.empty(r.numel())
@@ -511,7 +520,10 @@ def mgcycle(h: MgHierarchy, level: int, x, b):
     op = _explicit_operator(lvl.matvec)
     r = D.empty(b.numel())
     if op is not None:
-        D.call("bamg_bsr_residual", op.row_block_size, op._ptr, op._col, op.blocks, x, b, r, op.n_block_rows)
+        if op._symop is not None:
+            D.call("bamg_symop_residual", op._symop.handle, op.blocks, x, b, r)
+        else:
+            D.call("bamg_bsr_residual", op.row_block_size, op._ptr, op._col, op.blocks, x, b, r, op.n_block_rows)
     else:
         r.copy_(b)
         _axpby(-1.0, lvl.matvec(x), 1.0, r)

@@ -166,6 +166,17 @@ class ObsStructure:
         return self._symbolic
 
     @property
+    def symop(self):
+        """Half-storage view of S's pattern for the solve-phase products (blockmat.SymmetricPattern)."""
+        if getattr(self, "_symop", None) is None:
+            from .blockmat import SymmetricPattern
+
+            S_ptr, S_col, nnz, _ = self.covis
+            p = getattr(self, "_pairs", None) or self.symbolic
+            self._symop = SymmetricPattern(S_ptr, S_col, p["dpos"], p["up_blk"], p["up_tpos"], p["n_up"], self.nc)
+        return self._symop
+
+    @property
     def pair_lists(self):
         """Per-block point-pair lists (the block-owned alternative assembly)."""
         if getattr(self, "_pairs", None) is None:

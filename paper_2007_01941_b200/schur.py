@@ -162,8 +162,14 @@ def schur_explicit(sys: SchurSystem, variant: str = "pairs") -> BlockSparseMatri
         D.call("bamg_schur_numeric", st.cam_ptr, st.cm_list, J._J, sys.A.blocks, sym["dpos"],
                sys.n_cameras, sym["up_blk"], sym["up_tpos"], sym["n_up"], sym["blk_ptr"], sym["pair_a"],
                sym["pair_b"], blocks)
-    return BlockSparseMatrix(sys.n_cameras, sys.n_cameras, CAMERA_SIZE, CAMERA_SIZE, S_ptr, S_col, blocks,
-                             _validate=False)
+    S = BlockSparseMatrix(sys.n_cameras, sys.n_cameras, CAMERA_SIZE, CAMERA_SIZE, S_ptr, S_col, blocks,
+                          _validate=False)
+    if _SYMMETRIC:
+        S._symop = st.symop  # S_ji == S_ij^T bit for bit: half-storage products
+    return S
+
+
+_SYMMETRIC = __import__("os").environ.get("BAMG_SYM_SPMV", "1") == "1"
 
 
 def covisibility_block_count(sys: SchurSystem) -> int:

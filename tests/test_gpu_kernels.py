@@ -83,6 +83,39 @@ def test_bsr_spmv_and_fused_dot(P, bs):
     assert float(out.item()) == float(out2.item())
 
 
+def test_symmetric_half_storage_spmv(P):
+    """S products from the upper blocks + mirrored transposes equal the full-storage
+    BSR product (scipy on the host copy), the fused dot is deterministic, and the
+    lower blocks are exact transposes of the upper ones (the premise)."""
+    from paper_2007_01941_b200 import scenes
+
+    prob = P.BundleProblem(*scenes.random_problem(1003).arrays())
+    _, jac = P.evaluate(prob)
+    s = P.build_system(jac, P.Damping.from_jacobian(jac, 1e4))
+    S = P.schur_explicit(s)
+    assert S._symop is not None
+    ptr, col = D().host(S._ptr).astype(np.int64), D().host(S._col).astype(np.int64)
+    blocks = D().host(S.blocks)
+    rows = np.repeat(np.arange(S.n_block_rows), np.diff(ptr))
+    key = {(int(i), int(j)): q for q, (i, j) in enumerate(zip(rows, col))}
+    for q, (i, j) in enumerate(zip(rows, col)):
+        assert np.array_equal(blocks[key[(int(j), int(i))]], blocks[q].T)
+    rng = np.random.default_rng(5)
+    x = rng.normal(size=S.shape[0])
+    ref = sp.bsr_matrix((blocks, col, ptr), shape=S.shape) @ x
+    y = D().host(S.matvec(x))
+    assert np.max(np.abs(y - ref)) <= 1e-12 * np.max(np.abs(ref))
+    xd = D().f64(x)
+    outs = []
+    for _ in range(2):
+        out = D().empty(1)
+        y2 = D().empty(S.shape[0])
+        D().call("bamg_symop_spmv", S._symop.handle, S.blocks, xd, y2, out)
+        outs.append((float(out.item()), D().host(y2)))
+    assert abs(outs[0][0] - x @ ref) <= 1e-11 * abs(x @ ref)
+    assert outs[0][0] == outs[1][0] and np.array_equal(outs[0][1], outs[1][1])
+
+
 @pytest.mark.parametrize("bs", [1, 3, 9, 16])
 def test_block_cholesky_inverse(P, bs):
     rng = np.random.default_rng(10 + bs)

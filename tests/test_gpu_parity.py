@@ -198,7 +198,10 @@ def test_native_runtime_matches_stepwise_path(case, hier):
     v = rng.normal(size=h.levels[0].scalar_dim)
     a = H(h.apply(v))
     b = H(MG.mgcycle(h, 0, None, P._device.f64(v)))
-    assert np.max(np.abs(a - b)) <= 1e-13 * np.max(np.abs(b))
+    # Same kernels in both paths, but the native plan chunks the coarse-level SpMV and
+    # the stepwise one does not (different summation order). cond(S) reaches 7e8 on
+    # small_1001; there the two valid roundings differ by ~2e-13 of max|z|.
+    assert np.max(np.abs(a - b)) <= 1e-11 * np.max(np.abs(b))
     x1, r1 = P.pcg(s.matvec, h.apply, s.rhs_cam, tau=1e-30, max_iterations=2000, residual_tolerance=1e-6)
     x2, r2 = P.pcg(lambda u: s.matvec(u), lambda u: h.apply(u), s.rhs_cam, tau=1e-30, max_iterations=2000,
                    residual_tolerance=1e-6)

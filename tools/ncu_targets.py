@@ -28,6 +28,8 @@ def main(config=4, what="spmv,vcycle,schur,evaluate"):
     torch.cuda.nvtx.range_push("target")
     if "spmv" in what:
         D.call("bamg_bsr_spmv", 9, S._ptr, S._col, S.blocks, x, y, S.n_block_rows, None)
+    if "sym" in what:
+        S.matvec(x)  # half-storage product (k_sym9_upper + k_sym9_finish)
     if "vcycle" in what:
         h.apply(x)
     if "schur" in what:
