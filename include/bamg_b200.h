@@ -217,6 +217,8 @@ typedef struct bamg_symop bamg_symop;
 bamg_symop* bamg_symop_create(int32_t nbr, const int32_t* ptr, const int32_t* col, const int32_t* dpos,
                               const int32_t* up_blk, const int32_t* up_tpos, int32_t n_up, int64_t nnzb, void* stream);
 void bamg_symop_destroy(bamg_symop* sym);
+/* pass-1 work units (row chunks) of the view */
+int32_t bamg_symop_chunks(const bamg_symop* sym);
 int bamg_symop_spmv(bamg_ctx* ctx, const bamg_symop* sym, const double* blocks, const double* x, double* y,
                     double* dot_out_dev, void* stream);
 /* r = b - S x, and the fused Chebyshev step of bamg_cheb_step, through the half-storage view */

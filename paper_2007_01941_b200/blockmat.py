@@ -136,6 +136,7 @@ class SymmetricPattern:
             int(n_up), int(col.numel()), D.stream())
         if not self.handle:
             raise _lib.NativeError(f"bamg_symop_create: {_lib.last_error()}")
+        self.nch = int(_lib.lib().bamg_symop_chunks(self.handle))
 
     def matches(self, m: "BlockSparseMatrix") -> bool:
         return m._ptr is self._keep[0] and m._col is self._keep[1]

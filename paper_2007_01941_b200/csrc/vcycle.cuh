@@ -282,6 +282,8 @@ extern "C" void bamg_symop_destroy(bamg_symop* S) {
   delete S;
 }
 
+extern "C" int32_t bamg_symop_chunks(const bamg_symop* S) { return S ? S->nch : 0; }
+
 extern "C" int bamg_symop_spmv(bamg_ctx* ctx, const bamg_symop* S, const double* blocks, const double* x, double* y,
                                double* dot_out_dev, void* stream) {
   if (!S || S->nbr <= 0) return 0;
