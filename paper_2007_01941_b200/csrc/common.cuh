@@ -110,6 +110,35 @@ __device__ __forceinline__ bool grid_finish(double* partials, unsigned int* coun
   return true;
 }
 
+// cp.async (LDGSTS) helpers: 16 B global -> shared copies, L2 only (.cg).
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+// copies src_bytes (0..16) and zero-fills the rest of the 16 B destination
+__device__ __forceinline__ void cp_async16_zfill(void* sdst, const void* gsrc, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+// wait until at most `pending` (clamped to 0..7) of this thread's newest groups are in flight
+__device__ __forceinline__ void cp_async_wait_dyn(int pending) {
+  switch (pending <= 0 ? 0 : (pending >= 7 ? 7 : pending)) {
+    case 0: cp_async_wait<0>(); break;
+    case 1: cp_async_wait<1>(); break;
+    case 2: cp_async_wait<2>(); break;
+    case 3: cp_async_wait<3>(); break;
+    case 4: cp_async_wait<4>(); break;
+    case 5: cp_async_wait<5>(); break;
+    case 6: cp_async_wait<6>(); break;
+    default: cp_async_wait<7>(); break;
+  }
+}
+
 __device__ __forceinline__ int lower_bound_i32(const int* a, int n, int key) {
   int lo = 0, hi = n;
   while (lo < hi) {

@@ -239,6 +239,257 @@ k_aggregate(const int* __restrict__ G_ptr, const int* __restrict__ G_col, const 
   if (lane == 0) *n_agg_out = nagg;
 }
 
+// Same greedy scan (identical decisions), restructured around its real cost: the
+// rows. The scan visits nodes in index order, so the strength rows it reads are a
+// forward walk through the CSR arrays. A ring of AGR_NB batches of AGR_B entries is
+// streamed into shared memory with cp.async ahead of the scan (batches of skipped
+// nodes are loaded too -- sequential bytes are cheap, latency is not); the decision
+// for node i then touches shared memory only (row, agg, size, G_ptr all resident).
+#define AGR_B 512
+#define AGR_NB 8
+#define AGR_R (AGR_B * AGR_NB)
+
+// Each strength row re-ordered by (G desc, column asc) -- the aggregation's own
+// candidate key minus its dynamic "unaggregated first" tie-break -- so the scan can
+// stop at the first eligible neighbour and only look further along ties of its G.
+// Warp per row, bitonic network in shared memory; rows longer than RS_CAP are left
+// in column order and flagged in `unsorted` (bit per row) for the full scan.
+#define RS_CAP 1024
+__global__ void __launch_bounds__(128)
+k_rows_sort_desc(const int* __restrict__ G_ptr, const int* __restrict__ G_col, const double* __restrict__ G_val,
+                 int n, int* __restrict__ col_s, double* __restrict__ val_s, unsigned* __restrict__ unsorted) {
+  __shared__ unsigned long long sk[4][RS_CAP / 2];
+  __shared__ int sj[4][RS_CAP / 2];
+  // RS_CAP/2 per warp in the static arrays (48 KB limit); longer rows use the flag
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int CAP = RS_CAP / 2;
+  for (int row = warp; row < n; row += nwarps) {
+    int s = G_ptr[row], L = G_ptr[row + 1] - s;
+    if (L > CAP) {
+      for (int t = lane; t < L; t += 32) {
+        col_s[s + t] = G_col[s + t];
+        val_s[s + t] = G_val[s + t];
+      }
+      if (lane == 0) atomicOr(unsorted + (row >> 5), 1u << (row & 31));
+      continue;
+    }
+    int P = 32;
+    while (P < L) P <<= 1;
+    for (int t = lane; t < P; t += 32) {
+      bool ok = t < L;
+      double g = ok ? G_val[s + t] : 0.0;
+      // G >= 0: its bit pattern is monotone; complement for descending order
+      sk[w][t] = ok ? ~(unsigned long long)__double_as_longlong(g + 0.0) : ~0ull;
+      sj[w][t] = ok ? G_col[s + t] : 0x7fffffff;
+    }
+    __syncwarp();
+    for (int k = 2; k <= P; k <<= 1)
+      for (int jn = k >> 1; jn > 0; jn >>= 1) {
+        for (int t = lane; t < P; t += 32) {
+          int p = t ^ jn;
+          if (p > t) {
+            unsigned long long a = sk[w][t], b = sk[w][p];
+            int ja = sj[w][t], jb = sj[w][p];
+            bool gt = (a > b) || (a == b && ja > jb);
+            if (gt == ((t & k) == 0)) {
+              sk[w][t] = b;
+              sk[w][p] = a;
+              sj[w][t] = jb;
+              sj[w][p] = ja;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    for (int t = lane; t < L; t += 32) {
+      col_s[s + t] = sj[w][t];
+      val_s[s + t] = __longlong_as_double((long long)~sk[w][t]);
+    }
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ void agr_issue(int bt, int64_t E, const int* __restrict__ G_col,
+                                          const double* __restrict__ G_val, int* rcol, double* rval, int lane) {
+  int64_t e0 = (int64_t)bt * AGR_B;
+  int slot0 = (bt % AGR_NB) * AGR_B;
+  constexpr int CC = AGR_B / 4, CV = AGR_B / 2;  // 16 B chunks of columns / values
+#pragma unroll 4
+  for (int c = lane; c < CC + CV; c += 32) {
+    if (c < CC) {
+      int64_t e = e0 + 4 * c;
+      int valid = (int)max((int64_t)0, min((int64_t)16, (E - e) * 4));
+      cp_async16_zfill(rcol + slot0 + 4 * c, valid ? (const void*)(G_col + e) : (const void*)G_col, valid);
+    } else {
+      int cc = c - CC;
+      int64_t e = e0 + 2 * cc;
+      int valid = (int)max((int64_t)0, min((int64_t)16, (E - e) * 8));
+      cp_async16_zfill(rval + slot0 + 2 * cc, valid ? (const void*)(G_val + e) : (const void*)G_val, valid);
+    }
+  }
+  cp_async_commit();
+}
+
+__global__ void __launch_bounds__(32)
+k_aggregate_ring(const int* __restrict__ G_ptr, const int* __restrict__ G_col, const double* __restrict__ G_val,
+                 const unsigned* __restrict__ unsorted_g, int n, int max_size, int* __restrict__ agg_g,
+                 int* __restrict__ size_g, int* __restrict__ n_agg_out) {
+  extern __shared__ __align__(16) double shd[];
+  double* rval = shd;                                  // AGR_R
+  int* rcol = reinterpret_cast<int*>(rval + AGR_R);    // AGR_R
+  int* agg = rcol + AGR_R;                             // n
+  int* size = agg + n;                                 // n
+  int* ptr = size + n;                                 // n + 1
+  unsigned* unsorted = reinterpret_cast<unsigned*>(ptr + n + 1);  // (n + 31) / 32
+  int lane = threadIdx.x;
+  for (int i = lane; i < n; i += 32) {
+    agg[i] = -1;
+    size[i] = 0;
+  }
+  for (int i = lane; i <= n; i += 32) ptr[i] = G_ptr[i];
+  for (int i = lane; i < (n + 31) / 32; i += 32) unsorted[i] = unsorted_g[i];
+  __syncwarp();
+  const int64_t E = ptr[n];
+  const int nbt = (int)((E + AGR_B - 1) / AGR_B);
+  int issued = 0;
+  while (issued < nbt && issued < AGR_NB) agr_issue(issued++, E, G_col, G_val, rcol, rval, lane);
+  int nagg = 0;
+  for (int i = 0; i < n; ++i) {
+    if (agg[i] >= 0) continue;
+    int s = ptr[i], e = ptr[i + 1];
+    Cand best{0.0, 0, -1};
+    bool uniform = false;  // best already warp-uniform (sorted-row path)
+    if (e - s <= (AGR_NB - 1) * AGR_B) {
+      // recycle batches wholly below s, then wait for the batch holding entry e-1
+      int lowb = s / AGR_B;
+      while (issued < nbt && issued < lowb + AGR_NB) agr_issue(issued++, E, G_col, G_val, rcol, rval, lane);
+      if (e > s) cp_async_wait_dyn(issued - 1 - (e - 1) / AGR_B);
+      __syncwarp();
+      if (!((unsorted[i >> 5] >> (i & 31)) & 1u)) {
+        // sorted row: the answer is the first unaggregated entry among the ties of
+        // the first eligible entry's G, else that first eligible entry itself
+        bool have = false;
+        double gf = 0.0;
+        int jf = -1, ju = -1;
+        for (int q0 = s; q0 < e; q0 += 32) {
+          int q = q0 + lane;
+          int slot = q & (AGR_R - 1);
+          int j = q < e ? rcol[slot] : -1;
+          double g = rval[slot];
+          int a = j >= 0 ? agg[j] : -1;
+          bool elig = j >= 0 && (a < 0 || size[a] < max_size);
+          if (have) elig = elig && (g == gf);
+          unsigned m = __ballot_sync(FULL_MASK, elig);
+          if (!have) {
+            if (!m) continue;
+            int f = __ffs(m) - 1;
+            gf = __shfl_sync(FULL_MASK, g, f);
+            jf = __shfl_sync(FULL_MASK, j, f);
+            have = true;
+            m = __ballot_sync(FULL_MASK, elig && g == gf);
+          }
+          unsigned mu = __ballot_sync(FULL_MASK, elig && a < 0) & m;
+          if (mu) {
+            ju = __shfl_sync(FULL_MASK, j, __ffs(mu) - 1);
+            break;
+          }
+          // ties may continue into the next chunk only if this chunk ends on one
+          bool tail = __shfl_sync(FULL_MASK, q < e && g == gf, 31);
+          if (!tail) break;
+        }
+        best.j = ju >= 0 ? ju : jf;
+        uniform = true;
+      } else
+      // 4 entries per lane per round, loads hoisted so the smem chains
+      // (column -> agg -> size) of the four overlap
+      for (int q0 = s + lane; q0 < e; q0 += 128) {
+        int jj[4], aa[4], ss[4];
+        double gg[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int q = q0 + 32 * u;
+          int slot = q & (AGR_R - 1);
+          jj[u] = q < e ? rcol[slot] : -1;
+          gg[u] = rval[slot];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) aa[u] = jj[u] >= 0 ? agg[jj[u]] : -1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ss[u] = aa[u] >= 0 ? size[aa[u]] : 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (jj[u] >= 0 && (aa[u] < 0 || ss[u] < max_size)) {
+            Cand c{gg[u], aa[u] < 0 ? 1 : 0, jj[u]};
+            if (better(c, best)) best = c;
+          }
+      }
+    } else {
+      for (int q = s + lane; q < e; q += 32) {
+        int j = G_col[q];
+        int a = agg[j];
+        if ((a < 0) || (size[a] < max_size)) {
+          Cand c{G_val[q], a < 0 ? 1 : 0, j};
+          if (better(c, best)) best = c;
+        }
+      }
+    }
+    if (!uniform) best = warp_best(best);
+    if (best.j >= 0) {
+      int aj = agg[best.j];  // every lane reads the pre-update value
+      __syncwarp();
+      if (lane == 0) {
+        if (aj < 0) {
+          agg[i] = nagg;
+          agg[best.j] = nagg;
+          size[nagg] = 2;
+        } else {
+          agg[i] = aj;
+          size[aj] += 1;
+        }
+      }
+      if (aj < 0) ++nagg;
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+  // post-pass over leftovers in index order (few nodes: rows from global memory)
+  for (int i = 0; i < n; ++i) {
+    __syncwarp();
+    if (agg[i] >= 0) continue;
+    Cand best{0.0, 0, -1};
+    for (int q = ptr[i] + lane; q < ptr[i + 1]; q += 32) {
+      int j = G_col[q];
+      int a = agg[j];
+      if (a >= 0 && size[a] <= max_size) {
+        Cand c{G_val[q], 0, j};
+        if (better(c, best)) best = c;
+      }
+    }
+    best = warp_best(best);
+    __syncwarp();
+    if (lane == 0) {
+      if (best.j >= 0) {
+        int a = agg[best.j];
+        agg[i] = a;
+        size[a] += 1;
+      } else {
+        agg[i] = nagg;
+        size[nagg] = 1;
+      }
+    }
+    if (best.j < 0) ++nagg;
+    __syncwarp();
+  }
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) {
+    agg_g[i] = agg[i];
+    size_g[i] = size[i];
+  }
+  if (lane == 0) *n_agg_out = nagg;
+}
+
 extern "C" int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t* G_col, const double* G_val,
                               int32_t n, int32_t max_size, int32_t* agg, int32_t* size_work, int32_t* n_agg_dev,
                               void* stream) {
@@ -246,6 +497,39 @@ extern "C" int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t
   cudaStream_t st = as_stream(stream);
   if (n <= 0) {
     BAMG_CUDA_CHECK(cudaMemsetAsync(n_agg_dev, 0, sizeof(int), st));
+    return 0;
+  }
+  const int nwords = (n + 31) / 32;
+  size_t smr = (size_t)AGR_R * (sizeof(double) + sizeof(int)) + sizeof(int) * (3 * (size_t)n + 1) +
+               sizeof(unsigned) * (size_t)nwords;
+  static const bool ring_on = [] {
+    const char* e = getenv("BAMG_AGG_RING");
+    return !(e && e[0] == '0');
+  }();
+  if (ring_on && smr <= 220 * 1024) {
+    int E = 0;
+    BAMG_CUDA_CHECK(cudaMemcpyAsync(&E, G_ptr + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+    BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+    size_t ne = (size_t)(E > 0 ? E : 1);
+    int* col_s = nullptr;
+    double* val_s = nullptr;
+    unsigned* uns = nullptr;
+    BAMG_CUDA_CHECK(cudaMallocAsync(&val_s, sizeof(double) * ne, st));
+    BAMG_CUDA_CHECK(cudaMallocAsync(&col_s, sizeof(int) * ne, st));
+    BAMG_CUDA_CHECK(cudaMallocAsync(&uns, sizeof(unsigned) * (size_t)nwords, st));
+    BAMG_CUDA_CHECK(cudaMemsetAsync(uns, 0, sizeof(unsigned) * (size_t)nwords, st));
+    launch(k_rows_sort_desc, grid_for((int64_t)n * 32, 128, 8), 128, 0, st, G_ptr, G_col, G_val, n, col_s, val_s, uns);
+    static size_t attr = 0;
+    if (smr > attr) {
+      BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr));
+      attr = smr;
+    }
+    launch(k_aggregate_ring, 1, 32, smr, st, G_ptr, (const int*)col_s, (const double*)val_s, (const unsigned*)uns, n,
+           max_size, agg, size_work, n_agg_dev);
+    BAMG_CUDA_CHECK(cudaFreeAsync(val_s, st));
+    BAMG_CUDA_CHECK(cudaFreeAsync(col_s, st));
+    BAMG_CUDA_CHECK(cudaFreeAsync(uns, st));
+    BAMG_LAUNCH_CHECK();
     return 0;
   }
   size_t sm = sizeof(int) * 2 * (size_t)n;

@@ -390,16 +390,6 @@ k_schur_offdiag(const int* __restrict__ up_blk, const int* __restrict__ up_tpos,
 #define OFFP_STAGE_DOUBLES (2 * OFF_GROUPS * OFFP_RS)
 #define OFFP_WARP_DOUBLES (OFFP_STAGES * OFFP_STAGE_DOUBLES)
 
-__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
 // Copy one step's records: lanes 0..19 hold rec = observation index of (group r>>1,
 // side r&1) or -1. a side: F (chunks 0-8) + H (12-14); b side: F + E (chunks 0-11).
 __device__ __forceinline__ void offp_issue(double* stage, const double* __restrict__ J, int myrec, int lane) {

@@ -28,6 +28,10 @@ def main(config=4, what="spmv,vcycle,schur,evaluate"):
     torch.cuda.nvtx.range_push("target")
     if "spmv" in what:
         D.call("bamg_bsr_spmv", 9, S._ptr, S._col, S.blocks, x, y, S.n_block_rows, None)
+    if "agg" in what:
+        from paper_2007_01941_b200 import multigrid as MG
+
+        MG.aggregate(P.visibility_strength(prob), 20)  # level-0 greedy scan, uncached
     if "sym" in what:
         S.matvec(x)  # half-storage product (k_sym9_upper + k_sym9_finish)
     if "vcycle" in what:
