@@ -196,6 +196,24 @@ int bamg_canonicalize(bamg_ctx* ctx, double* cams, int32_t n, int32_t stride, vo
 /* number of library kernel launches so far (benchmark accounting) */
 int64_t bamg_launch_count(void);
 
+/* ---- visibility block-Jacobi (precond.py:59-144) ----
+ * Clusters c = 0..ncl-1 (aggregation with cap 100, multigrid.py:127-176), members
+ * mem[cptr[c]..cptr[c+1]) ascending, agg[camera] = cluster. Each cluster's principal
+ * submatrix of S (dim[c] = 9 |members|, row-major at off[c] doubles) is assembled
+ * from the explicit S (precond.py:96-111), Cholesky-factored (flags[c] = 1 when not
+ * positive definite: IndefiniteBlockError(c), precond.py:139-143) and inverted;
+ * the apply replaces the per-cluster cho_solve of VisibilityJacobi.apply (69-78). */
+int bamg_vj_assemble(bamg_ctx* ctx, const int32_t* S_ptr, const int32_t* S_col, const double* S_blocks, int32_t nc,
+                     const int32_t* agg, const int32_t* cptr, const int32_t* mem, const int64_t* off,
+                     const int32_t* dim, double* dense, int64_t total, void* stream);
+int bamg_vj_factor(bamg_ctx* ctx, int32_t ncl, int32_t dim_max, const int64_t* off, const int32_t* dim, double* work,
+                   double* tmp, double* inv, int32_t* flags, void* stream);
+typedef struct bamg_vj bamg_vj;
+bamg_vj* bamg_vj_create(int32_t ncl, int32_t dim_max, const int64_t* off, const int32_t* dim, const int32_t* cptr,
+                        const int32_t* mem, const double* inv);
+void bamg_vj_destroy(bamg_vj* vj);
+int bamg_vj_apply(bamg_ctx* ctx, const bamg_vj* vj, const double* r, double* z, void* stream);
+
 /* ---- native solve-phase runtime ----
  * A multigrid plan holds per-level operators (device pointers owned by the caller)
  * and its own work vectors; the V-cycle (mgcycle, multigrid.py:474-483, with the
@@ -234,7 +252,8 @@ int bamg_mg_apply(bamg_ctx* ctx, bamg_mg* mg, const double* r, double* z, void* 
  * blocks when mg == NULL); one host synchronisation per iteration. err codes:
  * 1 PreconditionerNotSPD, 2/3/4/5 CgDivergence (operator non-finite / curvature /
  * residual non-finite / preconditioner non-finite). */
-int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, int32_t bs, int32_t nbr, const int32_t* ptr,
+int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const bamg_vj* vj, int32_t bs, int32_t nbr,
+                 const int32_t* ptr,
                  const int32_t* col, const double* blocks, const double* b, double* x, double tau, int32_t max_it,
                  double rtol, double* work, int32_t* iterations_out, int32_t* reason_out, double* rel_out,
                  double* q_hist, int32_t* err_out, double* err_value_out, int32_t* err_iter_out,

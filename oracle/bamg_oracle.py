@@ -718,6 +718,68 @@ def pbj(s: System):
     return lambda r: bdiag_apply(Dinv, r)
 
 
+VJ_CLUSTER_CAP = 100  # precond.py:21
+
+
+def visibility_cluster(G, max_cluster=VJ_CLUSTER_CAP):
+    """precond.py:59-62: the MG aggregation with a larger cap -> (assignment, n)."""
+    return aggregate(G, max_cluster)
+
+
+def vj(s: System, agg, n_agg):
+    """precond.py:82-144 vj_setup + VisibilityJacobi.apply (69-78).
+
+    Per cluster, the principal submatrix of S over the members (ascending): copied
+    from the assembled S when present (96-111), else A's diagonal blocks minus the
+    in-cluster point contributions W_a C^-1 W_b^T (112-136); scipy cho_factor, and
+    cho_solve per cluster in the apply. Indefinite(cid) on a failed factor.
+    """
+    agg = np.asarray(agg)
+    if len(agg) != s.A.shape[0]:
+        raise ValueError(f"partition covers {len(agg)} cameras, system has {s.A.shape[0]}")
+    members = members_of(agg, n_agg)
+    factors = []
+    wrows = s.W.rows()
+    for cid, mem in enumerate(members):
+        m = len(mem)
+        local = np.zeros((m * CAM, m * CAM))
+        pos = {int(c): k for k, c in enumerate(mem)}
+        if s.S is not None:
+            S = s.S
+            for k, cam in enumerate(mem):
+                for q in range(S.indptr[cam], S.indptr[cam + 1]):
+                    o = pos.get(int(S.indices[q]))
+                    if o is not None:
+                        local[k * CAM:(k + 1) * CAM, o * CAM:(o + 1) * CAM] = S.blocks[q]
+        else:
+            for k, cam in enumerate(mem):
+                local[k * CAM:(k + 1) * CAM, k * CAM:(k + 1) * CAM] = s.A[cam]
+            inc = agg[wrows] == cid
+            for pt in np.unique(s.W.indices[inc]):
+                sel = np.flatnonzero((s.W.indices == pt) & inc)
+                cams_p = wrows[sel]
+                wk = s.W.blocks[sel]
+                y = wk @ s.Cinv[pt]
+                contrib = np.einsum("aij,bkj->aibk", y, wk)
+                for a, ca in enumerate(cams_p):
+                    for b, cb in enumerate(cams_p):
+                        ia, ib = pos[int(ca)], pos[int(cb)]
+                        local[ia * CAM:(ia + 1) * CAM, ib * CAM:(ib + 1) * CAM] -= contrib[a, :, b, :]
+        try:
+            factors.append(scipy.linalg.cho_factor(local))
+        except scipy.linalg.LinAlgError:
+            raise Indefinite(cid) from None
+
+    def apply(r):
+        out = np.empty_like(r)
+        rb, ob = r.reshape(-1, CAM), out.reshape(-1, CAM)
+        for mem, f in zip(members, factors):
+            ob[mem] = scipy.linalg.cho_solve(f, rb[mem].ravel()).reshape(-1, CAM)
+        return out
+
+    return apply
+
+
 # -- solver (solver.py) ---------------------------------------------------------
 
 
@@ -807,8 +869,11 @@ def lm_solve(prob: Problem, preconditioner="multigrid", tau=1e-30, max_iteration
     recs = [StepRecord(0, obj, 0, 0.0, 0.0, radius, True)]
     G = None
     l0 = None
-    if preconditioner == "multigrid":
+    clusters = None
+    if preconditioner in ("multigrid", "visibility"):
         G = visibility_strength(prob.ci, prob.pi, prob.nc, prob.npt)
+    if preconditioner == "visibility":
+        clusters = visibility_cluster(G)
     it = 0
     termination = "max_iterations"
     while it < max_iterations:
@@ -828,6 +893,8 @@ def lm_solve(prob: Problem, preconditioner="multigrid", tau=1e-30, max_iteration
             levels = hierarchy(s, gauge_nullspace(cams), G, mg_max_coarse_dim, mg_max_ratio,
                                mg_max_aggregate, level0_agg=l0)
             M = lambda r: vcycle(levels, 0, None, r)  # noqa: E731
+        elif preconditioner == "visibility":
+            M = vj(s, *clusters)
         else:
             if s.mode == "explicit":
                 s.explicit()
@@ -892,6 +959,10 @@ def linear_solve(prob: Problem, radius=1e4, preconditioner="multigrid", tau=1e-3
             l0 = aggregate(G)
         levels = hierarchy(s, gauge_nullspace(prob.cams), G, level0_agg=l0)
         M = lambda r: vcycle(levels, 0, None, r)  # noqa: E731
+    elif preconditioner == "visibility":
+        if G is None:
+            G = visibility_strength(prob.ci, prob.pi, prob.nc, prob.npt)
+        M = vj(s, *visibility_cluster(G))
     else:
         s.explicit()
         M = pbj(s)

@@ -18,7 +18,8 @@ _EXPORTS = {
     "multigrid": ["Aggregation", "ChebyshevSmoother", "MgHierarchy", "StrengthMatrix", "aggregate", "build_hierarchy",
                   "build_prolongation", "estimate_lambda_max", "hierarchy_stats", "mgcycle", "operator_strength",
                   "visibility_strength", "make_smoother"],
-    "precond": ["DEFAULT_CLUSTER_CAP", "PointBlockJacobi", "pbj_setup"],
+    "precond": ["DEFAULT_CLUSTER_CAP", "PointBlockJacobi", "pbj_setup", "VisibilityJacobi", "visibility_cluster",
+                "vj_setup"],
     "problem": ["CAMERA_SIZE", "POINT_SIZE", "BehindCameraError", "BundleProblem", "JacobianBlocks", "evaluate",
                 "gauge_nullspace", "huber", "loss_value", "loss_weight"],
     "schur": ["Damping", "SchurSystem", "back_substitute", "build_system", "choose_mode",

@@ -521,7 +521,7 @@ __global__ void k_ltl(const double* __restrict__ Li, int n, double* __restrict__
 __device__ __forceinline__ int tile_dim(int n, int t) { return min(DT, n - t * DT); }
 
 // factor diagonal tile k in place (lower); flag on a non-positive pivot
-__global__ void __launch_bounds__(1024) k_chol_diag(double* a, int n, int k, int* flag) {
+__device__ __forceinline__ void chol_diag_tile(double* a, int n, int k, int* flag) {
   __shared__ double T[DT][DT + 1];
   int tb = tile_dim(n, k);
   int r = threadIdx.x / DT, c = threadIdx.x % DT;
@@ -544,10 +544,10 @@ __global__ void __launch_bounds__(1024) k_chol_diag(double* a, int n, int k, int
 }
 
 // L_ik = A_ik L_kk^-T for every tile row i > k (one CTA per tile, warp per row)
-__global__ void __launch_bounds__(1024) k_chol_trsm(double* a, int n, int k) {
+__device__ __forceinline__ void chol_trsm_tile(double* a, int n, int k, int bx) {
   __shared__ double Lk[DT][DT + 1];
   __shared__ double X[DT][DT + 1];
-  int i = k + 1 + blockIdx.x;
+  int i = k + 1 + bx;
   int tk = tile_dim(n, k), ti = tile_dim(n, i);
   int r = threadIdx.x / DT, c = threadIdx.x % DT;
   if (r < tk && c < tk) Lk[r][c] = a[(int64_t)(k * DT + r) * n + k * DT + c];
@@ -567,11 +567,10 @@ __global__ void __launch_bounds__(1024) k_chol_trsm(double* a, int n, int k) {
 }
 
 // A_ij -= L_ik L_jk^T for k < j <= i (one CTA per lower tile of the trailing matrix)
-__global__ void __launch_bounds__(256) k_chol_update(double* a, int n, int k, int nt) {
+__device__ __forceinline__ void chol_update_tile(double* a, int n, int k, int nt, int t) {
   __shared__ double Li[DT][DT + 1];
   __shared__ double Lj[DT][DT + 1];
   int m = nt - k - 1;
-  int t = blockIdx.x;
   int ii = (int)((sqrt(8.0 * t + 1.0) - 1.0) / 2.0);
   while ((ii + 1) * (ii + 2) / 2 <= t) ++ii;
   while (ii * (ii + 1) / 2 > t) --ii;
@@ -596,10 +595,9 @@ __global__ void __launch_bounds__(256) k_chol_update(double* a, int n, int k, in
 }
 
 // inverse of each diagonal tile of L (lower), thread per column
-__global__ void __launch_bounds__(DT) k_tile_inv_diag(const double* __restrict__ L, int n, double* __restrict__ Li) {
+__device__ __forceinline__ void tile_inv_diag(const double* __restrict__ L, int n, double* __restrict__ Li, int k) {
   __shared__ double T[DT][DT + 1];
   __shared__ double X[DT][DT + 1];
-  int k = blockIdx.x;
   int tb = tile_dim(n, k);
   int c = threadIdx.x;
   for (int r = 0; r < tb; ++r) T[r][c] = (c < tb) ? L[(int64_t)(k * DT + r) * n + k * DT + c] : 0.0;
@@ -623,12 +621,11 @@ __global__ void __launch_bounds__(DT) k_tile_inv_diag(const double* __restrict__
 }
 
 // block column k of L^-1: Li_ik = -Li_ii (sum_{j=k}^{i-1} L_ij Li_jk), i = k+1.. (one CTA per k)
-__global__ void __launch_bounds__(256) k_tile_inv_col(const double* __restrict__ L, int n, int nt,
-                                                      double* __restrict__ Li) {
+__device__ __forceinline__ void tile_inv_col(const double* __restrict__ L, int n, int nt, double* __restrict__ Li,
+                                             int k) {
   __shared__ double A[DT][DT + 1];
   __shared__ double B[DT][DT + 1];
   __shared__ double S[DT][DT + 1];
-  int k = blockIdx.x;
   int tk = tile_dim(n, k);
   for (int i = k + 1; i < nt; ++i) {
     int ti = tile_dim(n, i);
@@ -677,10 +674,10 @@ __global__ void __launch_bounds__(256) k_tile_inv_col(const double* __restrict__
 }
 
 // inv = Li^T Li, one CTA per output tile (I, J)
-__global__ void __launch_bounds__(256) k_tile_ltl(const double* __restrict__ Li, int n, int nt, double* __restrict__ out) {
+__device__ __forceinline__ void tile_ltl(const double* __restrict__ Li, int n, int nt, double* __restrict__ out, int bx) {
   __shared__ double A[DT][DT + 1];
   __shared__ double B[DT][DT + 1];
-  int I = blockIdx.x / nt, J = blockIdx.x % nt;
+  int I = bx / nt, J = bx % nt;
   int tI = tile_dim(n, I), tJ = tile_dim(n, J);
   double acc[4] = {0, 0, 0, 0};
   for (int K = max(I, J); K < nt; ++K) {
@@ -708,6 +705,23 @@ __global__ void __launch_bounds__(256) k_tile_ltl(const double* __restrict__ Li,
     int r = q / DT, c = q % DT;
     if (r < tI && c < tJ) out[(int64_t)(I * DT + r) * n + J * DT + c] = acc[u];
   }
+}
+
+// single-matrix kernels (coarsest level)
+__global__ void __launch_bounds__(1024) k_chol_diag(double* a, int n, int k, int* flag) { chol_diag_tile(a, n, k, flag); }
+__global__ void __launch_bounds__(1024) k_chol_trsm(double* a, int n, int k) { chol_trsm_tile(a, n, k, blockIdx.x); }
+__global__ void __launch_bounds__(256) k_chol_update(double* a, int n, int k, int nt) {
+  chol_update_tile(a, n, k, nt, blockIdx.x);
+}
+__global__ void __launch_bounds__(DT) k_tile_inv_diag(const double* __restrict__ L, int n, double* __restrict__ Li) {
+  tile_inv_diag(L, n, Li, blockIdx.x);
+}
+__global__ void __launch_bounds__(256) k_tile_inv_col(const double* __restrict__ L, int n, int nt,
+                                                      double* __restrict__ Li) {
+  tile_inv_col(L, n, nt, Li, blockIdx.x);
+}
+__global__ void __launch_bounds__(256) k_tile_ltl(const double* __restrict__ Li, int n, int nt, double* __restrict__ out) {
+  tile_ltl(Li, n, nt, out, blockIdx.x);
 }
 
 // dense = sym(BSR); L = chol(dense) (in `work`), inv = L^-T L^-1 -- tiled, many CTAs.
@@ -757,6 +771,171 @@ extern "C" int bamg_dense_gemv(bamg_ctx* ctx, const double* M, const double* x, 
   (void)ctx;
   if (n <= 0) return 0;
   launch(k_gemv, grid_for((int64_t)n * 32, 128, 8), 128, 0, as_stream(stream), M, x, n, y);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Visibility block-Jacobi (precond.py:59-144): one dense principal submatrix of S
+// per camera cluster (clusters from the greedy aggregation with cap 100, members
+// ascending), factored with the tiled Cholesky above batched over clusters
+// (blockIdx.y = cluster; tiles beyond a cluster's size exit), then inverted
+// explicitly (L^-T L^-1) so the apply is one batched gather-GEMV-scatter.
+// Cluster c: dim[c] = 9 |members|, row-major dim x dim at off[c] doubles.
+
+// S blocks whose row and column cameras share a cluster land in that cluster's
+// matrix (positions by binary search in the ascending member list).
+__global__ void k_vj_assemble(const int* __restrict__ S_ptr, const int* __restrict__ S_col,
+                              const double* __restrict__ S_blocks, int nc, const int* __restrict__ agg,
+                              const int* __restrict__ cptr, const int* __restrict__ mem,
+                              const long long* __restrict__ off, const int* __restrict__ dim,
+                              double* __restrict__ dense) {
+  int lane = threadIdx.x & 31;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = warp; i < nc; i += nwarps) {
+    int c = agg[i];
+    int m0 = cptr[c], mlen = cptr[c + 1] - m0;
+    int pi = lower_bound_i32(mem + m0, mlen, i);
+    int n = dim[c];
+    double* M = dense + off[c];
+    for (int q = S_ptr[i]; q < S_ptr[i + 1]; ++q) {
+      int j = S_col[q];
+      if (agg[j] != c) continue;
+      int pj = lower_bound_i32(mem + m0, mlen, j);
+      const double* B = S_blocks + (int64_t)q * 81;
+      for (int e = lane; e < 81; e += 32) {
+        int r = e / 9, cc = e - 9 * r;
+        M[(int64_t)(9 * pi + r) * n + 9 * pj + cc] = B[e];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ int vj_tiles(int n) { return (n + DT - 1) / DT; }
+
+__global__ void __launch_bounds__(1024) k_bchol_diag(double* a, const long long* off, const int* dim, int k, int* flags) {
+  int c = blockIdx.y, n = dim[c];
+  if (k >= vj_tiles(n)) return;
+  chol_diag_tile(a + off[c], n, k, flags + c);
+}
+__global__ void __launch_bounds__(1024) k_bchol_trsm(double* a, const long long* off, const int* dim, int k) {
+  int c = blockIdx.y, n = dim[c];
+  if (k + 1 + (int)blockIdx.x >= vj_tiles(n)) return;
+  chol_trsm_tile(a + off[c], n, k, blockIdx.x);
+}
+__global__ void __launch_bounds__(256) k_bchol_update(double* a, const long long* off, const int* dim, int k) {
+  int c = blockIdx.y, n = dim[c], nt = vj_tiles(n);
+  int m = nt - k - 1;
+  if (m <= 0 || (int)blockIdx.x >= m * (m + 1) / 2) return;
+  chol_update_tile(a + off[c], n, k, nt, blockIdx.x);
+}
+__global__ void __launch_bounds__(DT) k_btile_inv_diag(const double* L, const long long* off, const int* dim, double* Li) {
+  int c = blockIdx.y, n = dim[c];
+  if ((int)blockIdx.x >= vj_tiles(n)) return;
+  tile_inv_diag(L + off[c], n, Li + off[c], blockIdx.x);
+}
+__global__ void __launch_bounds__(256) k_btile_inv_col(const double* L, const long long* off, const int* dim, double* Li) {
+  int c = blockIdx.y, n = dim[c], nt = vj_tiles(n);
+  if ((int)blockIdx.x >= nt) return;
+  tile_inv_col(L + off[c], n, nt, Li + off[c], blockIdx.x);
+}
+__global__ void __launch_bounds__(256) k_btile_ltl(const double* Li, const long long* off, const int* dim, double* out) {
+  int c = blockIdx.y, n = dim[c], nt = vj_tiles(n);
+  if ((int)blockIdx.x >= nt * nt) return;
+  tile_ltl(Li + off[c], n, nt, out + off[c], blockIdx.x);
+}
+
+// z[members] = inv_c r[members], warp per local row (blockIdx.y = cluster)
+__global__ void __launch_bounds__(128)
+k_vj_apply(const long long* __restrict__ off, const int* __restrict__ dim, const int* __restrict__ cptr,
+           const int* __restrict__ mem, const double* __restrict__ inv, const double* __restrict__ r,
+           double* __restrict__ z) {
+  int c = blockIdx.y, n = dim[c];
+  int lane = threadIdx.x & 31;
+  int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int rstride = (gridDim.x * blockDim.x) >> 5;
+  const int* mc = mem + cptr[c];
+  const double* M = inv + off[c];
+  for (; row < n; row += rstride) {
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) s = fma(M[(int64_t)row * n + j], r[(int64_t)mc[j / 9] * 9 + j % 9], s);
+    s = warp_sum(s);
+    if (lane == 0) z[(int64_t)mc[row / 9] * 9 + row % 9] = s;
+  }
+}
+
+extern "C" int bamg_vj_assemble(bamg_ctx* ctx, const int32_t* S_ptr, const int32_t* S_col, const double* S_blocks,
+                                int32_t nc, const int32_t* agg, const int32_t* cptr, const int32_t* mem,
+                                const int64_t* off, const int32_t* dim, double* dense, int64_t total, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (nc <= 0) return 0;
+  BAMG_CUDA_CHECK(cudaMemsetAsync(dense, 0, sizeof(double) * (size_t)total, st));
+  launch(k_vj_assemble, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, S_ptr, S_col, S_blocks, nc, agg, cptr, mem,
+         (const long long*)off, dim, dense);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// work: in A (assembled), out L; tmp: L^-1 scratch; inv: A^-1. flags[c] = 1 if
+// cluster c hit a non-positive pivot (precond.py:139-143).
+extern "C" int bamg_vj_factor(bamg_ctx* ctx, int32_t ncl, int32_t dim_max, const int64_t* off, const int32_t* dim,
+                              double* work, double* tmp, double* inv, int32_t* flags, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (ncl <= 0) return 0;
+  if (ncl > 65535) {
+    bamg_set_error("vj_factor: %d clusters exceed the grid's y range", ncl);
+    return BAMG_ERR_UNSUPPORTED;
+  }
+  const long long* o = (const long long*)off;
+  BAMG_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)ncl, st));
+  int ntm = (dim_max + DT - 1) / DT;
+  for (int k = 0; k < ntm; ++k) {
+    launch(k_bchol_diag, dim3(1, ncl), 1024, 0, st, work, o, dim, k, flags);
+    int m = ntm - k - 1;
+    if (m > 0) {
+      launch(k_bchol_trsm, dim3(m, ncl), 1024, 0, st, work, o, dim, k);
+      launch(k_bchol_update, dim3(m * (m + 1) / 2, ncl), 256, 0, st, work, o, dim, k);
+    }
+  }
+  launch(k_btile_inv_diag, dim3(ntm, ncl), DT, 0, st, (const double*)work, o, dim, tmp);
+  launch(k_btile_inv_col, dim3(ntm, ncl), 256, 0, st, (const double*)work, o, dim, tmp);
+  launch(k_btile_ltl, dim3(ntm * ntm, ncl), 256, 0, st, (const double*)tmp, o, dim, inv);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+static void vj_apply_launch(int ncl, int dim_max, const long long* off, const int* dim, const int* cptr, const int* mem,
+                            const double* inv, const double* r, double* z, cudaStream_t st) {
+  int gx = (dim_max + 3) / 4;
+  if (gx > 64) gx = 64;
+  launch(k_vj_apply, dim3(gx, ncl), 128, 0, st, off, dim, cptr, mem, inv, r, z);
+}
+
+struct bamg_vj {
+  int ncl, dim_max;
+  const long long* off;
+  const int *dim, *cptr, *mem;
+  const double* inv;
+};
+
+extern "C" bamg_vj* bamg_vj_create(int32_t ncl, int32_t dim_max, const int64_t* off, const int32_t* dim,
+                                   const int32_t* cptr, const int32_t* mem, const double* inv) {
+  return new bamg_vj{ncl, dim_max, (const long long*)off, dim, cptr, mem, inv};
+}
+
+extern "C" void bamg_vj_destroy(bamg_vj* v) { delete v; }
+
+static void vj_apply_dev(const bamg_vj* v, const double* r, double* z, cudaStream_t st) {
+  vj_apply_launch(v->ncl, v->dim_max, v->off, v->dim, v->cptr, v->mem, v->inv, r, z, st);
+}
+
+extern "C" int bamg_vj_apply(bamg_ctx* ctx, const bamg_vj* v, const double* r, double* z, void* stream) {
+  (void)ctx;
+  if (!v || v->ncl <= 0) return 0;
+  vj_apply_dev(v, r, z, as_stream(stream));
   BAMG_LAUNCH_CHECK();
   return 0;
 }

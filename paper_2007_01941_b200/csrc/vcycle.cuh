@@ -833,7 +833,7 @@ extern "C" int bamg_mg_apply(bamg_ctx* ctx, bamg_mg* m, const double* r, double*
 // rel, q_history[0..iterations], err (0 none, 1 not-SPD, 2 op non-finite,
 // 3 curvature, 4 residual non-finite, 5 preconditioner non-finite), err_value, err_iter.
 
-extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, int32_t bs, int32_t nbr,
+extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const bamg_vj* vj, int32_t bs, int32_t nbr,
                             const int32_t* ptr, const int32_t* col, const double* blocks, const double* b, double* x,
                             double tau, int32_t max_it, double rtol, double* work, int32_t* iterations_out,
                             int32_t* reason_out, double* rel_out, double* q_hist, int32_t* err_out,
@@ -856,6 +856,11 @@ extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, i
   *err_value_out = 0.0;
   auto precond = [&](const double* in, double* out) -> int {
     if (mg) return mg_apply_dev(mg, in, out, st);
+    if (vj) {
+      vj_apply_dev(vj, in, out, st);
+      BAMG_LAUNCH_CHECK();
+      return 0;
+    }
     launch(k_blockdiag_apply, grid_for(n, 256), 256, 0, st, pbj_inv, in, nbr, bs, out);
     BAMG_LAUNCH_CHECK();
     return 0;

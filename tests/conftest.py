@@ -57,3 +57,17 @@ def has_gpu():
         return torch.cuda.is_available()
     except Exception:  # pragma: no cover
         return False
+
+
+VJ_CASES = ["ring", "r1003", "r1004", "r1008"]
+
+
+def vj_inputs(tag, g):
+    """(cams, pts, ci, pi, pix) of a visibility-Jacobi golden case (tests/golden/vj_cases.npz)."""
+    from paper_2007_01941_b200 import scenes
+
+    if tag == "ring":
+        sc = scenes.ring()
+        assert sc.digest() == str(g["ring_digest"]), "scene generator drifted from the golden"
+        return sc.camera_params, sc.points, sc.cam_index, sc.pt_index, sc.pixels
+    return g[f"{tag}_cams"], g[f"{tag}_pts"], g[f"{tag}_ci"], g[f"{tag}_pi"], g[f"{tag}_pix"]
