@@ -35,6 +35,7 @@ extern "C" {
 #define BAMG_ERR_BEHIND 2       /* BehindCameraError (problem.py:28-36) */
 #define BAMG_ERR_NOT_PD 3       /* coarsest operator not PD (multigrid.py:434-440) */
 #define BAMG_ERR_UNSUPPORTED 4  /* size outside the kernels' supported range */
+#define BAMG_ERR_FORMAT 5       /* BalFormatError (balio.py:17-22): *err_line + message */
 #define BAMG_ERR_CUDA (-1)
 
 typedef struct bamg_ctx bamg_ctx;
@@ -195,6 +196,19 @@ double bamg_tridiag_max_eig(const double* a_host, const double* b_host, int32_t 
 int bamg_canonicalize(bamg_ctx* ctx, double* cams, int32_t n, int32_t stride, void* stream);
 /* number of library kernel launches so far (benchmark accounting) */
 int64_t bamg_launch_count(void);
+
+/* ---- problem files: balio.py:25-97 (host side, multi-threaded; HOST pointers) ----
+ * read: header counts first, then the caller sizes the arrays and reads. Return 0,
+ * BAMG_ERR_FORMAT with *err_line (1-based) and the reference's message, or <0 on an
+ * I/O failure (message in err_msg). n_threads <= 0: all hardware threads. */
+int bamg_bal_read_header(const char* path, int64_t* counts3, int64_t* err_line, char* err_msg, size_t err_len);
+int bamg_bal_read(const char* path, int64_t n_cam, int64_t n_pt, int64_t n_obs, int64_t* cam_index,
+                  int64_t* pt_index, double* pixels, double* cams, double* pts, int32_t n_threads,
+                  int64_t* err_line, char* err_msg, size_t err_len);
+/* write: "%d %d %.17g %.17g" observation lines, one %.17g scalar per line (bit-exact round trip) */
+int bamg_bal_write(const char* path, int64_t n_cam, int64_t n_pt, int64_t n_obs, const int64_t* cam_index,
+                   const int64_t* pt_index, const double* pixels, const double* cams, const double* pts,
+                   int32_t n_threads);
 
 /* ---- visibility block-Jacobi (precond.py:59-144) ----
  * Clusters c = 0..ncl-1 (aggregation with cap 100, multigrid.py:127-176), members

@@ -13,6 +13,7 @@ from __future__ import annotations
 import importlib
 
 _EXPORTS = {
+    "balio": ["BalFormatError", "read_bal", "write_bal", "read_bal_arrays", "write_bal_arrays"],
     "blockmat": ["BlockDiagMatrix", "BlockSparseMatrix", "DenseTall", "IndefiniteBlockError", "multiply",
                  "triple_product", "write_matrix_market"],
     "multigrid": ["Aggregation", "ChebyshevSmoother", "MgHierarchy", "StrengthMatrix", "aggregate", "build_hierarchy",
