@@ -248,6 +248,11 @@ int bamg_mg_set_level(bamg_mg* mg, int32_t level, int32_t bs, int32_t nbr, const
 typedef struct bamg_symop bamg_symop;
 bamg_symop* bamg_symop_create(int32_t nbr, const int32_t* ptr, const int32_t* col, const int32_t* dpos,
                               const int32_t* up_blk, const int32_t* up_tpos, int32_t n_up, int64_t nnzb, void* stream);
+/* the same view for any exactly symmetric BSR pattern (bs 9 or 16: the Galerkin
+ * coarse operators, multigrid.py:444-455 symmetrises them), diagonal slots and
+ * mirror positions derived from (ptr, col) */
+bamg_symop* bamg_symop_create_pattern(int32_t bs, int32_t nbr, const int32_t* ptr, const int32_t* col, int64_t nnzb,
+                                      void* stream);
 void bamg_symop_destroy(bamg_symop* sym);
 /* pass-1 work units (row chunks) of the view */
 int32_t bamg_symop_chunks(const bamg_symop* sym);

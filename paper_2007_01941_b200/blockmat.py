@@ -126,17 +126,29 @@ class SymmetricPattern:
     slots, block positions, mirror positions); shared by every S of that structure.
     """
 
-    def __init__(self, ptr, col, dpos, up_blk, up_tpos, n_up: int, nbr: int):
+    def __init__(self, ptr, col, dpos, up_blk, up_tpos, n_up: int, nbr: int, _handle=None):
         from . import _lib
 
         self._keep = (ptr, col, dpos)
         self.nbr = int(nbr)
-        self.handle = _lib.lib().bamg_symop_create(
-            self.nbr, ptr.data_ptr(), col.data_ptr(), dpos.data_ptr(), up_blk.data_ptr(), up_tpos.data_ptr(),
-            int(n_up), int(col.numel()), D.stream())
+        if _handle is None:
+            _handle = _lib.lib().bamg_symop_create(
+                self.nbr, ptr.data_ptr(), col.data_ptr(), dpos.data_ptr(), up_blk.data_ptr(), up_tpos.data_ptr(),
+                int(n_up), int(col.numel()), D.stream())
+        self.handle = _handle
         if not self.handle:
             raise _lib.NativeError(f"bamg_symop_create: {_lib.last_error()}")
         self.nch = int(_lib.lib().bamg_symop_chunks(self.handle))
+
+    @classmethod
+    def from_pattern(cls, ptr, col, nbr: int, bs: int) -> "SymmetricPattern":
+        """View of any exactly symmetric BSR pattern (diagonal slots and mirror map
+        derived on the device), e.g. a Galerkin coarse operator (bs 16)."""
+        from . import _lib
+
+        h = _lib.lib().bamg_symop_create_pattern(int(bs), int(nbr), ptr.data_ptr(), col.data_ptr(),
+                                                 int(col.numel()), D.stream())
+        return cls(ptr, col, None, None, None, 0, nbr, _handle=h)
 
     def matches(self, m: "BlockSparseMatrix") -> bool:
         return m._ptr is self._keep[0] and m._col is self._keep[1]

@@ -63,43 +63,66 @@ int scan_exclusive_int(const int* in, int* out, int64_t n, int* total, cudaStrea
 extern "C" void bamg_symop_destroy(bamg_symop* S);
 
 struct bamg_symop {
+  int bs = 9;              // 9 (S) or 16 (coarse Galerkin operators)
   int nbr = 0;
   int64_t nnzb = 0;
   const int* ptr = nullptr;
   const int* col = nullptr;
   const int* dpos = nullptr;
+  int* dpos_own = nullptr; // dpos derived here (pattern-only construction)
   int* tpos = nullptr;     // per full position: mirror position
-  double* T = nullptr;     // nnzb x 9, upper off-diagonal positions used
-  // pass-1 work units: chunks of <= SYM_CH upper blocks of one row (rows' upper
+  double* T = nullptr;     // nnzb x bs, upper off-diagonal positions used
+  // pass-1 work units: chunks of <= ch upper blocks of one row (rows' upper
   // parts range from 0 to 2x the mean length, so a warp per row is imbalanced)
+  int ch = 24;
   int nch = 0;
   int* ucptr = nullptr;    // nbr + 1: chunk range of each row
   int* cbeg = nullptr;     // nch: first upper position
   int* crow = nullptr;     // nch: row
-  double* yup = nullptr;   // nch x 9 partial row products
+  double* yup = nullptr;   // nch x bs partial row products
   cudaStream_t alloc_stream = nullptr;
 };
 
 #ifndef SYM_CH
 #define SYM_CH 24
 #endif
+#ifndef SYM_CH16
+#define SYM_CH16 8
+#endif
 #ifndef SYM_MINB
 #define SYM_MINB 1
 #endif
 
-__global__ void k_sym_chunk_counts(const int* __restrict__ ptr, const int* __restrict__ dpos, int nbr,
+__global__ void k_sym_chunk_counts(const int* __restrict__ ptr, const int* __restrict__ dpos, int nbr, int CH,
                                    int* __restrict__ cnt) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nbr; i += gridDim.x * blockDim.x)
-    cnt[i] = (ptr[i + 1] - dpos[i] + SYM_CH - 1) / SYM_CH;
+    cnt[i] = (ptr[i + 1] - dpos[i] + CH - 1) / CH;
 }
 
-__global__ void k_sym_chunk_fill(const int* __restrict__ dpos, const int* __restrict__ ucptr, int nbr,
+__global__ void k_sym_chunk_fill(const int* __restrict__ dpos, const int* __restrict__ ucptr, int nbr, int CH,
                                  int* __restrict__ cbeg, int* __restrict__ crow) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nbr; i += gridDim.x * blockDim.x)
     for (int c = ucptr[i]; c < ucptr[i + 1]; ++c) {
-      cbeg[c] = dpos[i] + (c - ucptr[i]) * SYM_CH;
+      cbeg[c] = dpos[i] + (c - ucptr[i]) * CH;
       crow[c] = i;
     }
+}
+
+// pattern-only construction: diagonal slot of every row and the mirror position of
+// every block (binary search of i in row j), warp per row
+__global__ void k_sym_pattern(const int* __restrict__ ptr, const int* __restrict__ col, int nbr,
+                              int* __restrict__ dpos, int* __restrict__ tpos) {
+  int lane = threadIdx.x & 31;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = warp; i < nbr; i += nwarps) {
+    int b0 = ptr[i], b1 = ptr[i + 1];
+    if (lane == 0) dpos[i] = b0 + lower_bound_i32(col + b0, b1 - b0, i);
+    for (int q = b0 + lane; q < b1; q += 32) {
+      int j = col[q];
+      tpos[q] = ptr[j] + lower_bound_i32(col + ptr[j], ptr[j + 1] - ptr[j], i);
+    }
+  }
 }
 
 __global__ void k_sym_mirror(const int* __restrict__ up_blk, const int* __restrict__ up_tpos, int n_up,
@@ -220,46 +243,159 @@ k_sym9_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const i
   }
 }
 
+// 16x16 pass 1: warp per chunk of <= SYM_CH16 upper blocks of row i. Every 2 KB
+// block is read as four coalesced 512 B double2 sweeps (lane l: column pair
+// cp = 2(l%8) of rows l/8 + 4k, k = 0..3). Row part: a_k += U[r_k][cp..] . x_j[cp..],
+// reduced over the 8 lanes of a row once per chunk. Mirror part: t[cp..] =
+// sum_k U[r_k][cp..] x_i[r_k], reduced over the 4 lanes sharing cp (xor 8, 16) and
+// stored by lanes 0..7 at the block's own position (128 B, coalesced).
+__global__ void __launch_bounds__(128)
+k_sym16_upper(const int* __restrict__ ptr, const int* __restrict__ col, const int* __restrict__ dpos,
+              const int* __restrict__ cbeg, const int* __restrict__ crow, int nch, const double* __restrict__ blocks,
+              const double* __restrict__ x, double* __restrict__ T, double* __restrict__ yup) {
+  int lane = threadIdx.x & 31;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int cp = 2 * (lane & 7), r0 = lane >> 3;
+  for (int ch = warp; ch < nch; ch += nwarps) {
+    int row = crow[ch];
+    const double* xr = x + (int64_t)row * 16;
+    double xi0 = __ldg(xr + r0), xi1 = __ldg(xr + r0 + 4), xi2 = __ldg(xr + r0 + 8), xi3 = __ldg(xr + r0 + 12);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int bd = dpos[row], b0 = cbeg[ch], be = min(b0 + SYM_CH16, ptr[row + 1]);
+    for (int b = b0; b < be; ++b) {
+      const double2* U = reinterpret_cast<const double2*>(blocks + (int64_t)b * 256) + lane;
+      double2 u0 = __ldg(U), u1 = __ldg(U + 32), u2 = __ldg(U + 64), u3 = __ldg(U + 96);
+      double2 xj = __ldg(reinterpret_cast<const double2*>(x + (int64_t)col[b] * 16 + cp));
+      a0 = fma(u0.x, xj.x, fma(u0.y, xj.y, a0));
+      a1 = fma(u1.x, xj.x, fma(u1.y, xj.y, a1));
+      a2 = fma(u2.x, xj.x, fma(u2.y, xj.y, a2));
+      a3 = fma(u3.x, xj.x, fma(u3.y, xj.y, a3));
+      double tx = fma(u3.x, xi3, fma(u2.x, xi2, fma(u1.x, xi1, u0.x * xi0)));
+      double ty = fma(u3.y, xi3, fma(u2.y, xi2, fma(u1.y, xi1, u0.y * xi0)));
+      tx += __shfl_xor_sync(FULL_MASK, tx, 8);
+      ty += __shfl_xor_sync(FULL_MASK, ty, 8);
+      tx += __shfl_xor_sync(FULL_MASK, tx, 16);
+      ty += __shfl_xor_sync(FULL_MASK, ty, 16);
+      if (b != bd && lane < 8) reinterpret_cast<double2*>(T + (int64_t)b * 16)[lane] = make_double2(tx, ty);
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      a0 += __shfl_xor_sync(FULL_MASK, a0, o);
+      a1 += __shfl_xor_sync(FULL_MASK, a1, o);
+      a2 += __shfl_xor_sync(FULL_MASK, a2, o);
+      a3 += __shfl_xor_sync(FULL_MASK, a3, o);
+    }
+    // row r = 4k + j lives in accumulator k of lanes 8j..8j+7
+    int src = 8 * (lane & 3);
+    double s0 = __shfl_sync(FULL_MASK, a0, src);
+    double s1 = __shfl_sync(FULL_MASK, a1, src);
+    double s2 = __shfl_sync(FULL_MASK, a2, src);
+    double s3 = __shfl_sync(FULL_MASK, a3, src);
+    int k = (lane >> 2) & 3;
+    double v = k == 0 ? s0 : (k == 1 ? s1 : (k == 2 ? s2 : s3));
+    if (lane < 16) yup[(int64_t)ch * 16 + lane] = v;
+  }
+}
+
+// 16x16 pass 2 + epilogue (modes as k_sym9_finish); two rows per warp, lane r of a
+// half-warp owns entry r of its row.
+__global__ void __launch_bounds__(128)
+k_sym16_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const int* __restrict__ tpos,
+               const double* __restrict__ T, const int* __restrict__ ucptr, const double* __restrict__ yup, int nbr,
+               int mode, const double* __restrict__ b, const double* __restrict__ Dinv, double* __restrict__ d,
+               const double* __restrict__ x_in, double* __restrict__ out, double c1, double c2, int divide,
+               double* partials, unsigned int* counter, double* dot_out) {
+  __shared__ double scratch[33];
+  int lane = threadIdx.x & 31;
+  int half = lane >> 4, r = lane & 15;
+  int row0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2;
+  int stride = ((gridDim.x * blockDim.x) >> 5) * 2;
+  double dsum = 0.0;
+  for (int base = row0; base < nbr; base += stride) {
+    int row = base + half;
+    bool ok = row < nbr;
+    double ax = 0.0;
+    if (ok) {
+      double lo = 0.0, up = 0.0;
+      int p1 = dpos[row];
+#pragma unroll 4
+      for (int p = ptr[row]; p < p1; ++p) lo += __ldg(T + (int64_t)__ldg(tpos + p) * 16 + r);
+      for (int k = ucptr[row]; k < ucptr[row + 1]; ++k) up += yup[(int64_t)k * 16 + r];
+      ax = lo + up;
+    }
+    int64_t e = (int64_t)(ok ? row : 0) * 16 + r;
+    if (mode == 0) {
+      if (ok) {
+        out[e] = ax;
+        if (dot_out) dsum = fma(x_in[e], ax, dsum);
+      }
+      continue;
+    }
+    double rr = ok ? b[e] - ax : 0.0;
+    if (mode == 1) {
+      if (ok) out[e] = rr;
+      continue;
+    }
+    double z = 0.0;
+    const double* Di = Dinv + ((int64_t)(ok ? row : 0) * 16 + r) * 16;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      double rc = __shfl_sync(FULL_MASK, rr, c, 16);
+      if (ok) z = fma(Di[c], rc, z);
+    }
+    if (ok) {
+      double dn = divide ? z / c2 : c1 * d[e] + c2 * z;
+      d[e] = dn;
+      out[e] = x_in[e] + dn;
+    }
+  }
+  if (dot_out) {
+    dsum = block_sum(dsum, scratch);
+    grid_finish(partials, counter, dsum, scratch, dot_out);
+  }
+}
+
 static int sym_grid(int nbr) { return grid_for((int64_t)nbr * 32, 128, 16); }
 
-// y = S x through the symmetric operator, with the chosen epilogue.
-static void sym9_apply(bamg_ctx* ctx, const bamg_symop* S, const double* blocks, const double* x, int mode,
-                       const double* b, const double* Dinv, double* d, double* out, double c1, double c2, int divide,
-                       double* dot_out, cudaStream_t st) {
+// y = A x through the symmetric operator (bs 9 or 16), with the chosen epilogue.
+static void sym_apply(bamg_ctx* ctx, const bamg_symop* S, const double* blocks, const double* x, int mode,
+                      const double* b, const double* Dinv, double* d, double* out, double c1, double c2, int divide,
+                      double* dot_out, cudaStream_t st) {
+  double* part = ctx ? ctx->partials : nullptr;
+  unsigned* ctr = ctx ? ctx->counters + BAMG_CTR_SPMV : nullptr;
+  if (S->bs == 16) {
+    launch(k_sym16_upper, sym_grid(S->nch), 128, 0, st, S->ptr, S->col, S->dpos, (const int*)S->cbeg,
+           (const int*)S->crow, S->nch, blocks, x, S->T, S->yup);
+    int g = grid_for((int64_t)((S->nbr + 1) / 2) * 32, 128, 16);
+    if (dot_out && g > BAMG_MAX_PARTIALS) g = BAMG_MAX_PARTIALS;
+    launch(k_sym16_finish, g, 128, 0, st, S->ptr, S->dpos, (const int*)S->tpos, (const double*)S->T,
+           (const int*)S->ucptr, (const double*)S->yup, S->nbr, mode, b, Dinv, d, x, out, c1, c2, divide, part, ctr,
+           dot_out);
+    return;
+  }
   launch(k_sym9_upper, sym_grid(S->nch), 128, 0, st, S->ptr, S->col, S->dpos, (const int*)S->tpos,
          (const int*)S->cbeg, (const int*)S->crow, S->nch, blocks, x, S->T, S->yup);
   int g = sym_grid(S->nbr);
   if (dot_out && g > BAMG_MAX_PARTIALS) g = BAMG_MAX_PARTIALS;
   launch(k_sym9_finish, g, 128, 0, st, S->ptr, S->dpos, (const int*)S->tpos, (const double*)S->T, (const int*)S->ucptr,
-         (const double*)S->yup, S->nbr, mode, b,
-         Dinv, d, x, out, c1, c2, divide, ctx ? ctx->partials : nullptr,
-         ctx ? ctx->counters + BAMG_CTR_SPMV : nullptr, dot_out);
+         (const double*)S->yup, S->nbr, mode, b, Dinv, d, x, out, c1, c2, divide, part, ctr, dot_out);
 }
 
-extern "C" bamg_symop* bamg_symop_create(int32_t nbr, const int32_t* ptr, const int32_t* col, const int32_t* dpos,
-                                         const int32_t* up_blk, const int32_t* up_tpos, int32_t n_up, int64_t nnzb,
-                                         void* stream) {
-  cudaStream_t st = as_stream(stream);
-  bamg_symop* S = new bamg_symop();
-  S->nbr = nbr;
-  S->nnzb = nnzb;
-  S->ptr = ptr;
-  S->col = col;
-  S->dpos = dpos;
-  S->alloc_stream = st;
-  size_t nn = (size_t)(nnzb > 0 ? nnzb : 1);
+// shared tail of both constructors: T, the chunk plan (one host readback)
+static bamg_symop* symop_finish(bamg_symop* S, cudaStream_t st) {
   auto fail = [&](const char* what) -> bamg_symop* {
     bamg_set_error("symop_create: %s", what);
     bamg_symop_destroy(S);
     return nullptr;
   };
-  if (cudaMallocAsync(&S->tpos, sizeof(int) * nn, st) != cudaSuccess ||
-      cudaMallocAsync(&S->T, sizeof(double) * 9 * nn, st) != cudaSuccess ||
+  size_t nn = (size_t)(S->nnzb > 0 ? S->nnzb : 1);
+  int nbr = S->nbr;
+  if (cudaMallocAsync(&S->T, sizeof(double) * S->bs * nn, st) != cudaSuccess ||
       cudaMallocAsync(&S->ucptr, sizeof(int) * ((size_t)nbr + 1), st) != cudaSuccess)
     return fail("allocation failed");
-  if (n_up > 0) launch(k_sym_mirror, grid_for(n_up, 256), 256, 0, st, up_blk, up_tpos, n_up, S->tpos);
   if (nbr > 0) {
-    launch(k_sym_chunk_counts, grid_for(nbr, 256), 256, 0, st, ptr, dpos, nbr, S->ucptr);
+    launch(k_sym_chunk_counts, grid_for(nbr, 256), 256, 0, st, S->ptr, S->dpos, nbr, S->ch, S->ucptr);
     if (scan_exclusive_int(S->ucptr, S->ucptr, (int64_t)nbr + 1, nullptr, st)) return fail("chunk scan failed");
     if (cudaMemcpyAsync(&S->nch, S->ucptr + nbr, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
@@ -268,15 +404,65 @@ extern "C" bamg_symop* bamg_symop_create(int32_t nbr, const int32_t* ptr, const 
   size_t nc = (size_t)(S->nch > 0 ? S->nch : 1);
   if (cudaMallocAsync(&S->cbeg, sizeof(int) * nc, st) != cudaSuccess ||
       cudaMallocAsync(&S->crow, sizeof(int) * nc, st) != cudaSuccess ||
-      cudaMallocAsync(&S->yup, sizeof(double) * 9 * nc, st) != cudaSuccess)
+      cudaMallocAsync(&S->yup, sizeof(double) * S->bs * nc, st) != cudaSuccess)
     return fail("allocation failed");
-  if (nbr > 0) launch(k_sym_chunk_fill, grid_for(nbr, 256), 256, 0, st, dpos, (const int*)S->ucptr, nbr, S->cbeg, S->crow);
+  if (nbr > 0)
+    launch(k_sym_chunk_fill, grid_for(nbr, 256), 256, 0, st, S->dpos, (const int*)S->ucptr, nbr, S->ch, S->cbeg,
+           S->crow);
   return S;
+}
+
+extern "C" bamg_symop* bamg_symop_create(int32_t nbr, const int32_t* ptr, const int32_t* col, const int32_t* dpos,
+                                         const int32_t* up_blk, const int32_t* up_tpos, int32_t n_up, int64_t nnzb,
+                                         void* stream) {
+  cudaStream_t st = as_stream(stream);
+  bamg_symop* S = new bamg_symop();
+  S->bs = 9;
+  S->ch = SYM_CH;
+  S->nbr = nbr;
+  S->nnzb = nnzb;
+  S->ptr = ptr;
+  S->col = col;
+  S->dpos = dpos;
+  S->alloc_stream = st;
+  if (cudaMallocAsync(&S->tpos, sizeof(int) * (size_t)(nnzb > 0 ? nnzb : 1), st) != cudaSuccess) {
+    bamg_set_error("symop_create: allocation failed");
+    bamg_symop_destroy(S);
+    return nullptr;
+  }
+  if (n_up > 0) launch(k_sym_mirror, grid_for(n_up, 256), 256, 0, st, up_blk, up_tpos, n_up, S->tpos);
+  return symop_finish(S, st);
+}
+
+extern "C" bamg_symop* bamg_symop_create_pattern(int32_t bs, int32_t nbr, const int32_t* ptr, const int32_t* col,
+                                                 int64_t nnzb, void* stream) {
+  if (bs != 9 && bs != 16) {
+    bamg_set_error("symop_create_pattern: unsupported block size %d", bs);
+    return nullptr;
+  }
+  cudaStream_t st = as_stream(stream);
+  bamg_symop* S = new bamg_symop();
+  S->bs = bs;
+  S->ch = bs == 16 ? SYM_CH16 : SYM_CH;
+  S->nbr = nbr;
+  S->nnzb = nnzb;
+  S->ptr = ptr;
+  S->col = col;
+  S->alloc_stream = st;
+  if (cudaMallocAsync(&S->tpos, sizeof(int) * (size_t)(nnzb > 0 ? nnzb : 1), st) != cudaSuccess ||
+      cudaMallocAsync(&S->dpos_own, sizeof(int) * (size_t)(nbr > 0 ? nbr : 1), st) != cudaSuccess) {
+    bamg_set_error("symop_create_pattern: allocation failed");
+    bamg_symop_destroy(S);
+    return nullptr;
+  }
+  S->dpos = S->dpos_own;
+  if (nbr > 0) launch(k_sym_pattern, grid_for((int64_t)nbr * 32, 128, 16), 128, 0, st, ptr, col, nbr, S->dpos_own, S->tpos);
+  return symop_finish(S, st);
 }
 
 extern "C" void bamg_symop_destroy(bamg_symop* S) {
   if (!S) return;
-  void* bufs[] = {S->tpos, S->T, S->ucptr, S->cbeg, S->crow, S->yup};
+  void* bufs[] = {S->tpos, S->dpos_own, S->T, S->ucptr, S->cbeg, S->crow, S->yup};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, S->alloc_stream);
   delete S;
@@ -287,7 +473,7 @@ extern "C" int32_t bamg_symop_chunks(const bamg_symop* S) { return S ? S->nch : 
 extern "C" int bamg_symop_spmv(bamg_ctx* ctx, const bamg_symop* S, const double* blocks, const double* x, double* y,
                                double* dot_out_dev, void* stream) {
   if (!S || S->nbr <= 0) return 0;
-  sym9_apply(ctx, S, blocks, x, 0, nullptr, nullptr, nullptr, y, 0.0, 0.0, 0, dot_out_dev, as_stream(stream));
+  sym_apply(ctx, S, blocks, x, 0, nullptr, nullptr, nullptr, y, 0.0, 0.0, 0, dot_out_dev, as_stream(stream));
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -295,7 +481,7 @@ extern "C" int bamg_symop_spmv(bamg_ctx* ctx, const bamg_symop* S, const double*
 extern "C" int bamg_symop_residual(bamg_ctx* ctx, const bamg_symop* S, const double* blocks, const double* x,
                                    const double* b, double* r, void* stream) {
   if (!S || S->nbr <= 0) return 0;
-  sym9_apply(ctx, S, blocks, x, 1, b, nullptr, nullptr, r, 0.0, 0.0, 0, nullptr, as_stream(stream));
+  sym_apply(ctx, S, blocks, x, 1, b, nullptr, nullptr, r, 0.0, 0.0, 0, nullptr, as_stream(stream));
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -304,7 +490,7 @@ extern "C" int bamg_symop_cheb_step(bamg_ctx* ctx, const bamg_symop* S, const do
                                     const double* b, const double* Dinv, double* d, double* x_out, double c1,
                                     double c2, int32_t divide, void* stream) {
   if (!S || S->nbr <= 0) return 0;
-  sym9_apply(ctx, S, blocks, x_in, 2, b, Dinv, d, x_out, c1, c2, divide, nullptr, as_stream(stream));
+  sym_apply(ctx, S, blocks, x_in, 2, b, Dinv, d, x_out, c1, c2, divide, nullptr, as_stream(stream));
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -675,7 +861,7 @@ static int finish_grid(int nbr) { return grid_for((int64_t)((nbr + 1) / 2) * 32,
 static void cheb(const MgLevelPlan& L, const double* x_in, double* x_out, double c1, double c2, int divide,
                  bool with_A, cudaStream_t st) {
   if (with_A && L.sym) {
-    sym9_apply(nullptr, L.sym, L.blocks, x_in, 2, L.b, L.Dinv, L.d, x_out, c1, c2, divide, nullptr, st);
+    sym_apply(nullptr, L.sym, L.blocks, x_in, 2, L.b, L.Dinv, L.d, x_out, c1, c2, divide, nullptr, st);
     return;
   }
   if (with_A && L.CH) {
@@ -719,7 +905,7 @@ static double* smooth(MgLevelPlan& L, double* x, cudaStream_t st) {
 
 static void residual(const MgLevelPlan& L, const double* x, cudaStream_t st) {
   if (L.sym) {
-    sym9_apply(nullptr, L.sym, L.blocks, x, 1, L.b, nullptr, nullptr, L.r, 0.0, 0.0, 0, nullptr, st);
+    sym_apply(nullptr, L.sym, L.blocks, x, 1, L.b, nullptr, nullptr, L.r, 0.0, 0.0, 0, nullptr, st);
     return;
   }
   if (L.CH) {
@@ -806,8 +992,8 @@ static int mg_apply_dev(bamg_mg* m, const double* r, double* z, cudaStream_t st)
 }
 
 extern "C" int bamg_mg_set_symmetric(bamg_mg* m, int32_t level, const bamg_symop* sym) {
-  if (level < 0 || level >= (int)m->lv.size() || (sym && m->lv[level].bs != 9)) {
-    bamg_set_error("mg_set_symmetric: level %d is not a 9x9 level", level);
+  if (level < 0 || level >= (int)m->lv.size() || (sym && m->lv[level].bs != sym->bs)) {
+    bamg_set_error("mg_set_symmetric: block size of level %d differs from the operator's", level);
     return BAMG_ERR_UNSUPPORTED;
   }
   m->lv[level].sym = sym;
@@ -841,8 +1027,8 @@ extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, c
                             void* stream) {
   cudaStream_t st = as_stream(stream);
   int64_t n = (int64_t)nbr * bs;
-  if (sym && bs != 9) {
-    bamg_set_error("pcg_run: the symmetric operator is 9x9 only");
+  if (sym && bs != sym->bs) {
+    bamg_set_error("pcg_run: symmetric operator block size %d, operator %d", sym->bs, bs);
     return BAMG_ERR_UNSUPPORTED;
   }
   double* r = work;
@@ -867,7 +1053,7 @@ extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, c
   };
   auto spmv_dot = [&](const double* v, double* out, double* dot) {
     if (sym) {
-      sym9_apply(ctx, sym, blocks, v, 0, nullptr, nullptr, nullptr, out, 0.0, 0.0, 0, dot, st);
+      sym_apply(ctx, sym, blocks, v, 0, nullptr, nullptr, nullptr, out, 0.0, 0.0, 0, dot, st);
       return;
     }
     int g = spmv_grid(nbr);
@@ -1031,7 +1217,7 @@ extern "C" int bamg_lanczos_lmax(bamg_ctx* ctx, int32_t bs, int32_t nbr, const i
     double* q = basis + (int64_t)s * n;
     double* qp = s > 0 ? basis + (int64_t)(s - 1) * n : qprev;
     unsigned* ctr = ctx->counters + BAMG_CTR_SPMV;
-    if (sym && bs == 9) sym9_apply(ctx, sym, blocks, q, 0, nullptr, nullptr, nullptr, u, 0.0, 0.0, 0, sc + s, st);
+    if (sym && sym->bs == bs) sym_apply(ctx, sym, blocks, q, 0, nullptr, nullptr, nullptr, u, 0.0, 0.0, 0, sc + s, st);
     else switch (bs) {
       case 9: launch(k_bsr_spmv<9>, sg, 128, 0, st, ptr, col, blocks, q, u, nbr, ctx->partials, ctr, sc + s); break;
       case 16: launch(k_bsr_spmv<16>, sg, 128, 0, st, ptr, col, blocks, q, u, nbr, ctx->partials, ctr, sc + s); break;

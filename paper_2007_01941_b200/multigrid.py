@@ -15,7 +15,7 @@ import torch
 
 from . import _device as D
 from . import _lib
-from .blockmat import BlockDiagMatrix, BlockSparseMatrix, DenseTall
+from .blockmat import BlockDiagMatrix, BlockSparseMatrix, DenseTall, SymmetricPattern
 from .problem import CAMERA_SIZE, BundleProblem, ObsStructure
 from .schur import SchurSystem
 
@@ -201,7 +201,15 @@ def galerkin(P: BlockSparseMatrix, A: BlockSparseMatrix, agg: Aggregation) -> Bl
     out = D.empty(max(nnzc, 1), NULLSPACE_DIM, NULLSPACE_DIM)
     D.call("bamg_galerkin_numeric", A.row_block_size, cblk_ptr, fine_sorted, fine_row, A._col, A.blocks, P.blocks,
            na, counts, Ccol, nnzc, P.padded_count, out)
-    return BlockSparseMatrix(na, na, NULLSPACE_DIM, NULLSPACE_DIM, counts, Ccol[:nnzc], out[:nnzc], _validate=False)
+    C = BlockSparseMatrix(na, na, NULLSPACE_DIM, NULLSPACE_DIM, counts, Ccol[:nnzc], out[:nnzc], _validate=False)
+    if _SYMMETRIC_COARSE and na > 0:
+        # symmetrised exactly (both mirror blocks written from one value): the
+        # solve-phase products read only the upper blocks
+        C._symop = SymmetricPattern.from_pattern(C._ptr, C._col, na, NULLSPACE_DIM)
+    return C
+
+
+_SYMMETRIC_COARSE = __import__("os").environ.get("BAMG_SYM_SPMV", "1") == "1"
 
 
 # -- smoother -----------------------------------------------------------------------

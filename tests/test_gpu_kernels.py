@@ -116,6 +116,45 @@ def test_symmetric_half_storage_spmv(P):
     assert outs[0][0] == outs[1][0] and np.array_equal(outs[0][1], outs[1][1])
 
 
+def test_symmetric_half_storage_coarse_operator(P):
+    """The same view for a 16x16 Galerkin operator (pattern-derived mirror map):
+    product, residual and Chebyshev epilogues against the full-storage kernels."""
+    from paper_2007_01941_b200 import scenes
+
+    prob = P.BundleProblem(*scenes.street(n_cameras=60, n_points=4000, seed=3).arrays())
+    _, jac = P.evaluate(prob)
+    s = P.build_system(jac, P.Damping.from_jacobian(jac, 1e4))
+    s.mode = P.choose_mode(s)
+    h = P.build_hierarchy(s, P.gauge_nullspace(prob), P.visibility_strength(prob), max_coarse_dim=40)
+    assert h.n_levels >= 3
+    A = h.levels[1].explicit
+    assert A._symop is not None and A.row_block_size == 16
+    blocks = D().host(A.blocks)
+    ptr, col = D().host(A._ptr).astype(np.int64), D().host(A._col).astype(np.int64)
+    full = sp.bsr_matrix((blocks, col, ptr), shape=A.shape)
+    assert abs(full - full.T).max() == 0.0  # exactly symmetric: the premise
+    rng = np.random.default_rng(9)
+    x, b = rng.normal(size=A.shape[0]), rng.normal(size=A.shape[0])
+    ref = full @ x
+    assert np.max(np.abs(D().host(A.matvec(x)) - ref)) <= 1e-12 * np.max(np.abs(ref))
+    xd, bd = D().f64(x), D().f64(b)
+    r_sym, r_full = D().empty(A.shape[0]), D().empty(A.shape[0])
+    D().call("bamg_symop_residual", A._symop.handle, A.blocks, xd, bd, r_sym)
+    D().call("bamg_bsr_residual", 16, A._ptr, A._col, A.blocks, xd, bd, r_full, A.n_block_rows)
+    assert np.max(np.abs(D().host(r_sym) - D().host(r_full))) <= 1e-12 * np.max(np.abs(ref))
+    Dinv = h.levels[1].smoother.jacobi.inverse_blocks()
+    outs = []
+    for fn in ("sym", "full"):
+        d = D().f64(np.ones(A.shape[0]))
+        o = D().empty(A.shape[0])
+        if fn == "sym":
+            D().call("bamg_symop_cheb_step", A._symop.handle, A.blocks, xd, bd, Dinv, d, o, 0.3, 0.7, 0)
+        else:
+            D().call("bamg_cheb_step", 16, A._ptr, A._col, A.blocks, xd, bd, Dinv, d, o, A.n_block_rows, 0.3, 0.7, 0)
+        outs.append(D().host(o))
+    assert np.max(np.abs(outs[0] - outs[1])) <= 1e-10 * np.max(np.abs(outs[1]))
+
+
 @pytest.mark.parametrize("bs", [1, 3, 9, 16])
 def test_block_cholesky_inverse(P, bs):
     rng = np.random.default_rng(10 + bs)
