@@ -155,8 +155,11 @@ int bamg_diag_blocks(bamg_ctx* ctx, const int32_t* ptr, const int32_t* col, cons
 int bamg_operator_strength(bamg_ctx* ctx, const int32_t* ptr, const int32_t* col, const double* blocks, int32_t n,
                            int64_t nnz, int32_t bs, double* nrm_work, double* dnorm_work, int32_t* G_ptr,
                            int32_t* G_col, double* G_val, int32_t* flags_dev, void* stream);
+/* n_agg_dev[0] = number of aggregates, n_agg_dev[1] = largest aggregate size;
+ * nnz_cap: capacity of G_col / G_val (>= G_ptr[n]; no size readback needed) */
 int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t* G_col, const double* G_val, int32_t n,
-                   int32_t max_size, int32_t* agg, int32_t* size_work, int32_t* n_agg_dev, void* stream);
+                   int32_t max_size, int32_t* agg, int32_t* size_work, int32_t* n_agg_dev, int64_t nnz_cap,
+                   void* stream);
 int bamg_aggregate_members(bamg_ctx* ctx, const int32_t* agg, int32_t n, int32_t n_agg, int32_t* agg_ptr,
                            int32_t* members, void* stream);
 int bamg_gauge_nullspace(bamg_ctx* ctx, const double* cams, int32_t nc, double* K, void* stream);

@@ -231,12 +231,20 @@ k_aggregate(const int* __restrict__ G_ptr, const int* __restrict__ G_col, const 
     __syncwarp();
   }
   __syncwarp();
-  if (use_smem)
-    for (int i = lane; i < n; i += 32) {
+  int mx = 0;
+  for (int i = lane; i < n; i += 32) {
+    if (use_smem) {
       agg_g[i] = agg[i];
       size_g[i] = size[i];
     }
-  if (lane == 0) *n_agg_out = nagg;
+    if (i < nagg) mx = max(mx, size[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL_MASK, mx, o));
+  if (lane == 0) {
+    n_agg_out[0] = nagg;
+    n_agg_out[1] = mx;
+  }
 }
 
 // Same greedy scan (identical decisions), restructured around its real cost: the
@@ -483,20 +491,27 @@ k_aggregate_ring(const int* __restrict__ G_ptr, const int* __restrict__ G_col, c
     __syncwarp();
   }
   __syncwarp();
+  int mx = 0;
   for (int i = lane; i < n; i += 32) {
     agg_g[i] = agg[i];
     size_g[i] = size[i];
+    if (i < nagg) mx = max(mx, size[i]);
   }
-  if (lane == 0) *n_agg_out = nagg;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL_MASK, mx, o));
+  if (lane == 0) {
+    n_agg_out[0] = nagg;
+    n_agg_out[1] = mx;  // largest aggregate (sizes the prolongation's shared memory)
+  }
 }
 
 extern "C" int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t* G_col, const double* G_val,
                               int32_t n, int32_t max_size, int32_t* agg, int32_t* size_work, int32_t* n_agg_dev,
-                              void* stream) {
+                              int64_t nnz_cap, void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
   if (n <= 0) {
-    BAMG_CUDA_CHECK(cudaMemsetAsync(n_agg_dev, 0, sizeof(int), st));
+    BAMG_CUDA_CHECK(cudaMemsetAsync(n_agg_dev, 0, 2 * sizeof(int), st));
     return 0;
   }
   const int nwords = (n + 31) / 32;
@@ -507,10 +522,7 @@ extern "C" int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t
     return !(e && e[0] == '0');
   }();
   if (ring_on && smr <= 220 * 1024) {
-    int E = 0;
-    BAMG_CUDA_CHECK(cudaMemcpyAsync(&E, G_ptr + n, sizeof(int), cudaMemcpyDeviceToHost, st));
-    BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
-    size_t ne = (size_t)(E > 0 ? E : 1);
+    size_t ne = (size_t)(nnz_cap > 0 ? nnz_cap : 1);  // sorted copies sized by capacity: no readback
     int* col_s = nullptr;
     double* val_s = nullptr;
     unsigned* uns = nullptr;

@@ -30,12 +30,28 @@ _CHEB_LOWER = 0.3
 class StrengthMatrix:
     """Symmetric nonnegative coupling strengths, CSR without diagonal (multigrid.py:33-49)."""
 
-    def __init__(self, indptr, indices, data, n):
+    def __init__(self, indptr, indices, data, n, _flags=None):
         self.indptr = D.i32(indptr)
-        self.indices = D.i32(indices)
-        self.data = D.f64(data)
+        self._col = D.i32(indices)  # capacity >= nnz when built on the device without a size readback
+        self._val = D.f64(data)
         self._n = int(n)
+        self._nnz = self._col.numel() if _flags is None else None
+        self._flags = _flags  # device flags of operator_strength, checked at the next readback
         self._agg_cache = {}
+
+    @property
+    def nnz(self) -> int:
+        if self._nnz is None:
+            self._nnz = int(self.indptr[self._n].item())
+        return self._nnz
+
+    @property
+    def indices(self):
+        return self._col[: self.nnz]
+
+    @property
+    def data(self):
+        return self._val[: self.nnz]
 
     @staticmethod
     def from_scipy(g) -> "StrengthMatrix":
@@ -82,19 +98,26 @@ def visibility_strength(problem_or_obs) -> StrengthMatrix:
 
 def operator_strength(op: BlockSparseMatrix) -> StrengthMatrix:
     """Block-Frobenius cosine coupling of a square block operator (multigrid.py:83-98)."""
+    st = _operator_strength(op)
+    if int(st._flags[0].item()):
+        raise ValueError("operator has a structurally zero diagonal block")
+    return st
+
+
+def _operator_strength(op: BlockSparseMatrix) -> StrengthMatrix:
+    """operator_strength without a host readback: the off-diagonal count is bounded
+    by nnz - n, and the zero-diagonal flag is checked at the aggregation readback."""
     n, nnz, bs = op.n_block_rows, op.n_block_entries, op.row_block_size
     nrm = D.empty(max(nnz, 1))
     dn = D.empty(max(n, 1))
     G_ptr = D.empty(n + 1, dtype=torch.int32)
     flags = D.empty(2, dtype=torch.int32)
     D.call("bamg_operator_strength", op._ptr, op._col, op.blocks, n, nnz, bs, nrm, dn, G_ptr, None, None, flags)
-    tot = int(G_ptr[n].item())
-    G_col = D.empty(max(tot, 1), dtype=torch.int32)
-    G_val = D.empty(max(tot, 1))
+    cap = max(nnz, 1)
+    G_col = D.empty(cap, dtype=torch.int32)
+    G_val = D.empty(cap)
     D.call("bamg_operator_strength", op._ptr, op._col, op.blocks, n, nnz, bs, nrm, dn, G_ptr, G_col, G_val, flags)
-    if int(flags[0].item()):
-        raise ValueError("operator has a structurally zero diagonal block")
-    return StrengthMatrix(G_ptr, G_col[:tot], G_val[:tot], n)
+    return StrengthMatrix(G_ptr, G_col, G_val, n, _flags=flags)
 
 
 class Aggregation:
@@ -136,9 +159,16 @@ def aggregate(strength: StrengthMatrix, max_size: int = 20) -> Aggregation:
     n = strength.n
     agg = D.empty(max(n, 1), dtype=torch.int32)
     work = D.empty(max(n, 1), dtype=torch.int32)
-    na = D.empty(1, dtype=torch.int32)
-    D.call("bamg_aggregate", strength.indptr, strength.indices, strength.data, n, int(max_size), agg, work, na)
-    return Aggregation(agg[:n], int(na.item()))
+    na = D.empty(2, dtype=torch.int32)
+    D.call("bamg_aggregate", strength.indptr, strength._col, strength._val, n, int(max_size), agg, work, na,
+           strength._col.numel())
+    # one readback: aggregate count, largest aggregate, and a pending strength flag
+    vals = (torch.cat([na, strength._flags[:1]]) if strength._flags is not None else na).tolist()
+    if strength._flags is not None and vals[2]:
+        raise ValueError("operator has a structurally zero diagonal block")
+    a = Aggregation(agg[:n], vals[0])
+    a.max_size = vals[1]
+    return a
 
 
 def _aggregate_cached(strength: StrengthMatrix, max_size: int) -> Aggregation:
@@ -162,24 +192,33 @@ def build_prolongation(agg: Aggregation, K: DenseTall, fine_block_size: int):
     if K.rows != n * bs:
         raise ValueError(f"near-nullspace has {K.rows} rows, expected {n * bs}")
     na = agg.n_aggregates
-    ptr, mem = agg.member_lists()
+    ptr, _ = agg.member_lists()
     max_members = int((ptr[1:] - ptr[:-1]).max().item()) if na else 0
+    P, Kc = _prolongation(agg, K, bs, max_members)
+    cnt = P.padded_count.to(torch.int64)
+    a_idx = torch.repeat_interleave(torch.arange(na, device=D.dev()), cnt)
+    start = torch.repeat_interleave(NULLSPACE_DIM - cnt, cnt)
+    off = torch.arange(int(cnt.sum().item()), device=D.dev()) - torch.repeat_interleave(torch.cumsum(cnt, 0) - cnt, cnt)
+    padded = a_idx * NULLSPACE_DIM + start + off
+    return P, Kc, padded
+
+
+def _prolongation(agg: Aggregation, K: DenseTall, bs: int, max_members: int):
+    """(P, K_coarse) without host synchronisation: `max_members` is a bound on the
+    aggregate sizes (the hierarchy passes max_aggregate + 1, multigrid.py:160-176)."""
+    n, na = agg._a32.numel(), agg.n_aggregates
+    ptr, mem = agg.member_lists()
     Pb = D.empty(max(n, 1), bs, NULLSPACE_DIM)
     Kc = D.empty(max(na, 1) * NULLSPACE_DIM, NULLSPACE_DIM)
     info = D.empty(max(na, 1), 2, dtype=torch.int32)
     pad = D.empty(max(na, 1), dtype=torch.int32)
-    D.call("bamg_prolongation_qr", ptr, mem, K.data, na, bs, max_members, Pb, Kc, info, pad)
+    D.call("bamg_prolongation_qr", ptr, mem, K.data, na, bs, int(max_members), Pb, Kc, info, pad)
     rows = torch.arange(n + 1, device=D.dev(), dtype=torch.int32)
     P = BlockSparseMatrix(n, na, bs, NULLSPACE_DIM, rows, agg._a32, Pb[:n], _validate=False)
     P._prolongator = (ptr, mem)
     P.qr_info = info[:na]
     P.padded_count = pad[:na]
-    cnt = pad[:na].to(torch.int64)
-    a_idx = torch.repeat_interleave(torch.arange(na, device=D.dev()), cnt)
-    start = torch.repeat_interleave(NULLSPACE_DIM - cnt, cnt)
-    off = torch.arange(int(cnt.sum().item()), device=D.dev()) - torch.repeat_interleave(torch.cumsum(cnt, 0) - cnt, cnt)
-    padded = a_idx * NULLSPACE_DIM + start + off
-    return P, DenseTall(Kc[: na * NULLSPACE_DIM]), padded
+    return P, DenseTall(Kc[: na * NULLSPACE_DIM])
 
 
 def galerkin(P: BlockSparseMatrix, A: BlockSparseMatrix, agg: Aggregation) -> BlockSparseMatrix:
@@ -491,13 +530,13 @@ def build_hierarchy(sys: SchurSystem, nullspace: DenseTall, strength: StrengthMa
         if cur.index == 0:
             agg = _aggregate_cached(strength, max_aggregate)
         else:
-            agg = aggregate(operator_strength(cur.explicit), max_size=max_aggregate)
+            agg = aggregate(_operator_strength(cur.explicit), max_size=max_aggregate)
         D.phase("mg.aggregate")
         ratio = (agg.n_aggregates * NULLSPACE_DIM) / cur.scalar_dim
         if ratio > max_ratio:
             break
         bs = CAMERA_SIZE if cur.index == 0 else NULLSPACE_DIM
-        P, K_next, padded = build_prolongation(agg, K, bs)
+        P, K_next = _prolongation(agg, K, bs, getattr(agg, "max_size", max_aggregate + 1))
         D.phase("mg.prolong")
         a_next = galerkin(P, cur.explicit, agg)
         D.phase("mg.galerkin")
