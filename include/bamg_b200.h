@@ -283,7 +283,12 @@ int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const bamg_v
 /* multigrid.py:243-284 estimate_lambda_max for a BSR operator; work: (steps+5)*n doubles */
 int bamg_lanczos_lmax(bamg_ctx* ctx, int32_t bs, int32_t nbr, const int32_t* ptr, const int32_t* col,
                       const double* blocks, const double* D, const double* Dinv, const double* v0, int32_t steps,
-                      double* work, double* lambda_out, int32_t* status, const bamg_symop* sym, void* stream);
+                      double* work, double* lambda_out, int32_t* status, const bamg_symop* sym,
+                      double* ab_out_dev, void* stream);
+/* ab_out_dev != NULL: no readback -- the 16 scalars [alpha_0..7 | beta^2_0..7] land in
+ * ab_out_dev and bamg_lanczos_finish (host) replays the break rule and the Ritz max
+ * later, so several levels share one readback */
+int bamg_lanczos_finish(const double* ab_host, int32_t steps, double* lambda_out, int32_t* status);
 
 #ifdef __cplusplus
 }

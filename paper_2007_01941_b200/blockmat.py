@@ -95,6 +95,17 @@ class BlockDiagMatrix:
             self._chol, self._inv = L, inv
         return self
 
+    def _factor_deferred(self):
+        """factor() without the readback: returns the device slot holding the first
+        failing block (0x7FFFFFFF = none); the caller checks it at its next readback."""
+        n, bs = self.n_blocks, self.block_size
+        L = D.empty(n, bs, bs)
+        inv = D.empty(n, bs, bs)
+        bad = D.empty(1, dtype=torch.int32)
+        D.call("bamg_block_chol_inv", self.blocks, n, bs, L, inv, bad)
+        self._chol, self._inv = L, inv
+        return bad
+
     @property
     def factored(self) -> bool:
         return self._inv is not None

@@ -1172,7 +1172,7 @@ __global__ void k_axpy_dev(const double* __restrict__ x, const double* __restric
                            int64_t n) {
   double a = s[i];
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
-    y[t] -= a * x[t];
+    y[t] = fma(-a, x[t], y[t]);
 }
 
 // y = x / sqrt(s[i])
@@ -1188,13 +1188,47 @@ __global__ void k_sqrt_slot(double* s, int i, int j) {
   if (threadIdx.x == 0 && blockIdx.x == 0) s[j] = sqrt(s[i]);
 }
 
+// One modified-Gram-Schmidt step in the D inner product, fused: first finish the
+// previous projection (z' = z - s[prev] q_prev, when q_prev != null; written to
+// z_out), then out = <w, D z'> with w = q_b, or w = z' (q_b == null: ||z'||_D^2).
+// The arithmetic is the unfused sequence's, element for element: the same
+// fma(-c, q, z) update as k_axpy_dev, the same per-row fma chain as
+// k_blockdiag_apply, and the same thread partition / block tree as k_dot (launch
+// with k_dot's grid) -- so the Lanczos scalars are bit-identical to the unfused path.
+__global__ void __launch_bounds__(256)
+k_reorth_step(const double* __restrict__ D, const double* __restrict__ z_in, double* __restrict__ z_out,
+              const double* __restrict__ q_prev, const double* __restrict__ s, int prev,
+              const double* __restrict__ qb, int bs, int64_t n, double* partials, unsigned int* counter,
+              double* out) {
+  __shared__ double scratch[33];
+  double c = q_prev ? s[prev] : 0.0;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = i / bs;
+    int r = (int)(i - b * bs);
+    const double* m = D + (b * bs + r) * bs;
+    const double* zb = z_in + b * bs;
+    const double* qpb = q_prev ? q_prev + b * bs : nullptr;
+    double dz = 0.0;
+    for (int cc = 0; cc < bs; ++cc) {
+      double zc = qpb ? fma(-c, qpb[cc], zb[cc]) : zb[cc];
+      dz = fma(m[cc], zc, dz);
+    }
+    double zi = q_prev ? fma(-c, q_prev[i], z_in[i]) : z_in[i];
+    if (q_prev) z_out[i] = zi;
+    acc = fma(qb ? qb[i] : zi, dz, acc);
+  }
+  acc = block_sum(acc, scratch);
+  grid_finish(partials, counter, acc, scratch, out);
+}
+
 // v0: seeded start vector (device). D: diagonal blocks, Dinv: their inverses.
 // work: (steps + 5) * n doubles. Returns lambda (host) and the Lanczos break
 // status through *status (0 ok, 1 non-finite).
 extern "C" int bamg_lanczos_lmax(bamg_ctx* ctx, int32_t bs, int32_t nbr, const int32_t* ptr, const int32_t* col,
                                  const double* blocks, const double* D, const double* Dinv, const double* v0,
                                  int32_t steps, double* work, double* lambda_out, int32_t* status,
-                                 const bamg_symop* sym, void* stream) {
+                                 const bamg_symop* sym, double* ab_out_dev, void* stream) {
   cudaStream_t st = as_stream(stream);
   int64_t n = (int64_t)nbr * bs;
   double* sc = ctx->scalars + 16;  // [0..15] per step: alpha[s]=sc[s], beta2[s]=sc[8+s]; extras at 64+
@@ -1213,6 +1247,7 @@ extern "C" int bamg_lanczos_lmax(bamg_ctx* ctx, int32_t bs, int32_t nbr, const i
   launch(k_scale_rsqrt_dev, g, 256, 0, st, v0, tmp, 0, basis, n);
   int sg = spmv_grid(nbr);
   if (sg > BAMG_MAX_PARTIALS) sg = BAMG_MAX_PARTIALS;
+  const int rg = grid_for(n, 256, 4);  // k_dot's grid (dot_dev): same partition, same sums
   for (int s = 0; s < steps; ++s) {
     double* q = basis + (int64_t)s * n;
     double* qp = s > 0 ? basis + (int64_t)(s - 1) * n : qprev;
@@ -1226,28 +1261,40 @@ extern "C" int bamg_lanczos_lmax(bamg_ctx* ctx, int32_t bs, int32_t nbr, const i
     // z = D^-1 u - alpha q - beta_prev q_prev   (beta_prev = sqrt(beta2[s-1]))
     if (s > 0) launch(k_sqrt_slot, 1, 1, 0, st, sc, 8 + s - 1, 40 + s - 1);
     launch(k_lanczos_z, g, 256, 0, st, Dinv, u, q, qp, sc, s, s > 0 ? 40 + s - 1 : -1, nbr, bs, z);
-    // full reorthogonalisation in the D inner product: z -= qb (qb . D z)
-    for (int b2 = 0; b2 <= s; ++b2) {
-      double* qb = basis + (int64_t)b2 * n;
-      launch(k_blockdiag_apply, g, 256, 0, st, D, z, nbr, bs, Dz);
-      rc = dot_dev(ctx, qb, Dz, n, tmp + 1, st);
-      if (rc) return rc;
-      launch(k_axpy_dev, g, 256, 0, st, qb, tmp, 1, z, n);
+    // full reorthogonalisation in the D inner product (modified Gram-Schmidt:
+    // z -= q_b <q_b, D z> for b = 0..s), each coefficient fused with the previous
+    // subtraction; the last pass finishes the subtraction and forms ||z||_D^2
+    double* zc = z;   // current z
+    double* zn = Dz;  // the other buffer
+    for (int b2 = 0; b2 <= s + 1; ++b2) {
+      const double* qprev_b = b2 > 0 ? basis + (int64_t)(b2 - 1) * n : nullptr;
+      const double* qb = b2 <= s ? basis + (int64_t)b2 * n : nullptr;
+      double* dst = b2 <= s ? tmp + 1 + (b2 & 1) : sc + 8 + s;  // alternate: the kernel reads the previous slot
+      launch(k_reorth_step, rg, 256, 0, st, D, (const double*)zc, zn, qprev_b, (const double*)tmp,
+             1 + ((b2 + 1) & 1), qb, bs, n, ctx->partials, ctx->counters + BAMG_CTR_DOT, dst);
+      if (qprev_b) std::swap(zc, zn);
     }
-    launch(k_blockdiag_apply, g, 256, 0, st, D, z, nbr, bs, Dz);
-    rc = dot_dev(ctx, z, Dz, n, sc + 8 + s, st);
-    if (rc) return rc;
-    launch(k_scale_rsqrt_dev, g, 256, 0, st, z, sc, 8 + s, basis + (int64_t)(s + 1) * n, n);
+    launch(k_scale_rsqrt_dev, g, 256, 0, st, zc, sc, 8 + s, basis + (int64_t)(s + 1) * n, n);
+  }
+  if (ab_out_dev) {  // deferred: the caller reads several levels' scalars at once
+    BAMG_CUDA_CHECK(cudaMemcpyAsync(ab_out_dev, sc, 16 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    BAMG_LAUNCH_CHECK();
+    return 0;
   }
   double h[16];
   BAMG_CUDA_CHECK(cudaMemcpyAsync(h, sc, 16 * sizeof(double), cudaMemcpyDeviceToHost, st));
   BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
   BAMG_LAUNCH_CHECK();
-  // host replay of the break logic
+  return bamg_lanczos_finish(h, steps, lambda_out, status);
+}
+
+// host replay of the Lanczos break rule (multigrid.py:268-281) on the 16 device
+// scalars [alpha_0..7 | beta^2_0..7], then the Ritz maximum
+extern "C" int bamg_lanczos_finish(const double* ab_host, int32_t steps, double* lambda_out, int32_t* status) {
   std::vector<double> al, be;
   *status = 0;
   for (int s = 0; s < steps; ++s) {
-    double alpha = h[s], beta2 = h[8 + s];
+    double alpha = ab_host[s], beta2 = ab_host[8 + s];
     al.push_back(alpha);
     if (!isfinite(beta2)) {
       *status = 1;

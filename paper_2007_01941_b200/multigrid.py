@@ -15,7 +15,7 @@ import torch
 
 from . import _device as D
 from . import _lib
-from .blockmat import BlockDiagMatrix, BlockSparseMatrix, DenseTall, SymmetricPattern
+from .blockmat import BlockDiagMatrix, BlockSparseMatrix, DenseTall, IndefiniteBlockError, SymmetricPattern
 from .problem import CAMERA_SIZE, BundleProblem, ObsStructure
 from .schur import SchurSystem
 
@@ -285,7 +285,7 @@ def estimate_lambda_max(matvec, jacobi: BlockDiagMatrix, n: int, steps: int = _L
         status = np.zeros(1, dtype=np.int32)
         D.call("bamg_lanczos_lmax", op.row_block_size, op.n_block_rows, op._ptr, op._col, op.blocks, jacobi.blocks,
                jacobi.inverse_blocks(), v, int(steps), work, lam.ctypes.data, status.ctypes.data,
-               op._symop.handle if op._symop is not None else None)
+               op._symop.handle if op._symop is not None else None, None)
         if status[0]:
             raise FloatingPointError("Lanczos iteration produced a non-finite value")
         return float(lam[0])
@@ -517,6 +517,50 @@ def _coarse_factor(op: BlockSparseMatrix):
     return {"inv": inv, "n": n, "L": work}
 
 
+def _setup_smoothers(levels, seed: int) -> None:
+    """Jacobi inverses + Lanczos spectral estimates + Chebyshev bounds for every
+    smoothing level (multigrid.py:425-430, 243-306), with ONE host readback for all
+    levels: the factorisations' failure slots and each level's 16 Lanczos scalars are
+    read together, then the break rule / Ritz value are replayed on the host in level
+    order (errors raised in the reference's order)."""
+    from . import _lib
+
+    pend = []
+    for lvl in levels:
+        jacobi = BlockDiagMatrix(lvl.explicit.diagonal_blocks())
+        op = _explicit_operator(lvl.matvec)
+        n = lvl.scalar_dim
+        if op is None or op.row_block_size != jacobi.block_size or op.shape[0] != n:
+            lvl.smoother = make_smoother(lvl.matvec, jacobi, n, seed=seed + lvl.index)
+            continue
+        bad = jacobi._factor_deferred()
+        v = _start_vector(n, seed + lvl.index)
+        ab = D.empty(16)
+        work = D.empty((_LANCZOS_STEPS + 5) * n)
+        D.call("bamg_lanczos_lmax", op.row_block_size, op.n_block_rows, op._ptr, op._col, op.blocks, jacobi.blocks,
+               jacobi._inv, v, _LANCZOS_STEPS, work, None, None,
+               op._symop.handle if op._symop is not None else None, ab)
+        pend.append((lvl, jacobi, bad, ab, work))
+    if not pend:
+        return
+    host = torch.cat([torch.cat([bad.to(torch.float64), ab]) for _, _, bad, ab, _ in pend]).cpu().numpy()
+    lam = np.zeros(1)
+    status = np.zeros(1, dtype=np.int32)
+    for k, (lvl, jacobi, _, _, _) in enumerate(pend):
+        rec = host[17 * k:17 * (k + 1)]
+        if int(rec[0]) != 0x7FFFFFFF:
+            jacobi._chol = jacobi._inv = None
+            raise IndefiniteBlockError(int(rec[0]))
+        ab = np.ascontiguousarray(rec[1:])
+        _lib.lib().bamg_lanczos_finish(ab.ctypes.data, _LANCZOS_STEPS, lam.ctypes.data, status.ctypes.data)
+        if status[0]:
+            raise FloatingPointError("Lanczos iteration produced a non-finite value")
+        lmax = float(lam[0])
+        if not lmax > 0:
+            raise ValueError(f"nonpositive spectral estimate {lmax}")
+        lvl.smoother = ChebyshevSmoother(jacobi, lmax, _CHEB_LOWER * lmax, _CHEB_UPPER * lmax)
+
+
 def build_hierarchy(sys: SchurSystem, nullspace: DenseTall, strength: StrengthMatrix, *, max_coarse_dim: int = 400,
                     max_ratio: float = 0.7, max_aggregate: int = 20, seed: int = _LANCZOS_SEED) -> MgHierarchy:
     """Coarsen the reduced camera system (multigrid.py:371-441)."""
@@ -545,9 +589,7 @@ def build_hierarchy(sys: SchurSystem, nullspace: DenseTall, strength: StrengthMa
         levels.append(MgLevel(cur.index + 1, a_next.matvec, agg.n_aggregates * NULLSPACE_DIM, a_next, a_next,
                               K_next))
         K = K_next
-    for lvl in levels[:-1]:
-        jacobi = BlockDiagMatrix(lvl.explicit.diagonal_blocks())
-        lvl.smoother = make_smoother(lvl.matvec, jacobi, lvl.scalar_dim, seed=seed + lvl.index)
+    _setup_smoothers(levels[:-1], seed)
     D.phase("mg.smoothers")
     levels[-1].coarse_factor = _coarse_factor(levels[-1].explicit)
     D.phase("mg.coarse")
