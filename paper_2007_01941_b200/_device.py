@@ -24,16 +24,26 @@ def dev() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_ctx_by_stream = {}
+
+
 def ctx() -> int:
+    """The library context of the current stream: every stream gets its own scratch
+    (reduction partials, counters, device scalars), so work on concurrent streams
+    never shares them."""
     global _ctx
     if _ctx is None:
         require_cuda()
         torch.cuda.init()
+        _ctx = True
+    s = torch.cuda.current_stream().cuda_stream
+    c = _ctx_by_stream.get(s)
+    if c is None:
         c = _lib.lib().bamg_ctx_create()
         if not c:
             raise _lib.NativeError(f"bamg_ctx_create failed: {_lib.last_error()}")
-        _ctx = c
-    return _ctx
+        _ctx_by_stream[s] = c
+    return c
 
 
 def stream() -> int:

@@ -517,30 +517,50 @@ def _coarse_factor(op: BlockSparseMatrix):
     return {"inv": inv, "n": n, "L": work}
 
 
+_OVERLAP = __import__("os").environ.get("BAMG_MG_OVERLAP", "1") == "1"
+_SIDE = {}
+
+
+def _side_stream():
+    dev = torch.cuda.current_device()
+    if dev not in _SIDE:
+        _SIDE[dev] = torch.cuda.Stream()
+    return _SIDE[dev]
+
+
 def _setup_smoothers(levels, seed: int) -> None:
     """Jacobi inverses + Lanczos spectral estimates + Chebyshev bounds for every
     smoothing level (multigrid.py:425-430, 243-306), with ONE host readback for all
     levels: the factorisations' failure slots and each level's 16 Lanczos scalars are
     read together, then the break rule / Ritz value are replayed on the host in level
     order (errors raised in the reference's order)."""
+    pend = [p for p in (_smoother_launch(lvl, seed) for lvl in levels) if p is not None]
+    _smoother_finish(pend)
+
+
+def _smoother_launch(lvl, seed: int):
+    """Queue one level's Jacobi factorisation and Lanczos run (no readback); returns
+    the pending record for _smoother_finish, or None when the level took the generic
+    (synchronous) path."""
+    jacobi = BlockDiagMatrix(lvl.explicit.diagonal_blocks())
+    op = _explicit_operator(lvl.matvec)
+    n = lvl.scalar_dim
+    if op is None or op.row_block_size != jacobi.block_size or op.shape[0] != n:
+        lvl.smoother = make_smoother(lvl.matvec, jacobi, n, seed=seed + lvl.index)
+        return None
+    bad = jacobi._factor_deferred()
+    v = _start_vector(n, seed + lvl.index)
+    ab = D.empty(16)
+    work = D.empty((_LANCZOS_STEPS + 5) * n)
+    D.call("bamg_lanczos_lmax", op.row_block_size, op.n_block_rows, op._ptr, op._col, op.blocks, jacobi.blocks,
+           jacobi._inv, v, _LANCZOS_STEPS, work, None, None,
+           op._symop.handle if op._symop is not None else None, ab)
+    return (lvl, jacobi, bad, ab, work)
+
+
+def _smoother_finish(pend) -> None:
     from . import _lib
 
-    pend = []
-    for lvl in levels:
-        jacobi = BlockDiagMatrix(lvl.explicit.diagonal_blocks())
-        op = _explicit_operator(lvl.matvec)
-        n = lvl.scalar_dim
-        if op is None or op.row_block_size != jacobi.block_size or op.shape[0] != n:
-            lvl.smoother = make_smoother(lvl.matvec, jacobi, n, seed=seed + lvl.index)
-            continue
-        bad = jacobi._factor_deferred()
-        v = _start_vector(n, seed + lvl.index)
-        ab = D.empty(16)
-        work = D.empty((_LANCZOS_STEPS + 5) * n)
-        D.call("bamg_lanczos_lmax", op.row_block_size, op.n_block_rows, op._ptr, op._col, op.blocks, jacobi.blocks,
-               jacobi._inv, v, _LANCZOS_STEPS, work, None, None,
-               op._symop.handle if op._symop is not None else None, ab)
-        pend.append((lvl, jacobi, bad, ab, work))
     if not pend:
         return
     host = torch.cat([torch.cat([bad.to(torch.float64), ab]) for _, _, bad, ab, _ in pend]).cpu().numpy()
@@ -569,6 +589,13 @@ def build_hierarchy(sys: SchurSystem, nullspace: DenseTall, strength: StrengthMa
     levels = [level0]
     K = nullspace
     D.phase("start")
+    # A level's smoother (Jacobi factor + Lanczos) depends only on its operator, so it
+    # is queued on a side stream as soon as the next level exists (the level is then
+    # known not to be the coarsest) and overlaps the next coarsening step -- above all
+    # the single-warp aggregation scan. One readback for all levels at the end.
+    main = torch.cuda.current_stream()
+    side = _side_stream() if _OVERLAP else None
+    pend = []
     while levels[-1].scalar_dim > max_coarse_dim:
         cur = levels[-1]
         if cur.index == 0:
@@ -589,7 +616,20 @@ def build_hierarchy(sys: SchurSystem, nullspace: DenseTall, strength: StrengthMa
         levels.append(MgLevel(cur.index + 1, a_next.matvec, agg.n_aggregates * NULLSPACE_DIM, a_next, a_next,
                               K_next))
         K = K_next
-    _setup_smoothers(levels[:-1], seed)
+        if side is not None:
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                p = _smoother_launch(cur, seed)
+            if p is not None:
+                pend.append(p)
+                jac = p[1]  # allocated on the side stream, used by V-cycles on the main one
+                for t in (jac.blocks, jac._inv, jac._chol):
+                    t.record_stream(main)
+    if side is not None:
+        main.wait_stream(side)
+        _smoother_finish(pend)
+    else:
+        _setup_smoothers(levels[:-1], seed)
     D.phase("mg.smoothers")
     levels[-1].coarse_factor = _coarse_factor(levels[-1].explicit)
     D.phase("mg.coarse")
