@@ -201,8 +201,12 @@ extern "C" int bamg_scan_exclusive_i32(bamg_ctx* ctx, const int32_t* in, int32_t
 // Tile = 8 warps x 8 rounds x 32 lanes = 2048 items; within a warp items are
 // ranked round by round with __match_any_sync, so ranks follow input order.
 
+// The scatter stages each tile in shared memory in digit order first, so that the
+// global writes are runs of consecutive addresses per digit (a tile of 4096 items
+// puts ~16 items in each of the 256 buckets) instead of 32 lanes writing to 32
+// different buckets; the permutation is the same (stable, input order per digit).
 #define RS_WARPS 8
-#define RS_ROUNDS 8
+#define RS_ROUNDS 16
 #define RS_TILE (RS_WARPS * RS_ROUNDS * 32)
 
 __global__ void __launch_bounds__(RS_WARPS * 32)
@@ -251,7 +255,8 @@ k_radix_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ v
     __syncwarp();
   }
   __syncthreads();
-  // per-digit exclusive prefix over warps
+  // per-digit exclusive prefix over warps, and the digit's total in the tile
+  __shared__ int dstart[257];
   for (int d = threadIdx.x; d < 256; d += blockDim.x) {
     int run = 0;
     for (int q = 0; q < RS_WARPS; ++q) {
@@ -259,17 +264,40 @@ k_radix_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ v
       wcount[q][d] = run;
       run += c;
     }
+    dstart[d + 1] = run;
   }
   __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive prefix over digits: where each digit starts in the tile
+    int s = 0;
+    dstart[0] = 0;
+    for (int d = 0; d < 256; ++d) {
+      int c = dstart[d + 1];
+      dstart[d] = s;
+      s += c;
+    }
+    dstart[256] = s;
+  }
+  __syncthreads();
+  __shared__ uint32_t skey[RS_TILE];
+  __shared__ uint32_t sval[RS_TILE];
 #pragma unroll
   for (int r = 0; r < RS_ROUNDS; ++r) {
     int64_t g = base + r * 32 + lane;
     if (g < n) {
       unsigned d = (key[r] >> shift) & 255u;
-      int64_t pos = (int64_t)tile_off[d] + wcount[w][d] + rank[r];
-      kout[pos] = key[r];
-      vout[pos] = val[r];
+      int lp = dstart[d] + wcount[w][d] + rank[r];
+      skey[lp] = key[r];
+      sval[lp] = val[r];
     }
+  }
+  __syncthreads();
+  int cnt = dstart[256];
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    uint32_t k = skey[i];
+    unsigned d = (k >> shift) & 255u;
+    int64_t pos = (int64_t)tile_off[d] + (i - dstart[d]);
+    kout[pos] = k;
+    vout[pos] = sval[i];
   }
 }
 
