@@ -421,6 +421,21 @@ def evaluate(problem: BundleProblem, camera_params=None, points=None, with_jacob
                                                    problem._pi)
 
 
+def _objective_dev(problem: BundleProblem, cams, pts, obj_out, n_behind_out) -> None:
+    """Objective-only evaluation into device slots (no readback): the LM driver's
+    candidate step (solver.py:282-286) decides on the device (bamg_lm_trial)."""
+    st = problem._st
+    k = st.k
+    if not k:
+        obj_out.zero_()
+        n_behind_out.zero_()
+        return
+    huber = 1 if problem.loss == "huber" else 0
+    behind = D.empty(k, dtype=torch.uint8)
+    D.call("bamg_evaluate", cams, pts, st.obs_cam_pm, st.obs_pt_pm, st.pix_pm, k, huber, 0, None, None, behind,
+           obj_out, n_behind_out)
+
+
 def gauge_nullspace(problem: BundleProblem, camera_params=None) -> DenseTall:
     """Camera-space near-nullspace basis, (9 n_cameras) x 16 (problem.py:332-352)."""
     cams, _ = _params(problem, camera_params, None)

@@ -195,3 +195,50 @@ def test_midsize_scene_matches_oracle(P, which):
     xo, repo = O.pcg(os_.matvec, lambda r: O.vcycle(lv, 0, None, r), os_.rhs, 1e-30, 20000, 1e-6)
     assert abs(rep.iterations - repo.iterations) <= 2, (rep.iterations, repo.iterations)
     assert relerr(H(x), xo) <= 1e-3
+
+
+def test_lm_trial_decision_on_device(P):
+    """bamg_lm_trial (solver.py:276-301): the device decision reproduces the host
+    formulas -- decrease, rho, acceptance, step norm -- and on acceptance moves the
+    canonicalised candidate into the parameters; rejection and behind-camera
+    candidates leave them untouched."""
+    import math
+
+    from paper_2007_01941_b200 import _device as D
+
+    nc, npt = 3, 4
+    rng = np.random.default_rng(0)
+    cams0 = rng.normal(size=(nc, 9))
+    cand = cams0 + 0.01
+    cand[1, :3] = [4.0, 0.0, 0.0]  # |aa| > pi: canonicalised on acceptance
+    pts0, cpts = rng.normal(size=(npt, 3)), rng.normal(size=(npt, 3))
+
+    def run(tvals, behind, min_rho=1e-3):
+        cams, pts = D.f64(cams0.copy()), D.f64(pts0.copy())
+        t = D.f64(np.array(tvals + [0.0]))
+        nb = D.i32(np.array([behind], dtype=np.int32))
+        out = D.empty(5)
+        D.call("bamg_lm_trial", t, nb, min_rho, cams, D.f64(cand), nc, pts, D.f64(cpts), npt, out)
+        return H(out), H(cams), H(pts)
+
+    a, b, c, dcn, dpn, f, fn = 3.0, 2.5, 0.75, 0.04, 0.09, 10.0, 9.0
+    out, cams, pts = run([a, b, c, dcn, dpn, f, fn], 0)
+    dec = a - 0.5 * b + 0.5 * c
+    rho = 0.5 * (f - fn) / dec
+    assert out[0] == rho and out[1] == 1.0 and out[2] == dec and out[3] == math.sqrt(dcn + dpn) and out[4] == fn
+    np.testing.assert_array_equal(pts, cpts)
+    np.testing.assert_array_equal(cams[0], cand[0])
+    th = 4.0
+    assert abs(cams[1, 0] - th * (1.0 - 2.0 * math.pi / th)) < 1e-15 and np.linalg.norm(cams[1, :3]) <= math.pi
+    # rejected: f_new > f
+    out, cams, pts = run([a, b, c, dcn, dpn, f, 11.0], 0)
+    assert out[0] < 0 and out[1] == 0.0
+    np.testing.assert_array_equal(cams, cams0)
+    np.testing.assert_array_equal(pts, pts0)
+    # candidate behind a camera: rho = -inf, objective kept
+    out, cams, _ = run([a, b, c, dcn, dpn, f, fn], 3)
+    assert out[0] == -np.inf and out[1] == 0.0 and out[4] == f
+    np.testing.assert_array_equal(cams, cams0)
+    # nonpositive model decrease: rho = -inf
+    out, _, _ = run([0.0, 2.0, 0.0, dcn, dpn, f, fn], 0)
+    assert out[0] == -np.inf and out[1] == 0.0
