@@ -201,9 +201,20 @@ k_sym9_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const i
   for (int row = warp; row < nbr; row += nwarps) {
     double s = 0.0;
     if (g < 3) {
-      int p1 = dpos[row];
-#pragma unroll 4
-      for (int p = ptr[row] + g; p < p1; p += 3) s += __ldg(T + (int64_t)__ldg(tpos + p) * 9 + c);
+      int p = ptr[row] + g, p1 = dpos[row];
+      // batches of 6 (this lane's p, p+3, ...): indices, then products, then the
+      // in-order additions -- same sums, 6 gathers in flight instead of 1
+      for (; p + 15 < p1; p += 18) {
+        int tp[6];
+        double v[6];
+#pragma unroll
+        for (int u = 0; u < 6; ++u) tp[u] = __ldg(tpos + p + 3 * u);
+#pragma unroll
+        for (int u = 0; u < 6; ++u) v[u] = __ldg(T + (int64_t)tp[u] * 9 + c);
+#pragma unroll
+        for (int u = 0; u < 6; ++u) s += v[u];
+      }
+      for (; p < p1; p += 3) s += __ldg(T + (int64_t)__ldg(tpos + p) * 9 + c);
     }
     double s1 = __shfl_down_sync(FULL_MASK, s, 9);
     double s2 = __shfl_down_sync(FULL_MASK, s, 18);
@@ -318,9 +329,20 @@ k_sym16_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const 
     double ax = 0.0;
     if (ok) {
       double lo = 0.0, up = 0.0;
-      int p1 = dpos[row];
-#pragma unroll 4
-      for (int p = ptr[row]; p < p1; ++p) lo += __ldg(T + (int64_t)__ldg(tpos + p) * 16 + r);
+      int p = ptr[row], p1 = dpos[row];
+      // batches of 8: the mirror indices, then the products, are loaded before the
+      // (in-order, so bit-identical) additions -- 8 gathers in flight, not 1
+      for (; p + 8 <= p1; p += 8) {
+        int tp[8];
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) tp[u] = __ldg(tpos + p + u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(T + (int64_t)tp[u] * 16 + r);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) lo += v[u];
+      }
+      for (; p < p1; ++p) lo += __ldg(T + (int64_t)__ldg(tpos + p) * 16 + r);
       for (int k = ucptr[row]; k < ucptr[row + 1]; ++k) up += yup[(int64_t)k * 16 + r];
       ax = lo + up;
     }
