@@ -139,6 +139,16 @@ __device__ __forceinline__ void cp_async_wait_dyn(int pending) {
   }
 }
 
+// Asynchronous form of gather_records (below) for warp-per-segment gathers: the
+// pieces of up to 32 observation records are copied by cp.async into a TRANSPOSED
+// shared layout -- piece p of lane l's record at buf + p*64 + 2l (16 B aligned,
+// conflict-free reads) -- so a warp can double-buffer: the copies of chunk c+1 are
+// in flight while chunk c is consumed. NA pieces from 16 B piece a0 of the record,
+// NB from b0. Commits one cp.async group.
+template <int NA, int NB, int NX>
+__device__ __forceinline__ void rec_issue(const double* __restrict__ J, int o_lane, bool valid, int a0, int b0,
+                                          const double* __restrict__ extra, double* buf, int lane);
+
 __device__ __forceinline__ int lower_bound_i32(const int* a, int n, int key) {
   int lo = 0, hi = n;
   while (lo < hi) {
@@ -187,5 +197,22 @@ __device__ __forceinline__ void gather_records(const double* __restrict__ J, int
     buf[l * ST + 2 * i + 1] = v[k].y;
   }
   __syncwarp();
+}
+
+template <int NA, int NB, int NX>
+__device__ __forceinline__ void rec_issue(const double* __restrict__ J, int o_lane, bool valid, int a0, int b0,
+                                          const double* __restrict__ extra, double* buf, int lane) {
+  constexpr int NP = NA + NB + NX;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    int idx = k * 32 + lane;
+    int l = idx / NP, i = idx - l * NP;
+    int o = __shfl_sync(FULL_MASK, o_lane, l);
+    int vv = __shfl_sync(FULL_MASK, (int)valid, l);
+    const double* src = i < NA + NB ? J + (int64_t)o * REC + 2 * (i < NA ? a0 + i : b0 + i - NA)
+                                    : extra + (int64_t)o * 2;  // NX: one 16 B piece per obs of `extra`
+    if (vv) cp_async16(buf + i * 64 + 2 * l, src);
+  }
+  cp_async_commit();
 }
 

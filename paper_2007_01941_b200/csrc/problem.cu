@@ -489,14 +489,18 @@ extern "C" int bamg_evaluate(bamg_ctx* ctx, const double* cams, const double* pt
 // normal-equation blocks (problem.py:255-269, schur.py:104-112)
 
 #define CN_ST 21  // 9 F pieces + residual piece = 20 doubles, odd stride
+#ifndef CN_STAGES
+#define CN_STAGES 4  // chunks of 32 records in flight per warp (k_cam_normal)
+#endif
 
 // Warp per camera: A_raw = sum F^T F (full 9x9), g = sum F^T r.
 __global__ void __launch_bounds__(128)
 k_cam_normal(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, const double* __restrict__ J, int nc,
              double* __restrict__ A_raw, double* __restrict__ g_cam) {
-  __shared__ double sbuf[4][32 * CN_ST];
-  int lane = threadIdx.x & 31;
-  double* buf = sbuf[threadIdx.x >> 5];
+  // CN_STAGES chunk buffers per warp (rec_issue layout): F pieces 0..8, residual 9
+  extern __shared__ __align__(16) double cn_smem[];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* wbuf = cn_smem + (size_t)w * CN_STAGES * 640;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int i = warp; i < nc; i += nwarps) {
@@ -506,14 +510,40 @@ k_cam_normal(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
     for (int q = 0; q < 45; ++q) a[q] = 0.0;
 #pragma unroll
     for (int q = 0; q < 9; ++q) g[q] = 0.0;
-    for (int base = cam_ptr[i]; base < cam_ptr[i + 1]; base += 32) {
-      int q = base + lane;
-      bool valid = q < cam_ptr[i + 1];
-      int o = valid ? cm_list[q] : 0;
-      gather_records<9, 1, 0, CN_ST>(J, o, valid, 0, RR / 2, nullptr, buf, lane);
-      const double* f = buf + lane * CN_ST;
+    const int q0 = cam_ptr[i], q1 = cam_ptr[i + 1];
+#pragma unroll
+    for (int s = 0; s < CN_STAGES - 1; ++s) {  // prologue: chunks 0 .. CN_STAGES-2
+      int cb = q0 + 32 * s;
+      if (cb < q1) {
+        bool v = cb + lane < q1;
+        rec_issue<9, 1, 0>(J, v ? cm_list[cb + lane] : 0, v, 0, RR / 2, nullptr, wbuf + s * 640, lane);
+      } else {
+        cp_async_commit();
+      }
+    }
+    int c = 0;
+    for (int base = q0; base < q1; base += 32, ++c) {
+      // chunk c + CN_STAGES - 1 goes out before chunk c is consumed
+      int nb = base + 32 * (CN_STAGES - 1);
+      if (nb < q1) {
+        bool vn = nb + lane < q1;
+        rec_issue<9, 1, 0>(J, vn ? cm_list[nb + lane] : 0, vn, 0, RR / 2, nullptr,
+                           wbuf + ((c + CN_STAGES - 1) % CN_STAGES) * 640, lane);
+      } else {
+        cp_async_commit();
+      }
+      cp_async_wait<CN_STAGES - 1>();
+      __syncwarp();
+      bool valid = base + lane < q1;
+      const double* b = wbuf + (c % CN_STAGES) * 640 + 2 * lane;
       if (valid) {
-        double r0 = f[18], r1 = f[19];
+        double f[18];
+#pragma unroll
+        for (int j = 0; j < 9; ++j) {
+          f[2 * j] = b[j * 64];
+          f[2 * j + 1] = b[j * 64 + 1];
+        }
+        double r0 = b[9 * 64], r1 = b[9 * 64 + 1];
         int t = 0;
 #pragma unroll
         for (int j = 0; j < 9; ++j) {
@@ -525,6 +555,7 @@ k_cam_normal(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
       }
       __syncwarp();
     }
+    cp_async_wait<0>();
 #pragma unroll
     for (int q = 0; q < 45; ++q) a[q] = warp_sum(a[q]);
 #pragma unroll
@@ -580,7 +611,13 @@ extern "C" int bamg_normal_blocks(bamg_ctx* ctx, const int32_t* cam_ptr, const i
   (void)ctx;
   cudaStream_t st = as_stream(stream);
   if (nc > 0) {
-    launch(k_cam_normal, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, J, nc, A_raw, g_cam);
+    const size_t sm = sizeof(double) * 4 * CN_STAGES * 640;
+    static bool attr = false;
+    if (!attr) {
+      BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_cam_normal, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      attr = true;
+    }
+    launch(k_cam_normal, grid_for((int64_t)nc * 32, 128, 8), 128, sm, st, cam_ptr, cm_list, J, nc, A_raw, g_cam);
     BAMG_LAUNCH_CHECK();
   }
   if (npt > 0) {
@@ -710,28 +747,55 @@ __global__ void __launch_bounds__(128)
 k_cam_gather(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, const double* __restrict__ J,
              const double* __restrict__ qo, const double* __restrict__ g_cam, const double* __restrict__ A,
              const double* __restrict__ x, int nc, double* __restrict__ out) {
-  __shared__ double sbuf[4][32 * CN_ST];
-  int lane = threadIdx.x & 31;
-  double* buf = sbuf[threadIdx.x >> 5];
+  // the k_cam_normal pipeline: F pieces 0..8 of the record + this obs's q (piece 9)
+  extern __shared__ __align__(16) double cn_smem[];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* wbuf = cn_smem + (size_t)w * CN_STAGES * 640;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int i = warp; i < nc; i += nwarps) {
     double s[9];
 #pragma unroll
     for (int j = 0; j < 9; ++j) s[j] = 0.0;
-    for (int base = cam_ptr[i]; base < cam_ptr[i + 1]; base += 32) {
-      int q = base + lane;
-      bool valid = q < cam_ptr[i + 1];
-      int o = valid ? cm_list[q] : 0;
-      gather_records<9, 0, 1, CN_ST>(J, o, valid, 0, 0, qo, buf, lane);
-      const double* f = buf + lane * CN_ST;
-      if (valid) {
-        double q0 = f[18], q1 = f[19];
+    const int q0 = cam_ptr[i], q1 = cam_ptr[i + 1];
 #pragma unroll
-        for (int j = 0; j < 9; ++j) s[j] += f[j] * q0 + f[9 + j] * q1;
+    for (int st = 0; st < CN_STAGES - 1; ++st) {
+      int cb = q0 + 32 * st;
+      if (cb < q1) {
+        bool v = cb + lane < q1;
+        rec_issue<9, 0, 1>(J, v ? cm_list[cb + lane] : 0, v, 0, 0, qo, wbuf + st * 640, lane);
+      } else {
+        cp_async_commit();
+      }
+    }
+    int c = 0;
+    for (int base = q0; base < q1; base += 32, ++c) {
+      int nb = base + 32 * (CN_STAGES - 1);
+      if (nb < q1) {
+        bool vn = nb + lane < q1;
+        rec_issue<9, 0, 1>(J, vn ? cm_list[nb + lane] : 0, vn, 0, 0, qo,
+                           wbuf + ((c + CN_STAGES - 1) % CN_STAGES) * 640, lane);
+      } else {
+        cp_async_commit();
+      }
+      cp_async_wait<CN_STAGES - 1>();
+      __syncwarp();
+      bool valid = base + lane < q1;
+      const double* b = wbuf + (c % CN_STAGES) * 640 + 2 * lane;
+      if (valid) {
+        double f[18];
+#pragma unroll
+        for (int j = 0; j < 9; ++j) {
+          f[2 * j] = b[j * 64];
+          f[2 * j + 1] = b[j * 64 + 1];
+        }
+        double q0v = b[9 * 64], q1v = b[9 * 64 + 1];
+#pragma unroll
+        for (int j = 0; j < 9; ++j) s[j] += f[j] * q0v + f[9 + j] * q1v;
       }
       __syncwarp();
     }
+    cp_async_wait<0>();
 #pragma unroll
     for (int j = 0; j < 9; ++j) s[j] = warp_sum(s[j]);
     if (lane < 9) {
@@ -754,6 +818,16 @@ k_cam_gather(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
   }
 }
 
+static size_t cam_gather_smem() {
+  const size_t sm = sizeof(double) * 4 * CN_STAGES * 640;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_cam_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  return sm;
+}
+
 extern "C" int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
                                  const int32_t* obs_pt_pm, double* J, int64_t k, const double* A_raw,
                                  const double* C_raw, const double* g_cam, const double* g_pt, const double* d_cam,
@@ -768,8 +842,8 @@ extern "C" int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const in
     launch(k_points_factor, grid_for(npt, 128, 16), 128, 0, st, C_raw, d_pt, g_pt, npt, C, Cinv, Cb, bad_min_dev);
   if (k) launch(k_obs_H, grid_for(k, 256, 8), 256, 0, st, obs_pt_pm, Cinv, Cb, k, J, qo);
   if (nc)
-    launch(k_cam_gather, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, J, qo, g_cam, nullptr,
-           nullptr, nc, rhs);
+    launch(k_cam_gather, grid_for((int64_t)nc * 32, 128, 8), 128, cam_gather_smem(), st, cam_ptr, cm_list, J, qo,
+           g_cam, nullptr, nullptr, nc, rhs);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -841,7 +915,8 @@ extern "C" int bamg_implicit_matvec(bamg_ctx* ctx, const int32_t* cam_ptr, const
   if (npt) launch(k_point_wtx, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, obs_cam_pm, J, Cinv, x, nullptr, npt,
                   nullptr, qo);
   if (nc)
-    launch(k_cam_gather, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, J, qo, nullptr, A, x, nc, y);
+    launch(k_cam_gather, grid_for((int64_t)nc * 32, 128, 8), 128, cam_gather_smem(), st, cam_ptr, cm_list, J, qo,
+           nullptr, A, x, nc, y);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
