@@ -230,25 +230,55 @@ extern "C" int bamg_schur_order_upper(bamg_ctx* ctx, int32_t* up_blk, int32_t* u
 // Diagonal blocks: warp per camera, S_ii = A_i - sum_o F_o^T (H_o E_o^T) F_o.
 // Records (F, E, H = pieces 0..14) are gathered 32 at a time into shared memory.
 #define SD_ST 31
+#ifndef SD_STAGES
+#define SD_STAGES 2
+#endif
 __global__ void __launch_bounds__(128)
 k_schur_diag(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, const double* __restrict__ J,
              const double* __restrict__ A, const int* __restrict__ dpos, int nc, double* __restrict__ S) {
-  __shared__ double sbuf[4][32 * SD_ST];
-  int lane = threadIdx.x & 31;
-  double* buf = sbuf[threadIdx.x >> 5];
+  // SD_STAGES-deep cp.async pipeline of 32-record chunks (pieces 0..14: F, E, H)
+  extern __shared__ __align__(16) double sd_smem[];
+  constexpr int CH = 15 * 64;
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* wbuf = sd_smem + (size_t)w * SD_STAGES * CH;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int i = warp; i < nc; i += nwarps) {
     double acc[45];
 #pragma unroll
     for (int q = 0; q < 45; ++q) acc[q] = 0.0;
-    for (int base = cam_ptr[i]; base < cam_ptr[i + 1]; base += 32) {
-      int q = base + lane;
-      bool valid = q < cam_ptr[i + 1];
-      int o = valid ? cm_list[q] : 0;
-      gather_records<15, 0, 0, SD_ST>(J, o, valid, 0, 0, nullptr, buf, lane);
-      const double* f = buf + lane * SD_ST;
+    const int q0 = cam_ptr[i], q1 = cam_ptr[i + 1];
+#pragma unroll
+    for (int s = 0; s < SD_STAGES - 1; ++s) {
+      int cb = q0 + 32 * s;
+      if (cb < q1) {
+        bool v = cb + lane < q1;
+        rec_issue<15, 0, 0>(J, v ? cm_list[cb + lane] : 0, v, 0, 0, nullptr, wbuf + s * CH, lane);
+      } else {
+        cp_async_commit();
+      }
+    }
+    int c = 0;
+    for (int base = q0; base < q1; base += 32, ++c) {
+      int nb = base + 32 * (SD_STAGES - 1);
+      if (nb < q1) {
+        bool vn = nb + lane < q1;
+        rec_issue<15, 0, 0>(J, vn ? cm_list[nb + lane] : 0, vn, 0, 0, nullptr,
+                            wbuf + ((c + SD_STAGES - 1) % SD_STAGES) * CH, lane);
+      } else {
+        cp_async_commit();
+      }
+      cp_async_wait<SD_STAGES - 1>();
+      __syncwarp();
+      bool valid = base + lane < q1;
+      const double* bsrc = wbuf + (c % SD_STAGES) * CH + 2 * lane;
+      double f[30];
       if (valid) {
+#pragma unroll
+        for (int p = 0; p < 15; ++p) {
+          f[2 * p] = bsrc[p * 64];
+          f[2 * p + 1] = bsrc[p * 64 + 1];
+        }
         const double* e = f + RE;
         const double* h = f + RH;
         double g00 = h[0] * e[0] + h[1] * e[1] + h[2] * e[2];
@@ -266,6 +296,7 @@ k_schur_diag(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
       }
       __syncwarp();
     }
+    cp_async_wait<0>();
 #pragma unroll
     for (int q = 0; q < 45; ++q) acc[q] = warp_sum(acc[q]);
     if (lane == 0) {
@@ -704,6 +735,16 @@ k_schur_rows(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
   }
 }
 
+static size_t schur_diag_smem() {
+  const size_t sm = sizeof(double) * 4 * SD_STAGES * 15 * 64;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_schur_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  return sm;
+}
+
 extern "C" int bamg_schur_numeric_rows(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
                                        const int32_t* pt_ptr, const int32_t* obs_cam_pm, const int32_t* obs_pt_pm,
                                        const double* J, const double* A, const int32_t* S_ptr, const int32_t* S_col,
@@ -711,7 +752,8 @@ extern "C" int bamg_schur_numeric_rows(bamg_ctx* ctx, const int32_t* cam_ptr, co
                                        double* S, void* stream) {
   cudaStream_t st = as_stream(stream);
   if (nc <= 0) return 0;
-  launch(k_schur_diag, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, J, A, dpos, nc, S);
+  launch(k_schur_diag, grid_for((int64_t)nc * 32, 128, 8), 128, schur_diag_smem(), st, cam_ptr, cm_list, J, A, dpos,
+         nc, S);
   const size_t budget = 200 * 1024;
   size_t fixed = sizeof(SrEntry) * SR_WARPS * SR_QCAP;
   int use_map = (nc <= 40000) ? 1 : 0;
@@ -739,7 +781,9 @@ extern "C" int bamg_schur_numeric(bamg_ctx* ctx, const int32_t* cam_ptr, const i
                                   const int32_t* pair_a, const int32_t* pair_b, double* S, void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
-  if (nc) launch(k_schur_diag, grid_for((int64_t)nc * 32, 128, 8), 128, 0, st, cam_ptr, cm_list, J, A, dpos, nc, S);
+  if (nc)
+    launch(k_schur_diag, grid_for((int64_t)nc * 32, 128, 8), 128, schur_diag_smem(), st, cam_ptr, cm_list, J, A, dpos,
+           nc, S);
   if (n_up) {
     int64_t warps = ceil_div(n_up, OFF_GROUPS);
     static const int variant = [] {
