@@ -120,6 +120,11 @@ __device__ __forceinline__ void cp_async16_zfill(void* sdst, const void* gsrc, i
   unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(src_bytes) : "memory");
 }
+// 8 B copy (L1-cached form; for sources that are only 8 B aligned)
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {

@@ -1095,6 +1095,83 @@ k_galerkin_cta(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_so
   }
 }
 
+// k_galerkin_cta with the fine-block operands streamed: each warp keeps two stages
+// of (A_ij, P_j, P_i) in shared memory and copies the next fine block's operands
+// with cp.async while it multiplies the current one. Same operands, same code,
+// same order -- bit-identical to k_galerkin_cta.
+template <int BS>
+__global__ void __launch_bounds__(128)
+k_galerkin_pipe(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_sorted, const int* __restrict__ fine_row,
+                const int* __restrict__ col, const double* __restrict__ blocks, const double* __restrict__ P,
+                int64_t nnz_coarse, double* __restrict__ out) {
+  constexpr int SA = BS * BS, SP = BS * NS, STG = SA + 2 * SP;  // one stage: A | Pj | Pi
+  extern __shared__ __align__(16) double gsm[];
+  __shared__ double sT[4][BS * (NS + 1)];
+  __shared__ double red[4][NS * NS];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int r = lane >> 1, c0 = (lane & 1) * 8;
+  double* stg = gsm + (size_t)w * 2 * STG;
+  double* T = sT[w];
+  auto issue = [&](int q, double* dst) {
+    int fb = fine_sorted[q];
+    int i = fine_row[fb], j = col[fb];
+    const double* a = blocks + (int64_t)fb * SA;
+    const double* pj = P + (int64_t)j * SP;
+    const double* pi = P + (int64_t)i * SP;
+    for (int t = lane; t < SA; t += 32) cp_async8(dst + t, a + t);
+    for (int t = lane; t < SP; t += 32) {
+      cp_async8(dst + SA + t, pj + t);
+      cp_async8(dst + SA + SP + t, pi + t);
+    }
+    cp_async_commit();
+  };
+  for (int64_t cb = blockIdx.x; cb < nnz_coarse; cb += gridDim.x) {
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    const int qb = cblk_ptr[cb], qe = cblk_ptr[cb + 1];
+    if (qb + w < qe) issue(qb + w, stg);
+    int k = 0;
+    for (int q = qb + w; q < qe; q += 4, ++k) {
+      if (q + 4 < qe) issue(q + 4, stg + ((k + 1) & 1) * STG);
+      else cp_async_commit();
+      cp_async_wait<1>();
+      __syncwarp();
+      const double* A = stg + (k & 1) * STG;
+      const double* Pj = A + SA;
+      const double* Pi = A + SA + SP;
+      if (r < BS) {  // T[r][c0..c0+7] = sum_k A[r][k] Pj[k][c0..]
+        double t8[8];
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2) t8[q2] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < BS; ++kk) {
+          double ark = A[r * BS + kk];
+#pragma unroll
+          for (int q2 = 0; q2 < 8; ++q2) t8[q2] = fma(ark, Pj[kk * NS + c0 + q2], t8[q2]);
+        }
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2) T[r * (NS + 1) + c0 + q2] = t8[q2];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int kk = 0; kk < BS; ++kk) {
+        double pik = Pi[kk * NS + r];
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2) acc[q2] = fma(pik, T[kk * (NS + 1) + c0 + q2], acc[q2]);
+      }
+      __syncwarp();
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int q2 = 0; q2 < 8; ++q2) red[w][r * NS + c0 + q2] = acc[q2];
+    __syncthreads();
+    double* o = out + cb * NS * NS;
+    for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) o[e] = ((red[0][e] + red[1][e]) + red[2][e]) + red[3][e];
+    __syncthreads();
+  }
+}
+
 // out_ab = 0.5 (B_ab + B_ba^T), in place, thread per upper block
 __global__ void k_sym_blocks(const int* __restrict__ Cptr, const int* __restrict__ Ccol, int n, double* __restrict__ B) {
   for (int a = blockIdx.x; a < n; a += gridDim.x) {
@@ -1179,10 +1256,31 @@ extern "C" int bamg_galerkin_numeric(bamg_ctx* ctx, int32_t bs, const int32_t* c
   cudaStream_t st = as_stream(stream);
   if (nnz_coarse <= 0) return 0;
   int g = grid_for(nnz_coarse, 1, 12);
-  switch (bs) {
-    case 9: launch(k_galerkin_cta<9>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
-    case 16: launch(k_galerkin_cta<16>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
-    default: bamg_set_error("galerkin: unsupported block size %d", bs); return BAMG_ERR_UNSUPPORTED;
+  static const bool pipe = [] {
+    const char* e = getenv("BAMG_GALERKIN_PIPE");
+    return !(e && e[0] == '0');
+  }();
+  if (pipe) {
+    static bool attr = false;
+    const size_t sm9 = sizeof(double) * 4 * 2 * (81 + 2 * 9 * NS), sm16 = sizeof(double) * 4 * 2 * (256 + 2 * 16 * NS);
+    if (!attr) {
+      BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_galerkin_pipe<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm9));
+      BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_galerkin_pipe<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm16));
+      attr = true;
+    }
+    switch (bs) {
+      case 9: launch(k_galerkin_pipe<9>, g, 128, sm9, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse,
+                     out); break;
+      case 16: launch(k_galerkin_pipe<16>, g, 128, sm16, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P,
+                      nnz_coarse, out); break;
+      default: bamg_set_error("galerkin: unsupported block size %d", bs); return BAMG_ERR_UNSUPPORTED;
+    }
+  } else {
+    switch (bs) {
+      case 9: launch(k_galerkin_cta<9>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
+      case 16: launch(k_galerkin_cta<16>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
+      default: bamg_set_error("galerkin: unsupported block size %d", bs); return BAMG_ERR_UNSUPPORTED;
+    }
   }
   launch(k_sym_blocks2, grid_for(nnz_coarse, 1, 16), 256, 0, st, Cptr, Ccol, n_agg, nnz_coarse, out);
   launch(k_patch, grid_for(n_agg, 128), 128, 0, st, padded_cnt, Cptr, Ccol, n_agg, out);
