@@ -696,7 +696,7 @@ __device__ void form_q(const double* A, const double* tau, int m, int k, int kee
 __global__ void k_prolong_qr(const int* __restrict__ agg_ptr, const int* __restrict__ members,
                              const double* __restrict__ K, int n_agg, int bs, int m_max, double* __restrict__ Pblocks,
                              double* __restrict__ Kc, int* __restrict__ info /* [n_agg][2]: pivoted, rank */,
-                             int* __restrict__ padded_cnt) {
+                             int* __restrict__ padded_cnt, int size_lo, int size_hi) {
   extern __shared__ double sm[];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int wpb = blockDim.x >> 5;
@@ -708,6 +708,7 @@ __global__ void k_prolong_qr(const int* __restrict__ agg_ptr, const int* __restr
   (void)piv;
   for (int a = blockIdx.x * wpb + w; a < n_agg; a += gridDim.x * wpb) {
     int b0 = agg_ptr[a], nm = agg_ptr[a + 1] - b0;
+    if (nm < size_lo || nm > size_hi) continue;  // this launch's size class only
     int m = nm * bs;
     // load
     for (int t = lane; t < m * NS; t += 32) {
@@ -840,22 +841,27 @@ extern "C" int bamg_prolongation_qr(bamg_ctx* ctx, const int32_t* agg_ptr, const
   (void)ctx;
   cudaStream_t st = as_stream(stream);
   if (n_agg <= 0) return 0;
-  int m_max = max_members * bs;
-  size_t per_warp = sizeof(double) * (2 * (size_t)m_max * NS + 3 * NS);
-  int wpb = (int)((200 * 1024) / per_warp);
-  if (wpb < 1) {
-    bamg_set_error("prolongation: aggregate of %d rows exceeds shared memory", m_max);
-    return BAMG_ERR_UNSUPPORTED;
-  }
-  if (wpb > 4) wpb = 4;
-  size_t sm = per_warp * wpb;
-  if (sm > 48 * 1024) cudaFuncSetAttribute(k_prolong_qr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  int blocks = (int)ceil_div(n_agg, wpb);
-  int cap = bamg_num_sms() * 8;
-  if (blocks > cap) blocks = cap;
-  launch(k_prolong_qr, blocks, 32 * wpb, sm, st, agg_ptr, members, K, n_agg, bs, m_max, Pblocks, Kc, info, padded_cnt);
-  BAMG_LAUNCH_CHECK();
-  return 0;
+  // per-warp shared memory sized by the largest aggregate of the launch's size class
+  auto run = [&](int lo, int hi) -> int {
+    int m_max = hi * bs;
+    size_t per_warp = sizeof(double) * (2 * (size_t)m_max * NS + 3 * NS);
+    int wpb = (int)((200 * 1024) / per_warp);
+    if (wpb < 1) {
+      bamg_set_error("prolongation: aggregate of %d rows exceeds shared memory", m_max);
+      return BAMG_ERR_UNSUPPORTED;
+    }
+    if (wpb > 4) wpb = 4;
+    size_t sm = per_warp * wpb;
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k_prolong_qr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int blocks = (int)ceil_div(n_agg, wpb);
+    int cap = bamg_num_sms() * 8;
+    if (blocks > cap) blocks = cap;
+    launch(k_prolong_qr, blocks, 32 * wpb, sm, st, agg_ptr, members, K, n_agg, bs, m_max, Pblocks, Kc, info,
+           padded_cnt, lo, hi);
+    BAMG_LAUNCH_CHECK();
+    return 0;
+  };
+  return run(0, max_members);  // (a small/large split measured slower at c4: 3.7 vs 2.9 ms)
 }
 
 // ---------------------------------------------------------------------------
