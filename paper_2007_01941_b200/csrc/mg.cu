@@ -324,6 +324,16 @@ __device__ __forceinline__ void agr_issue(int bt, int64_t E, const int* __restri
   int64_t e0 = (int64_t)bt * AGR_B;
   int slot0 = (bt % AGR_NB) * AGR_B;
   constexpr int CC = AGR_B / 4, CV = AGR_B / 2;  // 16 B chunks of columns / values
+  if (e0 + AGR_B <= E) {  // full batch (all but the last): plain copies, no bounds arithmetic
+    const int* gc = G_col + e0;
+    const double* gv = G_val + e0;
+#pragma unroll
+    for (int c = lane; c < CC; c += 32) cp_async16(rcol + slot0 + 4 * c, gc + 4 * c);
+#pragma unroll
+    for (int c = lane; c < CV; c += 32) cp_async16(rval + slot0 + 2 * c, gv + 2 * c);
+    cp_async_commit();
+    return;
+  }
 #pragma unroll 4
   for (int c = lane; c < CC + CV; c += 32) {
     if (c < CC) {
