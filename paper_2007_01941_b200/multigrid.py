@@ -175,8 +175,43 @@ def _aggregate_cached(strength: StrengthMatrix, max_size: int) -> Aggregation:
     # the level-0 graph is parameter independent (solver.py:221-230): same input,
     # same deterministic result, so the scan runs once per strength object
     if max_size not in strength._agg_cache:
-        strength._agg_cache[max_size] = aggregate(strength, max_size)
+        pend = getattr(strength, "_agg_pending", {}).pop(max_size, None)
+        if pend is not None:  # started early on the side stream (_aggregate_prefetch)
+            agg, na, ev = pend
+            torch.cuda.current_stream().wait_event(ev)
+            vals = na.tolist()
+            a = Aggregation(agg[: strength.n], vals[0])
+            a.max_size = vals[1]
+            strength._agg_cache[max_size] = a
+        else:
+            strength._agg_cache[max_size] = aggregate(strength, max_size)
     return strength._agg_cache[max_size]
+
+
+def _aggregate_prefetch(strength: StrengthMatrix, max_size: int) -> None:
+    """Start the level-0 scan of a fresh strength graph on the side stream, no
+    readback: it is a one-warp kernel, so it runs alongside the system assembly
+    that precedes the hierarchy build (first linear solve of a problem)."""
+    if max_size in strength._agg_cache or strength._flags is not None:
+        return
+    pending = strength.__dict__.setdefault("_agg_pending", {})
+    if max_size in pending or not _OVERLAP:
+        return
+    n = strength.n
+    main = torch.cuda.current_stream()
+    side = _side_stream()
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        agg = D.empty(max(n, 1), dtype=torch.int32)
+        work = D.empty(max(n, 1), dtype=torch.int32)
+        na = D.empty(2, dtype=torch.int32)
+        D.call("bamg_aggregate", strength.indptr, strength._col, strength._val, n, int(max_size), agg, work, na,
+               strength._col.numel())
+        ev = torch.cuda.Event()
+        ev.record(side)
+    for t in (agg, na):
+        t.record_stream(main)
+    pending[max_size] = (agg, na, ev)
 
 
 def build_prolongation(agg: Aggregation, K: DenseTall, fine_block_size: int):
