@@ -67,7 +67,7 @@ class ObsStructure:
     """
 
     def __init__(self, cam_index: torch.Tensor, pt_index: torch.Tensor, nc: int, npt: int,
-                 pixels: torch.Tensor):
+                 pixels: torch.Tensor, pix_ready=None):
         k = int(cam_index.numel())
         self.k, self.nc, self.npt = k, nc, npt
         i32 = torch.int32
@@ -80,6 +80,8 @@ class ObsStructure:
         D.call("bamg_obs_orders", cam_index, pt_index, k, nc, npt, self.pm_perm, self.obs_cam_pm,
                self.obs_pt_pm, self.pt_ptr, self.cm_list, self.cam_ptr)
         self.pix_pm = D.empty(k, 2)
+        if pix_ready is not None:  # the pixel copy ran on a copy stream during the sorts
+            torch.cuda.current_stream().wait_event(pix_ready)
         if k:
             D.call("bamg_gather_rows_f64", pixels, self.pm_perm, k, 2, self.pix_pm)
         self._covis = None
@@ -189,6 +191,20 @@ class ObsStructure:
 # -- problem ----------------------------------------------------------------------
 
 
+def _pinned(x) -> bool:
+    return isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned()
+
+
+_COPY_STREAMS = {}
+
+
+def _copy_stream():
+    dev = torch.cuda.current_device()
+    if dev not in _COPY_STREAMS:
+        _COPY_STREAMS[dev] = torch.cuda.Stream()
+    return _COPY_STREAMS[dev]
+
+
 class BundleProblem:
     """Cameras, points and pixel observations (problem.py:81-173), device resident."""
 
@@ -209,9 +225,24 @@ class BundleProblem:
         if _structure is not None:
             self._ci, self._pi, self._pix, self._st = _structure._ci, _structure._pi, _structure._pix, _structure
             return
-        ci = torch.as_tensor(cam_index, device=D.dev()).to(torch.int64).reshape(-1)
-        pi = torch.as_tensor(pt_index, device=D.dev()).to(torch.int64).reshape(-1)
-        pix = D.f64(pixels).reshape(-1, 2) if np.size(pixels) else D.empty(0, 2)
+        if _pinned(cam_index) and _pinned(pt_index) and _pinned(pixels):
+            # pinned host inputs: the index copies go first on the current stream (the
+            # orders sort needs them), the pixel copy runs on a copy stream behind it
+            ci = cam_index.to(D.dev(), non_blocking=True).to(torch.int64).reshape(-1)
+            pi = pt_index.to(D.dev(), non_blocking=True).to(torch.int64).reshape(-1)
+            main = torch.cuda.current_stream()
+            cs = _copy_stream()
+            cs.wait_stream(main)
+            with torch.cuda.stream(cs):
+                pix = pixels.to(D.dev(), dtype=torch.float64, non_blocking=True).reshape(-1, 2)
+            pix.record_stream(main)
+            self._pix_ready = torch.cuda.Event()
+            self._pix_ready.record(cs)
+        else:
+            ci = torch.as_tensor(cam_index, device=D.dev()).to(torch.int64).reshape(-1)
+            pi = torch.as_tensor(pt_index, device=D.dev()).to(torch.int64).reshape(-1)
+            pix = D.f64(pixels).reshape(-1, 2) if np.size(pixels) else D.empty(0, 2)
+            self._pix_ready = None
         if not (ci.numel() == pi.numel() == pix.shape[0]):
             raise ValueError("observation arrays disagree on length")
         k, nc, npt = ci.numel(), cams.shape[0], pts.shape[0]
@@ -221,7 +252,7 @@ class BundleProblem:
                 raise ValueError("camera index out of range")
             if lo_hi[2] < 0 or lo_hi[3] >= npt:
                 raise ValueError("point index out of range")
-        st = ObsStructure(ci.to(torch.int32), pi.to(torch.int32), nc, npt, pix)
+        st = ObsStructure(ci.to(torch.int32), pi.to(torch.int32), nc, npt, pix, self._pix_ready)
         st._ci, st._pi, st._pix = ci, pi, pix
         if k > 1:
             dup = ((st.obs_pt_pm[1:] == st.obs_pt_pm[:-1]) & (st.obs_cam_pm[1:] == st.obs_cam_pm[:-1])).any()
