@@ -373,7 +373,10 @@ __device__ __forceinline__ double loss_w(double s, int huber) {
 // One thread per observation (point-major); the CTA's records are staged in shared
 // memory and written back as contiguous double2 stores (H slots untouched). The
 // objective is reduced deterministically (last block finishes).
-__global__ void __launch_bounds__(EVAL_THREADS)
+#ifndef EVAL_MINB
+#define EVAL_MINB 1
+#endif
+__global__ void __launch_bounds__(EVAL_THREADS, EVAL_MINB)
 k_evaluate(const double* __restrict__ cams, const double* __restrict__ pts, const int* __restrict__ ocam,
            const int* __restrict__ opt, const double* __restrict__ pix, int64_t k, int huber, int with_jac,
            double* __restrict__ J, double* __restrict__ w, unsigned char* __restrict__ behind,

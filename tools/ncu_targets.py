@@ -28,6 +28,11 @@ def main(config=4, what="spmv,vcycle,schur,evaluate"):
     torch.cuda.nvtx.range_push("target")
     if "spmv" in what:
         D.call("bamg_bsr_spmv", 9, S._ptr, S._col, S.blocks, x, y, S.n_block_rows, None)
+    if "galerkin" in what:
+        from paper_2007_01941_b200 import multigrid as MG
+
+        lv = h.levels[0]
+        MG.galerkin(lv.P, lv.explicit, lv.aggregation)  # level 0 -> 1
     if "agg" in what:
         from paper_2007_01941_b200 import multigrid as MG
 
