@@ -1120,9 +1120,12 @@ __global__ void __launch_bounds__(128)
 k_galerkin_pipe(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_sorted, const int* __restrict__ fine_row,
                 const int* __restrict__ col, const double* __restrict__ blocks, const double* __restrict__ P,
                 int64_t nnz_coarse, double* __restrict__ out) {
-  constexpr int SA = BS * BS, SP = BS * NS, STG = SA + 2 * SP;  // one stage: A | Pj | Pi
+  // one stage: A (padded to an even count so P_j / P_i start 16 B aligned) | Pj | Pi.
+  // The kernel is bound by L1 wavefronts (ncu: 83% of peak), so P_j and T are read
+  // as double2 and P copied in 16 B chunks; the arithmetic is untouched.
+  constexpr int SA = BS * BS, SAP = (SA + 1) & ~1, SP = BS * NS, STG = SAP + 2 * SP, TS = NS + 2;
   extern __shared__ __align__(16) double gsm[];
-  __shared__ double sT[4][BS * (NS + 1)];
+  __shared__ __align__(16) double sT[4][BS * TS];
   __shared__ double red[4][NS * NS];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int r = lane >> 1, c0 = (lane & 1) * 8;
@@ -1135,9 +1138,9 @@ k_galerkin_pipe(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_s
     const double* pj = P + (int64_t)j * SP;
     const double* pi = P + (int64_t)i * SP;
     for (int t = lane; t < SA; t += 32) cp_async8(dst + t, a + t);
-    for (int t = lane; t < SP; t += 32) {
-      cp_async8(dst + SA + t, pj + t);
-      cp_async8(dst + SA + SP + t, pi + t);
+    for (int t = lane; t < SP / 2; t += 32) {
+      cp_async16(dst + SAP + 2 * t, pj + 2 * t);
+      cp_async16(dst + SAP + SP + 2 * t, pi + 2 * t);
     }
     cp_async_commit();
   };
@@ -1154,8 +1157,8 @@ k_galerkin_pipe(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_s
       cp_async_wait<1>();
       __syncwarp();
       const double* A = stg + (k & 1) * STG;
-      const double* Pj = A + SA;
-      const double* Pi = A + SA + SP;
+      const double* Pj = A + SAP;
+      const double* Pi = A + SAP + SP;
       if (r < BS) {  // T[r][c0..c0+7] = sum_k A[r][k] Pj[k][c0..]
         double t8[8];
 #pragma unroll
@@ -1163,18 +1166,29 @@ k_galerkin_pipe(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_s
 #pragma unroll
         for (int kk = 0; kk < BS; ++kk) {
           double ark = A[r * BS + kk];
+          const double2* pr = reinterpret_cast<const double2*>(Pj + kk * NS + c0);
 #pragma unroll
-          for (int q2 = 0; q2 < 8; ++q2) t8[q2] = fma(ark, Pj[kk * NS + c0 + q2], t8[q2]);
+          for (int h = 0; h < 4; ++h) {
+            double2 v = pr[h];
+            t8[2 * h] = fma(ark, v.x, t8[2 * h]);
+            t8[2 * h + 1] = fma(ark, v.y, t8[2 * h + 1]);
+          }
         }
+        double2* tw = reinterpret_cast<double2*>(T + r * TS + c0);
 #pragma unroll
-        for (int q2 = 0; q2 < 8; ++q2) T[r * (NS + 1) + c0 + q2] = t8[q2];
+        for (int h = 0; h < 4; ++h) tw[h] = make_double2(t8[2 * h], t8[2 * h + 1]);
       }
       __syncwarp();
 #pragma unroll
       for (int kk = 0; kk < BS; ++kk) {
         double pik = Pi[kk * NS + r];
+        const double2* tr = reinterpret_cast<const double2*>(T + kk * TS + c0);
 #pragma unroll
-        for (int q2 = 0; q2 < 8; ++q2) acc[q2] = fma(pik, T[kk * (NS + 1) + c0 + q2], acc[q2]);
+        for (int h = 0; h < 4; ++h) {
+          double2 v = tr[h];
+          acc[2 * h] = fma(pik, v.x, acc[2 * h]);
+          acc[2 * h + 1] = fma(pik, v.y, acc[2 * h + 1]);
+        }
       }
       __syncwarp();
     }
@@ -1278,7 +1292,7 @@ extern "C" int bamg_galerkin_numeric(bamg_ctx* ctx, int32_t bs, const int32_t* c
   }();
   if (pipe) {
     static bool attr = false;
-    const size_t sm9 = sizeof(double) * 4 * 2 * (81 + 2 * 9 * NS), sm16 = sizeof(double) * 4 * 2 * (256 + 2 * 16 * NS);
+    const size_t sm9 = sizeof(double) * 4 * 2 * (82 + 2 * 9 * NS), sm16 = sizeof(double) * 4 * 2 * (256 + 2 * 16 * NS);
     if (!attr) {
       BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_galerkin_pipe<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm9));
       BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_galerkin_pipe<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm16));
