@@ -116,14 +116,19 @@ def _arg(a):
     return a
 
 
+_fns: dict = {}
+
+
 def call(name: str, *args) -> int:
     """Invoke a bamg_* entry point; torch tensors pass their device pointers.
 
     Raises NativeError on CUDA failures (rc < 0) and returns domain codes (> 0)
     to the caller, which maps them onto the reference exception classes.
     """
-    fn = getattr(lib(), name)
-    rc = fn(*[_arg(a) for a in args])
+    fn = _fns.get(name)
+    if fn is None:
+        fn = _fns[name] = getattr(lib(), name)
+    rc = fn(*[a.data_ptr() if hasattr(a, "data_ptr") else a for a in args])
     if rc is None:
         return 0
     if isinstance(rc, float):

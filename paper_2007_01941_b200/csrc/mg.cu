@@ -262,17 +262,20 @@ k_aggregate(const int* __restrict__ G_ptr, const int* __restrict__ G_col, const 
 // stop at the first eligible neighbour and only look further along ties of its G.
 // Warp per row, bitonic network in shared memory; rows longer than RS_CAP are left
 // in column order and flagged in `unsorted` (bit per row) for the full scan.
-#define RS_CAP 1024
+// Coarse-level operator rows run to a few thousand entries (an aggregate couples to
+// the union of its members' neighbours), so the per-warp capacity lives in dynamic
+// shared memory: RS_CAP keys + columns per warp, 4 warps per CTA (96 KB).
+#define RS_CAP 2048
 __global__ void __launch_bounds__(128)
 k_rows_sort_desc(const int* __restrict__ G_ptr, const int* __restrict__ G_col, const double* __restrict__ G_val,
                  int n, int* __restrict__ col_s, double* __restrict__ val_s, unsigned* __restrict__ unsorted) {
-  __shared__ unsigned long long sk[4][RS_CAP / 2];
-  __shared__ int sj[4][RS_CAP / 2];
-  // RS_CAP/2 per warp in the static arrays (48 KB limit); longer rows use the flag
+  extern __shared__ __align__(16) unsigned long long rs_smem[];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long* skw = rs_smem + (size_t)w * RS_CAP;
+  int* sjw = reinterpret_cast<int*>(rs_smem + 4 * RS_CAP) + (size_t)w * RS_CAP;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int CAP = RS_CAP / 2;
+  const int CAP = RS_CAP;
   for (int row = warp; row < n; row += nwarps) {
     int s = G_ptr[row], L = G_ptr[row + 1] - s;
     if (L > CAP) {
@@ -289,8 +292,8 @@ k_rows_sort_desc(const int* __restrict__ G_ptr, const int* __restrict__ G_col, c
       bool ok = t < L;
       double g = ok ? G_val[s + t] : 0.0;
       // G >= 0: its bit pattern is monotone; complement for descending order
-      sk[w][t] = ok ? ~(unsigned long long)__double_as_longlong(g + 0.0) : ~0ull;
-      sj[w][t] = ok ? G_col[s + t] : 0x7fffffff;
+      skw[t] = ok ? ~(unsigned long long)__double_as_longlong(g + 0.0) : ~0ull;
+      sjw[t] = ok ? G_col[s + t] : 0x7fffffff;
     }
     __syncwarp();
     for (int k = 2; k <= P; k <<= 1)
@@ -298,22 +301,22 @@ k_rows_sort_desc(const int* __restrict__ G_ptr, const int* __restrict__ G_col, c
         for (int t = lane; t < P; t += 32) {
           int p = t ^ jn;
           if (p > t) {
-            unsigned long long a = sk[w][t], b = sk[w][p];
-            int ja = sj[w][t], jb = sj[w][p];
+            unsigned long long a = skw[t], b = skw[p];
+            int ja = sjw[t], jb = sjw[p];
             bool gt = (a > b) || (a == b && ja > jb);
             if (gt == ((t & k) == 0)) {
-              sk[w][t] = b;
-              sk[w][p] = a;
-              sj[w][t] = jb;
-              sj[w][p] = ja;
+              skw[t] = b;
+              skw[p] = a;
+              sjw[t] = jb;
+              sjw[p] = ja;
             }
           }
         }
         __syncwarp();
       }
     for (int t = lane; t < L; t += 32) {
-      col_s[s + t] = sj[w][t];
-      val_s[s + t] = __longlong_as_double((long long)~sk[w][t]);
+      col_s[s + t] = sjw[t];
+      val_s[s + t] = __longlong_as_double((long long)~skw[t]);
     }
     __syncwarp();
   }
@@ -540,7 +543,13 @@ extern "C" int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t
     BAMG_CUDA_CHECK(cudaMallocAsync(&col_s, sizeof(int) * ne, st));
     BAMG_CUDA_CHECK(cudaMallocAsync(&uns, sizeof(unsigned) * (size_t)nwords, st));
     BAMG_CUDA_CHECK(cudaMemsetAsync(uns, 0, sizeof(unsigned) * (size_t)nwords, st));
-    launch(k_rows_sort_desc, grid_for((int64_t)n * 32, 128, 8), 128, 0, st, G_ptr, G_col, G_val, n, col_s, val_s, uns);
+    static bool rs_attr = false;
+    const size_t rs_sm = (size_t)4 * RS_CAP * (sizeof(unsigned long long) + sizeof(int));
+    if (!rs_attr) {
+      BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_rows_sort_desc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_sm));
+      rs_attr = true;
+    }
+    launch(k_rows_sort_desc, grid_for((int64_t)n * 32, 128, 2), 128, rs_sm, st, G_ptr, G_col, G_val, n, col_s, val_s, uns);
     static size_t attr = 0;
     if (smr > attr) {
       BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr));

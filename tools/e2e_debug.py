@@ -23,3 +23,7 @@ for it in range(6):
     torch.cuda.current_stream().synchronize()
     free, tot = torch.cuda.mem_get_info()
     print(it, "%.1f ms" % ((time.perf_counter() - t0) * 1e3), "reserved %.1fG free %.1fG" % (torch.cuda.memory_reserved() / 1e9, free / 1e9), flush=True)
+    st = torch.cuda.memory_stats()
+    print("   retries", st.get("num_alloc_retries"), "device_alloc", st.get("num_device_alloc"), "device_free", st.get("num_device_free"), "peak %.1fG" % (st["reserved_bytes.all.peak"] / 1e9), flush=True)
+    if len(sys.argv) > 1:
+        del prob2, obj, jac, dc, dp, cg

@@ -37,6 +37,10 @@ def main(config=4, what="spmv,vcycle,schur,evaluate"):
         from paper_2007_01941_b200 import multigrid as MG
 
         MG.aggregate(P.visibility_strength(prob), 20)  # level-0 greedy scan, uncached
+    if "agg1" in what:
+        from paper_2007_01941_b200 import multigrid as MG
+
+        MG.aggregate(MG.operator_strength(h.levels[1].explicit), 20)  # level-1 scan
     if "sym" in what:
         S.matvec(x)  # half-storage product (k_sym9_upper + k_sym9_finish)
     if "vcycle" in what:

@@ -48,7 +48,18 @@ def main(config=4):
           f"{sum(v[0] for v in agg.values())} device ops; levels {[l.scalar_dim for l in h.levels]}")
     for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:40]:
         print(f"  {k[:50]:50s} n={v[0]:5d} {v[1] / 1e3:8.3f} ms")
+    if len(sys.argv) > 2:  # timeline of the hierarchy build: start offset, duration, gap
+        ev = sorted((e for e in prof.events() if e.device_type.name == "CUDA"),
+                    key=lambda e: e.time_range.start)
+        first = next(i for i, e in enumerate(ev) if e.name.startswith("k_aggregate") or "sort_desc" in e.name
+                     or "op_strength" in e.name or "block_fro" in e.name)
+        t0 = ev[first].time_range.start
+        prev_end = t0
+        for e in ev[first:]:
+            st, en = e.time_range.start, e.time_range.end
+            print(f"  {(st - t0) / 1e3:8.3f} ms  {en - st:8.1f} us  gap {st - prev_end:7.1f}  {e.name.split('(')[0][:44]}")
+            prev_end = max(prev_end, en)
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:])
+    main(*sys.argv[1:2])
