@@ -127,7 +127,7 @@ int bamg_schur_symbolic(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs
                         int32_t* up_tpos, void* stream);
 /* reorder the upper-block work list by descending pair count (load balance) */
 int bamg_schur_order_upper(bamg_ctx* ctx, int32_t* up_blk, int32_t* up_row, int32_t* up_tpos, int32_t n_up,
-                           const int32_t* blk_pair_ptr, void* stream);
+                           const int32_t* blk_pair_ptr, const int32_t* pair_a, void* stream);
 /* row-owned variant: no pair lists; one CTA per camera row, shared-memory
  * accumulators, deterministic per-warp slot ownership */
 int bamg_schur_numeric_rows(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* pt_ptr,

@@ -386,13 +386,42 @@ k_evaluate(const double* __restrict__ cams, const double* __restrict__ pts, cons
   double acc = 0.0;
   int nb = 0;
   double* my = rec + threadIdx.x * EVAL_STRIDE;
-  for (int64_t base = (int64_t)blockIdx.x * EVAL_THREADS; base < k; base += (int64_t)gridDim.x * EVAL_THREADS) {
+  // Software pipeline over the grid-stride tiles: the (camera, point, pixel) inputs of
+  // tile i+1 are gathered while tile i is written back, so the index -> parameter
+  // load chain (a DRAM then an L2 latency) no longer sits in front of every tile.
+  const int64_t stride = (int64_t)gridDim.x * EVAL_THREADS;
+  // Indices run two tiles ahead, parameters one tile ahead.
+  double cam[9], X[3], px[2];
+  int ic = 0, ip = 0;  // indices of the next tile to gather
+  auto load_idx = [&](int64_t tt) {
+    if (tt < k) {
+      ic = __ldg(ocam + tt);
+      ip = __ldg(opt + tt);
+    }
+  };
+  auto gather = [&](int64_t tt) {
+    if (tt < k) {
+      const double* c = cams + (int64_t)ic * 9;
+      const double* x = pts + (int64_t)ip * 3;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) cam[q] = __ldg(c + q);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) X[q] = __ldg(x + q);
+      px[0] = __ldg(pix + 2 * tt);
+      px[1] = __ldg(pix + 2 * tt + 1);
+    }
+  };
+  {
+    int64_t t0 = (int64_t)blockIdx.x * EVAL_THREADS + threadIdx.x;
+    load_idx(t0);
+    gather(t0);
+    load_idx(t0 + stride);
+  }
+  for (int64_t base = (int64_t)blockIdx.x * EVAL_THREADS; base < k; base += stride) {
     int64_t t = base + threadIdx.x;
     if (t < k) {
-      const double* cam = cams + (int64_t)ocam[t] * 9;
-      const double* X = pts + (int64_t)opt[t] * 3;
       ProjOut o;
-      bool ok = project_one(cam, X, pix + 2 * t, o);
+      bool ok = project_one(cam, X, px, o);
       if (behind) behind[t] = ok ? 0 : 1;
       if (!ok) {
         ++nb;
@@ -455,6 +484,8 @@ k_evaluate(const double* __restrict__ cams, const double* __restrict__ pts, cons
         }
       }
     }
+    gather(t + stride);  // next tile's inputs in flight during the write-back
+    load_idx(t + 2 * stride);
     if (with_jac) {
       __syncthreads();
       // coalesced write-back of the CTA's records (16 double2 each, skip H = 12..14)

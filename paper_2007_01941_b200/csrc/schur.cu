@@ -174,6 +174,17 @@ __global__ void k_band_keys(const uint32_t* __restrict__ perm, const int* __rest
     key[u] = (uint32_t)(up_row[perm[u]] / band);
 }
 
+__global__ void k_pband_keys(const uint32_t* __restrict__ perm, const int* __restrict__ up_blk,
+                             const int* __restrict__ blk_pair_ptr, const int* __restrict__ pair_a, int n, int pband,
+                             uint32_t* __restrict__ key) {
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+    int b = up_blk[perm[u]];
+    int q0 = blk_pair_ptr[b], q1 = blk_pair_ptr[b + 1];
+    // middle pair's a-side record: the centre of the block's stretch of points
+    key[u] = q1 > q0 ? (uint32_t)(pair_a[(q0 + q1) >> 1] / pband) : 0u;
+  }
+}
+
 __global__ void k_permute3(const uint32_t* __restrict__ perm, int n, int* __restrict__ a, int* __restrict__ b,
                            int* __restrict__ c, int* __restrict__ tmp) {
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
@@ -188,7 +199,8 @@ __global__ void k_copy_i32(const int* __restrict__ src, int* __restrict__ dst, i
 }
 
 extern "C" int bamg_schur_order_upper(bamg_ctx* ctx, int32_t* up_blk, int32_t* up_row, int32_t* up_tpos,
-                                      int32_t n_up, const int32_t* blk_pair_ptr, void* stream) {
+                                      int32_t n_up, const int32_t* blk_pair_ptr, const int32_t* pair_a,
+                                      void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
   if (n_up <= 1) return 0;
@@ -206,9 +218,17 @@ extern "C" int bamg_schur_order_upper(bamg_ctx* ctx, int32_t* up_blk, int32_t* u
   if (rc) return rc;
   // optional row bands (BAMG_SCHUR_BAND rows): blocks of nearby camera rows run
   // together so their observation records stay in L2; count order inside a band
-  int band = 0;
+  int band = 0, pband = 0;
   if (const char* e = getenv("BAMG_SCHUR_BAND")) band = atoi(e);
-  if (band > 0) {
+  if (const char* e = getenv("BAMG_SCHUR_PBAND")) pband = atoi(e);
+  if (pband > 0 && pair_a) {
+    // bands of observation records (point-major): blocks whose pair lists start in
+    // the same stretch of points run together
+    launch(k_pband_keys, grid_for(n_up, 256), 256, 0, st, pv, up_blk, blk_pair_ptr, pair_a, n_up, pband, ck);
+    rc = radix_sort_pairs(ck, pv, sk, io, n_up, 31, st);
+    if (rc) return rc;
+    std::swap(pv, io);
+  } else if (band > 0) {
     launch(k_band_keys, grid_for(n_up, 256), 256, 0, st, pv, up_row, n_up, band, ck);
     rc = radix_sort_pairs(ck, pv, sk, io, n_up, 31, st);
     if (rc) return rc;

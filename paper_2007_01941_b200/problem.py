@@ -183,7 +183,8 @@ class ObsStructure:
         """Per-block point-pair lists (the block-owned alternative assembly)."""
         if getattr(self, "_pairs", None) is None:
             p = self._schur_symbolic(True)
-            D.call("bamg_schur_order_upper", p["up_blk"], p["up_row"], p["up_tpos"], p["n_up"], p["blk_ptr"])
+            D.call("bamg_schur_order_upper", p["up_blk"], p["up_row"], p["up_tpos"], p["n_up"], p["blk_ptr"],
+                   p["pair_a"])
             self._pairs = p
         return self._pairs
 
