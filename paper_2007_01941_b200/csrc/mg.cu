@@ -518,6 +518,232 @@ k_aggregate_ring(const int* __restrict__ G_ptr, const int* __restrict__ G_col, c
   }
 }
 
+// Same greedy scan again (identical decisions), built around the observation that
+// a visit almost always ends inside the first few entries of the sorted row: the
+// first eligible neighbour is the strongest one unless its aggregate is full. Each
+// row's top AH_K entries ("head": columns, strengths, row length) are packed once,
+// in parallel, into a node-ordered array that the scan streams into shared memory
+// in batches of AH_B nodes with cp.async, AH_NB batches ahead. A visit is then
+// eight lanes doing one agg/size lookup each plus two ballots; only a visit whose
+// head holds no eligible entry, or whose tie run reaches the head's end, scans the
+// full sorted row (from global memory), and rows too long to sort take the
+// exhaustive scan -- both with the ring kernel's exact rules.
+#define AH_K 8
+#define AH_B 32
+#define AH_NB 8
+
+__global__ void k_agg_heads(const int* __restrict__ G_ptr, const int* __restrict__ col_s,
+                            const double* __restrict__ val_s, const unsigned* __restrict__ unsorted, int n,
+                            int n_pad, int* __restrict__ hcol, double* __restrict__ hval, int* __restrict__ hlen) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n_pad * AH_K;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(t / AH_K), e = (int)(t - (int64_t)i * AH_K);
+    int c = -1;
+    double g = 0.0;
+    if (i < n) {
+      int s = G_ptr[i], L = G_ptr[i + 1] - s;
+      bool uns = (unsorted[i >> 5] >> (i & 31)) & 1u;
+      if (uns) {
+        c = e == 0 ? -2 : -1;  // marker: exhaustive scan
+      } else if (e < L) {
+        c = col_s[s + e];
+        g = val_s[s + e];
+      }
+      if (e == 0) hlen[i] = L;
+    } else if (e == 0) {
+      hlen[i] = 0;
+    }
+    hcol[t] = c;
+    hval[t] = g;
+  }
+}
+
+__device__ __forceinline__ void ah_issue(int bt, const int* __restrict__ hcol_g, const double* __restrict__ hval_g,
+                                         const int* __restrict__ hlen_g, int* scol, double* sval, int* slen,
+                                         int lane) {
+  const int slot = bt % AH_NB;
+  const int64_t e0 = (int64_t)bt * AH_B * AH_K;
+  constexpr int CC = AH_B * AH_K / 4, CV = AH_B * AH_K / 2, CL = AH_B / 4;  // 16 B chunks
+#pragma unroll
+  for (int c = lane; c < CC; c += 32) cp_async16(scol + slot * AH_B * AH_K + 4 * c, hcol_g + e0 + 4 * c);
+#pragma unroll
+  for (int c = lane; c < CV; c += 32) cp_async16(sval + slot * AH_B * AH_K + 2 * c, hval_g + e0 + 2 * c);
+  if (lane < CL) cp_async16(slen + slot * AH_B + 4 * lane, hlen_g + (int64_t)bt * AH_B + 4 * lane);
+  cp_async_commit();
+}
+
+__global__ void __launch_bounds__(32)
+k_aggregate_head(const int* __restrict__ G_ptr, const int* __restrict__ G_col, const double* __restrict__ G_val,
+                 const int* __restrict__ hcol_g, const double* __restrict__ hval_g, const int* __restrict__ hlen_g,
+                 int n, int max_size, int* __restrict__ agg_g, int* __restrict__ size_g, int* __restrict__ n_agg_out) {
+  extern __shared__ __align__(16) double shh[];
+  double* sval = shh;                                           // AH_NB * AH_B * AH_K
+  int* scol = reinterpret_cast<int*>(sval + AH_NB * AH_B * AH_K);  // AH_NB * AH_B * AH_K
+  int* slen = scol + AH_NB * AH_B * AH_K;                       // AH_NB * AH_B
+  int* agg = slen + AH_NB * AH_B;                               // n
+  int* size = agg + n;                                          // n
+  const int lane = threadIdx.x;
+  for (int i = lane; i < n; i += 32) {
+    agg[i] = -1;
+    size[i] = 0;
+  }
+  const int nbt = (n + AH_B - 1) / AH_B;
+#pragma unroll 1
+  for (int b = 0; b < AH_NB; ++b) {
+    if (b < nbt) ah_issue(b, hcol_g, hval_g, hlen_g, scol, sval, slen, lane);
+    else cp_async_commit();
+  }
+  __syncwarp();
+  int nagg = 0;
+  for (int b = 0; b < nbt; ++b) {
+    cp_async_wait<AH_NB - 1>();
+    __syncwarp();
+    const int slot = b % AH_NB;
+    const int iend = min(AH_B, n - b * AH_B);
+    for (int ii = 0; ii < iend; ++ii) {
+      const int i = b * AH_B + ii;
+      if (agg[i] >= 0) continue;
+      int j = -1;
+      double g = 0.0;
+      if (lane < AH_K) {
+        j = scol[(slot * AH_B + ii) * AH_K + lane];
+        g = sval[(slot * AH_B + ii) * AH_K + lane];
+      }
+      const int len = slen[slot * AH_B + ii];
+      int bj = -1;
+      bool full_scan = __shfl_sync(FULL_MASK, j, 0) == -2;
+      bool row_scan = false;
+      if (!full_scan) {
+        int a = j >= 0 ? agg[j] : -1;
+        bool elig = j >= 0 && (a < 0 || size[a] < max_size);
+        unsigned m = __ballot_sync(FULL_MASK, elig);
+        if (m) {
+          int f = __ffs(m) - 1;
+          double gf = __shfl_sync(FULL_MASK, g, f);
+          unsigned tie = __ballot_sync(FULL_MASK, elig && g == gf);
+          unsigned mu = __ballot_sync(FULL_MASK, elig && g == gf && a < 0);
+          if (mu) {
+            bj = __shfl_sync(FULL_MASK, j, __ffs(mu) - 1);
+          } else {
+            // the last head entry continuing the tie run: later entries may hold an
+            // unaggregated tie, which would win
+            bool tail = __shfl_sync(FULL_MASK, j >= 0 && g == gf, AH_K - 1);
+            if (tail && len > AH_K) row_scan = true;
+            else bj = __shfl_sync(FULL_MASK, j, f);
+            (void)tie;
+          }
+        } else if (len > AH_K) {
+          row_scan = true;
+        }
+      }
+      if (row_scan) {
+        // sorted row from global memory, the ring kernel's rule
+        const int s = G_ptr[i], e = G_ptr[i + 1];
+        bool have = false;
+        double gf = 0.0;
+        int jf = -1, ju = -1;
+        for (int q0 = s; q0 < e; q0 += 32) {
+          int q = q0 + lane;
+          int jj = q < e ? G_col[q] : -1;
+          double gg = q < e ? G_val[q] : 0.0;
+          int a = jj >= 0 ? agg[jj] : -1;
+          bool elig = jj >= 0 && (a < 0 || size[a] < max_size);
+          if (have) elig = elig && (gg == gf);
+          unsigned m = __ballot_sync(FULL_MASK, elig);
+          if (!have) {
+            if (!m) continue;
+            int f = __ffs(m) - 1;
+            gf = __shfl_sync(FULL_MASK, gg, f);
+            jf = __shfl_sync(FULL_MASK, jj, f);
+            have = true;
+            m = __ballot_sync(FULL_MASK, elig && gg == gf);
+          }
+          unsigned mu = __ballot_sync(FULL_MASK, elig && a < 0) & m;
+          if (mu) {
+            ju = __shfl_sync(FULL_MASK, jj, __ffs(mu) - 1);
+            break;
+          }
+          bool tail = __shfl_sync(FULL_MASK, q < e && gg == gf, 31);
+          if (!tail) break;
+        }
+        bj = ju >= 0 ? ju : jf;
+      } else if (full_scan) {
+        Cand best{0.0, 0, -1};
+        for (int q = G_ptr[i] + lane; q < G_ptr[i + 1]; q += 32) {
+          int jj = G_col[q];
+          int a = agg[jj];
+          if ((a < 0) || (size[a] < max_size)) {
+            Cand c{G_val[q], a < 0 ? 1 : 0, jj};
+            if (better(c, best)) best = c;
+          }
+        }
+        bj = warp_best(best).j;
+      }
+      if (bj >= 0) {
+        int aj = agg[bj];  // every lane reads the pre-update value
+        __syncwarp();
+        if (lane == 0) {
+          if (aj < 0) {
+            agg[i] = nagg;
+            agg[bj] = nagg;
+            size[nagg] = 2;
+          } else {
+            agg[i] = aj;
+            size[aj] += 1;
+          }
+        }
+        if (aj < 0) ++nagg;
+      }
+      __syncwarp();
+    }
+    __syncwarp();  // every lane is done with this slot before it is refilled
+    if (b + AH_NB < nbt) ah_issue(b + AH_NB, hcol_g, hval_g, hlen_g, scol, sval, slen, lane);
+    else cp_async_commit();
+  }
+  cp_async_wait<0>();
+  // post-pass over leftovers in index order (few nodes: rows from global memory)
+  for (int i = 0; i < n; ++i) {
+    __syncwarp();
+    if (agg[i] >= 0) continue;
+    Cand best{0.0, 0, -1};
+    for (int q = G_ptr[i] + lane; q < G_ptr[i + 1]; q += 32) {
+      int j = G_col[q];
+      int a = agg[j];
+      if (a >= 0 && size[a] <= max_size) {
+        Cand c{G_val[q], 0, j};
+        if (better(c, best)) best = c;
+      }
+    }
+    best = warp_best(best);
+    __syncwarp();
+    if (lane == 0) {
+      if (best.j >= 0) {
+        int a = agg[best.j];
+        agg[i] = a;
+        size[a] += 1;
+      } else {
+        agg[i] = nagg;
+        size[nagg] = 1;
+      }
+    }
+    if (best.j < 0) ++nagg;
+    __syncwarp();
+  }
+  __syncwarp();
+  int mx = 0;
+  for (int i = lane; i < n; i += 32) {
+    agg_g[i] = agg[i];
+    size_g[i] = size[i];
+    if (i < nagg) mx = max(mx, size[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL_MASK, mx, o));
+  if (lane == 0) {
+    n_agg_out[0] = nagg;
+    n_agg_out[1] = mx;
+  }
+}
+
 extern "C" int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t* G_col, const double* G_val,
                               int32_t n, int32_t max_size, int32_t* agg, int32_t* size_work, int32_t* n_agg_dev,
                               int64_t nnz_cap, void* stream) {
@@ -555,8 +781,35 @@ extern "C" int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t
       BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr));
       attr = smr;
     }
-    launch(k_aggregate_ring, 1, 32, smr, st, G_ptr, (const int*)col_s, (const double*)val_s, (const unsigned*)uns, n,
-           max_size, agg, size_work, n_agg_dev);
+    static const bool head_on = [] {
+      const char* e = getenv("BAMG_AGG_HEAD");
+      return !(e && e[0] == '0');
+    }();
+    const int n_pad = ((n + AH_B - 1) / AH_B) * AH_B;
+    const size_t smh = (size_t)AH_NB * AH_B * AH_K * (sizeof(double) + sizeof(int)) +
+                       (size_t)AH_NB * AH_B * sizeof(int) + 2 * sizeof(int) * (size_t)n;
+    if (head_on && smh <= 220 * 1024) {
+      int *hcol = nullptr, *hlen = nullptr;
+      double* hval = nullptr;
+      BAMG_CUDA_CHECK(cudaMallocAsync(&hcol, sizeof(int) * (size_t)n_pad * AH_K, st));
+      BAMG_CUDA_CHECK(cudaMallocAsync(&hval, sizeof(double) * (size_t)n_pad * AH_K, st));
+      BAMG_CUDA_CHECK(cudaMallocAsync(&hlen, sizeof(int) * (size_t)n_pad, st));
+      launch(k_agg_heads, grid_for((int64_t)n_pad * AH_K, 256), 256, 0, st, G_ptr, (const int*)col_s,
+             (const double*)val_s, (const unsigned*)uns, n, n_pad, hcol, hval, hlen);
+      static size_t hattr = 0;
+      if (smh > hattr) {
+        BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smh));
+        hattr = smh;
+      }
+      launch(k_aggregate_head, 1, 32, smh, st, G_ptr, (const int*)col_s, (const double*)val_s, (const int*)hcol,
+             (const double*)hval, (const int*)hlen, n, max_size, agg, size_work, n_agg_dev);
+      BAMG_CUDA_CHECK(cudaFreeAsync(hcol, st));
+      BAMG_CUDA_CHECK(cudaFreeAsync(hval, st));
+      BAMG_CUDA_CHECK(cudaFreeAsync(hlen, st));
+    } else {
+      launch(k_aggregate_ring, 1, 32, smr, st, G_ptr, (const int*)col_s, (const double*)val_s, (const unsigned*)uns,
+             n, max_size, agg, size_work, n_agg_dev);
+    }
     BAMG_CUDA_CHECK(cudaFreeAsync(val_s, st));
     BAMG_CUDA_CHECK(cudaFreeAsync(col_s, st));
     BAMG_CUDA_CHECK(cudaFreeAsync(uns, st));
