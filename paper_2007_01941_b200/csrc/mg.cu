@@ -912,6 +912,51 @@ extern "C" int bamg_aggregate_members(bamg_ctx* ctx, const int32_t* agg, int32_t
 
 #define NS 16
 
+// The per-column dot products of one reflector application are independent, so
+// they are accumulated together and their warp reductions interleaved: sixteen
+// butterfly trees in flight instead of sixteen back-to-back (the scan is latency
+// bound, one warp per aggregate). Every column keeps its own accumulation order and
+// tree, so the results are bit-identical to the column-at-a-time loops below.
+#ifndef BAMG_QR_BATCH
+#define BAMG_QR_BATCH 1
+#endif
+
+__device__ __forceinline__ void warp_sum16(double* v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < 16; ++c) v[c] += __shfl_xor_sync(FULL_MASK, v[c], o);
+}
+
+// apply H_j (reflector in column j below the diagonal, tau) to columns [from, NS) of A
+__device__ __forceinline__ void reflect_cols(double* A, int m, int j, int from, double tau, int lane) {
+  double w[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) w[c] = 0.0;
+  for (int i = j + 1 + lane; i < m; i += 32) {
+    double v = A[i * 16 + j];
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      if (c >= from) w[c] += v * A[i * 16 + c];
+  }
+  warp_sum16(w);
+#pragma unroll
+  for (int c = 0; c < 16; ++c) w[c] = w[c] + A[j * 16 + c];
+  __syncwarp();
+  for (int i = j + 1 + lane; i < m; i += 32) {
+    double v = A[i * 16 + j];
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      if (c >= from) A[i * 16 + c] -= tau * w[c] * v;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      if (c >= from) A[j * 16 + c] -= tau * w[c];
+  }
+  __syncwarp();
+}
+
 __device__ void householder_step(double* A, int m, int j, int lane, double* tau_out, int ncols_apply_from,
                                  double* diag_out) {
   // column j, rows j..m-1
@@ -932,7 +977,9 @@ __device__ void householder_step(double* A, int m, int j, int lane, double* tau_
   *tau_out = tau;
   *diag_out = beta;
   __syncwarp();
-  if (tau != 0.0) {
+  if (BAMG_QR_BATCH && tau != 0.0) {
+    reflect_cols(A, m, j, ncols_apply_from, tau, lane);
+  } else if (tau != 0.0) {
     for (int c = ncols_apply_from; c < NS; ++c) {
       double w = 0.0;
       for (int i = j + 1 + lane; i < m; i += 32) w += A[i * NS + j] * A[i * NS + c];
@@ -950,6 +997,38 @@ __device__ void form_q(const double* A, const double* tau, int m, int k, int kee
   for (int i = lane; i < m; i += 32)
     for (int c = 0; c < NS; ++c) Q[i * NS + c] = (i == c && c < keep) ? 1.0 : 0.0;
   __syncwarp();
+  if (BAMG_QR_BATCH) {
+    for (int j = k - 1; j >= 0; --j) {
+      const double tj = tau[j];
+      if (tj == 0.0) continue;
+      double w[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) w[c] = 0.0;
+      for (int i = j + 1 + lane; i < m; i += 32) {
+        double v = A[i * NS + j];
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c >= j && c < keep) w[c] += v * Q[i * NS + c];
+      }
+      warp_sum16(w);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) w[c] = Q[j * NS + c] + w[c];
+      __syncwarp();
+      for (int i = j + 1 + lane; i < m; i += 32) {
+        double v = A[i * NS + j];
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c >= j && c < keep) Q[i * NS + c] -= tj * w[c] * v;
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c >= j && c < keep) Q[j * NS + c] -= tj * w[c];
+      }
+      __syncwarp();
+    }
+    return;
+  }
   for (int j = k - 1; j >= 0; --j) {
     if (tau[j] == 0.0) continue;
     for (int c = j; c < keep; ++c) {
@@ -1048,13 +1127,31 @@ __global__ void k_prolong_qr(const int* __restrict__ agg_ptr, const int* __restr
       for (int j = 0; j < k; ++j) {
         int bestc = j;
         double bestn = -1.0;
-        for (int c = j; c < NS; ++c) {
-          double s = 0.0;
-          for (int i = j + lane; i < m; i += 32) s += A[i * NS + c] * A[i * NS + c];
-          s = warp_sum(s);
-          if (s > bestn) {
-            bestn = s;
-            bestc = c;
+        if (BAMG_QR_BATCH) {
+          double s[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) s[c] = 0.0;
+          for (int i = j + lane; i < m; i += 32) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+              if (c >= j) s[c] += A[i * NS + c] * A[i * NS + c];
+          }
+          warp_sum16(s);
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            if (c >= j && s[c] > bestn) {
+              bestn = s[c];
+              bestc = c;
+            }
+        } else {
+          for (int c = j; c < NS; ++c) {
+            double s = 0.0;
+            for (int i = j + lane; i < m; i += 32) s += A[i * NS + c] * A[i * NS + c];
+            s = warp_sum(s);
+            if (s > bestn) {
+              bestn = s;
+              bestc = c;
+            }
           }
         }
         if (bestc != j) {
