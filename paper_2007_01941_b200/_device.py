@@ -23,10 +23,11 @@ _devices: dict = {}
 
 
 def dev() -> torch.device:
+    if not _devices:
+        require_cuda()
     i = torch.cuda.current_device()
     d = _devices.get(i)
     if d is None:
-        require_cuda()
         d = _devices[i] = torch.device("cuda", i)
     return d
 
