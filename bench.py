@@ -142,16 +142,17 @@ def spmv_bytes(nnzb, nbr, b):
     return nnzb * (8 * b * b + 4) + 4 * (nbr + 1) + 8 * b * nbr + 8 * b * nbr
 
 
-def sym_bytes(nnzb, nbr, nch):
-    """Bytes the 9x9 half-storage pair must move: pass 1 reads the upper blocks
-    (incl. diagonal) + their column ids + x, writes one 72 B mirrored product per
-    off-diagonal upper block and a 72 B partial per chunk; pass 2 reads the mirror
-    index + mirrored product per lower block, the chunk partials, ptr/dpos/ucptr,
-    and writes y."""
+def sym_bytes(nnzb, nbr, nch, b=9):
+    """Bytes the half-storage pair must move (block size b): pass 1 reads the upper
+    blocks (incl. diagonal) + their column ids + the mirror slot of each off-diagonal
+    block + x, writes one b-vector mirrored product per off-diagonal upper block and a
+    b-vector partial per chunk (chunk descriptors 8 B); pass 2 reads each row's
+    contiguous mirrored products, the chunk partials, ptr/dpos/ucptr, and writes y."""
     n_up = (nnzb + nbr) // 2
     n_off = (nnzb - nbr) // 2
-    p1 = n_up * (648 + 4) + 72 * nbr + 8 * nch + 72 * n_off + 72 * nch
-    p2 = n_off * (4 + 72) + 72 * nch + 12 * nbr + 72 * nbr
+    vb = 8 * b
+    p1 = n_up * (8 * b * b + 4) + n_off * 4 + vb * nbr + 8 * nch + vb * n_off + vb * nch
+    p2 = n_off * vb + vb * nch + 12 * nbr + vb * nbr
     return p1 + p2
 
 
@@ -260,16 +261,24 @@ def gpu_arm(args, rank, world):
         torch.cuda.synchronize()
         t_v = e0.elapsed_time(e1) / 10 / 1e3
         bv = 0
+        kinds = []
         for li, lvl in enumerate(h.levels[:-1]):
             A = lvl.explicit
             b = A.row_block_size
             n = A.n_block_rows
-            bsp = (sym_bytes(A.n_block_entries, n, A._symop.nch) if A._symop is not None
+            kind = int(_lib.lib().bamg_mg_level_kind(h._plan.handle, li)) if h._plan is not None else 3
+            kinds.append(kind)
+            # products as the plan runs them: half-storage pair, or full storage
+            bsp = (sym_bytes(A.n_block_entries, n, A._symop.nch, b) if kind == 0
                    else spmv_bytes(A.n_block_entries, n, b))
             bv += 4 * bsp + 4 * 8 * b * b * n + 2 * (8 * 16 * b * n + 4 * n) + 10 * 8 * b * n
         nL = h.levels[-1].scalar_dim
         bv += 8 * nL * nL
-        vcyc = {"achieved_gbs": bv / t_v / 1e9, "ms": t_v * 1e3, "bytes": bv, "frac": bv / t_v / 1e9 / peak}
+        vcyc = {"achieved_gbs": bv / t_v / 1e9, "ms": t_v * 1e3, "bytes": bv, "frac": bv / t_v / 1e9 / peak,
+                "level_kinds": kinds,
+                "bytes_formula": "SURVEY 8(d) V-cycle: per level 4 products (half-storage pair bytes where the plan "
+                                 "runs one, full BSR otherwise) + 4 D^-1 applies + P^T, P + 10 vector passes; "
+                                 "coarsest 8 n^2"}
 
     # e2e: public API from pinned host arrays, H2D + structure + solve + D2H
     import torch as T

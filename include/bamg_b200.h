@@ -278,6 +278,10 @@ int bamg_symop_cheb_step(bamg_ctx* ctx, const bamg_symop* sym, const double* blo
 int bamg_mg_set_symmetric(bamg_mg* mg, int32_t level, const bamg_symop* sym);
 int bamg_mg_use_graph(bamg_mg* mg, int32_t on);
 int bamg_mg_apply(bamg_ctx* ctx, bamg_mg* mg, const double* r, double* z, void* stream);
+/* how the prepared plan runs level l's products (measurement only): 0 half-storage
+ * pair, 1 one-CTA-per-row full storage, 2 chunked full storage, 3 warp-per-row full
+ * storage, 4 coarsest (dense inverse); -1 before the first application */
+int32_t bamg_mg_level_kind(const bamg_mg* mg, int32_t level);
 /* solver.py:70-128 pcg with a BSR operator and the MG plan (or block-Jacobi inverse
  * blocks when mg == NULL); one host synchronisation per iteration. err codes:
  * 1 PreconditionerNotSPD, 2/3/4/5 CgDivergence (operator non-finite / curvature /

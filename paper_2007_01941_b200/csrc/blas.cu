@@ -229,16 +229,25 @@ extern "C" int bamg_cheb_step(bamg_ctx* ctx, int32_t bs, const int32_t* ptr, con
 // fine node, block column = aggregate (multigrid.py:234-236).
 
 // y_i (+)= P_i xc_agg(i)
-__global__ void k_prolong(const int* __restrict__ agg, const double* __restrict__ P, const double* __restrict__ xc,
-                          int nf, int bs, double* __restrict__ y, int accumulate) {
+// (min-blocks 1 lets ptxas issue the row's eight 16 B loads of P and of xc before
+// the fma chain instead of interleaving them at 32 registers)
+__global__ void __launch_bounds__(256, 1)
+k_prolong(const int* __restrict__ agg, const double* __restrict__ P, const double* __restrict__ xc, int nf, int bs,
+          double* __restrict__ y, int accumulate) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)nf * bs; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = t / bs;
     int r = (int)(t - i * bs);
-    const double* p = P + (i * bs + r) * 16;
-    const double* xa = xc + (int64_t)agg[i] * 16;
+    const double2* p = reinterpret_cast<const double2*>(P + (i * bs + r) * 16);
+    const double2* xa = reinterpret_cast<const double2*>(xc + (int64_t)__ldg(agg + i) * 16);
+    double2 pv[8], xv[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      pv[c] = __ldg(p + c);
+      xv[c] = __ldg(xa + c);
+    }
     double s = 0.0;
 #pragma unroll
-    for (int c = 0; c < 16; ++c) s = fma(p[c], xa[c], s);
+    for (int c = 0; c < 8; ++c) s = fma(pv[c].y, xv[c].y, fma(pv[c].x, xv[c].x, s));
     y[t] = accumulate ? y[t] + s : s;
   }
 }

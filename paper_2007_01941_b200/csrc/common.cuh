@@ -110,6 +110,42 @@ __device__ __forceinline__ bool grid_finish(double* partials, unsigned int* coun
   return true;
 }
 
+// L2 eviction-priority policies (createpolicy) and hinted loads/stores. The solve
+// phase streams operators far larger than L2 (evict_first) while small arrays that
+// are written by one kernel and gathered by the next -- the mirrored products of
+// the half-storage products -- stay resident (evict_last).
+enum { L2_NORMAL = 0, L2_FIRST = 1, L2_LAST = 2 };
+__device__ __forceinline__ uint64_t l2_policy(int kind) {
+  uint64_t p;
+#ifdef NO_L2_HINTS
+  kind = L2_NORMAL;
+#endif
+  if (kind == L2_FIRST)
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else if (kind == L2_LAST)
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_pol(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ld2_pol(const double2* p, uint64_t pol) {
+  double2 v;
+  asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_pol(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st2_pol(double2* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+               : "memory");
+}
+
 // cp.async (LDGSTS) helpers: 16 B global -> shared copies, L2 only (.cg).
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
   unsigned s = (unsigned)__cvta_generic_to_shared(sdst);

@@ -83,6 +83,19 @@ struct bamg_symop {
   cudaStream_t alloc_stream = nullptr;
 };
 
+// Where the mirrored product of upper block b lives. Destination order (default):
+// at the position of its mirror (lower) block, so pass 2 streams each row's lower
+// range contiguously with no index indirection, and pass 1's 72 / 128 B stores are
+// scattered (fire-and-forget). SYM_SRC_ORDER: at b itself (coalesced stores,
+// gathered reads through tpos).
+#ifdef SYM_SRC_ORDER
+#define T_SLOT(b) (b)
+#define T_READ(p) __ldg(tpos + (p))
+#else
+#define T_SLOT(b) __ldg(tpos + (b))
+#define T_READ(p) (p)
+#endif
+
 #ifndef SYM_CH
 #define SYM_CH 24
 #endif
@@ -141,8 +154,9 @@ __global__ void __launch_bounds__(128, SYM_MINB)
 k_sym9_upper(const int* __restrict__ ptr, const int* __restrict__ col, const int* __restrict__ dpos,
              const int* __restrict__ tpos, const int* __restrict__ cbeg, const int* __restrict__ crow, int nch,
              const double* __restrict__ blocks, const double* __restrict__ x, double* __restrict__ T,
-             double* __restrict__ yup) {
+             double* __restrict__ yup, int blk_policy) {
   __shared__ double red[4][27 * 9];
+  const uint64_t pb = l2_policy(blk_policy), pt = l2_policy(L2_LAST);
   int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -164,11 +178,11 @@ k_sym9_upper(const int* __restrict__ ptr, const int* __restrict__ col, const int
         double t = 0.0;
 #pragma unroll
         for (int r = 0; r < 9; ++r) {
-          double v = __ldg(U + 9 * r);
+          double v = ld_pol(U + 9 * r, pb);
           acc[r] = fma(v, xjc, acc[r]);
           t = fma(v, xi[r], t);
         }
-        if (b != bd) T[(int64_t)b * 9 + c] = t;  // coalesced: T lives at the upper position
+        if (b != bd) st_pol(T + (int64_t)T_SLOT(b) * 9 + c, t, pt);
       }
 #pragma unroll
       for (int r = 0; r < 9; ++r) red[wib][lane * 9 + r] = acc[r];
@@ -183,9 +197,13 @@ k_sym9_upper(const int* __restrict__ ptr, const int* __restrict__ col, const int
   }
 }
 
+#ifndef SYM_FB
+#define SYM_FB 12
+#endif
 // pass 2 + epilogue. mode 0: out = ax (dot_out: <x_in, ax>, deterministic);
 // mode 1: out = b - ax; mode 2: the fused Chebyshev step of k_cheb_step.
-__global__ void __launch_bounds__(128)
+template <int FB>
+__global__ void __launch_bounds__(128, 1)
 k_sym9_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const int* __restrict__ tpos,
               const double* __restrict__ T,
               const int* __restrict__ ucptr, const double* __restrict__ yup, int nbr, int mode, const double* __restrict__ b,
@@ -193,6 +211,7 @@ k_sym9_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const i
               double* __restrict__ out, double c1, double c2, int divide, double* partials, unsigned int* counter,
               double* dot_out) {
   __shared__ double scratch[33];
+  const uint64_t pt = l2_policy(L2_LAST);
   int lane = threadIdx.x & 31;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -202,19 +221,19 @@ k_sym9_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const i
     double s = 0.0;
     if (g < 3) {
       int p = ptr[row] + g, p1 = dpos[row];
-      // batches of 6 (this lane's p, p+3, ...): indices, then products, then the
-      // in-order additions -- same sums, 6 gathers in flight instead of 1
-      for (; p + 15 < p1; p += 18) {
-        int tp[6];
-        double v[6];
+      // batches of FB (this lane's p, p+3, ...): indices, then products, then the
+      // in-order additions -- same sums, FB loads in flight instead of 1
+      for (; p + 3 * (FB - 1) < p1; p += 3 * FB) {
+        int tp[FB];
+        double v[FB];
 #pragma unroll
-        for (int u = 0; u < 6; ++u) tp[u] = __ldg(tpos + p + 3 * u);
+        for (int u = 0; u < FB; ++u) tp[u] = T_READ(p + 3 * u);
 #pragma unroll
-        for (int u = 0; u < 6; ++u) v[u] = __ldg(T + (int64_t)tp[u] * 9 + c);
+        for (int u = 0; u < FB; ++u) v[u] = ld_pol(T + (int64_t)tp[u] * 9 + c, pt);
 #pragma unroll
-        for (int u = 0; u < 6; ++u) s += v[u];
+        for (int u = 0; u < FB; ++u) s += v[u];
       }
-      for (; p < p1; p += 3) s += __ldg(T + (int64_t)__ldg(tpos + p) * 9 + c);
+      for (; p < p1; p += 3) s += ld_pol(T + (int64_t)T_READ(p) * 9 + c, pt);
     }
     double s1 = __shfl_down_sync(FULL_MASK, s, 9);
     double s2 = __shfl_down_sync(FULL_MASK, s, 18);
@@ -262,8 +281,9 @@ k_sym9_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const i
 // stored by lanes 0..7 at the block's own position (128 B, coalesced).
 __global__ void __launch_bounds__(128)
 k_sym16_upper(const int* __restrict__ ptr, const int* __restrict__ col, const int* __restrict__ dpos,
-              const int* __restrict__ cbeg, const int* __restrict__ crow, int nch, const double* __restrict__ blocks,
-              const double* __restrict__ x, double* __restrict__ T, double* __restrict__ yup) {
+              const int* __restrict__ tpos, const int* __restrict__ cbeg, const int* __restrict__ crow, int nch, const double* __restrict__ blocks,
+              const double* __restrict__ x, double* __restrict__ T, double* __restrict__ yup, int blk_policy) {
+  const uint64_t pb = l2_policy(blk_policy), pt = l2_policy(L2_LAST);
   int lane = threadIdx.x & 31;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -276,7 +296,7 @@ k_sym16_upper(const int* __restrict__ ptr, const int* __restrict__ col, const in
     int bd = dpos[row], b0 = cbeg[ch], be = min(b0 + SYM_CH16, ptr[row + 1]);
     for (int b = b0; b < be; ++b) {
       const double2* U = reinterpret_cast<const double2*>(blocks + (int64_t)b * 256) + lane;
-      double2 u0 = __ldg(U), u1 = __ldg(U + 32), u2 = __ldg(U + 64), u3 = __ldg(U + 96);
+      double2 u0 = ld2_pol(U, pb), u1 = ld2_pol(U + 32, pb), u2 = ld2_pol(U + 64, pb), u3 = ld2_pol(U + 96, pb);
       double2 xj = __ldg(reinterpret_cast<const double2*>(x + (int64_t)col[b] * 16 + cp));
       a0 = fma(u0.x, xj.x, fma(u0.y, xj.y, a0));
       a1 = fma(u1.x, xj.x, fma(u1.y, xj.y, a1));
@@ -288,7 +308,8 @@ k_sym16_upper(const int* __restrict__ ptr, const int* __restrict__ col, const in
       ty += __shfl_xor_sync(FULL_MASK, ty, 8);
       tx += __shfl_xor_sync(FULL_MASK, tx, 16);
       ty += __shfl_xor_sync(FULL_MASK, ty, 16);
-      if (b != bd && lane < 8) reinterpret_cast<double2*>(T + (int64_t)b * 16)[lane] = make_double2(tx, ty);
+      if (b != bd && lane < 8)
+        st2_pol(reinterpret_cast<double2*>(T + (int64_t)T_SLOT(b) * 16) + lane, make_double2(tx, ty), pt);
     }
 #pragma unroll
     for (int o = 1; o < 8; o <<= 1) {
@@ -318,6 +339,7 @@ k_sym16_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const 
                const double* __restrict__ x_in, double* __restrict__ out, double c1, double c2, int divide,
                double* partials, unsigned int* counter, double* dot_out) {
   __shared__ double scratch[33];
+  const uint64_t pt = l2_policy(L2_LAST);
   int lane = threadIdx.x & 31;
   int half = lane >> 4, r = lane & 15;
   int row0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2;
@@ -336,13 +358,13 @@ k_sym16_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const 
         int tp[8];
         double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) tp[u] = __ldg(tpos + p + u);
+        for (int u = 0; u < 8; ++u) tp[u] = T_READ(p + u);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldg(T + (int64_t)tp[u] * 16 + r);
+        for (int u = 0; u < 8; ++u) v[u] = ld_pol(T + (int64_t)tp[u] * 16 + r, pt);
 #pragma unroll
         for (int u = 0; u < 8; ++u) lo += v[u];
       }
-      for (; p < p1; ++p) lo += __ldg(T + (int64_t)__ldg(tpos + p) * 16 + r);
+      for (; p < p1; ++p) lo += ld_pol(T + (int64_t)T_READ(p) * 16 + r, pt);
       for (int k = ucptr[row]; k < ucptr[row + 1]; ++k) up += yup[(int64_t)k * 16 + r];
       ax = lo + up;
     }
@@ -380,6 +402,16 @@ k_sym16_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const 
 
 static int sym_grid(int nbr) { return grid_for((int64_t)nbr * 32, 128, 16); }
 
+// operators whose upper half exceeds ~half of L2 are streamed evict_first, so the
+// stream does not displace the resident mirrored products and the small operators
+#ifndef SYM_STREAM_BYTES
+#define SYM_STREAM_BYTES (64ll << 20)
+#endif
+static int sym_block_policy(const bamg_symop* S) {
+  int64_t up_bytes = (S->nnzb + S->nbr) / 2 * (int64_t)S->bs * S->bs * 8;
+  return up_bytes > SYM_STREAM_BYTES ? L2_FIRST : L2_NORMAL;
+}
+
 // y = A x through the symmetric operator (bs 9 or 16), with the chosen epilogue.
 static void sym_apply(bamg_ctx* ctx, const bamg_symop* S, const double* blocks, const double* x, int mode,
                       const double* b, const double* Dinv, double* d, double* out, double c1, double c2, int divide,
@@ -387,8 +419,9 @@ static void sym_apply(bamg_ctx* ctx, const bamg_symop* S, const double* blocks, 
   double* part = ctx ? ctx->partials : nullptr;
   unsigned* ctr = ctx ? ctx->counters + BAMG_CTR_SPMV : nullptr;
   if (S->bs == 16) {
-    launch(k_sym16_upper, sym_grid(S->nch), 128, 0, st, S->ptr, S->col, S->dpos, (const int*)S->cbeg,
-           (const int*)S->crow, S->nch, blocks, x, S->T, S->yup);
+    launch(k_sym16_upper, sym_grid(S->nch), 128, 0, st, S->ptr, S->col, S->dpos, (const int*)S->tpos,
+           (const int*)S->cbeg,
+           (const int*)S->crow, S->nch, blocks, x, S->T, S->yup, sym_block_policy(S));
     int g = grid_for((int64_t)((S->nbr + 1) / 2) * 32, 128, 16);
     if (dot_out && g > BAMG_MAX_PARTIALS) g = BAMG_MAX_PARTIALS;
     launch(k_sym16_finish, g, 128, 0, st, S->ptr, S->dpos, (const int*)S->tpos, (const double*)S->T,
@@ -397,10 +430,12 @@ static void sym_apply(bamg_ctx* ctx, const bamg_symop* S, const double* blocks, 
     return;
   }
   launch(k_sym9_upper, sym_grid(S->nch), 128, 0, st, S->ptr, S->col, S->dpos, (const int*)S->tpos,
-         (const int*)S->cbeg, (const int*)S->crow, S->nch, blocks, x, S->T, S->yup);
-  int g = sym_grid(S->nbr);
+         (const int*)S->cbeg, (const int*)S->crow, S->nch, blocks, x, S->T, S->yup, sym_block_policy(S));
+  // one row per warp (the hardware balances CTAs over SMs as rows finish); the
+  // fused dot's grid is capped by the partials buffer and strides instead
+  int g = (int)ceil_div(S->nbr, 4);
   if (dot_out && g > BAMG_MAX_PARTIALS) g = BAMG_MAX_PARTIALS;
-  launch(k_sym9_finish, g, 128, 0, st, S->ptr, S->dpos, (const int*)S->tpos, (const double*)S->T, (const int*)S->ucptr,
+  launch(k_sym9_finish<SYM_FB>, g, 128, 0, st, S->ptr, S->dpos, (const int*)S->tpos, (const double*)S->T, (const int*)S->ucptr,
          (const double*)S->yup, S->nbr, mode, b, Dinv, d, x, out, c1, c2, divide, part, ctr, dot_out);
 }
 
@@ -584,6 +619,48 @@ k_spmv16_chunks(const int* __restrict__ ptr, const int* __restrict__ col, const 
   }
 }
 
+// Single-pass 16x16 product for the small coarse operators (full storage; every
+// level below ROWCTA_MAX_BYTES): CTA per row, warp w takes the w-th quarter of the
+// row's blocks, the four partials combine in warp order, and the epilogue of
+// k_rows16_finish follows in the same kernel -- one launch per product instead of
+// the half-storage pair, whose two latency-bound launches dominate at these sizes.
+#ifndef ROWCTA_MAX_BYTES
+#define ROWCTA_MAX_BYTES (32ll << 20)
+#endif
+__global__ void __launch_bounds__(128)
+k_row16_cta(const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ blocks,
+            const double* __restrict__ x, int nbr, int mode, const double* __restrict__ b,
+            const double* __restrict__ Dinv, double* __restrict__ d, double* __restrict__ out, double c1, double c2,
+            int divide) {
+  __shared__ double part[4][16];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int row = blockIdx.x;
+  int b0 = ptr[row], b1 = ptr[row + 1];
+  int q = (b1 - b0 + 3) >> 2;
+  int lo = min(b0 + w * q, b1), hi = min(lo + q, b1);
+  double v = warp_blocks16(col, blocks, x, lo, hi, lane);
+  if (lane < 16) part[w][lane] = v;
+  __syncthreads();
+  if (w != 0) return;
+  int r = lane & 15;
+  double ax = ((part[0][r] + part[1][r]) + part[2][r]) + part[3][r];
+  int64_t e = (int64_t)row * 16 + r;
+  double rr = b[e] - ax;
+  if (mode == 0) {
+    if (lane < 16) out[e] = rr;
+    return;
+  }
+  double z = 0.0;
+  const double* Di = Dinv + e * 16;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) z = fma(Di[c], __shfl_sync(FULL_MASK, rr, c, 16), z);
+  if (lane < 16) {
+    double dn = divide ? z / c2 : c1 * d[e] + c2 * z;
+    d[e] = dn;
+    out[e] = x[e] + dn;
+  }
+}
+
 // Row finish: ax = sum of the row's partials (chunk order); then
 //   mode 0: r = b - ax
 //   mode 1: fused Chebyshev step (as k_cheb_step): r = b - ax; z = D^-1 r;
@@ -623,11 +700,15 @@ k_rows16_finish(const int* __restrict__ cptr, const double* __restrict__ partial
   }
 }
 
-// warp per aggregate restriction: bc_a = sum_{i in a} P_i^T r_i. The member ids
-// are loaded once (one per lane) and broadcast, so the P / r loads of all members
-// are independent; lane (c, h) accumulates column c over rows k = h (mod 2).
+// warp per aggregate restriction: bc_a = sum_{i in a} P_i^T r_i. Half-warp h takes
+// members h, h + 2, ...; lane c of a half owns column c and sums the BS rows of each
+// member's block (per row k the 16 lanes read one coalesced 128 B row of P; r_i is a
+// broadcast). Two members per half are loaded before their fma chains, so 4 members'
+// loads are in flight per warp; the halves combine once at the end (fixed order).
+// (min-blocks 1: without it ptxas holds the kernel at 32 registers and interleaves
+// every load with its fma, one member's row in flight at a time)
 template <int BS>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 1)
 k_restrict_warp(const int* __restrict__ agg_ptr, const int* __restrict__ members, const double* __restrict__ P,
                 const double* __restrict__ r, int nagg, double* __restrict__ bc) {
   int lane = threadIdx.x & 31;
@@ -635,20 +716,33 @@ k_restrict_warp(const int* __restrict__ agg_ptr, const int* __restrict__ members
   int nwarps = (gridDim.x * blockDim.x) >> 5;
   int c = lane & 15, h = lane >> 4;
   for (int a = warp; a < nagg; a += nwarps) {
-    int q0 = agg_ptr[a], m = agg_ptr[a + 1] - q0;
+    int q = agg_ptr[a] + h, q1 = agg_ptr[a + 1];
     double s = 0.0;
-    for (int qb = 0; qb < m; qb += 32) {
-      int mine = (qb + lane < m) ? members[q0 + qb + lane] : 0;
-      int mm = min(32, m - qb);
-#pragma unroll 4
-      for (int q = 0; q < mm; ++q) {
-        int64_t node = __shfl_sync(FULL_MASK, mine, q);
-        const double* pr = P + node * BS * 16 + c;
-        const double* rr = r + node * BS;
+    for (; q + 2 < q1; q += 4) {
+      int64_t i0 = __ldg(members + q), i1 = __ldg(members + q + 2);
+      double u0[BS], u1[BS], r0[BS], r1[BS];
 #pragma unroll
-        for (int k = 0; k < BS; k += 2)
-          if (k + h < BS) s = fma(pr[(k + h) * 16], rr[k + h], s);
+      for (int k = 0; k < BS; ++k) {
+        u0[k] = __ldg(P + (i0 * BS + k) * 16 + c);
+        u1[k] = __ldg(P + (i1 * BS + k) * 16 + c);
+        r0[k] = __ldg(r + i0 * BS + k);
+        r1[k] = __ldg(r + i1 * BS + k);
       }
+#pragma unroll
+      for (int k = 0; k < BS; ++k) s = fma(u0[k], r0[k], s);
+#pragma unroll
+      for (int k = 0; k < BS; ++k) s = fma(u1[k], r1[k], s);
+    }
+    if (q < q1) {
+      int64_t i0 = __ldg(members + q);
+      double u0[BS], r0[BS];
+#pragma unroll
+      for (int k = 0; k < BS; ++k) {
+        u0[k] = __ldg(P + (i0 * BS + k) * 16 + c);
+        r0[k] = __ldg(r + i0 * BS + k);
+      }
+#pragma unroll
+      for (int k = 0; k < BS; ++k) s = fma(u0[k], r0[k], s);
     }
     s += __shfl_down_sync(FULL_MASK, s, 16);
     if (lane < 16) bc[(int64_t)a * 16 + c] = s;
@@ -697,6 +791,8 @@ struct MgLevelPlan {
   const double* inv = nullptr;
   // symmetric half-storage operator (bs 9), when set
   const bamg_symop* sym = nullptr;
+  // single-pass CTA-per-row products (small 16x16 levels)
+  bool rowcta = false;
   // work
   double *b = nullptr, *x = nullptr, *xs = nullptr, *d = nullptr, *r = nullptr;
 };
@@ -787,6 +883,10 @@ static int mg_alloc(bamg_mg* m, cudaStream_t st) {
     BAMG_CUDA_CHECK(cudaMemcpyAsync(&nnzb[l], L.ptr + L.nbr, sizeof(int), cudaMemcpyDeviceToHost, st));
   }
   BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+  for (size_t l = 0; l < m->lv.size(); ++l) {
+    MgLevelPlan& L = m->lv[l];
+    L.rowcta = !L.inv && L.bs == 16 && L.ptr && L.nbr > 0 && (int64_t)nnzb[l] * 2048 <= ROWCTA_MAX_BYTES;
+  }
   size_t total = 2 * (size_t)m->lv[0].n;
   size_t itotal = 0;
   for (size_t l = 0; l < m->lv.size(); ++l) {
@@ -882,6 +982,11 @@ static int finish_grid(int nbr) { return grid_for((int64_t)((nbr + 1) / 2) * 32,
 
 static void cheb(const MgLevelPlan& L, const double* x_in, double* x_out, double c1, double c2, int divide,
                  bool with_A, cudaStream_t st) {
+  if (with_A && L.rowcta) {
+    launch(k_row16_cta, L.nbr, 128, 0, st, L.ptr, L.col, L.blocks, x_in, L.nbr, 1, L.b, L.Dinv, L.d, x_out, c1, c2,
+           divide);
+    return;
+  }
   if (with_A && L.sym) {
     sym_apply(nullptr, L.sym, L.blocks, x_in, 2, L.b, L.Dinv, L.d, x_out, c1, c2, divide, nullptr, st);
     return;
@@ -926,6 +1031,11 @@ static double* smooth(MgLevelPlan& L, double* x, cudaStream_t st) {
 }
 
 static void residual(const MgLevelPlan& L, const double* x, cudaStream_t st) {
+  if (L.rowcta) {
+    launch(k_row16_cta, L.nbr, 128, 0, st, L.ptr, L.col, L.blocks, x, L.nbr, 0, L.b, nullptr, nullptr, L.r, 0.0, 0.0,
+           0);
+    return;
+  }
   if (L.sym) {
     sym_apply(nullptr, L.sym, L.blocks, x, 1, L.b, nullptr, nullptr, L.r, 0.0, 0.0, 0, nullptr, st);
     return;
@@ -1027,6 +1137,16 @@ extern "C" int bamg_mg_use_graph(bamg_mg* m, int32_t on) {
   m->use_graph = on != 0;
   m->dirty = true;
   return 0;
+}
+
+extern "C" int32_t bamg_mg_level_kind(const bamg_mg* m, int32_t level) {
+  if (!m || m->dirty || level < 0 || level >= (int)m->lv.size()) return -1;
+  const MgLevelPlan& L = m->lv[level];
+  if (L.inv) return 4;
+  if (L.rowcta) return 1;
+  if (L.sym) return 0;
+  if (L.CH) return 2;
+  return 3;
 }
 
 extern "C" int bamg_mg_apply(bamg_ctx* ctx, bamg_mg* m, const double* r, double* z, void* stream) {

@@ -114,6 +114,17 @@ def test_symmetric_half_storage_spmv(P):
         outs.append((float(out.item()), D().host(y2)))
     assert abs(outs[0][0] - x @ ref) <= 1e-11 * abs(x @ ref)
     assert outs[0][0] == outs[1][0] and np.array_equal(outs[0][1], outs[1][1])
+    # with and without the fused dot, and the residual epilogue: the same sums,
+    # bit for bit, on every rerun
+    for _ in range(3):
+        y1 = D().empty(S.shape[0])
+        D().call("bamg_symop_spmv", S._symop.handle, S.blocks, xd, y1, None)
+        assert np.array_equal(D().host(y1), outs[0][1])
+    b = rng.normal(size=S.shape[0])
+    bd = D().f64(b)
+    r1 = D().empty(S.shape[0])
+    D().call("bamg_symop_residual", S._symop.handle, S.blocks, xd, bd, r1)
+    assert np.array_equal(D().host(r1), b - outs[0][1])
 
 
 def test_symmetric_half_storage_coarse_operator(P):

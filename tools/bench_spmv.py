@@ -36,9 +36,11 @@ def main(config=4):
     nnz = S.n_block_entries
     full = timeit(lambda: D.call("bamg_bsr_spmv", 9, S._ptr, S._col, S.blocks, x, y, S.n_block_rows, None))
     sym = timeit(lambda: D.call("bamg_symop_spmv", S._symop.handle, S.blocks, x, y, None))
+    dot = D.empty(1)
+    two = timeit(lambda: D.call("bamg_symop_spmv", S._symop.handle, S.blocks, x, y, dot))
     B = nnz * (8 * 81 + 4) + 4 * (S.n_block_rows + 1) + 16 * n
     print(f"nnzb={nnz} full {full*1e3:.1f} us ({B/full/1e6:.0f} GB/s)  sym {sym*1e3:.1f} us "
-          f"(effective {B/sym/1e6:.0f} GB/s)")
+          f"(effective {B/sym/1e6:.0f} GB/s)  two-pass+dot {two*1e3:.1f} us")
 
 
 if __name__ == "__main__":
