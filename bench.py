@@ -156,6 +156,16 @@ def sym_bytes(nnzb, nbr, nch, b=9):
     return p1 + p2
 
 
+def ncu_traffic():
+    """DRAM bytes per launch of the roofline kernel pair from the committed ncu --set full
+    capture (profiles/r1/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1", "traffic.json")) as fh:
+            return float(json.load(fh)["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def measured_peak_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -344,7 +354,8 @@ def gpu_arm(args, rank, world):
         "roofline": {"kernel": ("k_sym9_upper + k_sym9_finish (level-0 S product, half storage)" if has_sym
                                 else "k_bsr_spmv<9> (level-0 S SpMV)"),
                      "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "bytes_per_launch": b_spmv,
+                     "frac": achieved / peak, "traffic": ncu_traffic() if has_sym else None,
+                     "traffic_source": "profiles/r1/traffic.json (ncu --set full, cold L2)", "bytes_per_launch": b_spmv,
                      "launch_ms": t_spmv * 1e3, "effective_gbs": b_full / t_spmv / 1e9,
                      "full_bsr_bytes": b_full},
         "vcycle": vcyc,
