@@ -9,6 +9,8 @@
 #include "common.cuh"
 #include "ctx.h"
 
+#include <mutex>
+
 template <int BS>
 struct Lanes {
   static constexpr int G = 32 / BS;  // lane groups per warp

@@ -1357,49 +1357,41 @@ extern "C" int bamg_galerkin_map(bamg_ctx* ctx, const int32_t* ptr, const int32_
   return 0;
 }
 
-// Warp per coarse block; lane owns 8 entries (row lane/2, cols 8*(lane&1)..+7).
-// T = A_ij P_j (bs x 16) staged in shared memory per fine block.
-template <int BS>
-__global__ void __launch_bounds__(128)
-k_galerkin_numeric(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_sorted,
-                   const int* __restrict__ fine_row, const int* __restrict__ col, const double* __restrict__ blocks,
-                   const double* __restrict__ P, int64_t nnz_coarse, double* __restrict__ out) {
-  __shared__ double Ts[4][BS * NS];
-  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int r = lane >> 1, c0 = (lane & 1) * 8;
-  double* T = Ts[w];
-  for (int64_t cb = warp; cb < nnz_coarse; cb += nwarps) {
-    double acc[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-    for (int q = cblk_ptr[cb]; q < cblk_ptr[cb + 1]; ++q) {
-      int fb = fine_sorted[q];
-      int i = fine_row[fb], j = col[fb];
-      const double* a = blocks + (int64_t)fb * BS * BS;
-      const double* pj = P + (int64_t)j * BS * NS;
-      // T = A_ij P_j
-      for (int t = lane; t < BS * NS; t += 32) {
-        int rr = t / NS, cc = t - rr * NS;
-        double s = 0.0;
-#pragma unroll
-        for (int k = 0; k < BS; ++k) s = fma(a[rr * BS + k], pj[k * NS + cc], s);
-        T[t] = s;
-      }
-      __syncwarp();
-      const double* pi = P + (int64_t)i * BS * NS;
-#pragma unroll
-      for (int k = 0; k < BS; ++k) {
-        double pik = pi[k * NS + r];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q] = fma(pik, T[k * NS + c0 + q], acc[q]);
-      }
-      __syncwarp();
+// Coarse block q = (a, b): the row a is the last a with Cptr[a] <= q.
+__device__ __forceinline__ int coarse_row_of(const int* __restrict__ Cptr, int n, int64_t q) {
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (Cptr[mid] <= q) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Output stage of the Galerkin kernels for an upper coarse block (a, b), a <= b, from
+// the four warp partials in `red` (summed in warp order): (a, b) = C and its mirror
+// (b, a) = C^T, so the stored operator is exactly symmetric; a diagonal block is
+// 0.5 (C + C^T), the symmetrisation of multigrid.py:444-455. The lower blocks are
+// never multiplied out (half the Galerkin flops, no separate symmetrisation pass).
+__device__ __forceinline__ void galerkin_store_sym(const double (*red)[NS * NS], int a, int b,
+                                                   const int* __restrict__ Cptr, const int* __restrict__ Ccol,
+                                                   int64_t cb, double* __restrict__ out) {
+  double* o = out + cb * NS * NS;
+  if (a == b) {
+    for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+      int r = e / NS, c = e - r * NS;
+      double v = ((red[0][e] + red[1][e]) + red[2][e]) + red[3][e];
+      int et = c * NS + r;
+      double vt = ((red[0][et] + red[1][et]) + red[2][et]) + red[3][et];
+      o[e] = 0.5 * (v + vt);
     }
-    double* o = out + cb * NS * NS + r * NS + c0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) o[q] = acc[q];
+    return;
+  }
+  int t = Cptr[b] + lower_bound_i32(Ccol + Cptr[b], Cptr[b + 1] - Cptr[b], a);
+  double* y = out + (int64_t)t * NS * NS;
+  for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+    o[e] = ((red[0][e] + red[1][e]) + red[2][e]) + red[3][e];
+    int r = e / NS, c = e - r * NS, et = c * NS + r;
+    y[e] = ((red[0][et] + red[1][et]) + red[2][et]) + red[3][et];
   }
 }
 
@@ -1411,7 +1403,8 @@ template <int BS>
 __global__ void __launch_bounds__(128)
 k_galerkin_cta(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_sorted, const int* __restrict__ fine_row,
                const int* __restrict__ col, const double* __restrict__ blocks, const double* __restrict__ P,
-               int64_t nnz_coarse, double* __restrict__ out) {
+               int64_t nnz_coarse, const int* __restrict__ Cptr, const int* __restrict__ Ccol, int n_agg,
+               double* __restrict__ out) {
   __shared__ double sA[4][BS * BS];
   __shared__ double sPj[4][BS * NS];
   __shared__ double sPi[4][BS * NS];
@@ -1424,6 +1417,8 @@ k_galerkin_cta(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_so
   double* Pi = sPi[w];
   double* T = sT[w];
   for (int64_t cb = blockIdx.x; cb < nnz_coarse; cb += gridDim.x) {
+    const int ca = coarse_row_of(Cptr, n_agg, cb), cbc = Ccol[cb];
+    if (cbc < ca) continue;  // lower block: written as its upper partner's mirror
     double acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.0;
@@ -1464,8 +1459,7 @@ k_galerkin_cta(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_so
 #pragma unroll
     for (int q2 = 0; q2 < 8; ++q2) red[w][r * NS + c0 + q2] = acc[q2];
     __syncthreads();
-    double* o = out + cb * NS * NS;
-    for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) o[e] = ((red[0][e] + red[1][e]) + red[2][e]) + red[3][e];
+    galerkin_store_sym(red, ca, cbc, Cptr, Ccol, cb, out);
     __syncthreads();
   }
 }
@@ -1478,7 +1472,8 @@ template <int BS>
 __global__ void __launch_bounds__(128)
 k_galerkin_pipe(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_sorted, const int* __restrict__ fine_row,
                 const int* __restrict__ col, const double* __restrict__ blocks, const double* __restrict__ P,
-                int64_t nnz_coarse, double* __restrict__ out) {
+                int64_t nnz_coarse, const int* __restrict__ Cptr, const int* __restrict__ Ccol, int n_agg,
+                double* __restrict__ out) {
   // one stage: A (padded to an even count so P_j / P_i start 16 B aligned) | Pj | Pi.
   // The kernel is bound by L1 wavefronts (ncu: 83% of peak), so P_j and T are read
   // as double2 and P copied in 16 B chunks; the arithmetic is untouched.
@@ -1504,6 +1499,8 @@ k_galerkin_pipe(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_s
     cp_async_commit();
   };
   for (int64_t cb = blockIdx.x; cb < nnz_coarse; cb += gridDim.x) {
+    const int ca = coarse_row_of(Cptr, n_agg, cb), cbc = Ccol[cb];
+    if (cbc < ca) continue;  // lower block: written as its upper partner's mirror
     double acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.0;
@@ -1555,71 +1552,7 @@ k_galerkin_pipe(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_s
 #pragma unroll
     for (int q2 = 0; q2 < 8; ++q2) red[w][r * NS + c0 + q2] = acc[q2];
     __syncthreads();
-    double* o = out + cb * NS * NS;
-    for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) o[e] = ((red[0][e] + red[1][e]) + red[2][e]) + red[3][e];
-    __syncthreads();
-  }
-}
-
-// out_ab = 0.5 (B_ab + B_ba^T), in place, thread per upper block
-__global__ void k_sym_blocks(const int* __restrict__ Cptr, const int* __restrict__ Ccol, int n, double* __restrict__ B) {
-  for (int a = blockIdx.x; a < n; a += gridDim.x) {
-    for (int q = Cptr[a]; q < Cptr[a + 1]; ++q) {
-      int b = Ccol[q];
-      if (b < a) continue;
-      int t = Cptr[b] + lower_bound_i32(Ccol + Cptr[b], Cptr[b + 1] - Cptr[b], a);
-      double* X = B + (int64_t)q * NS * NS;
-      double* Y = B + (int64_t)t * NS * NS;
-      __syncthreads();
-      if (b == a) {
-        for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
-          int r = e / NS, c = e - r * NS;
-          if (c < r) continue;
-          double v = 0.5 * (X[r * NS + c] + X[c * NS + r]);
-          X[r * NS + c] = v;
-          X[c * NS + r] = v;
-        }
-      } else {
-        for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
-          int r = e / NS, c = e - r * NS;
-          double v = 0.5 * (X[r * NS + c] + Y[c * NS + r]);
-          X[r * NS + c] = v;
-          Y[c * NS + r] = v;
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
-// Same symmetrisation, one CTA per stored block q = (a, b) with a <= b: the row of q
-// comes from a binary search in Cptr, the mirror block from one in row b.
-__global__ void __launch_bounds__(256)
-k_sym_blocks2(const int* __restrict__ Cptr, const int* __restrict__ Ccol, int n, int64_t nnz, double* __restrict__ B) {
-  for (int64_t q = blockIdx.x; q < nnz; q += gridDim.x) {
-    int b = Ccol[q];
-    // row a: last a with Cptr[a] <= q
-    int lo = 0, hi = n;
-    while (hi - lo > 1) {
-      int mid = (lo + hi) >> 1;
-      if (Cptr[mid] <= q) lo = mid; else hi = mid;
-    }
-    int a = lo;
-    if (b < a) continue;
-    int t = Cptr[b] + lower_bound_i32(Ccol + Cptr[b], Cptr[b + 1] - Cptr[b], a);
-    double* X = B + q * NS * NS;
-    double* Y = B + (int64_t)t * NS * NS;
-    int e = threadIdx.x, r = e / NS, c = e - r * NS;
-    if (b == a) {
-      double v = 0.5 * (X[r * NS + c] + X[c * NS + r]);
-      __syncthreads();
-      X[r * NS + c] = v;
-    } else {
-      double v = 0.5 * (X[r * NS + c] + Y[c * NS + r]);
-      __syncthreads();
-      X[r * NS + c] = v;
-      Y[c * NS + r] = v;
-    }
+    galerkin_store_sym(red, ca, cbc, Cptr, Ccol, cb, out);
     __syncthreads();
   }
 }
@@ -1659,19 +1592,20 @@ extern "C" int bamg_galerkin_numeric(bamg_ctx* ctx, int32_t bs, const int32_t* c
     }
     switch (bs) {
       case 9: launch(k_galerkin_pipe<9>, g, 128, sm9, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse,
-                     out); break;
+                     Cptr, Ccol, n_agg, out); break;
       case 16: launch(k_galerkin_pipe<16>, g, 128, sm16, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P,
-                      nnz_coarse, out); break;
+                      nnz_coarse, Cptr, Ccol, n_agg, out); break;
       default: bamg_set_error("galerkin: unsupported block size %d", bs); return BAMG_ERR_UNSUPPORTED;
     }
   } else {
     switch (bs) {
-      case 9: launch(k_galerkin_cta<9>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
-      case 16: launch(k_galerkin_cta<16>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse, out); break;
+      case 9: launch(k_galerkin_cta<9>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse,
+                     Cptr, Ccol, n_agg, out); break;
+      case 16: launch(k_galerkin_cta<16>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse,
+                      Cptr, Ccol, n_agg, out); break;
       default: bamg_set_error("galerkin: unsupported block size %d", bs); return BAMG_ERR_UNSUPPORTED;
     }
   }
-  launch(k_sym_blocks2, grid_for(nnz_coarse, 1, 16), 256, 0, st, Cptr, Ccol, n_agg, nnz_coarse, out);
   launch(k_patch, grid_for(n_agg, 128), 128, 0, st, padded_cnt, Cptr, Ccol, n_agg, out);
   BAMG_LAUNCH_CHECK();
   return 0;

@@ -816,12 +816,34 @@ extern "C" bamg_mg* bamg_mg_create(int32_t n_levels) {
   return m;
 }
 
+// One instantiated V-cycle graph outlives its plan: the next hierarchy (the next LM
+// step's, usually with the same levels and kernel kinds) captures its own graph and
+// re-targets the parked executable with cudaGraphExecUpdate instead of paying a
+// full instantiation (~1 ms of host time for ~60 nodes). Updates affect only later
+// launches, so a parked executable may still be in flight.
+static std::mutex g_exec_mu;
+static cudaGraphExec_t g_parked_exec = nullptr;
+
+static void park_exec(cudaGraphExec_t e) {
+  if (!e) return;
+  std::lock_guard<std::mutex> lk(g_exec_mu);
+  if (g_parked_exec) cudaGraphExecDestroy(g_parked_exec);
+  g_parked_exec = e;
+}
+
+static cudaGraphExec_t take_parked_exec() {
+  std::lock_guard<std::mutex> lk(g_exec_mu);
+  cudaGraphExec_t e = g_parked_exec;
+  g_parked_exec = nullptr;
+  return e;
+}
+
 static void mg_free_work(bamg_mg* m) {
   if (m->arena) cudaFreeAsync(m->arena, m->arena_stream);
   m->arena = nullptr;
   for (auto& L : m->lv) L.b = L.x = L.xs = L.d = L.r = nullptr;
   m->in = m->out = nullptr;
-  if (m->exec) cudaGraphExecDestroy(m->exec);
+  if (m->exec) park_exec(m->exec);
   if (m->graph) cudaGraphDestroy(m->graph);
   m->exec = nullptr;
   m->graph = nullptr;
@@ -1100,6 +1122,16 @@ static int mg_prepare(bamg_mg* m, cudaStream_t st) {
   if (rc) return rc;
   BAMG_CUDA_CHECK(e);
   m->graph = g;
+  cudaGraphExec_t pe = take_parked_exec();
+  if (pe) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(pe, g, &info) == cudaSuccess) {
+      m->exec = pe;
+      return 0;
+    }
+    cudaGetLastError();  // clear the update failure; instantiate instead
+    cudaGraphExecDestroy(pe);
+  }
   BAMG_CUDA_CHECK(cudaGraphInstantiate(&m->exec, g, 0));
   (void)st;
   return 0;

@@ -50,6 +50,13 @@ gaps.sort(reverse=True)
 print("largest idle gaps (us, at ms, next kernel):")
 for g, at, name in gaps[:25]:
     print(f"  {g:8.1f} at {at / 1e3:7.2f}  {name}")
+if len(sys.argv) > 2:  # full ordered listing (start ms, gap us, duration us, stream)
+    with open(sys.argv[2], "w") as fh:
+        prev = t0
+        for e in ev:
+            s_, f_ = e.time_range.start, e.time_range.end
+            fh.write(f"{(s_ - t0) / 1e3:9.3f} gap {s_ - prev:8.1f} dur {f_ - s_:8.1f}  {e.name.split('(')[0][:60]}\n")
+            prev = max(prev, f_)
 agg = {}
 for e in ev:
     k = e.name.split("(")[0][:50]
