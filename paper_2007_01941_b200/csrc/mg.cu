@@ -1357,14 +1357,27 @@ extern "C" int bamg_galerkin_map(bamg_ctx* ctx, const int32_t* ptr, const int32_
   return 0;
 }
 
-// Coarse block q = (a, b): the row a is the last a with Cptr[a] <= q.
-__device__ __forceinline__ int coarse_row_of(const int* __restrict__ Cptr, int n, int64_t q) {
-  int lo = 0, hi = n;
-  while (hi - lo > 1) {
-    int mid = (lo + hi) >> 1;
-    if (Cptr[mid] <= q) lo = mid; else hi = mid;
+// Upper coarse blocks (a <= b) of a symmetric coarse pattern as a work list for the
+// Galerkin kernels: block position and the position of its mirror (b, a).
+__global__ void k_gal_upper_count(const int* __restrict__ Cptr, const int* __restrict__ Ccol, int n,
+                                  int* __restrict__ cnt) {
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
+    int b0 = Cptr[a], nn = Cptr[a + 1] - b0;
+    cnt[a] = nn - lower_bound_i32(Ccol + b0, nn, a);
   }
-  return lo;
+}
+
+__global__ void k_gal_upper_fill(const int* __restrict__ Cptr, const int* __restrict__ Ccol, int n,
+                                 const int* __restrict__ off, int* __restrict__ ublk, int* __restrict__ umir) {
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
+    int b0 = Cptr[a], nn = Cptr[a + 1] - b0;
+    int o = off[a];
+    for (int q = b0 + lower_bound_i32(Ccol + b0, nn, a); q < b0 + nn; ++q, ++o) {
+      int b = Ccol[q];
+      ublk[o] = q;
+      umir[o] = Cptr[b] + lower_bound_i32(Ccol + Cptr[b], Cptr[b + 1] - Cptr[b], a);
+    }
+  }
 }
 
 // Output stage of the Galerkin kernels for an upper coarse block (a, b), a <= b, from
@@ -1372,11 +1385,10 @@ __device__ __forceinline__ int coarse_row_of(const int* __restrict__ Cptr, int n
 // (b, a) = C^T, so the stored operator is exactly symmetric; a diagonal block is
 // 0.5 (C + C^T), the symmetrisation of multigrid.py:444-455. The lower blocks are
 // never multiplied out (half the Galerkin flops, no separate symmetrisation pass).
-__device__ __forceinline__ void galerkin_store_sym(const double (*red)[NS * NS], int a, int b,
-                                                   const int* __restrict__ Cptr, const int* __restrict__ Ccol,
-                                                   int64_t cb, double* __restrict__ out) {
+__device__ __forceinline__ void galerkin_store_sym(const double (*red)[NS * NS], int64_t cb, int64_t t,
+                                                   double* __restrict__ out) {
   double* o = out + cb * NS * NS;
-  if (a == b) {
+  if (t == cb) {
     for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
       int r = e / NS, c = e - r * NS;
       double v = ((red[0][e] + red[1][e]) + red[2][e]) + red[3][e];
@@ -1386,8 +1398,7 @@ __device__ __forceinline__ void galerkin_store_sym(const double (*red)[NS * NS],
     }
     return;
   }
-  int t = Cptr[b] + lower_bound_i32(Ccol + Cptr[b], Cptr[b + 1] - Cptr[b], a);
-  double* y = out + (int64_t)t * NS * NS;
+  double* y = out + t * NS * NS;
   for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
     o[e] = ((red[0][e] + red[1][e]) + red[2][e]) + red[3][e];
     int r = e / NS, c = e - r * NS, et = c * NS + r;
@@ -1403,8 +1414,7 @@ template <int BS>
 __global__ void __launch_bounds__(128)
 k_galerkin_cta(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_sorted, const int* __restrict__ fine_row,
                const int* __restrict__ col, const double* __restrict__ blocks, const double* __restrict__ P,
-               int64_t nnz_coarse, const int* __restrict__ Cptr, const int* __restrict__ Ccol, int n_agg,
-               double* __restrict__ out) {
+               int n_up, const int* __restrict__ ublk, const int* __restrict__ umir, double* __restrict__ out) {
   __shared__ double sA[4][BS * BS];
   __shared__ double sPj[4][BS * NS];
   __shared__ double sPi[4][BS * NS];
@@ -1416,9 +1426,8 @@ k_galerkin_cta(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_so
   double* Pj = sPj[w];
   double* Pi = sPi[w];
   double* T = sT[w];
-  for (int64_t cb = blockIdx.x; cb < nnz_coarse; cb += gridDim.x) {
-    const int ca = coarse_row_of(Cptr, n_agg, cb), cbc = Ccol[cb];
-    if (cbc < ca) continue;  // lower block: written as its upper partner's mirror
+  for (int u = blockIdx.x; u < n_up; u += gridDim.x) {
+    const int64_t cb = ublk[u], cmir = umir[u];  // lower blocks: written as mirrors
     double acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.0;
@@ -1459,7 +1468,7 @@ k_galerkin_cta(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_so
 #pragma unroll
     for (int q2 = 0; q2 < 8; ++q2) red[w][r * NS + c0 + q2] = acc[q2];
     __syncthreads();
-    galerkin_store_sym(red, ca, cbc, Cptr, Ccol, cb, out);
+    galerkin_store_sym(red, cb, cmir, out);
     __syncthreads();
   }
 }
@@ -1472,8 +1481,7 @@ template <int BS>
 __global__ void __launch_bounds__(128)
 k_galerkin_pipe(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_sorted, const int* __restrict__ fine_row,
                 const int* __restrict__ col, const double* __restrict__ blocks, const double* __restrict__ P,
-                int64_t nnz_coarse, const int* __restrict__ Cptr, const int* __restrict__ Ccol, int n_agg,
-                double* __restrict__ out) {
+                int n_up, const int* __restrict__ ublk, const int* __restrict__ umir, double* __restrict__ out) {
   // one stage: A (padded to an even count so P_j / P_i start 16 B aligned) | Pj | Pi.
   // The kernel is bound by L1 wavefronts (ncu: 83% of peak), so P_j and T are read
   // as double2 and P copied in 16 B chunks; the arithmetic is untouched.
@@ -1498,9 +1506,8 @@ k_galerkin_pipe(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_s
     }
     cp_async_commit();
   };
-  for (int64_t cb = blockIdx.x; cb < nnz_coarse; cb += gridDim.x) {
-    const int ca = coarse_row_of(Cptr, n_agg, cb), cbc = Ccol[cb];
-    if (cbc < ca) continue;  // lower block: written as its upper partner's mirror
+  for (int u = blockIdx.x; u < n_up; u += gridDim.x) {
+    const int64_t cb = ublk[u], cmir = umir[u];  // lower blocks: written as mirrors
     double acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.0;
@@ -1552,7 +1559,7 @@ k_galerkin_pipe(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_s
 #pragma unroll
     for (int q2 = 0; q2 < 8; ++q2) red[w][r * NS + c0 + q2] = acc[q2];
     __syncthreads();
-    galerkin_store_sym(red, ca, cbc, Cptr, Ccol, cb, out);
+    galerkin_store_sym(red, cb, cmir, out);
     __syncthreads();
   }
 }
@@ -1577,7 +1584,16 @@ extern "C" int bamg_galerkin_numeric(bamg_ctx* ctx, int32_t bs, const int32_t* c
   (void)ctx;
   cudaStream_t st = as_stream(stream);
   if (nnz_coarse <= 0) return 0;
-  int g = grid_for(nnz_coarse, 1, 12);
+  // upper coarse blocks (the pattern is symmetric: (nnz + n) / 2 of them)
+  const int n_up = (int)((nnz_coarse + n_agg) / 2);
+  int* ub = nullptr;
+  BAMG_CUDA_CHECK(cudaMallocAsync(&ub, sizeof(int) * (2 * (size_t)n_up + n_agg + 1), st));
+  int *ublk = ub, *umir = ub + n_up, *uoff = ub + 2 * (size_t)n_up;
+  launch(k_gal_upper_count, grid_for(n_agg, 128), 128, 0, st, Cptr, Ccol, n_agg, uoff);
+  int rc = scan_exclusive_int(uoff, uoff, (int64_t)n_agg + 1, nullptr, st);
+  if (rc) return rc;
+  launch(k_gal_upper_fill, grid_for(n_agg, 128), 128, 0, st, Cptr, Ccol, n_agg, (const int*)uoff, ublk, umir);
+  int g = grid_for(n_up, 1, 12);
   static const bool pipe = [] {
     const char* e = getenv("BAMG_GALERKIN_PIPE");
     return !(e && e[0] == '0');
@@ -1591,22 +1607,23 @@ extern "C" int bamg_galerkin_numeric(bamg_ctx* ctx, int32_t bs, const int32_t* c
       attr = true;
     }
     switch (bs) {
-      case 9: launch(k_galerkin_pipe<9>, g, 128, sm9, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse,
-                     Cptr, Ccol, n_agg, out); break;
-      case 16: launch(k_galerkin_pipe<16>, g, 128, sm16, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P,
-                      nnz_coarse, Cptr, Ccol, n_agg, out); break;
+      case 9: launch(k_galerkin_pipe<9>, g, 128, sm9, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, n_up,
+                     (const int*)ublk, (const int*)umir, out); break;
+      case 16: launch(k_galerkin_pipe<16>, g, 128, sm16, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, n_up,
+                      (const int*)ublk, (const int*)umir, out); break;
       default: bamg_set_error("galerkin: unsupported block size %d", bs); return BAMG_ERR_UNSUPPORTED;
     }
   } else {
     switch (bs) {
-      case 9: launch(k_galerkin_cta<9>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse,
-                     Cptr, Ccol, n_agg, out); break;
-      case 16: launch(k_galerkin_cta<16>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, nnz_coarse,
-                      Cptr, Ccol, n_agg, out); break;
+      case 9: launch(k_galerkin_cta<9>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, n_up,
+                     (const int*)ublk, (const int*)umir, out); break;
+      case 16: launch(k_galerkin_cta<16>, g, 128, 0, st, cblk_ptr, fine_sorted, fine_row, col, blocks, P, n_up,
+                      (const int*)ublk, (const int*)umir, out); break;
       default: bamg_set_error("galerkin: unsupported block size %d", bs); return BAMG_ERR_UNSUPPORTED;
     }
   }
   launch(k_patch, grid_for(n_agg, 128), 128, 0, st, padded_cnt, Cptr, Ccol, n_agg, out);
+  cudaFreeAsync(ub, st);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
