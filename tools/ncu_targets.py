@@ -49,6 +49,10 @@ def main(config=4, what="spmv,vcycle,schur,evaluate"):
         SC.schur_explicit(s)
     if "evaluate" in what:
         P.evaluate(prob)
+    if "backsub" in what:
+        P.back_substitute(s, dc)
+    if "build" in what:
+        P.build_system(jac, P.Damping.from_jacobian(jac, 1e4))
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
     print("done", cg.iterations)
