@@ -172,10 +172,13 @@ int bamg_galerkin_pattern(bamg_ctx* ctx, const int32_t* agg_ptr, const int32_t* 
 int bamg_galerkin_map(bamg_ctx* ctx, const int32_t* ptr, const int32_t* col, const int32_t* agg, int32_t n,
                       int64_t nnz_fine, const int32_t* Cptr, const int32_t* Ccol, int64_t nnz_coarse,
                       int32_t* fine_sorted, int32_t* cblk_ptr, int32_t* fine_row, void* stream);
+/* A_{l+1} = sym(P^T A_l P) (multigrid.py:409, 444-471): only the upper coarse blocks are
+ * multiplied out; each is stored with its transpose at the mirror position (diagonal
+ * blocks: 0.5 (C + C^T)), then the padded-dof patch. nnz_fine = fine blocks in the map. */
 int bamg_galerkin_numeric(bamg_ctx* ctx, int32_t bs, const int32_t* cblk_ptr, const int32_t* fine_sorted,
                           const int32_t* fine_row, const int32_t* col, const double* blocks, const double* P,
-                          int32_t n_agg, const int32_t* Cptr, const int32_t* Ccol, int64_t nnz_coarse,
-                          const int32_t* padded_cnt, double* out, void* stream);
+                          int64_t nnz_fine, int32_t n_agg, const int32_t* Cptr, const int32_t* Ccol,
+                          int64_t nnz_coarse, const int32_t* padded_cnt, double* out, void* stream);
 /* coarsest direct solve: multigrid.py:431-440 (cho_factor) / 477-478 (cho_solve) */
 int bamg_coarse_factor(bamg_ctx* ctx, const int32_t* ptr, const int32_t* col, const double* blocks, int32_t nbr,
                        int32_t bs, double* dense, double* work, double* inv, int32_t* flag_dev, void* stream);

@@ -1564,6 +1564,171 @@ k_galerkin_pipe(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_s
   }
 }
 
+// Row and column of every fine block of the coarse-block-sorted list (gathered once,
+// so the Galerkin warps read them coalesced instead of through fine_sorted).
+__global__ void k_gal_gather_ij(const int* __restrict__ fine_sorted, const int* __restrict__ fine_row,
+                                const int* __restrict__ col, int64_t nnz_fine, int* __restrict__ fsi,
+                                int* __restrict__ fsj) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz_fine; q += (int64_t)gridDim.x * blockDim.x) {
+    int fb = fine_sorted[q];
+    fsi[q] = fine_row[fb];
+    fsj[q] = col[fb];
+  }
+}
+
+// Warp per upper coarse block with ONE operand pipeline running across the warp's
+// blocks: while fine block q is multiplied, the operands (A_ij, P_j, P_i) of the next
+// fine block -- of this coarse block or already of the next one -- are in flight
+// (cp.async, two stages), and the (fb, i, j) triples of 32 fine blocks at a time are
+// held one per lane (the next coarse block's first 32 are loaded a block ahead). The
+// CTA-per-block kernels paid the index chain and the pipeline fill on every coarse
+// block. One warp sums a block's fine blocks in list order (deterministic).
+template <int BS>
+__global__ void __launch_bounds__(128, BS == 9 ? 4 : 3)
+k_galerkin_warp(const int* __restrict__ cblk_ptr, const int* __restrict__ fine_sorted, const int* __restrict__ fsi,
+                const int* __restrict__ fsj, const double* __restrict__ blocks, const double* __restrict__ P, int n_up,
+                const int* __restrict__ ublk, const int* __restrict__ umir, double* __restrict__ out) {
+  constexpr int SA = BS * BS, SAP = (SA + 1) & ~1, SP = BS * NS, STG = SAP + 2 * SP, TS = NS + 2;
+  constexpr int WSM = 2 * STG + BS * TS + NS * (NS + 1);
+  extern __shared__ __align__(16) double gsm[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* stg = gsm + (size_t)w * WSM;
+  double* T = stg + 2 * STG;
+  double* D = T + BS * TS;  // diagonal-block transpose scratch
+  const int r = lane >> 1, c0 = (lane & 1) * 8;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (u >= n_up) return;
+  auto issue = [&](int fb, int i, int j, double* dst) {
+    const double* a = blocks + (int64_t)fb * SA;
+    const double* pj = P + (int64_t)j * SP;
+    const double* pi = P + (int64_t)i * SP;
+    for (int t = lane; t < SA; t += 32) cp_async8(dst + t, a + t);
+    for (int t = lane; t < SP / 2; t += 32) {
+      cp_async16(dst + SAP + 2 * t, pj + 2 * t);
+      cp_async16(dst + SAP + SP + 2 * t, pi + 2 * t);
+    }
+    cp_async_commit();
+  };
+  // current block
+  int64_t cb = ublk[u], cm = umir[u];
+  int q = cblk_ptr[cb], qe = cblk_ptr[cb + 1];
+  int base = q;  // first list position held in the index registers
+  int xfb = 0, xi = 0, xj = 0;
+  if (base + lane < qe) { xfb = fine_sorted[base + lane]; xi = fsi[base + lane]; xj = fsj[base + lane]; }
+  // next block (one block ahead)
+  int un = u + nwarps;
+  int64_t cbn = 0, cmn = 0;
+  int qn = 0, qne = 0, nfb = 0, ni = 0, nj = 0;
+  auto prefetch_next = [&]() {
+    if (un < n_up) {
+      cbn = ublk[un];
+      cmn = umir[un];
+      qn = cblk_ptr[cbn];
+      qne = cblk_ptr[cbn + 1];
+      if (qn + lane < qne) { nfb = fine_sorted[qn + lane]; ni = fsi[qn + lane]; nj = fsj[qn + lane]; }
+    }
+  };
+  prefetch_next();
+  issue(__shfl_sync(FULL_MASK, xfb, 0), __shfl_sync(FULL_MASK, xi, 0), __shfl_sync(FULL_MASK, xj, 0), stg);
+  double acc[8];
+#pragma unroll
+  for (int k2 = 0; k2 < 8; ++k2) acc[k2] = 0.0;
+  for (int k = 0;; ++k) {
+    const bool last = (q + 1 == qe);
+    // the item after q: in this block (refill the index registers every 32), or the
+    // first of the next block
+    if (!last) {
+      int q2 = q + 1;
+      if (q2 - base == 32) {
+        base = q2;
+        if (base + lane < qe) { xfb = fine_sorted[base + lane]; xi = fsi[base + lane]; xj = fsj[base + lane]; }
+      }
+      int s2 = q2 - base;
+      issue(__shfl_sync(FULL_MASK, xfb, s2), __shfl_sync(FULL_MASK, xi, s2), __shfl_sync(FULL_MASK, xj, s2),
+            stg + ((k + 1) & 1) * STG);
+    } else if (un < n_up) {
+      issue(__shfl_sync(FULL_MASK, nfb, 0), __shfl_sync(FULL_MASK, ni, 0), __shfl_sync(FULL_MASK, nj, 0),
+            stg + ((k + 1) & 1) * STG);
+    } else {
+      cp_async_commit();
+    }
+    cp_async_wait<1>();
+    __syncwarp();
+    const double* A = stg + (k & 1) * STG;
+    const double* Pj = A + SAP;
+    const double* Pi = A + SAP + SP;
+    if (r < BS) {  // T[r][c0..c0+7] = sum_k A[r][k] Pj[k][c0..]
+      double t8[8];
+#pragma unroll
+      for (int q2 = 0; q2 < 8; ++q2) t8[q2] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < BS; ++kk) {
+        double ark = A[r * BS + kk];
+        const double2* pr = reinterpret_cast<const double2*>(Pj + kk * NS + c0);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          double2 v = pr[h];
+          t8[2 * h] = fma(ark, v.x, t8[2 * h]);
+          t8[2 * h + 1] = fma(ark, v.y, t8[2 * h + 1]);
+        }
+      }
+      double2* tw = reinterpret_cast<double2*>(T + r * TS + c0);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) tw[h] = make_double2(t8[2 * h], t8[2 * h + 1]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int kk = 0; kk < BS; ++kk) {
+      double pik = Pi[kk * NS + r];
+      const double2* tr = reinterpret_cast<const double2*>(T + kk * TS + c0);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        double2 v = tr[h];
+        acc[2 * h] = fma(pik, v.x, acc[2 * h]);
+        acc[2 * h + 1] = fma(pik, v.y, acc[2 * h + 1]);
+      }
+    }
+    __syncwarp();
+    if (!last) {
+      ++q;
+      continue;
+    }
+    // block done: (a, b) = C, mirror (b, a) = C^T; diagonal: 0.5 (C + C^T)
+    double* o = out + cb * NS * NS;
+    if (cm == cb) {
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2) D[r * (NS + 1) + c0 + k2] = acc[k2];
+      __syncwarp();
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2) o[r * NS + c0 + k2] = 0.5 * (acc[k2] + D[(c0 + k2) * (NS + 1) + r]);
+      __syncwarp();
+    } else {
+      double* y = out + cm * NS * NS;
+      double2* o2 = reinterpret_cast<double2*>(o + r * NS + c0);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) o2[h] = make_double2(acc[2 * h], acc[2 * h + 1]);
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2) y[(c0 + k2) * NS + r] = acc[k2];
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < 8; ++k2) acc[k2] = 0.0;
+    if (un >= n_up) break;
+    u = un;
+    cb = cbn;
+    cm = cmn;
+    q = qn;
+    qe = qne;
+    base = q;
+    xfb = nfb;
+    xi = ni;
+    xj = nj;
+    un = u + nwarps;
+    prefetch_next();
+  }
+  cp_async_wait<0>();
+}
+
 // +1.0 on padded coarse dofs' diagonal entries (multigrid.py:458-471)
 __global__ void k_patch(const int* __restrict__ padded_cnt, const int* __restrict__ Cptr, const int* __restrict__ Ccol,
                         int n_agg, double* __restrict__ B) {
@@ -1579,8 +1744,9 @@ __global__ void k_patch(const int* __restrict__ padded_cnt, const int* __restric
 
 extern "C" int bamg_galerkin_numeric(bamg_ctx* ctx, int32_t bs, const int32_t* cblk_ptr, const int32_t* fine_sorted,
                                      const int32_t* fine_row, const int32_t* col, const double* blocks,
-                                     const double* P, int32_t n_agg, const int32_t* Cptr, const int32_t* Ccol,
-                                     int64_t nnz_coarse, const int32_t* padded_cnt, double* out, void* stream) {
+                                     const double* P, int64_t nnz_fine, int32_t n_agg, const int32_t* Cptr,
+                                     const int32_t* Ccol, int64_t nnz_coarse, const int32_t* padded_cnt, double* out,
+                                     void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
   if (nnz_coarse <= 0) return 0;
@@ -1598,7 +1764,32 @@ extern "C" int bamg_galerkin_numeric(bamg_ctx* ctx, int32_t bs, const int32_t* c
     const char* e = getenv("BAMG_GALERKIN_PIPE");
     return !(e && e[0] == '0');
   }();
-  if (pipe) {
+  static const int gmode = [] {
+    const char* e = getenv("BAMG_GALERKIN_WARP");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  // warp pipeline for the 9x9 fine level (1.96 -> 1.12 ms at c4 level 0); the coarse
+  // 16x16 levels keep the CTA kernel (0.65 vs 0.70 ms: the 16x16 stages cost the warp
+  // kernel occupancy)
+  if (gmode == 1 && bs == 9) {
+    int* ij = nullptr;
+    BAMG_CUDA_CHECK(cudaMallocAsync(&ij, sizeof(int) * 2 * (size_t)(nnz_fine > 0 ? nnz_fine : 1), st));
+    int *fsi = ij, *fsj = ij + nnz_fine;
+    if (nnz_fine > 0)
+      launch(k_gal_gather_ij, grid_for(nnz_fine, 256), 256, 0, st, fine_sorted, fine_row, col, nnz_fine, fsi, fsj);
+    const int wsm9 = 2 * ((81 + 1) + 2 * 9 * NS) + 9 * (NS + 2) + NS * (NS + 1);
+    const size_t sm9 = sizeof(double) * 4 * wsm9;
+    static bool wattr = false;
+    if (!wattr) {
+      BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_galerkin_warp<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm9));
+      wattr = true;
+    }
+    int64_t warps = n_up < (int64_t)bamg_num_sms() * 24 ? n_up : (int64_t)bamg_num_sms() * 24;
+    int gw = (int)ceil_div(warps, 4);
+    launch(k_galerkin_warp<9>, gw, 128, sm9, st, cblk_ptr, fine_sorted, (const int*)fsi, (const int*)fsj, blocks, P,
+           n_up, (const int*)ublk, (const int*)umir, out);
+    cudaFreeAsync(ij, st);
+  } else if (pipe) {
     static bool attr = false;
     const size_t sm9 = sizeof(double) * 4 * 2 * (82 + 2 * 9 * NS), sm16 = sizeof(double) * 4 * 2 * (256 + 2 * 16 * NS);
     if (!attr) {

@@ -274,7 +274,7 @@ def galerkin(P: BlockSparseMatrix, A: BlockSparseMatrix, agg: Aggregation) -> Bl
            fine_row)
     out = D.empty(max(nnzc, 1), NULLSPACE_DIM, NULLSPACE_DIM)
     D.call("bamg_galerkin_numeric", A.row_block_size, cblk_ptr, fine_sorted, fine_row, A._col, A.blocks, P.blocks,
-           na, counts, Ccol, nnzc, P.padded_count, out)
+           nnzf, na, counts, Ccol, nnzc, P.padded_count, out)
     C = BlockSparseMatrix(na, na, NULLSPACE_DIM, NULLSPACE_DIM, counts, Ccol[:nnzc], out[:nnzc], _validate=False)
     if _SYMMETRIC_COARSE and na > 0:
         # symmetrised exactly (both mirror blocks written from one value): the
