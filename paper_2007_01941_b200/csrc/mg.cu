@@ -928,31 +928,34 @@ __device__ __forceinline__ void warp_sum16(double* v) {
     for (int c = 0; c < 16; ++c) v[c] += __shfl_xor_sync(FULL_MASK, v[c], o);
 }
 
+// Shared-memory leading dimension of the QR panels: 17, not 16 -- with 16-double rows
+// every column access (lane = row) hit one bank pair (32-way conflicts).
+#define QLD 17
 // apply H_j (reflector in column j below the diagonal, tau) to columns [from, NS) of A
 __device__ __forceinline__ void reflect_cols(double* A, int m, int j, int from, double tau, int lane) {
   double w[16];
 #pragma unroll
   for (int c = 0; c < 16; ++c) w[c] = 0.0;
   for (int i = j + 1 + lane; i < m; i += 32) {
-    double v = A[i * 16 + j];
+    double v = A[i * QLD + j];
 #pragma unroll
     for (int c = 0; c < 16; ++c)
-      if (c >= from) w[c] += v * A[i * 16 + c];
+      if (c >= from) w[c] += v * A[i * QLD + c];
   }
   warp_sum16(w);
 #pragma unroll
-  for (int c = 0; c < 16; ++c) w[c] = w[c] + A[j * 16 + c];
+  for (int c = 0; c < 16; ++c) w[c] = w[c] + A[j * QLD + c];
   __syncwarp();
   for (int i = j + 1 + lane; i < m; i += 32) {
-    double v = A[i * 16 + j];
+    double v = A[i * QLD + j];
 #pragma unroll
     for (int c = 0; c < 16; ++c)
-      if (c >= from) A[i * 16 + c] -= tau * w[c] * v;
+      if (c >= from) A[i * QLD + c] -= tau * w[c] * v;
   }
   if (lane == 0) {
 #pragma unroll
     for (int c = 0; c < 16; ++c)
-      if (c >= from) A[j * 16 + c] -= tau * w[c];
+      if (c >= from) A[j * QLD + c] -= tau * w[c];
   }
   __syncwarp();
 }
@@ -961,19 +964,19 @@ __device__ void householder_step(double* A, int m, int j, int lane, double* tau_
                                  double* diag_out) {
   // column j, rows j..m-1
   double xs = 0.0;
-  for (int i = j + 1 + lane; i < m; i += 32) xs += A[i * NS + j] * A[i * NS + j];
+  for (int i = j + 1 + lane; i < m; i += 32) xs += A[i * QLD + j] * A[i * QLD + j];
   xs = warp_sum(xs);
-  double alpha = A[j * NS + j];
+  double alpha = A[j * QLD + j];
   double tau = 0.0, beta = alpha;
   if (xs > 0.0) {
     double xnorm = sqrt(xs);
     beta = -copysign(hypot(alpha, xnorm), alpha);
     tau = (beta - alpha) / beta;
     double scal = 1.0 / (alpha - beta);
-    for (int i = j + 1 + lane; i < m; i += 32) A[i * NS + j] *= scal;
+    for (int i = j + 1 + lane; i < m; i += 32) A[i * QLD + j] *= scal;
   }
   __syncwarp();
-  if (lane == 0) A[j * NS + j] = beta;
+  if (lane == 0) A[j * QLD + j] = beta;
   *tau_out = tau;
   *diag_out = beta;
   __syncwarp();
@@ -982,11 +985,11 @@ __device__ void householder_step(double* A, int m, int j, int lane, double* tau_
   } else if (tau != 0.0) {
     for (int c = ncols_apply_from; c < NS; ++c) {
       double w = 0.0;
-      for (int i = j + 1 + lane; i < m; i += 32) w += A[i * NS + j] * A[i * NS + c];
-      w = warp_sum(w) + A[j * NS + c];
+      for (int i = j + 1 + lane; i < m; i += 32) w += A[i * QLD + j] * A[i * QLD + c];
+      w = warp_sum(w) + A[j * QLD + c];
       __syncwarp();
-      for (int i = j + 1 + lane; i < m; i += 32) A[i * NS + c] -= tau * w * A[i * NS + j];
-      if (lane == 0) A[j * NS + c] -= tau * w;
+      for (int i = j + 1 + lane; i < m; i += 32) A[i * QLD + c] -= tau * w * A[i * QLD + j];
+      if (lane == 0) A[j * QLD + c] -= tau * w;
       __syncwarp();
     }
   }
@@ -995,7 +998,7 @@ __device__ void householder_step(double* A, int m, int j, int lane, double* tau_
 // Q[:, :keep] = H_0 ... H_{k-1} I[:, :keep] (reflectors stored below the diagonal of A)
 __device__ void form_q(const double* A, const double* tau, int m, int k, int keep, double* Q, int lane) {
   for (int i = lane; i < m; i += 32)
-    for (int c = 0; c < NS; ++c) Q[i * NS + c] = (i == c && c < keep) ? 1.0 : 0.0;
+    for (int c = 0; c < NS; ++c) Q[i * QLD + c] = (i == c && c < keep) ? 1.0 : 0.0;
   __syncwarp();
   if (BAMG_QR_BATCH) {
     for (int j = k - 1; j >= 0; --j) {
@@ -1005,25 +1008,25 @@ __device__ void form_q(const double* A, const double* tau, int m, int k, int kee
 #pragma unroll
       for (int c = 0; c < 16; ++c) w[c] = 0.0;
       for (int i = j + 1 + lane; i < m; i += 32) {
-        double v = A[i * NS + j];
+        double v = A[i * QLD + j];
 #pragma unroll
         for (int c = 0; c < 16; ++c)
-          if (c >= j && c < keep) w[c] += v * Q[i * NS + c];
+          if (c >= j && c < keep) w[c] += v * Q[i * QLD + c];
       }
       warp_sum16(w);
 #pragma unroll
-      for (int c = 0; c < 16; ++c) w[c] = Q[j * NS + c] + w[c];
+      for (int c = 0; c < 16; ++c) w[c] = Q[j * QLD + c] + w[c];
       __syncwarp();
       for (int i = j + 1 + lane; i < m; i += 32) {
-        double v = A[i * NS + j];
+        double v = A[i * QLD + j];
 #pragma unroll
         for (int c = 0; c < 16; ++c)
-          if (c >= j && c < keep) Q[i * NS + c] -= tj * w[c] * v;
+          if (c >= j && c < keep) Q[i * QLD + c] -= tj * w[c] * v;
       }
       if (lane == 0) {
 #pragma unroll
         for (int c = 0; c < 16; ++c)
-          if (c >= j && c < keep) Q[j * NS + c] -= tj * w[c];
+          if (c >= j && c < keep) Q[j * QLD + c] -= tj * w[c];
       }
       __syncwarp();
     }
@@ -1032,13 +1035,13 @@ __device__ void form_q(const double* A, const double* tau, int m, int k, int kee
   for (int j = k - 1; j >= 0; --j) {
     if (tau[j] == 0.0) continue;
     for (int c = j; c < keep; ++c) {
-      double w = Q[j * NS + c];
+      double w = Q[j * QLD + c];
       double part = 0.0;
-      for (int i = j + 1 + lane; i < m; i += 32) part += A[i * NS + j] * Q[i * NS + c];
+      for (int i = j + 1 + lane; i < m; i += 32) part += A[i * QLD + j] * Q[i * QLD + c];
       w += warp_sum(part);
       __syncwarp();
-      for (int i = j + 1 + lane; i < m; i += 32) Q[i * NS + c] -= tau[j] * w * A[i * NS + j];
-      if (lane == 0) Q[j * NS + c] -= tau[j] * w;
+      for (int i = j + 1 + lane; i < m; i += 32) Q[i * QLD + c] -= tau[j] * w * A[i * QLD + j];
+      if (lane == 0) Q[j * QLD + c] -= tau[j] * w;
       __syncwarp();
     }
   }
@@ -1051,9 +1054,9 @@ __global__ void k_prolong_qr(const int* __restrict__ agg_ptr, const int* __restr
   extern __shared__ double sm[];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int wpb = blockDim.x >> 5;
-  double* A = sm + (size_t)w * (2 * m_max * NS + 2 * NS + NS);
-  double* Q = A + m_max * NS;
-  double* tau = Q + m_max * NS;
+  double* A = sm + (size_t)w * (2 * m_max * QLD + 2 * NS + NS);
+  double* Q = A + m_max * QLD;
+  double* tau = Q + m_max * QLD;
   double* dg = tau + NS;
   int* piv = (int*)(dg + NS);  // NS ints packed in the NS-double tail... use separate region
   (void)piv;
@@ -1065,7 +1068,7 @@ __global__ void k_prolong_qr(const int* __restrict__ agg_ptr, const int* __restr
     for (int t = lane; t < m * NS; t += 32) {
       int r = t / NS, c = t - r * NS;
       int node = members[b0 + r / bs];
-      A[t] = K[((int64_t)node * bs + (r % bs)) * NS + c];
+      A[r * QLD + c] = K[((int64_t)node * bs + (r % bs)) * NS + c];
     }
     __syncwarp();
     int keep = m < NS ? m : NS;
@@ -1091,15 +1094,15 @@ __global__ void k_prolong_qr(const int* __restrict__ agg_ptr, const int* __restr
         form_q(A, tau, m, NS, NS, Q, lane);
         // sign fix: s = sign(diag R); P = Q s; Kc = s R
         for (int t = lane; t < m * NS; t += 32) {
-          int c = t % NS;
+          int r = t / NS, c = t - r * NS;
           double s = dg[c] < 0.0 ? -1.0 : 1.0;
-          Q[t] *= s;
+          Q[r * QLD + c] *= s;
         }
         double* kc = Kc + (int64_t)a * NS * NS;
         for (int t = lane; t < NS * NS; t += 32) {
           int r = t / NS, c = t - r * NS;
           double s = dg[r] < 0.0 ? -1.0 : 1.0;
-          kc[t] = (c >= r) ? s * A[r * NS + c] : 0.0;
+          kc[t] = (c >= r) ? s * A[r * QLD + c] : 0.0;
         }
         if (lane == 0) {
           info[2 * a] = 0;
@@ -1113,7 +1116,7 @@ __global__ void k_prolong_qr(const int* __restrict__ agg_ptr, const int* __restr
         for (int t = lane; t < m * NS; t += 32) {
           int r = t / NS, c = t - r * NS;
           int node = members[b0 + r / bs];
-          A[t] = K[((int64_t)node * bs + (r % bs)) * NS + c];
+          A[r * QLD + c] = K[((int64_t)node * bs + (r % bs)) * NS + c];
         }
         __syncwarp();
       }
@@ -1134,7 +1137,7 @@ __global__ void k_prolong_qr(const int* __restrict__ agg_ptr, const int* __restr
           for (int i = j + lane; i < m; i += 32) {
 #pragma unroll
             for (int c = 0; c < 16; ++c)
-              if (c >= j) s[c] += A[i * NS + c] * A[i * NS + c];
+              if (c >= j) s[c] += A[i * QLD + c] * A[i * QLD + c];
           }
           warp_sum16(s);
 #pragma unroll
@@ -1146,7 +1149,7 @@ __global__ void k_prolong_qr(const int* __restrict__ agg_ptr, const int* __restr
         } else {
           for (int c = j; c < NS; ++c) {
             double s = 0.0;
-            for (int i = j + lane; i < m; i += 32) s += A[i * NS + c] * A[i * NS + c];
+            for (int i = j + lane; i < m; i += 32) s += A[i * QLD + c] * A[i * QLD + c];
             s = warp_sum(s);
             if (s > bestn) {
               bestn = s;
@@ -1156,9 +1159,9 @@ __global__ void k_prolong_qr(const int* __restrict__ agg_ptr, const int* __restr
         }
         if (bestc != j) {
           for (int i = lane; i < m; i += 32) {
-            double t = A[i * NS + j];
-            A[i * NS + j] = A[i * NS + bestc];
-            A[i * NS + bestc] = t;
+            double t = A[i * QLD + j];
+            A[i * QLD + j] = A[i * QLD + bestc];
+            A[i * QLD + bestc] = t;
           }
           int t = perm[j];
           perm[j] = perm[bestc];
@@ -1185,7 +1188,7 @@ __global__ void k_prolong_qr(const int* __restrict__ agg_ptr, const int* __restr
       // r_unpiv[:rank, perm] = R[:rank, :]
       for (int t = lane; t < rank * NS; t += 32) {
         int r = t / NS, c = t - r * NS;
-        kc[r * NS + perm[c]] = (c >= r) ? A[r * NS + c] : 0.0;
+        kc[r * NS + perm[c]] = (c >= r) ? A[r * QLD + c] : 0.0;
       }
       if (lane == 0) {
         info[2 * a] = 1;
@@ -1198,7 +1201,7 @@ __global__ void k_prolong_qr(const int* __restrict__ agg_ptr, const int* __restr
     for (int t = lane; t < m * NS; t += 32) {
       int r = t / NS, c = t - r * NS;
       int node = members[b0 + r / bs];
-      Pblocks[((int64_t)node * bs + (r % bs)) * NS + c] = (c < keep) ? Q[t] : 0.0;
+      Pblocks[((int64_t)node * bs + (r % bs)) * NS + c] = (c < keep) ? Q[r * QLD + c] : 0.0;
     }
     __syncwarp();
   }
@@ -1213,7 +1216,7 @@ extern "C" int bamg_prolongation_qr(bamg_ctx* ctx, const int32_t* agg_ptr, const
   // per-warp shared memory sized by the largest aggregate of the launch's size class
   auto run = [&](int lo, int hi) -> int {
     int m_max = hi * bs;
-    size_t per_warp = sizeof(double) * (2 * (size_t)m_max * NS + 3 * NS);
+    size_t per_warp = sizeof(double) * (2 * (size_t)m_max * QLD + 3 * NS);
     int wpb = (int)((200 * 1024) / per_warp);
     if (wpb < 1) {
       bamg_set_error("prolongation: aggregate of %d rows exceeds shared memory", m_max);
