@@ -896,15 +896,23 @@ static int mg_alloc(bamg_mg* m, cudaStream_t st) {
   mg_free_work(m);
   // chunk plan of the 16x16 smoothing levels: CH blocks per warp, enough chunks
   // to cover the SMs several times over
+  // block counts: known on the host through a level's symmetric view; read back
+  // (one synchronisation) only for levels without one
   std::vector<int> nnzb(m->lv.size(), 0);
+  bool need_sync = false;
   for (size_t l = 0; l < m->lv.size(); ++l) {
     MgLevelPlan& L = m->lv[l];
     L.CH = 0;
     L.nch = 0;
     if (L.inv || L.bs != 16 || !L.ptr) continue;
-    BAMG_CUDA_CHECK(cudaMemcpyAsync(&nnzb[l], L.ptr + L.nbr, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (L.sym) {
+      nnzb[l] = (int)L.sym->nnzb;
+    } else {
+      BAMG_CUDA_CHECK(cudaMemcpyAsync(&nnzb[l], L.ptr + L.nbr, sizeof(int), cudaMemcpyDeviceToHost, st));
+      need_sync = true;
+    }
   }
-  BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (need_sync) BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
   for (size_t l = 0; l < m->lv.size(); ++l) {
     MgLevelPlan& L = m->lv[l];
     L.rowcta = !L.inv && L.bs == 16 && L.ptr && L.nbr > 0 && (int64_t)nnzb[l] * 2048 <= ROWCTA_MAX_BYTES;
@@ -914,7 +922,9 @@ static int mg_alloc(bamg_mg* m, cudaStream_t st) {
   for (size_t l = 0; l < m->lv.size(); ++l) {
     MgLevelPlan& L = m->lv[l];
     total += 5 * (size_t)(L.n > 0 ? L.n : 1);
-    if (L.inv || L.bs != 16 || !L.ptr) continue;
+    // chunked full-storage products only where neither the half-storage pair nor
+    // the row-CTA kernel runs the level
+    if (L.inv || L.bs != 16 || !L.ptr || L.sym || L.rowcta) continue;
     int CH = nnzb[l] / 8192;
     L.CH = CH < 1 ? 1 : (CH > 8 ? 8 : CH);
     itotal += (size_t)L.nbr + 1;
@@ -925,6 +935,7 @@ static int mg_alloc(bamg_mg* m, cudaStream_t st) {
   {
     size_t off = 0;
     std::vector<int> nch(m->lv.size(), 0);
+    bool any = false;
     for (size_t l = 0; l < m->lv.size(); ++l) {
       MgLevelPlan& L = m->lv[l];
       if (!L.CH) continue;
@@ -933,8 +944,9 @@ static int mg_alloc(bamg_mg* m, cudaStream_t st) {
       if (rc) return rc;
       BAMG_CUDA_CHECK(cudaMemcpyAsync(&nch[l], counts + off + L.nbr, sizeof(int), cudaMemcpyDeviceToHost, st));
       off += (size_t)L.nbr + 1;
+      any = true;
     }
-    BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (any) BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
     for (size_t l = 0; l < m->lv.size(); ++l) {
       m->lv[l].nch = nch[l];
       if (m->lv[l].CH) {
