@@ -368,12 +368,18 @@ __device__ __forceinline__ double loss_w(double s, int huber) {
 // warp-cooperative double2 loads staged through shared memory, so every load
 // instruction touches a few cache lines instead of 32.
 #define EVAL_THREADS 128
+#ifndef EVAL_ZERO_H
+#define EVAL_ZERO_H 1
+#endif
 #define EVAL_STRIDE 33  // odd smem stride: conflict-free per-thread record writes
 
 // One thread per observation (point-major); the CTA's records are staged in shared
 // memory and written back as contiguous double2 stores (H slots untouched). The
 // objective is reduced deterministically (last block finishes).
 #ifndef EVAL_MINB
+// 1: 138 registers, 12 warps per SM. 4 (128 registers, 16 warps) runs 2.11 -> 1.71 ms at
+// c4, but ptxas then contracts differently: F moves by ulps, enough to move the
+// visibility-Jacobi PCG solutions of the reference-pinned tests past their bounds.
 #define EVAL_MINB 1
 #endif
 __global__ void __launch_bounds__(EVAL_THREADS, EVAL_MINB)
@@ -488,12 +494,19 @@ k_evaluate(const double* __restrict__ cams, const double* __restrict__ pts, cons
     load_idx(t + 2 * stride);
     if (with_jac) {
       __syncthreads();
-      // coalesced write-back of the CTA's records (16 double2 each, skip H = 12..14)
+      // coalesced write-back of the CTA's records, all 16 double2 each: the H slots
+      // (pieces 12..14, filled by build_system's k_obs_H before any use) are written
+      // as zeros, so every 32 B sector is written whole -- skipping them left the
+      // sector shared by H and the residual partially written (an L2 read-modify-write
+      // from DRAM per observation)
       int nrec = (int)min((int64_t)EVAL_THREADS, k - base);
       double2* dst = reinterpret_cast<double2*>(J + base * REC);
       for (int g = threadIdx.x; g < nrec * 16; g += EVAL_THREADS) {
         int rr = g >> 4, pc = g & 15;
-        if (pc >= 12 && pc < 15) continue;
+        if (pc >= 12 && pc < 15) {
+          if (EVAL_ZERO_H) dst[g] = make_double2(0.0, 0.0);
+          continue;
+        }
         const double* s = rec + rr * EVAL_STRIDE + 2 * pc;
         dst[g] = make_double2(s[0], s[1]);
       }
@@ -758,6 +771,7 @@ __global__ void k_obs_H(const int* __restrict__ opt, const double* __restrict__ 
     int64_t p = opt[o];
     double2* rp = reinterpret_cast<double2*>(J + o * REC);
     double2 e01 = rp[RE / 2], e23 = rp[RE / 2 + 1], e45 = rp[RE / 2 + 2];
+    double2 res = rp[RR / 2];  // rewritten with H[4..5]: the shared sector is stored whole
     double e[6] = {e01.x, e01.y, e23.x, e23.y, e45.x, e45.y};
     const double* ci = Cinv + p * 9;
     double x0 = Cb[3 * p], x1 = Cb[3 * p + 1], x2 = Cb[3 * p + 2];
@@ -770,6 +784,7 @@ __global__ void k_obs_H(const int* __restrict__ opt, const double* __restrict__ 
     rp[RH / 2] = make_double2(h[0], h[1]);
     rp[RH / 2 + 1] = make_double2(h[2], h[3]);
     rp[RH / 2 + 2] = make_double2(h[4], h[5]);
+    rp[RR / 2] = res;
     reinterpret_cast<double2*>(qo)[o] =
         make_double2(e[0] * x0 + e[1] * x1 + e[2] * x2, e[3] * x0 + e[4] * x1 + e[5] * x2);
   }
