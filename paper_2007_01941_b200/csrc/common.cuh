@@ -65,6 +65,12 @@ __device__ __forceinline__ int warp_sum_int(int v) {
   return v;
 }
 
+__device__ __forceinline__ int warp_max_int(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(FULL_MASK, v, o));
+  return v;
+}
+
 // Deterministic block-wide sum (fixed tree). `scratch` >= 32 doubles. All threads
 // receive the result.
 __device__ __forceinline__ double block_sum(double v, double* scratch) {

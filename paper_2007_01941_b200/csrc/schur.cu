@@ -48,6 +48,47 @@ __global__ void k_pair_emit(const int* __restrict__ pt_ptr, const int* __restric
   }
 }
 
+// Packed form of k_pair_emit: the pair is carried through the sort as its value,
+// a << 7 | (b - a) (a < 2^25 observations, b - a < 128 inside a point's segment), so
+// the sort needs no index payload and no gather afterwards.
+__global__ void k_pair_emit_packed(const int* __restrict__ pt_ptr, const int* __restrict__ ocam,
+                                   const int* __restrict__ S_ptr, const int* __restrict__ S_col,
+                                   const int* __restrict__ off, int npt, uint32_t* __restrict__ key,
+                                   uint32_t* __restrict__ val) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npt; p += gridDim.x * blockDim.x) {
+    int s = pt_ptr[p], e = pt_ptr[p + 1];
+    int pos = off[p];
+    for (int a = s; a < e; ++a) {
+      int ca = ocam[a];
+      const int* cols = S_col + S_ptr[ca];
+      int n = S_ptr[ca + 1] - S_ptr[ca];
+      for (int b = a + 1; b < e; ++b) {
+        int q = lower_bound_i32(cols, n, ocam[b]);
+        key[pos] = (uint32_t)(S_ptr[ca] + q);
+        val[pos] = ((uint32_t)a << 7) | (uint32_t)(b - a);
+        ++pos;
+      }
+    }
+  }
+}
+
+__global__ void k_unpack_pairs(const uint32_t* __restrict__ v, int64_t n, int* __restrict__ pa, int* __restrict__ pb) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t x = v[i];
+    int a = (int)(x >> 7);
+    pa[i] = a;
+    pb[i] = a + (int)(x & 127u);
+  }
+}
+
+__global__ void k_max_segment(const int* __restrict__ pt_ptr, int npt, int* __restrict__ mx) {
+  int m = 0;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npt; p += gridDim.x * blockDim.x)
+    m = max(m, pt_ptr[p + 1] - pt_ptr[p]);
+  m = warp_max_int(m);
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
+}
+
 __global__ void k_iota_u32(uint32_t* a, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     a[i] = (uint32_t)i;
@@ -127,6 +168,42 @@ extern "C" int bamg_schur_symbolic(bamg_ctx* ctx, const int32_t* pt_ptr, const i
   if (n_pairs == 0) {
     BAMG_CUDA_CHECK(cudaMemsetAsync(blk_pair_ptr, 0, sizeof(int) * (nnz + 1), st));
     return 0;
+  }
+  // packed path: observation indices below 2^25 and point segments below 128
+  {
+    int64_t n_obs = 0;
+    int h[2] = {0, 0};
+    int* dev = nullptr;
+    BAMG_CUDA_CHECK(cudaMallocAsync(&dev, 2 * sizeof(int), st));
+    BAMG_CUDA_CHECK(cudaMemsetAsync(dev, 0, 2 * sizeof(int), st));
+    launch(k_max_segment, grid_for(npt, 256), 256, 0, st, pt_ptr, npt, dev);
+    BAMG_CUDA_CHECK(cudaMemcpyAsync(dev + 1, pt_ptr + npt, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    BAMG_CUDA_CHECK(cudaMemcpyAsync(h, dev, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+    cudaFreeAsync(dev, st);
+    n_obs = h[1];
+    if (n_obs < (1ll << 25) && h[0] <= 128) {
+      uint32_t *key = nullptr, *val = nullptr, *skey = nullptr, *sval = nullptr;
+      BAMG_CUDA_CHECK(cudaMallocAsync(&key, 4 * n_pairs, st));
+      BAMG_CUDA_CHECK(cudaMallocAsync(&val, 4 * n_pairs, st));
+      BAMG_CUDA_CHECK(cudaMallocAsync(&skey, 4 * n_pairs, st));
+      BAMG_CUDA_CHECK(cudaMallocAsync(&sval, 4 * n_pairs, st));
+      launch(k_pair_emit_packed, grid_for(npt, 128), 128, 0, st, pt_ptr, obs_cam_pm, S_ptr, S_col, pair_off, npt, key,
+             val);
+      int bits = 1;
+      while ((1ll << bits) < nnz) ++bits;
+      int rc = radix_sort_pairs(key, val, skey, sval, n_pairs, bits, st);
+      if (rc) return rc;
+      launch(k_unpack_pairs, grid_for(n_pairs, 256), 256, 0, st, (const uint32_t*)sval, n_pairs, pair_a, pair_b);
+      rc = segment_ptr((const int*)skey, n_pairs, (int)nnz, blk_pair_ptr, st);
+      if (rc) return rc;
+      BAMG_LAUNCH_CHECK();
+      cudaFreeAsync(key, st);
+      cudaFreeAsync(val, st);
+      cudaFreeAsync(skey, st);
+      cudaFreeAsync(sval, st);
+      return 0;
+    }
   }
   uint32_t *key = nullptr, *iota = nullptr, *skey = nullptr, *perm = nullptr;
   int *oa = nullptr, *ob = nullptr;
