@@ -79,15 +79,25 @@ class ObsStructure:
         self.cam_ptr = D.empty(nc + 1, dtype=i32)
         D.call("bamg_obs_orders", cam_index, pt_index, k, nc, npt, self.pm_perm, self.obs_cam_pm,
                self.obs_pt_pm, self.pt_ptr, self.cm_list, self.cam_ptr)
-        self.pix_pm = D.empty(k, 2)
-        if pix_ready is not None:  # the pixel copy ran on a copy stream during the sorts
-            torch.cuda.current_stream().wait_event(pix_ready)
-        if k:
-            D.call("bamg_gather_rows_f64", pixels, self.pm_perm, k, 2, self.pix_pm)
+        # the point-major pixels are gathered on first use (evaluate): a pixel copy
+        # still running on the copy stream then overlaps the structural passes
+        # (covisibility, strength, pair lists) instead of stalling them
+        self._pixels, self._pix_ready_ev, self._pix_pm = pixels, pix_ready, None
         self._covis = None
         self._strength = None
         self._symbolic = None
         self._wcache = None
+
+    @property
+    def pix_pm(self) -> torch.Tensor:
+        if self._pix_pm is None:
+            pm = D.empty(self.k, 2)
+            if self._pix_ready_ev is not None:  # the pixel copy ran on a copy stream
+                torch.cuda.current_stream().wait_event(self._pix_ready_ev)
+            if self.k:
+                D.call("bamg_gather_rows_f64", self._pixels, self.pm_perm, self.k, 2, pm)
+            self._pix_pm, self._pixels = pm, None
+        return self._pix_pm
 
     # point-major array (k, ...) -> caller order
     def to_input_order(self, a: torch.Tensor) -> torch.Tensor:
@@ -288,6 +298,9 @@ class BundleProblem:
 
     @property
     def pixels(self) -> torch.Tensor:
+        ev = getattr(self, "_pix_ready", None)
+        if ev is not None:  # the copy-stream upload must be complete for the caller's stream
+            torch.cuda.current_stream().wait_event(ev)
         return self._pix
 
     @property
@@ -319,7 +332,7 @@ class BundleProblem:
                 and self._pts.shape == other._pts.shape
                 and bool(torch.equal(self._cams, other._cams)) and bool(torch.equal(self._pts, other._pts))
                 and bool(torch.equal(self._ci, other._ci)) and bool(torch.equal(self._pi, other._pi))
-                and bool(torch.equal(self._pix, other._pix)))
+                and bool(torch.equal(self.pixels, other.pixels)))
 
 
 # -- Jacobian blocks --------------------------------------------------------------
