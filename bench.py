@@ -213,11 +213,16 @@ def gpu_arm(args, rank, world):
 
     with ClockSampler(torch.cuda.current_device()) as clk:
         lc0 = _lib.lib().bamg_launch_count()
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         ev0.record()
-        for _ in range(args.steps):
+        marks[0].record()
+        for i in range(args.steps):
             out = one_step(prob)
+            marks[i + 1].record()
         ev1.record()
         torch.cuda.synchronize()
+        log("[bench] device steps (ms): " + " ".join(f"{marks[i].elapsed_time(marks[i + 1]):.2f}"
+                                                      for i in range(args.steps)))
         launches_timed = _lib.lib().bamg_launch_count() - lc0
     ms = ev0.elapsed_time(ev1) / args.steps
     setup_s, solve_s = out[4], out[5]
@@ -303,12 +308,14 @@ def gpu_arm(args, rank, world):
     import gc
 
     gc.collect()  # release the measured objects' native handles before, not inside, the timed loop
-    dbg = os.environ.get("BAMG_E2E_DEBUG") == "1"
+    dbg = os.environ.get("BAMG_E2E_DEBUG") in ("1", "2")
+    dbg_sync = os.environ.get("BAMG_E2E_DEBUG") == "1"
     t_host = time.perf_counter()
 
     def mark(tag):
         if dbg:
-            torch.cuda.synchronize()
+            if dbg_sync:
+                torch.cuda.synchronize()
             st = torch.cuda.memory_stats()
             log(f"[bench]   {tag}: {(time.perf_counter() - t_host) * 1e3:.1f} ms, "
                 f"device_alloc {st.get('num_device_alloc')} gc {gc.get_count()}")

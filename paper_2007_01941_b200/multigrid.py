@@ -93,6 +93,7 @@ def visibility_strength(problem_or_obs) -> StrengthMatrix:
         raise ValueError(f"{s['n_empty']} camera(s) observe no points; visibility strength undefined")
     G = StrengthMatrix(s["G_ptr"], s["G_col"], s["G_val"], st.nc)
     G._agg_cache = s.setdefault("agg_cache", {})
+    G._agg_pending = s.setdefault("agg_pending", {})  # a side-stream scan already started
     return G
 
 
@@ -194,7 +195,9 @@ def _aggregate_prefetch(strength: StrengthMatrix, max_size: int) -> None:
     that precedes the hierarchy build (first linear solve of a problem)."""
     if max_size in strength._agg_cache or strength._flags is not None:
         return
-    pending = strength.__dict__.setdefault("_agg_pending", {})
+    pending = getattr(strength, "_agg_pending", None)
+    if pending is None:
+        pending = strength.__dict__.setdefault("_agg_pending", {})
     if max_size in pending or not _OVERLAP:
         return
     n = strength.n

@@ -216,6 +216,9 @@ def _copy_stream():
     return _COPY_STREAMS[dev]
 
 
+_EAGER_STRUCTURE = __import__("os").environ.get("BAMG_EAGER_STRUCTURE", "1") == "1"
+
+
 class BundleProblem:
     """Cameras, points and pixel observations (problem.py:81-173), device resident."""
 
@@ -278,6 +281,16 @@ class BundleProblem:
         if n_weak:
             warnings.warn(f"{n_weak} point(s) observed by fewer than 2 cameras", stacklevel=2)
         self._ci, self._pi, self._pix, self._st = ci, pi, pix, st
+        if self._pix_ready is not None and k and nc > 1 and not n_empty and _EAGER_STRUCTURE:
+            # pinned inputs: the pixel upload is still running on the copy stream, so
+            # the parameter-independent passes every linear solve needs anyway run now,
+            # in its shadow -- covisibility, visibility strength, the level-0
+            # aggregation scan (side stream) and the Schur pair lists
+            from . import multigrid
+
+            G = multigrid.visibility_strength(self)
+            multigrid._aggregate_prefetch(G, 20)
+            st.pair_lists
 
     # -- reference attributes (device tensors, caller order) --
     @property
