@@ -225,7 +225,27 @@ class BundleProblem:
     def __init__(self, camera_params, points, cam_index, pt_index, pixels, loss: str = "trivial",
                  _structure: ObsStructure | None = None):
         cams = D.f64(camera_params).clone()
-        pts = D.f64(points).clone()
+        pinned = (_structure is None and _pinned(points) and _pinned(cam_index) and _pinned(pt_index)
+                  and _pinned(pixels))
+        if pinned:
+            # pinned host inputs: the index copies go first on the current stream (the
+            # orders sort needs them); points and pixels follow on a copy stream, and
+            # every consumer waits on `_pix_ready` (points / pixels properties, the
+            # point-major pixel gather in front of evaluate)
+            ci = cam_index.to(D.dev(), non_blocking=True).to(torch.int64).reshape(-1)
+            pi = pt_index.to(D.dev(), non_blocking=True).to(torch.int64).reshape(-1)
+            main = torch.cuda.current_stream()
+            cs = _copy_stream()
+            cs.wait_stream(main)
+            with torch.cuda.stream(cs):
+                pts = points.to(D.dev(), dtype=torch.float64, non_blocking=True)
+                pix = pixels.to(D.dev(), dtype=torch.float64, non_blocking=True).reshape(-1, 2)
+            pts.record_stream(main)
+            pix.record_stream(main)
+            self._pix_ready = torch.cuda.Event()
+            self._pix_ready.record(cs)
+        else:
+            pts = D.f64(points).clone()
         if cams.dim() != 2 or cams.shape[1] != CAMERA_SIZE:
             raise ValueError(f"camera_params must be (n, 9), got {tuple(cams.shape)}")
         if pts.dim() != 2 or pts.shape[1] != POINT_SIZE:
@@ -239,19 +259,8 @@ class BundleProblem:
         if _structure is not None:
             self._ci, self._pi, self._pix, self._st = _structure._ci, _structure._pi, _structure._pix, _structure
             return
-        if _pinned(cam_index) and _pinned(pt_index) and _pinned(pixels):
-            # pinned host inputs: the index copies go first on the current stream (the
-            # orders sort needs them), the pixel copy runs on a copy stream behind it
-            ci = cam_index.to(D.dev(), non_blocking=True).to(torch.int64).reshape(-1)
-            pi = pt_index.to(D.dev(), non_blocking=True).to(torch.int64).reshape(-1)
-            main = torch.cuda.current_stream()
-            cs = _copy_stream()
-            cs.wait_stream(main)
-            with torch.cuda.stream(cs):
-                pix = pixels.to(D.dev(), dtype=torch.float64, non_blocking=True).reshape(-1, 2)
-            pix.record_stream(main)
-            self._pix_ready = torch.cuda.Event()
-            self._pix_ready.record(cs)
+        if pinned:
+            pass  # copies issued above
         else:
             ci = torch.as_tensor(cam_index, device=D.dev()).to(torch.int64).reshape(-1)
             pi = torch.as_tensor(pt_index, device=D.dev()).to(torch.int64).reshape(-1)
@@ -299,6 +308,9 @@ class BundleProblem:
 
     @property
     def points(self) -> torch.Tensor:
+        ev = getattr(self, "_pix_ready", None)
+        if ev is not None:  # pinned inputs: the copy-stream upload must be complete
+            torch.cuda.current_stream().wait_event(ev)
         return self._pts
 
     @property
@@ -333,7 +345,7 @@ class BundleProblem:
         return int(self._ci.numel())
 
     def copy(self) -> "BundleProblem":
-        return BundleProblem(self._cams, self._pts, None, None, None, self.loss, _structure=self._st)
+        return BundleProblem(self._cams, self.points, None, None, None, self.loss, _structure=self._st)
 
     def with_params(self, camera_params, points) -> "BundleProblem":
         return BundleProblem(camera_params, points, None, None, None, self.loss, _structure=self._st)
@@ -343,7 +355,7 @@ class BundleProblem:
             return NotImplemented
         return (self.loss == other.loss and self._cams.shape == other._cams.shape
                 and self._pts.shape == other._pts.shape
-                and bool(torch.equal(self._cams, other._cams)) and bool(torch.equal(self._pts, other._pts))
+                and bool(torch.equal(self._cams, other._cams)) and bool(torch.equal(self.points, other.points))
                 and bool(torch.equal(self._ci, other._ci)) and bool(torch.equal(self._pi, other._pi))
                 and bool(torch.equal(self.pixels, other.pixels)))
 
