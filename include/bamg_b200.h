@@ -280,6 +280,8 @@ int bamg_symop_cheb_step(bamg_ctx* ctx, const bamg_symop* sym, const double* blo
                          int32_t divide, void* stream);
 int bamg_mg_set_symmetric(bamg_mg* mg, int32_t level, const bamg_symop* sym);
 int bamg_mg_use_graph(bamg_mg* mg, int32_t on);
+/* arena + graph ahead of the first bamg_mg_apply (optional; apply prepares lazily) */
+int bamg_mg_prepare(bamg_ctx* ctx, bamg_mg* mg, void* stream);
 int bamg_mg_apply(bamg_ctx* ctx, bamg_mg* mg, const double* r, double* z, void* stream);
 /* how the prepared plan runs level l's products (measurement only): 0 half-storage
  * pair, 1 one-CTA-per-row full storage, 2 chunked full storage, 3 warp-per-row full

@@ -1193,6 +1193,13 @@ extern "C" int32_t bamg_mg_level_kind(const bamg_mg* m, int32_t level) {
   return 3;
 }
 
+// Work arena, chunk plans and the V-cycle graph (capture + instantiate or re-target)
+// ahead of the first application, so the host work can overlap device work.
+extern "C" int bamg_mg_prepare(bamg_ctx* ctx, bamg_mg* m, void* stream) {
+  (void)ctx;
+  return mg_prepare(m, as_stream(stream));
+}
+
 extern "C" int bamg_mg_apply(bamg_ctx* ctx, bamg_mg* m, const double* r, double* z, void* stream) {
   (void)ctx;
   return mg_apply_dev(m, r, z, as_stream(stream));

@@ -505,6 +505,9 @@ class _NativePlan:
         _lib.call("bamg_mg_apply", D.ctx(), self.handle, r, z, D.stream())
         return z
 
+    def prepare(self):
+        _lib.call("bamg_mg_prepare", D.ctx(), self.handle, D.stream())
+
     def __del__(self):
         try:
             _lib.lib().bamg_mg_destroy(self.handle)
@@ -542,6 +545,14 @@ class MgHierarchy:
 
 
 def _coarse_factor(op: BlockSparseMatrix):
+    cf = _coarse_factor_launch(op)
+    _coarse_check(cf)
+    return cf
+
+
+def _coarse_factor_launch(op: BlockSparseMatrix):
+    """Queue the coarsest Cholesky factorisation + explicit inverse (multigrid.py:431-440);
+    the not-PD flag stays on the device until _coarse_check."""
     n = op.shape[0]
     dense = D.empty(n, n)
     work = D.empty(n, n)
@@ -549,10 +560,14 @@ def _coarse_factor(op: BlockSparseMatrix):
     flag = D.empty(1, dtype=torch.int32)
     D.call("bamg_coarse_factor", op._ptr, op._col, op.blocks, op.n_block_rows, op.row_block_size, dense, work,
            inv, flag)
-    if int(flag.item()):
+    return {"inv": inv, "n": n, "L": work, "_flag": flag}
+
+
+def _coarse_check(cf) -> None:
+    flag = cf.pop("_flag", None)
+    if flag is not None and int(flag.item()):
         raise ValueError("coarsest-level operator is not positive definite "
                          "(damping too small for the given geometry)")
-    return {"inv": inv, "n": n, "L": work}
 
 
 _OVERLAP = __import__("os").environ.get("BAMG_MG_OVERLAP", "1") == "1"
@@ -663,16 +678,25 @@ def build_hierarchy(sys: SchurSystem, nullspace: DenseTall, strength: StrengthMa
                 jac = p[1]  # allocated on the side stream, used by V-cycles on the main one
                 for t in (jac.blocks, jac._inv, jac._chol):
                     t.record_stream(main)
+    # The coarsest factorisation is queued first; the smoothers' readback then waits
+    # for the side stream only, and the native plan (work arena, V-cycle graph capture
+    # / re-target: host work) is prepared while the factorisation runs. The errors
+    # keep the reference's order: smoothers first, then the coarsest factor.
+    cf = _coarse_factor_launch(levels[-1].explicit)
     if side is not None:
+        with torch.cuda.stream(side):
+            _smoother_finish(pend)
         main.wait_stream(side)
-        _smoother_finish(pend)
     else:
         _setup_smoothers(levels[:-1], seed)
     D.phase("mg.smoothers")
-    levels[-1].coarse_factor = _coarse_factor(levels[-1].explicit)
-    D.phase("mg.coarse")
+    levels[-1].coarse_factor = cf
     h = MgHierarchy(levels)
+    if h._plan is not None:
+        h._plan.prepare()
     D.phase("mg.plan")
+    _coarse_check(cf)
+    D.phase("mg.coarse")
     return h
 
 
