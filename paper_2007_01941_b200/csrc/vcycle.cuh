@@ -1139,13 +1139,14 @@ static int mg_prepare(bamg_mg* m, cudaStream_t st) {
     cudaGraphExecUpdateResultInfo info;
     if (cudaGraphExecUpdate(pe, g, &info) == cudaSuccess) {
       m->exec = pe;
+      cudaGraphUpload(m->exec, st);  // device-side setup now, not in front of the first launch
       return 0;
     }
     cudaGetLastError();  // clear the update failure; instantiate instead
     cudaGraphExecDestroy(pe);
   }
   BAMG_CUDA_CHECK(cudaGraphInstantiate(&m->exec, g, 0));
-  (void)st;
+  cudaGraphUpload(m->exec, st);
   return 0;
 }
 
@@ -1226,6 +1227,16 @@ extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, c
   }
   double* r = work;
   double* z = work + n;
+  if (mg) {
+    // the plan's own level-0 input / output vectors: the V-cycle reads r in place and
+    // leaves z where the PCG reads it (no copies around every preconditioner application)
+    int rc0 = mg_prepare(mg, st);
+    if (rc0) return rc0;
+    if (mg->lv[0].n == n) {
+      r = mg->in;
+      z = mg->out;
+    }
+  }
   double* p = work + 2 * n;
   double* ap = work + 3 * n;
   double* sc = ctx->scalars;      // [0] pap [1] rr [2] rz slot A [3] rz slot B [4] bb
