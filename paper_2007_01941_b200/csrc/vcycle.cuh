@@ -53,10 +53,11 @@ __global__ void k_xpby_dev(const double* __restrict__ z, const double* __restric
 // value), so the solve phase streams only the upper blocks U_ij (j >= i): positions
 // dpos[i]..ptr[i+1]-1 of each row. Two deterministic passes, no atomics:
 //   pass 1 (warp per chunk of row i): y_i^up = sum_{j>=i} U_ij x_j, and for j > i the
-//          mirror product t = U_ij^T x_i, stored at the block's own (upper) position
-//          so the writes are coalesced;
-//   pass 2 (warp per row j): y_j = sum_{lower p of row j, column order} T_tpos[p] + y_j^up,
-//          followed by the consumer's epilogue (plain / residual / Chebyshev step).
+//          mirror product t = U_ij^T x_i, stored at the position of the mirror block
+//          (j, i) (destination order, T_SLOT; evict_last so it stays in L2);
+//   pass 2 (warp per row j): y_j = sum_{lower p of row j, column order} T[p] + y_j^up,
+//          the row's lower range read contiguously, then the consumer's epilogue
+//          (plain / residual / Chebyshev step).
 // Bytes per product: (nnz+n)/2 blocks + 2 x 72 B per off-diagonal pair instead of
 // nnz blocks -- 0.6x of the full-storage stream.
 int scan_exclusive_int(const int* in, int* out, int64_t n, int* total, cudaStream_t st);
@@ -278,7 +279,7 @@ k_sym9_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const i
 // cp = 2(l%8) of rows l/8 + 4k, k = 0..3). Row part: a_k += U[r_k][cp..] . x_j[cp..],
 // reduced over the 8 lanes of a row once per chunk. Mirror part: t[cp..] =
 // sum_k U[r_k][cp..] x_i[r_k], reduced over the 4 lanes sharing cp (xor 8, 16) and
-// stored by lanes 0..7 at the block's own position (128 B, coalesced).
+// stored by lanes 0..7 at the mirror block's position (128 B, destination order).
 __global__ void __launch_bounds__(128)
 k_sym16_upper(const int* __restrict__ ptr, const int* __restrict__ col, const int* __restrict__ dpos,
               const int* __restrict__ tpos, const int* __restrict__ cbeg, const int* __restrict__ crow, int nch, const double* __restrict__ blocks,
