@@ -333,7 +333,10 @@ k_sym16_upper(const int* __restrict__ ptr, const int* __restrict__ col, const in
 
 // 16x16 pass 2 + epilogue (modes as k_sym9_finish); two rows per warp, lane r of a
 // half-warp owns entry r of its row.
-__global__ void __launch_bounds__(128)
+#ifndef SYM16_FB
+#define SYM16_FB 16
+#endif
+__global__ void __launch_bounds__(128, 1)
 k_sym16_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const int* __restrict__ tpos,
                const double* __restrict__ T, const int* __restrict__ ucptr, const double* __restrict__ yup, int nbr,
                int mode, const double* __restrict__ b, const double* __restrict__ Dinv, double* __restrict__ d,
@@ -353,17 +356,17 @@ k_sym16_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const 
     if (ok) {
       double lo = 0.0, up = 0.0;
       int p = ptr[row], p1 = dpos[row];
-      // batches of 8: the mirror indices, then the products, are loaded before the
-      // (in-order, so bit-identical) additions -- 8 gathers in flight, not 1
-      for (; p + 8 <= p1; p += 8) {
-        int tp[8];
-        double v[8];
+      // batches of SYM16_FB: the mirror indices, then the products, are loaded before
+      // the (in-order, so bit-identical) additions -- a batch of loads in flight, not 1
+      for (; p + SYM16_FB <= p1; p += SYM16_FB) {
+        int tp[SYM16_FB];
+        double v[SYM16_FB];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) tp[u] = T_READ(p + u);
+        for (int u = 0; u < SYM16_FB; ++u) tp[u] = T_READ(p + u);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = ld_pol(T + (int64_t)tp[u] * 16 + r, pt);
+        for (int u = 0; u < SYM16_FB; ++u) v[u] = ld_pol(T + (int64_t)tp[u] * 16 + r, pt);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) lo += v[u];
+        for (int u = 0; u < SYM16_FB; ++u) lo += v[u];
       }
       for (; p < p1; ++p) lo += ld_pol(T + (int64_t)T_READ(p) * 16 + r, pt);
       for (int k = ucptr[row]; k < ucptr[row + 1]; ++k) up += yup[(int64_t)k * 16 + r];
