@@ -242,3 +242,31 @@ def test_lm_trial_decision_on_device(P):
     # nonpositive model decrease: rho = -inf
     out, _, _ = run([0.0, 2.0, 0.0, dcn, dpn, f, fn], 0)
     assert out[0] == -np.inf and out[1] == 0.0
+
+
+def test_pinned_inputs_match_host_inputs(P):
+    """BundleProblem from pinned host tensors (uploads on a copy stream, structural
+    passes in their shadow, point-major pixels gathered at the first evaluate) gives
+    bit-for-bit the objective, system and step of the plain host-array path, and its
+    points / pixels properties read the uploaded values."""
+    import torch
+
+    from paper_2007_01941_b200 import scenes, solver
+
+    sc = scenes.street(n_cameras=40, n_points=3000, seed=11)
+    arrays = sc.arrays()
+    pinned = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in arrays]
+    cfg = P.SolveConfig(preconditioner="multigrid", tau=1e-30, cg_max_iterations=2000, mg_max_coarse_dim=40,
+                        cg_residual_tolerance=1e-6)
+    out = []
+    for args in (arrays, pinned):
+        prob = P.BundleProblem(*args)
+        obj, jac = P.evaluate(prob)
+        dc, dp, cg, sys_, *_ = solver.linear_solve(prob, jac, 1e4, cfg)
+        out.append((obj, H(dc), H(dp), cg.iterations, H(sys_.rhs_cam), H(prob.points), H(prob.pixels)))
+    a, b = out
+    assert a[0] == b[0] and a[3] == b[3]
+    for u, v in zip(a[1:3] + a[4:], b[1:3] + b[4:]):
+        assert np.array_equal(u, v)
+    np.testing.assert_array_equal(a[5], arrays[1])
+    np.testing.assert_array_equal(a[6], arrays[4])
