@@ -466,8 +466,10 @@ def evaluate(problem: BundleProblem, camera_params=None, points=None, with_jacob
     st = problem._st
     k = st.k
     huber = 1 if problem.loss == "huber" else 0
-    obj = D.empty(1)
-    nb = D.empty(1, dtype=torch.int32)
+    # objective (f64) and behind-camera count (i32) share one 16 B buffer: one readback
+    res = D.empty(2)
+    obj = res[:1]
+    nb = res[1:].view(torch.int32)[:1]
     behind = D.empty(max(k, 1), dtype=torch.uint8)
     if with_jacobian:
         J, w = D.empty(max(k, 1), JacobianBlocks.REC)[:k], D.empty(k)
@@ -476,15 +478,15 @@ def evaluate(problem: BundleProblem, camera_params=None, points=None, with_jacob
     if k:
         D.call("bamg_evaluate", cams, pts, st.obs_cam_pm, st.obs_pt_pm, st.pix_pm, k, huber,
                1 if with_jacobian else 0, J, w, behind, obj, nb)
-        n_behind = int(nb.item())
+        host = res.cpu()
+        n_behind = int(host[1:].view(torch.int32)[0])
+        objective = float(host[0])
     else:
-        obj.zero_()
-        n_behind = 0
+        n_behind, objective = 0, 0.0
     if n_behind:
         flagged = st.pm_perm[behind[:k].bool()].to(torch.int64)
         idx = torch.sort(flagged).values.cpu().numpy()
         raise BehindCameraError(idx)
-    objective = float(obj.item())
     if not with_jacobian:
         return objective, None
     return objective, JacobianBlocks._from_records(st, J, w, problem.n_cameras, problem.n_points, problem._ci,
