@@ -1334,14 +1334,19 @@ extern "C" int bamg_galerkin_pattern(bamg_ctx* ctx, const int32_t* agg_ptr, cons
 }
 
 // coarse block index of each fine block
+// warp per fine row: lanes take the row's blocks (coalesced column reads and key
+// writes), each searching the same coarse row
 __global__ void k_fine_to_coarse(const int* __restrict__ ptr, const int* __restrict__ col, const int* __restrict__ agg,
                                  int n, const int* __restrict__ Cptr, const int* __restrict__ Ccol,
                                  uint32_t* __restrict__ key) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
     int a = agg[i];
-    const int* cc = Ccol + Cptr[a];
-    int nn = Cptr[a + 1] - Cptr[a];
-    for (int b = ptr[i]; b < ptr[i + 1]; ++b) key[b] = (uint32_t)(Cptr[a] + lower_bound_i32(cc, nn, agg[col[b]]));
+    int c0 = Cptr[a];
+    const int* cc = Ccol + c0;
+    int nn = Cptr[a + 1] - c0;
+    for (int b = ptr[i] + lane; b < ptr[i + 1]; b += 32) key[b] = (uint32_t)(c0 + lower_bound_i32(cc, nn, agg[col[b]]));
   }
 }
 
@@ -1360,7 +1365,7 @@ extern "C" int bamg_galerkin_map(bamg_ctx* ctx, const int32_t* ptr, const int32_
   BAMG_CUDA_CHECK(cudaMallocAsync(&key, 4 * nnz_fine, st));
   BAMG_CUDA_CHECK(cudaMallocAsync(&iota, 4 * nnz_fine, st));
   BAMG_CUDA_CHECK(cudaMallocAsync(&skey, 4 * nnz_fine, st));
-  launch(k_fine_to_coarse, grid_for(n, 128), 128, 0, st, ptr, col, agg, n, Cptr, Ccol, key);
+  launch(k_fine_to_coarse, grid_for((int64_t)n * 32, 128, 16), 128, 0, st, ptr, col, agg, n, Cptr, Ccol, key);
   launch(k_iota_i, grid_for(nnz_fine, 256), 256, 0, st, iota, (int)nnz_fine);
   launch(k_row_of_block, grid_for(n, 128), 128, 0, st, ptr, n, fine_row);
   BAMG_LAUNCH_CHECK();
