@@ -1391,15 +1391,19 @@ __global__ void k_gal_upper_count(const int* __restrict__ Cptr, const int* __res
   }
 }
 
+// warp per coarse row: lanes take the row's upper blocks (coalesced writes)
 __global__ void k_gal_upper_fill(const int* __restrict__ Cptr, const int* __restrict__ Ccol, int n,
                                  const int* __restrict__ off, int* __restrict__ ublk, int* __restrict__ umir) {
-  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < n; a += nw) {
     int b0 = Cptr[a], nn = Cptr[a + 1] - b0;
-    int o = off[a];
-    for (int q = b0 + lower_bound_i32(Ccol + b0, nn, a); q < b0 + nn; ++q, ++o) {
+    int qd = b0 + lower_bound_i32(Ccol + b0, nn, a);
+    int o0 = off[a];
+    for (int q = qd + lane; q < b0 + nn; q += 32) {
       int b = Ccol[q];
-      ublk[o] = q;
-      umir[o] = Cptr[b] + lower_bound_i32(Ccol + Cptr[b], Cptr[b + 1] - Cptr[b], a);
+      ublk[o0 + (q - qd)] = q;
+      umir[o0 + (q - qd)] = Cptr[b] + lower_bound_i32(Ccol + Cptr[b], Cptr[b + 1] - Cptr[b], a);
     }
   }
 }
@@ -1782,7 +1786,8 @@ extern "C" int bamg_galerkin_numeric(bamg_ctx* ctx, int32_t bs, const int32_t* c
   launch(k_gal_upper_count, grid_for(n_agg, 128), 128, 0, st, Cptr, Ccol, n_agg, uoff);
   int rc = scan_exclusive_int(uoff, uoff, (int64_t)n_agg + 1, nullptr, st);
   if (rc) return rc;
-  launch(k_gal_upper_fill, grid_for(n_agg, 128), 128, 0, st, Cptr, Ccol, n_agg, (const int*)uoff, ublk, umir);
+  launch(k_gal_upper_fill, grid_for((int64_t)n_agg * 32, 128, 16), 128, 0, st, Cptr, Ccol, n_agg, (const int*)uoff, ublk,
+         umir);
   int g = grid_for(n_up, 1, 12);
   static const bool pipe = [] {
     const char* e = getenv("BAMG_GALERKIN_PIPE");
