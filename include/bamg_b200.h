@@ -151,6 +151,39 @@ int bamg_blockdiag_apply(bamg_ctx* ctx, const double* M, const double* x, int32_
 int bamg_diag_blocks(bamg_ctx* ctx, const int32_t* ptr, const int32_t* col, const double* blocks, int32_t nbr,
                      int32_t bs, double* D, void* stream);
 
+/* ---- generic block-sparse API (blockmat.py:152-360; the path's own operators use the
+ *      dedicated kernels above) ---- */
+/* blockmat.py:186-191 checks: flags_dev[0] = 1 when indptr decreases, flags_dev[1] = 1 when a
+ * column index lies outside [0, nbc) */
+int bamg_bsr_validate(bamg_ctx* ctx, const int32_t* ptr, int32_t nbr, const int32_t* col, int64_t nnz, int32_t nbc,
+                      int32_t* flags_dev, void* stream);
+/* blockmat.py:195-230 from_triplets. Step 1: stable (row, col) order (np.lexsort) -> perm (n),
+ * seg (n: distinct entries before each sorted position); count_dev[0] = distinct entries,
+ * count_dev[1] = 1 when a row / column index is out of range. Step 2: duplicates summed in
+ * input order (np.add.reduceat), CSR out (ptr nbr+1, col nu, blocks nu*bsz). */
+int bamg_triplets_order(bamg_ctx* ctx, const int64_t* rows, const int64_t* cols, int64_t n, int32_t nbr, int32_t nbc,
+                        int32_t* perm, int32_t* seg, int32_t* count_dev, void* stream);
+int bamg_triplets_reduce(bamg_ctx* ctx, const int64_t* rows, const int64_t* cols, const double* blocks, int64_t n,
+                         int32_t bsz, const int32_t* perm, const int32_t* seg, int64_t nu, int32_t nbr, int32_t* ptr,
+                         int32_t* col_out, double* blocks_out, void* stream);
+/* blockmat.py:295-306 matvec of any block shape (rbs x cbs), scipy bsr_matvec summation order */
+int bamg_bsr_matvec_gen(bamg_ctx* ctx, int32_t rbs, int32_t cbs, const int32_t* ptr, const int32_t* col,
+                        const double* blocks, const double* x, int32_t nbr, double* y, void* stream);
+/* blockmat.py:321-334 scale_block_columns: out_n = blocks_n @ col_blocks[col_n] (rbs x cbs @ cbs x k) */
+int bamg_bsr_scale_cols(bamg_ctx* ctx, const double* blocks, const double* col_blocks, const int32_t* col,
+                        int64_t nnz, int32_t rbs, int32_t cbs, int32_t k, double* out, void* stream);
+/* blockmat.py:337-360 multiply / triple_product: block SpGEMM with scipy csr_matmat's summation
+ * order and zero-drop. create -> *nu_host candidate blocks; numeric -> *nkeep_host kept blocks;
+ * finish -> CSR (ptr a_nbr+1, col nkeep, blocks nkeep*rbs*cbs). */
+typedef struct bamg_spgemm bamg_spgemm;
+bamg_spgemm* bamg_spgemm_create(bamg_ctx* ctx, const int32_t* a_ptr, const int32_t* a_col, int32_t a_nbr,
+                                int64_t a_nnz, const int32_t* b_ptr, const int32_t* b_col, int32_t b_nbc,
+                                int64_t* nu_host, void* stream);
+int bamg_spgemm_numeric(bamg_ctx* ctx, bamg_spgemm* sp, const double* a_blocks, int32_t rbs, int32_t kbs,
+                        const double* b_blocks, int32_t cbs, int64_t* nkeep_host, void* stream);
+int bamg_spgemm_finish(bamg_ctx* ctx, bamg_spgemm* sp, int32_t* ptr, int32_t* col, double* blocks, void* stream);
+void bamg_spgemm_destroy(bamg_spgemm* sp);
+
 /* ---- multigrid setup: multigrid.py:83-98, 127-176, 179-237, 409-471; problem.py:332-352 ---- */
 int bamg_operator_strength(bamg_ctx* ctx, const int32_t* ptr, const int32_t* col, const double* blocks, int32_t n,
                            int64_t nnz, int32_t bs, double* nrm_work, double* dnorm_work, int32_t* G_ptr,

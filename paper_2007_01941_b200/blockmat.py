@@ -12,6 +12,8 @@ and `indices` are int64 views of the int32 device arrays).
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -192,12 +194,20 @@ class BlockSparseMatrix:
             if self._ptr.shape != (self.n_block_rows + 1,):
                 raise ValueError(f"indptr has length {self._ptr.shape[0]}, expected {self.n_block_rows + 1}")
             nnz = self._col.numel()
-            last = int(self._ptr[-1].item())
-            if last != nnz:
-                raise ValueError(f"indptr[-1]={last} but {nnz} indices stored")
             expect = (nnz, self.row_block_size, self.col_block_size)
             if tuple(self.blocks.shape) != expect:
                 raise ValueError(f"blocks shaped {tuple(self.blocks.shape)}, expected {expect}")
+            # one readback: indptr[-1], nondecreasing indptr, column range (blockmat.py:174-191)
+            chk = D.empty(3, dtype=torch.int32)
+            D.call("bamg_bsr_validate", self._ptr, self.n_block_rows, self._col, nnz, self.n_block_cols, chk)
+            chk[2:3].copy_(self._ptr[-1:])
+            bad_ptr, bad_col, last = chk.tolist()
+            if last != nnz:
+                raise ValueError(f"indptr[-1]={last} but {nnz} indices stored")
+            if bad_ptr:
+                raise ValueError("indptr must be nondecreasing")
+            if bad_col:
+                raise ValueError("block column index out of range")
 
     @property
     def indptr(self):
@@ -255,14 +265,13 @@ class BlockSparseMatrix:
 
     @staticmethod
     def _rect_matvec(m, x):
-        # rectangular blocks (API views of W and of transposes): per-block products
-        # gathered in row order -- not on the measured path.
-        rows = m.block_rows_expanded()
-        xb = x.reshape(m.n_block_cols, m.col_block_size)[m._col.to(torch.int64)]
-        prod = torch.einsum("nij,nj->ni", m.blocks, xb)
-        y = D.zeros(m.n_block_rows, m.row_block_size)
-        y.index_add_(0, rows, prod)
-        return y.reshape(-1)
+        # any block shape (API views of W, transposes, user matrices): scipy
+        # bsr_matvec summation order, so the result equals the reference bit for bit
+        y = D.empty(m.shape[0])
+        if m.shape[0]:
+            D.call("bamg_bsr_matvec_gen", m.row_block_size, m.col_block_size, m._ptr, m._col, m.blocks, x,
+                   m.n_block_rows, y)
+        return y
 
     def rmatvec(self, x):
         x = D.f64(x).reshape(-1)
@@ -291,68 +300,101 @@ class BlockSparseMatrix:
         return out.reshape(n, m)
 
     def scale_block_columns(self, col_blocks) -> "BlockSparseMatrix":
+        """Right-multiply by a block-diagonal matrix given as (n, cbs, k) blocks (blockmat.py:321-334)."""
         col_blocks = D.f64(col_blocks)
         if col_blocks.shape[0] != self.n_block_cols or col_blocks.shape[1] != self.col_block_size:
             raise ValueError("column block array does not match matrix")
-        nb = torch.einsum("nij,njk->nik", self.blocks, col_blocks[self._col.to(torch.int64)])
-        return BlockSparseMatrix(self.n_block_rows, self.n_block_cols, self.row_block_size, col_blocks.shape[2],
-                                 self._ptr.clone(), self._col.clone(), nb)
+        k = col_blocks.shape[2]
+        nb = D.empty(self.n_block_entries, self.row_block_size, k)
+        D.call("bamg_bsr_scale_cols", self.blocks, col_blocks, self._col, self.n_block_entries, self.row_block_size,
+               self.col_block_size, k, nb)
+        return BlockSparseMatrix(self.n_block_rows, self.n_block_cols, self.row_block_size, k,
+                                 self._ptr.clone(), self._col.clone(), nb, _validate=False)
 
     @staticmethod
     def from_triplets(n_block_rows, n_block_cols, rows, cols, blocks) -> "BlockSparseMatrix":
-        """Assemble from (row, col, block) triplets; duplicates are summed (blockmat.py:195-230)."""
-        rows = torch.as_tensor(rows, device=D.dev()).to(torch.int64).reshape(-1)
-        cols = torch.as_tensor(cols, device=D.dev()).to(torch.int64).reshape(-1)
+        """Assemble from (row, col, block) triplets; duplicates are summed (blockmat.py:195-230).
+
+        Stable (row, col) order and sequential duplicate sums in input order, as
+        np.lexsort + np.add.reduceat: bit-identical to the reference."""
+        rows = torch.as_tensor(rows, device=D.dev()).to(torch.int64).reshape(-1).contiguous()
+        cols = torch.as_tensor(cols, device=D.dev()).to(torch.int64).reshape(-1).contiguous()
         blocks = D.f64(blocks)
         if blocks.dim() != 3 or not (blocks.shape[0] == rows.numel() == cols.numel()):
             raise ValueError("triplet arrays disagree on entry count")
         rbs, cbs = blocks.shape[1], blocks.shape[2]
-        if rows.numel() == 0:
-            return BlockSparseMatrix(n_block_rows, n_block_cols, rbs, cbs,
-                                     torch.zeros(n_block_rows + 1, dtype=torch.int32), torch.zeros(0),
-                                     D.zeros(0, rbs, cbs))
-        key = rows * max(int(n_block_cols), 1) + cols
-        order = torch.sort(key, stable=True).indices
-        key, blocks = key[order], blocks[order]
-        first = torch.ones_like(key, dtype=torch.bool)
-        first[1:] = key[1:] != key[:-1]
-        seg = torch.cumsum(first.to(torch.int64), 0) - 1
-        nseg = int(seg[-1].item()) + 1
-        summed = D.zeros(nseg, rbs, cbs)
-        summed.index_add_(0, seg, blocks)
-        ukey = key[first]
-        urow, ucol = ukey // max(int(n_block_cols), 1), ukey % max(int(n_block_cols), 1)
-        counts = torch.bincount(urow, minlength=n_block_rows)
-        ptr = torch.zeros(n_block_rows + 1, dtype=torch.int64, device=D.dev())
-        ptr[1:] = torch.cumsum(counts, 0)
-        return BlockSparseMatrix(n_block_rows, n_block_cols, rbs, cbs, ptr, ucol, summed)
+        n = rows.numel()
+        nbr, nbc = int(n_block_rows), int(n_block_cols)
+        if n == 0:
+            return BlockSparseMatrix(nbr, nbc, rbs, cbs, torch.zeros(nbr + 1, dtype=torch.int32),
+                                     torch.zeros(0, dtype=torch.int32), D.zeros(0, rbs, cbs), _validate=False)
+        perm = D.empty(n, dtype=torch.int32)
+        seg = D.empty(n, dtype=torch.int32)
+        cnt = D.empty(2, dtype=torch.int32)
+        D.call("bamg_triplets_order", rows, cols, n, nbr, nbc, perm, seg, cnt)
+        nu, bad = cnt.tolist()
+        if bad:
+            raise ValueError("block column index out of range")
+        ptr = D.empty(nbr + 1, dtype=torch.int32)
+        col = D.empty(max(nu, 1), dtype=torch.int32)
+        out = D.empty(max(nu, 1), rbs, cbs)
+        D.call("bamg_triplets_reduce", rows, cols, blocks.contiguous(), n, rbs * cbs, perm, seg, nu, nbr, ptr, col,
+               out)
+        return BlockSparseMatrix(nbr, nbc, rbs, cbs, ptr, col[:nu], out[:nu], _validate=False)
 
 
 def multiply(a: BlockSparseMatrix, b: BlockSparseMatrix) -> BlockSparseMatrix:
-    """Sparse block product a @ b (blockmat.py:337-353) -- API convenience via dense
-    row panels; the measured path uses the dedicated Galerkin / Schur kernels."""
+    """Sparse block product a @ b (blockmat.py:337-353): block SpGEMM on the device in
+    scipy csr_matmat's summation order, with its zero-drop (a block is kept iff one
+    of its scalars is nonzero)."""
+    from . import _lib
+
     if a.n_block_cols != b.n_block_rows or a.col_block_size != b.row_block_size:
-        raise ValueError("block product mismatch")
-    dense = a.to_dense() @ b.to_dense()
-    rbs, cbs = a.row_block_size, b.col_block_size
-    blk = dense.reshape(a.n_block_rows, rbs, b.n_block_cols, cbs).permute(0, 2, 1, 3)
-    nz = (blk != 0).flatten(2).any(-1)
-    r, c = torch.nonzero(nz, as_tuple=True)
-    return BlockSparseMatrix.from_triplets(a.n_block_rows, b.n_block_cols, r, c, blk[r, c])
+        raise ValueError(
+            f"block product mismatch: ({a.n_block_rows}x{a.n_block_cols} of {a.row_block_size}x{a.col_block_size})"
+            f" @ ({b.n_block_rows}x{b.n_block_cols} of {b.row_block_size}x{b.col_block_size})")
+    rbs, kbs, cbs = a.row_block_size, a.col_block_size, b.col_block_size
+    nbr, nbc = a.n_block_rows, b.n_block_cols
+    L = _lib.lib()
+    s = D.stream()
+    nu = ctypes.c_int64(0)
+    h = L.bamg_spgemm_create(D.ctx(s), a._ptr.data_ptr(), a._col.data_ptr(), nbr, a.n_block_entries,
+                             b._ptr.data_ptr(), b._col.data_ptr(), nbc, ctypes.byref(nu), s)
+    if not h:
+        raise _lib.NativeError(f"bamg_spgemm_create: {_lib.last_error()}")
+    try:
+        nk = ctypes.c_int64(0)
+        _lib.call("bamg_spgemm_numeric", D.ctx(s), h, a.blocks, rbs, kbs, b.blocks, cbs, ctypes.byref(nk), s)
+        nkeep = nk.value
+        ptr = D.empty(nbr + 1, dtype=torch.int32)
+        col = D.empty(max(nkeep, 1), dtype=torch.int32)
+        out = D.empty(max(nkeep, 1), rbs, cbs)
+        _lib.call("bamg_spgemm_finish", D.ctx(s), h, ptr, col, out, s)
+        torch.cuda.current_stream().synchronize()  # before the handle's buffers are freed
+    finally:
+        L.bamg_spgemm_destroy(h)
+    return BlockSparseMatrix(nbr, nbc, rbs, cbs, ptr, col[:nkeep], out[:nkeep], _validate=False)
 
 
 def triple_product(r, a, p):
+    """r @ a @ p as two successive sparse products (blockmat.py:356-360)."""
     return multiply(multiply(r, a), p)
 
 
 def write_matrix_market(mat, path) -> None:
-    """MatrixMarket coordinate file of the scalar entries (blockmat.py:363-372)."""
+    """MatrixMarket coordinate file of the stored scalar entries (blockmat.py:363-372):
+    every scalar of every stored block (explicit zeros included), blocks in storage
+    order and row-major inside a block -- the order of scipy's bsr.tocoo()."""
     if isinstance(mat, BlockDiagMatrix):
         mat = mat.to_block_sparse()
-    dense = D.host(mat.to_dense())
-    r, c = np.nonzero(dense)
+    ptr, col, blk = D.host(mat.indptr), D.host(mat.indices), D.host(mat.blocks)
+    R, C = mat.row_block_size, mat.col_block_size
+    nnz = len(col)
+    brow = np.repeat(np.arange(mat.n_block_rows, dtype=np.int64), np.diff(ptr))
+    row = np.repeat(R * brow, R * C) + np.tile(np.repeat(np.arange(R), C), nnz)
+    cols = np.repeat(C * col, R * C) + np.tile(np.arange(C), R * nnz)
+    data = blk.reshape(-1)
     with open(path, "w") as fh:
         fh.write("%%MatrixMarket matrix coordinate real general\n")
-        fh.write(f"{dense.shape[0]} {dense.shape[1]} {len(r)}\n")
-        for i, j in zip(r, c):
-            fh.write(f"{i + 1} {j + 1} {dense[i, j]:.17g}\n")
+        fh.write(f"{mat.shape[0]} {mat.shape[1]} {len(data)}\n")
+        fh.writelines(f"{i + 1} {j + 1} {v:.17g}\n" for i, j, v in zip(row.tolist(), cols.tolist(), data.tolist()))

@@ -1,0 +1,162 @@
+"""Parity at the BASELINE sizes (north-star row N1): the CUDA path
+on the full config-2 / 3 / 4 / 5 scenes against fingerprints of the REAL reference
+run on the same seeded scenes (tests/golden/full_c*.npz, oracle/make_golden_full.py).
+
+Per config:
+  bit-exact : scene digest, S pattern (sha256 of indptr / indices) and block count,
+              W pattern, visibility strength (pattern AND value bytes), number of
+              levels, every level's dims and aggregation, every coarse pattern,
+              choose_mode and the covisibility count
+  1e-10     : objective, sampled F / E / residual / A / C^-1 / rhs / gradient /
+              W / S blocks (per-block max-abs normalisation, App. B.2), lambda_0
+  iterations: PCG (multigrid and point-block Jacobi) to rel-res 1e-6 within +-1
+  LM        : where recorded (10 steps on c2 / c3 / c5, 2 on c4), CG iterations
+              +-1 per step, the same accept / reject sequence on the numerically
+              determined steps, final objective within 1e-8 relative.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, block_rel, relerr
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = [2, 5, 3, 4]
+
+
+def H(t):
+    from paper_2007_01941_b200 import _device
+
+    return _device.host(t)
+
+
+def _fp(a):
+    from oracle.make_golden_full import fp
+
+    return fp(a)
+
+
+def _rows_sel(t, sel):
+    import torch
+
+    return H(t[torch.as_tensor(sel, device=t.device)])
+
+
+@pytest.fixture(scope="module", params=CONFIGS, ids=lambda n: f"c{n}")
+def full(request):
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    path = os.path.join(GOLDEN, f"full_c{request.param}.npz")
+    if not os.path.exists(path):
+        pytest.fail(f"missing golden {path} (oracle/make_golden_full.py)")
+    g = dict(np.load(path, allow_pickle=False))
+    import paper_2007_01941_b200 as P
+    from paper_2007_01941_b200 import scenes
+
+    sc = scenes.config(request.param)
+    assert sc.digest() == str(g["digest"]), "scene generator drifted from the golden"
+    prob = P.BundleProblem(*sc.arrays())
+    obj, jac = P.evaluate(prob)
+    damp = P.Damping.from_jacobian(jac, 1e4)
+    s = P.build_system(jac, damp)
+    s.mode = P.choose_mode(s)
+    yield request.param, g, P, prob, obj, jac, s
+    del prob, jac, s
+    torch.cuda.empty_cache()
+
+
+def test_evaluate_and_system(full):
+    n, g, P, prob, obj, jac, s = full
+    assert abs(obj - g["objective"]) <= 1e-10 * abs(g["objective"])
+    osel, psel, csel, dsel = g["obs_sel"], g["pt_sel"], g["cam_sel"], g["dof_sel"]
+    assert block_rel(_rows_sel(jac.camera, osel), g["F"]) <= 1e-10
+    assert block_rel(_rows_sel(jac.point, osel), g["E"]) <= 1e-10
+    assert block_rel(_rows_sel(jac.residual, osel), g["res"]) <= 1e-10
+    gc, gp = jac.gradient()
+    assert relerr(_rows_sel(gc.reshape(-1), dsel), g["g_cam"]) <= 1e-10
+    assert relerr(_rows_sel(gp, psel), g["g_pt"]) <= 1e-10
+    assert block_rel(_rows_sel(s.A.blocks, csel), g["A"]) <= 1e-10
+    assert block_rel(_rows_sel(s.C.inverse_blocks(), psel), g["Cinv"]) <= 1e-10
+    rhs = s.rhs_cam
+    assert relerr(_rows_sel(rhs, dsel), g["rhs"]) <= 1e-10
+    assert abs(float(rhs.norm()) - g["rhs_norm"]) <= 1e-10 * g["rhs_norm"]
+    assert P.choose_mode(s) == str(g["mode"])
+    assert P.covisibility_block_count(s) == int(g["covis"])
+    W = s.W
+    assert _fp(H(W.indptr)) == str(g["W_indptr_fp"])
+    assert _fp(H(W.indices)) == str(g["W_indices_fp"])
+    assert block_rel(_rows_sel(W.blocks, g["W_sel"]), g["W_blocks"]) <= 1e-10
+    s._W = None  # 25M x 216 B at c4
+
+
+def test_schur_pattern_and_blocks(full):
+    n, g, P, prob, obj, jac, s = full
+    S = s.ensure_explicit()
+    assert S.n_block_entries == int(g["S_nnzb"])
+    assert _fp(H(S.indptr)) == str(g["S_indptr_fp"])
+    assert _fp(H(S.indices)) == str(g["S_indices_fp"])
+    assert block_rel(_rows_sel(S.blocks, g["S_sel"]), g["S_blocks"]) <= 1e-10
+
+
+def test_strength_hierarchy_pcg(full):
+    n, g, P, prob, obj, jac, s = full
+    G = P.visibility_strength(prob)
+    assert _fp(H(G.indptr)) == str(g["G_indptr_fp"])
+    assert _fp(H(G.indices)) == str(g["G_indices_fp"])
+    assert _fp(H(G.data)) == str(g["G_data_fp"])
+    h = P.build_hierarchy(s, P.gauge_nullspace(prob), G)
+    assert h.n_levels == int(g["n_levels"])
+    for li, lvl in enumerate(h.levels):
+        assert lvl.scalar_dim == int(g[f"L{li}_dim"]), li
+        if lvl.aggregation is not None:
+            np.testing.assert_array_equal(H(lvl.aggregation.assignment), g[f"L{li}_agg"], err_msg=f"level {li}")
+        if li > 0:
+            assert lvl.explicit.n_block_entries == int(g[f"L{li}_nnzb"]), li
+            assert _fp(H(lvl.explicit.indptr)) == str(g[f"L{li}_indptr_fp"]), li
+            assert _fp(H(lvl.explicit.indices)) == str(g[f"L{li}_indices_fp"]), li
+    lam = h.levels[0].smoother.lambda_max
+    assert abs(lam - g["L0_lambda"]) <= 1e-9 * g["L0_lambda"]
+    x, rep = P.pcg(s.matvec, h.apply, s.rhs_cam, tau=1e-30, max_iterations=20000, residual_tolerance=1e-6)
+    assert abs(rep.iterations - int(g["pcg_its"])) <= 1, (rep.iterations, int(g["pcg_its"]))
+    assert rep.stop_reason == str(g["pcg_reason"])
+    assert relerr(_rows_sel(x, g["dof_sel"]), g["pcg_x"]) <= 1e-4
+    assert abs(float(x.norm()) - g["pcg_x_norm"]) <= 1e-4 * g["pcg_x_norm"]
+    dp = P.back_substitute(s, x)
+    assert relerr(_rows_sel(dp.reshape(-1, 3), g["pt_sel"]), g["dp"]) <= 1e-4
+    md = P.model_decrease(s, x)
+    assert abs(md - g["model_decrease"]) <= 1e-6 * abs(g["model_decrease"])
+    del h
+    if "pbj_its" in g:
+        pb = P.pbj_setup(s)
+        xb, repb = P.pcg(s.matvec, pb.apply, s.rhs_cam, tau=1e-30, max_iterations=20000, residual_tolerance=1e-6)
+        assert abs(repb.iterations - int(g["pbj_its"])) <= 1, (repb.iterations, int(g["pbj_its"]))
+
+
+def _check_lm(rep, g, prefix):
+    cg = np.array([r.cg_iterations for r in rep.records])
+    acc = np.array([r.accepted for r in rep.records])
+    want = g[f"{prefix}_cg"]
+    assert len(cg) == len(want)
+    obj = g[f"{prefix}_obj"]
+    determined = np.abs(obj - obj[-1]) > 1e-9 * abs(obj[-1])
+    determined = np.concatenate([[True], determined[:-1]])
+    np.testing.assert_array_equal(acc[determined], g[f"{prefix}_accepted"][determined])
+    assert np.all(np.abs(cg - want) <= 1), (cg.tolist(), want.tolist())
+    assert abs(rep.final_objective - obj[-1]) <= 1e-8 * abs(obj[-1]), (rep.final_objective, obj[-1])
+
+
+def test_lm_records(full):
+    n, g, P, prob, *_ = full
+    if "lm_cg" not in g:
+        pytest.skip("no LM records in this golden")
+    steps = len(g["lm_cg"]) - 1
+    cfg = P.SolveConfig(preconditioner="multigrid", tau=1e-30, max_iterations=steps, function_tolerance=0.0,
+                        gradient_tolerance=0.0, parameter_tolerance=0.0, initial_radius=1e4,
+                        cg_max_iterations=20000, cg_residual_tolerance=1e-6)
+    sol, rep = P.lm_solve(prob, cfg)
+    _check_lm(rep, g, "lm")
