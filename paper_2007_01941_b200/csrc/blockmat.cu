@@ -7,7 +7,8 @@
 // bit-identical, with every product and sum rounded separately (__dmul_rn /
 // __dadd_rn, no FMA contraction):
 //   * from_triplets: np.lexsort((cols, rows)) is stable -> duplicates in input
-//     order; np.add.reduceat along axis 0 adds them sequentially;
+//     order; np.add.reduceat along axis 0 is the first block plus numpy's pairwise
+//     sum of the rest (measured against numpy 2.3, tests/test_gpu_blockmat.py);
 //   * matvec: scipy bsr_matvec / gemv -- y_r starts at 0, then blocks of the row
 //     in column order, inside a block columns in order;
 //   * multiply: scipy csr_matmat -- output scalar (r, c) accumulates A[r, k] B[k, c]
@@ -126,6 +127,36 @@ __global__ void k_trip_starts(const int* __restrict__ seg, int64_t n, int nu, in
   }
 }
 
+// numpy's pairwise_sum (the add reduction's inner loop over a strided axis): below 8
+// terms a running sum from +0; up to 128 eight interleaved partial sums combined as
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus the tail; beyond, split at a multiple of 8
+__device__ double np_pairwise(const double* __restrict__ blocks, const uint32_t* __restrict__ perm, int s, int n,
+                              int bsz, int e) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res = __dadd_rn(res, blocks[(int64_t)perm[s + i] * bsz + e]);
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = blocks[(int64_t)perm[s + j] * bsz + e];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], blocks[(int64_t)perm[s + i + j] * bsz + e]);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, blocks[(int64_t)perm[s + i] * bsz + e]);
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(np_pairwise(blocks, perm, s, n2, bsz, e), np_pairwise(blocks, perm, s + n2, n - n2, bsz, e));
+}
+
+// np.add.reduceat along axis 0: the segment's first block, plus numpy's pairwise sum
+// of the remaining ones (the strided reduction loop)
 __global__ void k_trip_sum(const int64_t* __restrict__ rows, const int64_t* __restrict__ cols,
                            const double* __restrict__ blocks, int bsz, const uint32_t* __restrict__ perm,
                            const int* __restrict__ start, int64_t nu, int* __restrict__ urow, int* __restrict__ ucol,
@@ -136,7 +167,7 @@ __global__ void k_trip_sum(const int64_t* __restrict__ rows, const int64_t* __re
     int s0 = start[u], s1 = start[u + 1];
     uint32_t p = perm[s0];
     double acc = blocks[(int64_t)p * bsz + e];
-    for (int s = s0 + 1; s < s1; ++s) acc = __dadd_rn(acc, blocks[(int64_t)perm[s] * bsz + e]);
+    if (s1 - s0 > 1) acc = __dadd_rn(acc, np_pairwise(blocks, perm, s0 + 1, s1 - s0 - 1, bsz, e));
     out[t] = acc;
     if (e == 0) {
       urow[u] = (int)rows[p];

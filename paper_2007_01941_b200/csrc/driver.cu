@@ -7,15 +7,18 @@
 #include "common.cuh"
 #include "ctx.h"
 
-// aa <- aa * (1 - 2 pi / |aa|) while |aa| > pi (rotation.py:124-137)
+// aa <- aa * (1 - 2 pi / |aa|) while |aa| > pi (rotation.py:124-137). numpy's
+// np.linalg.norm over 3 entries is sqrt((a0^2 + a1^2) + a2^2) with every operation
+// rounded; the explicit _rn intrinsics keep nvcc from contracting them into FMAs,
+// so the wrap decision near |aa| = pi is the reference's.
 __device__ __noinline__ void canon_row(double* a) {
   for (int it = 0; it < 64; ++it) {
-    double th = sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+    double th = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(a[0], a[0]), __dmul_rn(a[1], a[1])), __dmul_rn(a[2], a[2])));
     if (!(th > M_PI)) break;
-    double s = 1.0 - 2.0 * M_PI / th;
-    a[0] *= s;
-    a[1] *= s;
-    a[2] *= s;
+    double s = __dsub_rn(1.0, __ddiv_rn(2.0 * M_PI, th));
+    a[0] = __dmul_rn(a[0], s);
+    a[1] = __dmul_rn(a[1], s);
+    a[2] = __dmul_rn(a[2], s);
   }
 }
 

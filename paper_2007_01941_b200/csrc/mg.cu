@@ -760,6 +760,281 @@ k_aggregate_head(const int* __restrict__ G_ptr, const int* __restrict__ G_col, c
   }
 }
 
+// ---------------------------------------------------------------------------
+// Speculative form of the same scan (identical decisions, fewer dependent steps).
+// The 32 nodes of a head batch are decided in parallel, one per lane, from the state
+// at the batch start; the batch is then committed in index order. A lane's decision
+// depends only on its examined head entries (the first eligible entry, the tie run of
+// its strength, the chosen entry) through two facts per entry: assigned or not, and
+// whether its aggregate is full. Both change monotonically and only through commits,
+// so every commit broadcasts (node, partner, aggregate, became-full) and later lanes
+// whose examined entries it touches fall back to the cooperative visit of
+// k_aggregate_head at their turn (as do visits that need the sorted row or the
+// exhaustive scan). The result equals the sequential scan's decision for decision.
+
+// cooperative visit of node i (the whole warp; state in shared memory)
+__device__ __forceinline__ int agg_visit_coop(int i, const int* __restrict__ G_ptr, const int* __restrict__ G_col,
+                                              const double* __restrict__ G_val, const int* hc, const double* hv,
+                                              int len, const int* agg, const int* size, int max_size, int lane) {
+  int j = -1;
+  double g = 0.0;
+  if (lane < AH_K) {
+    j = hc[lane];
+    g = hv[lane];
+  }
+  int bj = -1;
+  bool full_scan = __shfl_sync(FULL_MASK, j, 0) == -2;
+  bool row_scan = false;
+  if (!full_scan) {
+    int a = j >= 0 ? agg[j] : -1;
+    bool elig = j >= 0 && (a < 0 || size[a] < max_size);
+    unsigned m = __ballot_sync(FULL_MASK, elig);
+    if (m) {
+      int f = __ffs(m) - 1;
+      double gf = __shfl_sync(FULL_MASK, g, f);
+      unsigned mu = __ballot_sync(FULL_MASK, elig && g == gf && a < 0);
+      if (mu) {
+        bj = __shfl_sync(FULL_MASK, j, __ffs(mu) - 1);
+      } else {
+        bool tail = __shfl_sync(FULL_MASK, j >= 0 && g == gf, AH_K - 1);
+        if (tail && len > AH_K) row_scan = true;
+        else bj = __shfl_sync(FULL_MASK, j, f);
+      }
+    } else if (len > AH_K) {
+      row_scan = true;
+    }
+  }
+  if (row_scan) {
+    const int s0 = G_ptr[i], e0 = G_ptr[i + 1];
+    bool have = false;
+    double gf = 0.0;
+    int jf = -1, ju = -1;
+    for (int q0 = s0; q0 < e0; q0 += 32) {
+      int q = q0 + lane;
+      int jj = q < e0 ? G_col[q] : -1;
+      double gg = q < e0 ? G_val[q] : 0.0;
+      int a = jj >= 0 ? agg[jj] : -1;
+      bool elig = jj >= 0 && (a < 0 || size[a] < max_size);
+      if (have) elig = elig && (gg == gf);
+      unsigned m = __ballot_sync(FULL_MASK, elig);
+      if (!have) {
+        if (!m) continue;
+        int f = __ffs(m) - 1;
+        gf = __shfl_sync(FULL_MASK, gg, f);
+        jf = __shfl_sync(FULL_MASK, jj, f);
+        have = true;
+        m = __ballot_sync(FULL_MASK, elig && gg == gf);
+      }
+      unsigned mu = __ballot_sync(FULL_MASK, elig && a < 0) & m;
+      if (mu) {
+        ju = __shfl_sync(FULL_MASK, jj, __ffs(mu) - 1);
+        break;
+      }
+      bool tail = __shfl_sync(FULL_MASK, q < e0 && gg == gf, 31);
+      if (!tail) break;
+    }
+    bj = ju >= 0 ? ju : jf;
+  } else if (full_scan) {
+    Cand best{0.0, 0, -1};
+    for (int q = G_ptr[i] + lane; q < G_ptr[i + 1]; q += 32) {
+      int jj = G_col[q];
+      int a = agg[jj];
+      if ((a < 0) || (size[a] < max_size)) {
+        Cand c{G_val[q], a < 0 ? 1 : 0, jj};
+        if (better(c, best)) best = c;
+      }
+    }
+    bj = warp_best(best).j;
+  }
+  return bj;
+}
+
+__global__ void __launch_bounds__(32)
+k_aggregate_spec(const int* __restrict__ G_ptr, const int* __restrict__ G_col, const double* __restrict__ G_val,
+                 const int* __restrict__ hcol_g, const double* __restrict__ hval_g, const int* __restrict__ hlen_g,
+                 int n, int max_size, int* __restrict__ agg_g, int* __restrict__ size_g, int* __restrict__ n_agg_out) {
+  extern __shared__ __align__(16) double shh[];
+  double* sval = shh;                                           // AH_NB * AH_B * AH_K
+  int* scol = reinterpret_cast<int*>(sval + AH_NB * AH_B * AH_K);  // AH_NB * AH_B * AH_K
+  int* slen = scol + AH_NB * AH_B * AH_K;                       // AH_NB * AH_B
+  int* agg = slen + AH_NB * AH_B;                               // n
+  int* size = agg + n;                                          // n
+  const int lane = threadIdx.x;
+  for (int i = lane; i < n; i += 32) {
+    agg[i] = -1;
+    size[i] = 0;
+  }
+  const int nbt = (n + AH_B - 1) / AH_B;
+#pragma unroll 1
+  for (int b = 0; b < AH_NB; ++b) {
+    if (b < nbt) ah_issue(b, hcol_g, hval_g, hlen_g, scol, sval, slen, lane);
+    else cp_async_commit();
+  }
+  __syncwarp();
+  int nagg = 0;
+  for (int b = 0; b < nbt; ++b) {
+    cp_async_wait<AH_NB - 1>();
+    __syncwarp();
+    const int slot = b % AH_NB;
+    const int iend = min(AH_B, n - b * AH_B);
+    const int i_me = b * AH_B + lane;
+    const int* hc = scol + (slot * AH_B + lane) * AH_K;
+    const double* hv = sval + (slot * AH_B + lane) * AH_K;
+    // ---- phase 1: every lane decides its node from the batch-start state
+    int ex[AH_K];     // examined entries (node ids; -1 unused)
+    int exa[AH_K];    // their aggregate at decision time
+    int dec = -1;     // chosen partner / aggregate member
+    bool spec = false;  // a usable speculative decision (false: visit cooperatively at its turn)
+#pragma unroll
+    for (int e = 0; e < AH_K; ++e) {
+      ex[e] = -1;
+      exa[e] = -1;
+    }
+    if (lane < iend && agg[i_me] < 0) {
+      const int len = slen[slot * AH_B + lane];
+      int jj[AH_K];
+      double gg[AH_K];
+      int aa[AH_K];
+#pragma unroll
+      for (int e = 0; e < AH_K; ++e) {
+        jj[e] = hc[e];
+        gg[e] = hv[e];
+      }
+#pragma unroll
+      for (int e = 0; e < AH_K; ++e) aa[e] = jj[e] >= 0 ? agg[jj[e]] : -1;
+      bool el[AH_K];
+#pragma unroll
+      for (int e = 0; e < AH_K; ++e) el[e] = jj[e] >= 0 && (aa[e] < 0 || size[aa[e]] < max_size);
+      if (jj[0] != -2) {
+        int f = -1;
+#pragma unroll
+        for (int e = AH_K - 1; e >= 0; --e)
+          if (el[e]) f = e;
+        if (f < 0) {
+          spec = len <= AH_K;  // no eligible neighbour at all: stays unassigned for now
+          // examined: the whole (short) row
+#pragma unroll
+          for (int e = 0; e < AH_K; ++e) {
+            ex[e] = jj[e];
+            exa[e] = aa[e];
+          }
+        } else {
+          double gf = gg[f];
+          int cu = -1, last = f;
+#pragma unroll
+          for (int e = 0; e < AH_K; ++e) {
+            if (e >= f && jj[e] >= 0 && gg[e] == gf) {
+              if (cu < 0) last = e;
+              if (cu < 0 && el[e] && aa[e] < 0) cu = e;
+            }
+          }
+          bool tail = jj[AH_K - 1] >= 0 && gg[AH_K - 1] == gf;
+          if (cu >= 0) {
+            dec = jj[cu];
+            spec = true;
+          } else if (!(tail && len > AH_K)) {
+            dec = jj[f];
+            spec = true;
+          }
+#pragma unroll
+          for (int e = 0; e < AH_K; ++e)
+            if (e <= last) {
+              ex[e] = jj[e];
+              exa[e] = aa[e];
+            }
+        }
+      }
+    }
+    // ---- phase 2: commit in index order
+    for (int ii = 0; ii < iend; ++ii) {
+      const int i = b * AH_B + ii;
+      __syncwarp();
+      if (agg[i] >= 0) continue;  // partnered by an earlier commit (or before the batch)
+      bool ok = __shfl_sync(FULL_MASK, spec ? 1 : 0, ii) != 0;
+      int bj;
+      if (ok) {
+        bj = __shfl_sync(FULL_MASK, dec, ii);
+      } else {
+        bj = agg_visit_coop(i, G_ptr, G_col, G_val, scol + (slot * AH_B + ii) * AH_K,
+                            sval + (slot * AH_B + ii) * AH_K, slen[slot * AH_B + ii], agg, size, max_size, lane);
+      }
+      if (bj < 0) continue;  // nothing eligible: left for the post-pass
+      int aj = agg[bj];
+      int a_new, sz_new;
+      if (aj < 0) {
+        a_new = nagg;
+        sz_new = 2;
+      } else {
+        a_new = aj;
+        sz_new = size[aj] + 1;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        agg[i] = a_new;
+        if (aj < 0) agg[bj] = a_new;
+        size[a_new] = sz_new;
+      }
+      if (aj < 0) ++nagg;
+      // later lanes whose examined entries this commit touched decide again at their turn
+      const bool became_full = sz_new >= max_size;
+      if (lane > ii && spec) {
+        bool hit = false;
+#pragma unroll
+        for (int e = 0; e < AH_K; ++e) {
+          int j = ex[e];
+          hit |= j >= 0 && (j == i || j == bj || (became_full && exa[e] == a_new));
+        }
+        if (hit) spec = false;
+      }
+    }
+    __syncwarp();
+    if (b + AH_NB < nbt) ah_issue(b + AH_NB, hcol_g, hval_g, hlen_g, scol, sval, slen, lane);
+    else cp_async_commit();
+  }
+  cp_async_wait<0>();
+  // post-pass over leftovers in index order (multigrid.py:164-175)
+  for (int i = 0; i < n; ++i) {
+    __syncwarp();
+    if (agg[i] >= 0) continue;
+    Cand best{0.0, 0, -1};
+    for (int q = G_ptr[i] + lane; q < G_ptr[i + 1]; q += 32) {
+      int j = G_col[q];
+      int a = agg[j];
+      if (a >= 0 && size[a] <= max_size) {
+        Cand c{G_val[q], 0, j};
+        if (better(c, best)) best = c;
+      }
+    }
+    best = warp_best(best);
+    __syncwarp();
+    if (lane == 0) {
+      if (best.j >= 0) {
+        int a = agg[best.j];
+        agg[i] = a;
+        size[a] += 1;
+      } else {
+        agg[i] = nagg;
+        size[nagg] = 1;
+      }
+    }
+    if (best.j < 0) ++nagg;
+    __syncwarp();
+  }
+  __syncwarp();
+  int mx = 0;
+  for (int i = lane; i < n; i += 32) {
+    agg_g[i] = agg[i];
+    size_g[i] = size[i];
+    if (i < nagg) mx = max(mx, size[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL_MASK, mx, o));
+  if (lane == 0) {
+    n_agg_out[0] = nagg;
+    n_agg_out[1] = mx;
+  }
+}
+
 extern "C" int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t* G_col, const double* G_val,
                               int32_t n, int32_t max_size, int32_t* agg, int32_t* size_work, int32_t* n_agg_dev,
                               int64_t nnz_cap, void* stream) {
@@ -817,8 +1092,22 @@ extern "C" int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t
         BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smh));
         hattr = smh;
       }
-      launch(k_aggregate_head, 1, 32, smh, st, G_ptr, (const int*)col_s, (const double*)val_s, (const int*)hcol,
-             (const double*)hval, (const int*)hlen, n, max_size, agg, size_work, n_agg_dev);
+      static const bool spec_on = [] {
+        const char* e = getenv("BAMG_AGG_SPEC");
+        return !(e && e[0] == '0');
+      }();
+      if (spec_on) {
+        static size_t sattr = 0;
+        if (smh > sattr) {
+          BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smh));
+          sattr = smh;
+        }
+        launch(k_aggregate_spec, 1, 32, smh, st, G_ptr, (const int*)col_s, (const double*)val_s, (const int*)hcol,
+               (const double*)hval, (const int*)hlen, n, max_size, agg, size_work, n_agg_dev);
+      } else {
+        launch(k_aggregate_head, 1, 32, smh, st, G_ptr, (const int*)col_s, (const double*)val_s, (const int*)hcol,
+               (const double*)hval, (const int*)hlen, n, max_size, agg, size_work, n_agg_dev);
+      }
       BAMG_CUDA_CHECK(cudaFreeAsync(hcol, st));
       BAMG_CUDA_CHECK(cudaFreeAsync(hval, st));
       BAMG_CUDA_CHECK(cudaFreeAsync(hlen, st));

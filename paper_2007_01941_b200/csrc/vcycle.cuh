@@ -1217,6 +1217,316 @@ extern "C" int bamg_mg_apply(bamg_ctx* ctx, bamg_mg* m, const double* r, double*
 // rel, q_history[0..iterations], err (0 none, 1 not-SPD, 2 op non-finite,
 // 3 curvature, 4 residual non-finite, 5 preconditioner non-finite), err_value, err_iter.
 
+// ---------------------------------------------------------------------------
+// The same PCG as ONE CUDA graph with device-side control flow: a WHILE
+// conditional node runs the iterations and an IF node inside its body skips the
+// preconditioner tail once a stop test fired. The stop tests of solver.py:70-128
+// run in single-thread kernels in the reference's order, with every scalar formed
+// by separately rounded operations (the host loop's arithmetic, bit for bit); the
+// host reads the outcome once, after the solve. No host synchronisation per
+// iteration.
+
+struct PcgDev {
+  double bnorm, rz, rzn, pap, rr, q, rel, errv;
+  int it, done, reason, err, erri, pad0, pad1, pad2;
+};
+
+__global__ void k_pcg_g_init(const double* __restrict__ bb, PcgDev* s, double* qh) {
+  if (threadIdx.x | blockIdx.x) return;
+  double bn = __dsqrt_rn(*bb);
+  s->bnorm = bn;
+  s->q = 0.0;
+  s->rel = 1.0;
+  s->it = 0;
+  s->err = 0;
+  s->erri = 0;
+  s->errv = 0.0;
+  s->reason = 2;  // max_iterations unless a stop test fires
+  s->done = 0;
+  qh[0] = 0.0;
+  if (bn == 0.0) {  // solver.py:93-94
+    s->done = 1;
+    s->reason = 0;
+    s->rel = 0.0;
+  }
+}
+
+// iteration-0 checks of <r, M r> (solver.py:97-101), then the loop condition
+__global__ void k_pcg_g_rz0(PcgDev* s, int max_it, cudaGraphConditionalHandle hw) {
+  if (threadIdx.x | blockIdx.x) return;
+  if (!s->done) {
+    double rz = s->rz;
+    if (!isfinite(rz)) {
+      s->err = 5;
+      s->done = 1;
+    } else if (rz <= 0.0) {
+      s->err = 1;
+      s->errv = rz;
+      s->done = 1;
+    }
+  }
+  cudaGraphSetConditional(hw, (!s->done && max_it > 0) ? 1u : 0u);
+}
+
+// after <p, Ap> and the x / r update: curvature, Q, relative residual, residual
+// tolerance, forcing (solver.py:104-120, ForcingCriterion.satisfied 52-59)
+__global__ void k_pcg_g_check1(PcgDev* s, double* qh, double rtol, double tau, cudaGraphConditionalHandle hw,
+                               cudaGraphConditionalHandle hif) {
+  if (threadIdx.x | blockIdx.x) return;
+  int i = ++s->it;
+  double pap = s->pap;
+  if (!isfinite(pap)) {
+    s->err = 2;
+    s->erri = i;
+    s->done = 1;
+  } else if (pap <= 0.0) {
+    s->err = 3;
+    s->errv = pap;
+    s->erri = i;
+    s->done = 1;
+  } else {
+    double rz = s->rz;
+    double alpha = __ddiv_rn(rz, pap);
+    double q = __dsub_rn(s->q, __dmul_rn(__dmul_rn(0.5, alpha), rz));
+    s->q = q;
+    qh[i] = q;
+    double rel = __ddiv_rn(__dsqrt_rn(s->rr), s->bnorm);
+    s->rel = rel;
+    if (!isfinite(rel)) {
+      s->err = 4;
+      s->erri = i;
+      s->done = 1;
+    } else if (rel <= rtol) {
+      s->reason = 0;
+      s->done = 1;
+    } else {
+      double qc = q, qp = qh[i - 1];
+      if (qc != 0.0 && __ddiv_rn(__dmul_rn((double)i, __dsub_rn(qc, qp)), qc) <= tau) {
+        s->reason = 1;
+        s->done = 1;
+      }
+    }
+  }
+  unsigned go = s->done ? 0u : 1u;
+  cudaGraphSetConditional(hif, go);
+  cudaGraphSetConditional(hw, go);
+}
+
+// after z = M r and <r, z>: preconditioner checks (solver.py:121-125), last iteration
+__global__ void k_pcg_g_check2(PcgDev* s, int max_it) {
+  if (threadIdx.x | blockIdx.x) return;
+  double rzn = s->rzn;
+  if (!isfinite(rzn)) {
+    s->err = 5;
+    s->erri = s->it;
+    s->done = 1;
+  } else if (rzn <= 0.0) {
+    s->err = 1;
+    s->errv = rzn;
+    s->erri = s->it;
+    s->done = 1;
+  } else if (s->it >= max_it) {
+    s->reason = 2;
+    s->done = 1;
+  }
+}
+
+// after p = z + (rz_next / rz) p: rz <- rz_next, loop condition
+__global__ void k_pcg_g_next(PcgDev* s, cudaGraphConditionalHandle hw) {
+  if (threadIdx.x | blockIdx.x) return;
+  s->rz = s->rzn;
+  cudaGraphSetConditional(hw, s->done ? 0u : 1u);
+}
+
+static cudaGraphExec_t g_pcg_parked = nullptr;  // last PCG executable: re-targeted by the next solve
+
+static int pcg_graph(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const bamg_vj* vj, int32_t bs, int32_t nbr,
+                     const int32_t* ptr, const int32_t* col, const double* blocks, const double* b, double* x,
+                     double tau, int32_t max_it, double rtol, double* work, int32_t* iterations_out,
+                     int32_t* reason_out, double* rel_out, double* q_hist, int32_t* err_out, double* err_value_out,
+                     int32_t* err_iter_out, const bamg_symop* sym, cudaStream_t st) {
+  int64_t n = (int64_t)nbr * bs;
+  double* r = work;
+  double* z = work + n;
+  if (mg) {
+    int rc0 = mg_prepare(mg, st);  // arena + chunk plans before the capture
+    if (rc0) return rc0;
+    if (mg->lv[0].n == n) {
+      r = mg->in;
+      z = mg->out;
+    }
+  }
+  double* p = work + 2 * n;
+  double* ap = work + 3 * n;
+  PcgDev* dev = nullptr;
+  double* qh = nullptr;
+  double* bb = ctx->scalars + 4;
+  BAMG_CUDA_CHECK(cudaMallocAsync(&dev, sizeof(PcgDev), st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&qh, sizeof(double) * ((size_t)max_it + 2), st));
+  auto precond = [&](cudaStream_t cs) -> int {
+    if (mg) {
+      int rc = mg_record(mg, cs);  // kernels of one V-cycle: in = mg->in, result in mg->out
+      if (rc) return rc;
+      if (r != mg->in || z != mg->out) return BAMG_ERR_UNSUPPORTED;
+      return 0;
+    }
+    if (vj) {
+      vj_apply_dev(vj, r, z, cs);
+      return 0;
+    }
+    launch(k_blockdiag_apply, grid_for(n, 256), 256, 0, cs, pbj_inv, (const double*)r, nbr, bs, z);
+    return 0;
+  };
+  auto spmv_dot = [&](cudaStream_t cs) {
+    if (sym) {
+      sym_apply(ctx, sym, blocks, p, 0, nullptr, nullptr, nullptr, ap, 0.0, 0.0, 0, &dev->pap, cs);
+      return;
+    }
+    int g = spmv_grid(nbr);
+    if (g > BAMG_MAX_PARTIALS) g = BAMG_MAX_PARTIALS;
+    unsigned* ctr = ctx->counters + BAMG_CTR_SPMV;
+    switch (bs) {
+      case 9: launch(k_bsr_spmv<9>, g, 128, 0, cs, ptr, col, blocks, (const double*)p, ap, nbr, ctx->partials, ctr, &dev->pap); break;
+      case 16: launch(k_bsr_spmv<16>, g, 128, 0, cs, ptr, col, blocks, (const double*)p, ap, nbr, ctx->partials, ctr, &dev->pap); break;
+      default: launch(k_bsr_spmv<1>, g, 128, 0, cs, ptr, col, blocks, (const double*)p, ap, nbr, ctx->partials, ctr, &dev->pap); break;
+    }
+  };
+
+  // ---- build the graph: init segment, WHILE { check body, IF { preconditioner tail } }
+  cudaGraph_t graph = nullptr;
+  BAMG_CUDA_CHECK(cudaGraphCreate(&graph, 0));
+  cudaGraphConditionalHandle hw, hif;
+  BAMG_CUDA_CHECK(cudaGraphConditionalHandleCreate(&hw, graph, 0, cudaGraphCondAssignDefault));
+  cudaStream_t cs;
+  BAMG_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  long long before = g_bamg_launches.load();
+  int rc = 0;
+  int k_init = 0, k_body = 0, k_tail = 0;
+  cudaGraph_t body = nullptr, tail = nullptr;
+  do {
+    if (cudaStreamBeginCaptureToGraph(cs, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) { rc = BAMG_ERR_CUDA; break; }
+    long long c0 = g_bamg_launches.load();
+    cudaMemsetAsync(x, 0, sizeof(double) * n, cs);
+    dot_dev(ctx, b, b, n, bb, cs);
+    launch(k_copy, grid_for(n, 256), 256, 0, cs, b, r, n);
+    launch(k_pcg_g_init, 1, 32, 0, cs, (const double*)bb, dev, qh);
+    if ((rc = precond(cs))) break;
+    dot_dev(ctx, r, z, n, &dev->rz, cs);
+    launch(k_pcg_g_rz0, 1, 32, 0, cs, dev, max_it, hw);
+    launch(k_copy, grid_for(n, 256), 256, 0, cs, (const double*)z, p, n);
+    k_init = (int)(g_bamg_launches.load() - c0);
+    // WHILE node after the init segment
+    cudaStreamCaptureStatus cst;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    cudaGraph_t cg = nullptr;
+    if (cudaStreamGetCaptureInfo(cs, &cst, nullptr, &cg, &deps, &ndeps)) { rc = BAMG_ERR_CUDA; break; }
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = hw;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    if (cudaGraphAddNode(&wnode, cg, deps, ndeps, &wp)) { rc = BAMG_ERR_CUDA; break; }
+    body = wp.conditional.phGraph_out[0];
+    if (cudaStreamUpdateCaptureDependencies(cs, &wnode, 1, cudaStreamSetCaptureDependencies)) { rc = BAMG_ERR_CUDA; break; }
+    if (cudaStreamEndCapture(cs, &graph)) { rc = BAMG_ERR_CUDA; break; }
+
+    // body: S p, <p, S p>, x/r update + |r|^2, checks, IF { M r, <r, z>, checks, p update }
+    if (cudaGraphConditionalHandleCreate(&hif, body, 0, cudaGraphCondAssignDefault)) { rc = BAMG_ERR_CUDA; break; }
+    if (cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) { rc = BAMG_ERR_CUDA; break; }
+    c0 = g_bamg_launches.load();
+    spmv_dot(cs);
+    launch(k_pcg_update_dev, grid_for(n, 256, 4), 256, 0, cs, x, r, (const double*)p, (const double*)ap,
+           (const double*)&dev->rz, (const double*)&dev->pap, n, ctx->partials, ctx->counters + BAMG_CTR_PCG0,
+           &dev->rr);
+    launch(k_pcg_g_check1, 1, 32, 0, cs, dev, qh, rtol, tau, hw, hif);
+    k_body = (int)(g_bamg_launches.load() - c0);
+    if (cudaStreamGetCaptureInfo(cs, &cst, nullptr, &cg, &deps, &ndeps)) { rc = BAMG_ERR_CUDA; break; }
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = hif;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t inode;
+    if (cudaGraphAddNode(&inode, cg, deps, ndeps, &ip)) { rc = BAMG_ERR_CUDA; break; }
+    tail = ip.conditional.phGraph_out[0];
+    if (cudaStreamUpdateCaptureDependencies(cs, &inode, 1, cudaStreamSetCaptureDependencies)) { rc = BAMG_ERR_CUDA; break; }
+    if (cudaStreamEndCapture(cs, &body)) { rc = BAMG_ERR_CUDA; break; }
+
+    if (cudaStreamBeginCaptureToGraph(cs, tail, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) { rc = BAMG_ERR_CUDA; break; }
+    c0 = g_bamg_launches.load();
+    if ((rc = precond(cs))) break;
+    dot_dev(ctx, r, z, n, &dev->rzn, cs);
+    launch(k_pcg_g_check2, 1, 32, 0, cs, dev, max_it);
+    launch(k_xpby_dev, grid_for(n, 256), 256, 0, cs, (const double*)z, (const double*)&dev->rzn,
+           (const double*)&dev->rz, p, n);
+    launch(k_pcg_g_next, 1, 32, 0, cs, dev, hw);
+    k_tail = (int)(g_bamg_launches.load() - c0);
+    if (cudaStreamEndCapture(cs, &tail)) { rc = BAMG_ERR_CUDA; break; }
+  } while (0);
+  g_bamg_launches.store(before);  // capture is not execution
+  if (rc) {
+    cudaStreamCaptureStatus cst;
+    if (cudaStreamIsCapturing(cs, &cst) == cudaSuccess && cst != cudaStreamCaptureStatusNone) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(cs, &junk);
+      if (junk && junk != graph) cudaGraphDestroy(junk);
+    }
+    cudaGetLastError();
+    cudaStreamDestroy(cs);
+    cudaGraphDestroy(graph);
+    cudaFreeAsync(dev, st);
+    cudaFreeAsync(qh, st);
+    if (rc == BAMG_ERR_CUDA) bamg_set_error("pcg graph capture failed");
+    return rc;
+  }
+  cudaStreamDestroy(cs);
+  cudaGraphExec_t exec = nullptr;
+  if (g_pcg_parked) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(g_pcg_parked, graph, &info) == cudaSuccess) {
+      exec = g_pcg_parked;
+    } else {
+      cudaGetLastError();
+      cudaGraphExecDestroy(g_pcg_parked);
+    }
+    g_pcg_parked = nullptr;
+  }
+  if (!exec) {
+    cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    if (e != cudaSuccess) {
+      cudaGraphDestroy(graph);
+      cudaFreeAsync(dev, st);
+      cudaFreeAsync(qh, st);
+      BAMG_CUDA_CHECK(e);
+    }
+  }
+  cudaGraphDestroy(graph);
+  BAMG_CUDA_CHECK(cudaGraphLaunch(exec, st));
+  PcgDev h;
+  BAMG_CUDA_CHECK(cudaMemcpyAsync(&h, dev, sizeof(PcgDev), cudaMemcpyDeviceToHost, st));
+  BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+  g_pcg_parked = exec;
+  int its = h.it;
+  if (its > 0) BAMG_CUDA_CHECK(cudaMemcpy(q_hist + 1, qh + 1, sizeof(double) * (size_t)its, cudaMemcpyDeviceToHost));
+  q_hist[0] = 0.0;
+  cudaFreeAsync(dev, st);
+  cudaFreeAsync(qh, st);
+  // launch accounting: init + every body + every executed tail
+  int tails = its - ((h.err >= 2 && h.err <= 4) || (h.done && h.err == 0 && h.reason != 2) ? 1 : 0);
+  if (tails < 0) tails = 0;
+  g_bamg_launches.fetch_add((long long)k_init + (long long)its * k_body + (long long)tails * k_tail);
+  *err_out = h.err;
+  *err_value_out = h.errv;
+  *err_iter_out = h.erri;
+  *iterations_out = (h.err == 0 && h.reason == 2) ? max_it : its;
+  *reason_out = h.reason;
+  *rel_out = h.rel;
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
 extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const bamg_vj* vj, int32_t bs, int32_t nbr,
                             const int32_t* ptr, const int32_t* col, const double* blocks, const double* b, double* x,
                             double tau, int32_t max_it, double rtol, double* work, int32_t* iterations_out,
@@ -1229,6 +1539,13 @@ extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, c
     bamg_set_error("pcg_run: symmetric operator block size %d, operator %d", sym->bs, bs);
     return BAMG_ERR_UNSUPPORTED;
   }
+  static const bool host_loop = [] {
+    const char* e = getenv("BAMG_PCG_HOSTLOOP");
+    return e && e[0] == '1';
+  }();
+  if (!host_loop && max_it >= 0 && (!mg || mg->lv[0].n == n))
+    return pcg_graph(ctx, mg, pbj_inv, vj, bs, nbr, ptr, col, blocks, b, x, tau, max_it, rtol, work, iterations_out,
+                     reason_out, rel_out, q_hist, err_out, err_value_out, err_iter_out, sym, st);
   double* r = work;
   double* z = work + n;
   if (mg) {

@@ -69,6 +69,10 @@ def test_from_triplets_bit_exact(P, rbs, cbs):
     nbr, nbc, n = 37, 53, 900
     r = rng.integers(0, nbr, n)
     c = rng.integers(0, nbc, n)
+    # duplicate runs of every length class of numpy's pairwise sum (<8, 8..128, >128)
+    r = np.concatenate([r, np.full(5, 3), np.full(20, 4), np.full(300, 5)])
+    c = np.concatenate([c, np.full(5, 7), np.full(20, 8), np.full(300, 9)])
+    n = len(r)
     blocks = rng.standard_normal((n, rbs, cbs)) * 10.0 ** rng.integers(-8, 8, (n, 1, 1))
     M = P.BlockSparseMatrix.from_triplets(nbr, nbc, r, c, blocks)
     ptr, col, summed = _ref_from_triplets(nbr, nbc, r, c, blocks)

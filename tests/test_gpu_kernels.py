@@ -274,3 +274,31 @@ def test_chebyshev_matches_oracle(P):
     assert relerr(got, ch.apply(mv, None, b)) <= 1e-12
     got = D().host(sm.apply(Bd.matvec, x0, b))
     assert relerr(got, ch.apply(mv, x0, b)) <= 1e-12
+
+
+@pytest.mark.parametrize("seed,n,deg,max_size,levels", [
+    (1, 300, 6, 20, 4), (2, 2000, 12, 20, 8), (3, 700, 30, 3, 3), (4, 500, 9, 2, 5), (5, 4000, 40, 20, 16),
+    (6, 1500, 3, 20, 2)])
+def test_aggregate_speculative_scan_matches_oracle(P, seed, n, deg, max_size, levels):
+    """The speculative batch scan (k_aggregate_spec) against the oracle's sequential
+    greedy scan (multigrid.py:127-176) on random graphs built to collide: local
+    neighbourhoods (consecutive nodes are neighbours, as coarse aggregates are),
+    few distinct strengths (ties everywhere), rows longer than the 8-entry head,
+    tiny aggregate caps (full aggregates)."""
+    import scipy.sparse as sp
+
+    from oracle import bamg_oracle as O
+
+    rng = np.random.default_rng(seed)
+    r = np.repeat(np.arange(n), deg)
+    c = (r + rng.integers(-3 * deg, 3 * deg + 1, r.size)) % n
+    keep = r != c
+    v = rng.integers(1, levels + 1, r.size) / levels
+    g = sp.csr_matrix((v[keep], (r[keep], c[keep])), shape=(n, n))
+    g = g.maximum(g.T).tocsr()
+    g.sort_indices()
+    G = P.StrengthMatrix(g.indptr, g.indices, g.data, n)
+    agg = P.aggregate(G, max_size=max_size)
+    want, na = O.aggregate(g, max_size)
+    assert agg.n_aggregates == na
+    np.testing.assert_array_equal(D().host(agg.assignment), want)
