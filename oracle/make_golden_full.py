@@ -65,6 +65,8 @@ def main():
     ap.add_argument("--pbj-lm-steps", type=int, default=0)
     ap.add_argument("--no-pbj", action="store_true")
     ap.add_argument("--out", default=os.path.join(ROOT, "tests", "golden"))
+    ap.add_argument("--tag", default="", help="file suffix (e.g. _pbj for a comparator-only run)")
+    ap.add_argument("--lm-only", action="store_true", help="only the LM runs, no per-function fingerprints")
     args = ap.parse_args()
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.abspath(args.ref))
@@ -85,6 +87,49 @@ def main():
         warnings.simplefilter("ignore")
         prob = bamg.BundleProblem(*sc.arrays())
     k = prob.n_observations
+
+    def lm(precond: str, steps: int, prefix: str):
+        orig = solver.pcg
+        solver.pcg = functools.partial(orig, residual_tolerance=1e-6)
+        try:
+            cfg = solver.SolveConfig(preconditioner=precond, tau=1e-30, max_iterations=steps,
+                                     function_tolerance=0.0, gradient_tolerance=0.0, parameter_tolerance=0.0,
+                                     initial_radius=1e4, cg_max_iterations=20000)
+            t = time.perf_counter()
+            sol, rp = solver.lm_solve(prob, cfg)
+            wall = time.perf_counter() - t
+        finally:
+            solver.pcg = orig
+        recs = rp.records
+        out[f"{prefix}_cg"] = np.array([r.cg_iterations for r in recs])
+        out[f"{prefix}_obj"] = np.array([r.objective for r in recs])
+        out[f"{prefix}_radius"] = np.array([r.radius for r in recs])
+        out[f"{prefix}_accepted"] = np.array([r.accepted for r in recs])
+        out[f"{prefix}_rho"] = np.array([r.rho for r in recs])
+        out[f"{prefix}_setup_s"] = np.array([r.setup_seconds for r in recs])
+        out[f"{prefix}_solve_s"] = np.array([r.solve_seconds for r in recs])
+        out[f"{prefix}_wall_s"] = np.float64(wall)
+        log(f"{prefix} {wall:.1f}s cg {out[f'{prefix}_cg'].tolist()} acc {out[f'{prefix}_accepted'].astype(int).tolist()}")
+
+    def finish():
+        import numpy
+        import scipy
+
+        out["host"] = np.array(f"{platform.processor() or platform.machine()} cpus={os.cpu_count()} "
+                               f"numpy={numpy.__version__} scipy={scipy.__version__} "
+                               f"OMP_NUM_THREADS={os.environ.get('OMP_NUM_THREADS', '')}")
+        out["ref_path"] = np.array(os.path.abspath(args.ref))
+        os.makedirs(args.out, exist_ok=True)
+        path = os.path.join(args.out, f"full_c{args.config}{args.tag}.npz")
+        np.savez_compressed(path, **out)
+        log(f"wrote {path} ({os.path.getsize(path) / 1e6:.1f} MB) total {time.perf_counter() - t0:.0f}s")
+
+    if args.lm_only:
+        if args.lm_steps:
+            lm("multigrid", args.lm_steps, "lm")
+        if args.pbj_lm_steps:
+            lm("pbj", args.pbj_lm_steps, "pbj_lm")
+        return finish()
 
     t = time.perf_counter()
     obj, jac = evaluate(prob)
@@ -174,45 +219,11 @@ def main():
         log(f"pbj pcg {out['time_pbj_pcg']:.1f}s its {repb.iterations}")
     del h, S, s, jac
 
-    def lm(precond: str, steps: int, prefix: str):
-        orig = solver.pcg
-        solver.pcg = functools.partial(orig, residual_tolerance=1e-6)
-        try:
-            cfg = solver.SolveConfig(preconditioner=precond, tau=1e-30, max_iterations=steps,
-                                     function_tolerance=0.0, gradient_tolerance=0.0, parameter_tolerance=0.0,
-                                     initial_radius=1e4, cg_max_iterations=20000)
-            t = time.perf_counter()
-            sol, rp = solver.lm_solve(prob, cfg)
-            wall = time.perf_counter() - t
-        finally:
-            solver.pcg = orig
-        recs = rp.records
-        out[f"{prefix}_cg"] = np.array([r.cg_iterations for r in recs])
-        out[f"{prefix}_obj"] = np.array([r.objective for r in recs])
-        out[f"{prefix}_radius"] = np.array([r.radius for r in recs])
-        out[f"{prefix}_accepted"] = np.array([r.accepted for r in recs])
-        out[f"{prefix}_rho"] = np.array([r.rho for r in recs])
-        out[f"{prefix}_setup_s"] = np.array([r.setup_seconds for r in recs])
-        out[f"{prefix}_solve_s"] = np.array([r.solve_seconds for r in recs])
-        out[f"{prefix}_wall_s"] = np.float64(wall)
-        log(f"{prefix} {wall:.1f}s cg {out[f'{prefix}_cg'].tolist()} acc {out[f'{prefix}_accepted'].astype(int).tolist()}")
-
     if args.lm_steps:
         lm("multigrid", args.lm_steps, "lm")
     if args.pbj_lm_steps:
         lm("pbj", args.pbj_lm_steps, "pbj_lm")
-
-    import numpy
-    import scipy
-
-    out["host"] = np.array(f"{platform.processor() or platform.machine()} cpus={os.cpu_count()} "
-                           f"numpy={numpy.__version__} scipy={scipy.__version__} "
-                           f"OMP_NUM_THREADS={os.environ.get('OMP_NUM_THREADS', '')}")
-    out["ref_path"] = np.array(os.path.abspath(args.ref))
-    os.makedirs(args.out, exist_ok=True)
-    path = os.path.join(args.out, f"full_c{args.config}.npz")
-    np.savez_compressed(path, **out)
-    log(f"wrote {path} ({os.path.getsize(path) / 1e6:.1f} MB) total {time.perf_counter() - t0:.0f}s")
+    finish()
 
 
 if __name__ == "__main__":

@@ -111,7 +111,7 @@ class SchurSystem:
 
     def ensure_explicit(self) -> BlockSparseMatrix:
         if self.S_explicit is None:
-            self.S_explicit = schur_explicit(self)
+            self.S_explicit = schur_explicit(self, _VARIANT)
         return self.S_explicit
 
 
@@ -170,6 +170,7 @@ def schur_explicit(sys: SchurSystem, variant: str = "pairs") -> BlockSparseMatri
 
 
 _SYMMETRIC = __import__("os").environ.get("BAMG_SYM_SPMV", "1") == "1"
+_VARIANT = __import__("os").environ.get("BAMG_SCHUR", "pairs")  # A/B: pairs | rows
 
 
 def covisibility_block_count(sys: SchurSystem) -> int:
