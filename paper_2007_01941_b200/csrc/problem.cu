@@ -569,15 +569,22 @@ k_cam_normal(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
       }
     }
     int c = 0;
+    // observation ids of the next chunk to issue, loaded one iteration ahead so the
+    // copies never wait on the index load
+    int nidx = (q0 + 32 * (CN_STAGES - 1) + lane < q1) ? cm_list[q0 + 32 * (CN_STAGES - 1) + lane] : 0;
     for (int base = q0; base < q1; base += 32, ++c) {
       // chunk c + CN_STAGES - 1 goes out before chunk c is consumed
       int nb = base + 32 * (CN_STAGES - 1);
       if (nb < q1) {
         bool vn = nb + lane < q1;
-        rec_issue<9, 1, 0>(J, vn ? cm_list[nb + lane] : 0, vn, 0, RR / 2, nullptr,
+        rec_issue<9, 1, 0>(J, nidx, vn, 0, RR / 2, nullptr,
                            wbuf + ((c + CN_STAGES - 1) % CN_STAGES) * 640, lane);
       } else {
         cp_async_commit();
+      }
+      {
+        int pb = nb + 32;
+        nidx = (pb + lane < q1) ? cm_list[pb + lane] : 0;
       }
       cp_async_wait<CN_STAGES - 1>();
       __syncwarp();
@@ -818,14 +825,21 @@ k_cam_gather(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
       }
     }
     int c = 0;
+    // observation ids of the next chunk to issue, loaded one iteration ahead so the
+    // copies never wait on the index load
+    int nidx = (q0 + 32 * (CN_STAGES - 1) + lane < q1) ? cm_list[q0 + 32 * (CN_STAGES - 1) + lane] : 0;
     for (int base = q0; base < q1; base += 32, ++c) {
       int nb = base + 32 * (CN_STAGES - 1);
       if (nb < q1) {
         bool vn = nb + lane < q1;
-        rec_issue<9, 0, 1>(J, vn ? cm_list[nb + lane] : 0, vn, 0, 0, qo,
+        rec_issue<9, 0, 1>(J, nidx, vn, 0, 0, qo,
                            wbuf + ((c + CN_STAGES - 1) % CN_STAGES) * 640, lane);
       } else {
         cp_async_commit();
+      }
+      {
+        int pb = nb + 32;
+        nidx = (pb + lane < q1) ? cm_list[pb + lane] : 0;
       }
       cp_async_wait<CN_STAGES - 1>();
       __syncwarp();

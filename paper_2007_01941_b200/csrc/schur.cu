@@ -356,14 +356,21 @@ k_schur_diag(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
       }
     }
     int c = 0;
+    // observation ids of the next chunk to issue, loaded one iteration ahead so the
+    // copies never wait on the index load
+    int nidx = (q0 + 32 * (SD_STAGES - 1) + lane < q1) ? cm_list[q0 + 32 * (SD_STAGES - 1) + lane] : 0;
     for (int base = q0; base < q1; base += 32, ++c) {
       int nb = base + 32 * (SD_STAGES - 1);
       if (nb < q1) {
         bool vn = nb + lane < q1;
-        rec_issue<15, 0, 0>(J, vn ? cm_list[nb + lane] : 0, vn, 0, 0, nullptr,
+        rec_issue<15, 0, 0>(J, nidx, vn, 0, 0, nullptr,
                             wbuf + ((c + SD_STAGES - 1) % SD_STAGES) * CH, lane);
       } else {
         cp_async_commit();
+      }
+      {
+        int pb = nb + 32;
+        nidx = (pb + lane < q1) ? cm_list[pb + lane] : 0;
       }
       cp_async_wait<SD_STAGES - 1>();
       __syncwarp();
