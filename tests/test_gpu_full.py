@@ -172,3 +172,26 @@ def test_lm_records(full):
                         cg_max_iterations=20000, cg_residual_tolerance=1e-6)
     sol, rep = P.lm_solve(prob, cfg)
     _check_lm(rep, g, "lm")
+
+
+def test_pbj_lm_records_config5():
+    """BASELINE config 5 asks for PCG iterations versus the reference's block-Jacobi:
+    the 10-step LM with point-block Jacobi against the real reference's records
+    (tests/golden/full_c5_pbj.npz), same bar as the multigrid run."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    g = dict(np.load(os.path.join(GOLDEN, "full_c5_pbj.npz"), allow_pickle=False))
+    import paper_2007_01941_b200 as P
+    from paper_2007_01941_b200 import scenes
+
+    sc = scenes.config(5)
+    assert sc.digest() == str(g["digest"])
+    prob = P.BundleProblem(*sc.arrays())
+    steps = len(g["pbj_lm_cg"]) - 1
+    cfg = P.SolveConfig(preconditioner="pbj", tau=1e-30, max_iterations=steps, function_tolerance=0.0,
+                        gradient_tolerance=0.0, parameter_tolerance=0.0, initial_radius=1e4,
+                        cg_max_iterations=20000, cg_residual_tolerance=1e-6)
+    sol, rep = P.lm_solve(prob, cfg)
+    _check_lm(rep, g, "pbj_lm")
