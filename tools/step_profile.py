@@ -32,6 +32,12 @@ def main(config=4, top=45):
     for _ in range(3):
         step()
     torch.cuda.synchronize()
+    from paper_2007_01941_b200 import _device as D
+
+    if D._PHASE_ON:  # BAMG_PHASES=1: sync-timed phases of one step (diagnostic)
+        D.PHASES.clear()
+        step()
+        print("phases (ms):", {k: round(v * 1e3, 2) for k, v in D.PHASES.items()})
     t0 = time.perf_counter()
     out = step()
     torch.cuda.synchronize()
