@@ -101,6 +101,10 @@ int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_l
                       const double* g_pt, const double* d_cam, const double* d_pt, int32_t nc, int32_t npt,
                       double* A, double* C, double* Cinv, double* Cb, double* qo, double* rhs,
                       int32_t* bad_min_dev, void* stream);
+/* rhs == NULL in bamg_build_system skips the right-hand side (formed later by
+ * bamg_rhs_gather, or by bamg_schur_numeric's diagonal pass in the same sweep) */
+int bamg_rhs_gather(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const double* J, const double* qo,
+                    const double* g_cam, int32_t nc, double* rhs, void* stream);
 /* recompute the H slots of J (and q) from a system's C^-1 / C^-1 b */
 int bamg_obs_H(bamg_ctx* ctx, const int32_t* obs_pt_pm, const double* Cinv, const double* Cb, int64_t k, double* J,
                double* qo, void* stream);
@@ -134,10 +138,12 @@ int bamg_schur_numeric_rows(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t
                             const int32_t* obs_cam_pm, const int32_t* obs_pt_pm, const double* J, const double* A,
                             const int32_t* S_ptr, const int32_t* S_col, const int32_t* dpos, const int32_t* up_off,
                             const int32_t* up_tpos, int32_t nc, double* S, void* stream);
+/* diagonal blocks (and, rhs != NULL, the right-hand side -g - sum F^T q in the same pass)
+ * plus the upper off-diagonal blocks from the pair lists */
 int bamg_schur_numeric(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const double* J,
                        const double* A, const int32_t* dpos, int32_t nc, const int32_t* up_blk, const int32_t* up_tpos,
                        int32_t n_up, const int32_t* blk_pair_ptr, const int32_t* pair_a, const int32_t* pair_b,
-                       double* S, void* stream);
+                       const double* qo, const double* g_cam, double* rhs, double* S, void* stream);
 
 /* ---- BSR kernels: blockmat.py:295-299 (matvec), 91-129 (block-diagonal), 270-282 ---- */
 int bamg_bsr_spmv(bamg_ctx* ctx, int32_t bs, const int32_t* ptr, const int32_t* col, const double* blocks,

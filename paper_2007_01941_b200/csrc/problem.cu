@@ -904,6 +904,18 @@ extern "C" int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const in
   if (npt)
     launch(k_points_factor, grid_for(npt, 128, 16), 128, 0, st, C_raw, d_pt, g_pt, npt, C, Cinv, Cb, bad_min_dev);
   if (k) launch(k_obs_H, grid_for(k, 256, 8), 256, 0, st, obs_pt_pm, Cinv, Cb, k, J, qo);
+  if (nc && rhs)  // rhs == NULL: formed later by bamg_rhs_gather or the Schur diagonal pass
+    launch(k_cam_gather, grid_for((int64_t)nc * 32, 128, 8), 128, cam_gather_smem(), st, cam_ptr, cm_list, J, qo,
+           g_cam, nullptr, nullptr, nc, rhs);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+// schur.py:122 rhs_cam = -g - sum_o F_o^T q_o on its own (camera-major gather)
+extern "C" int bamg_rhs_gather(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const double* J,
+                               const double* qo, const double* g_cam, int32_t nc, double* rhs, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
   if (nc)
     launch(k_cam_gather, grid_for((int64_t)nc * 32, 128, 8), 128, cam_gather_smem(), st, cam_ptr, cm_list, J, qo,
            g_cam, nullptr, nullptr, nc, rhs);

@@ -326,16 +326,21 @@ extern "C" int bamg_schur_order_upper(bamg_ctx* ctx, int32_t* up_blk, int32_t* u
 
 // Diagonal blocks: warp per camera, S_ii = A_i - sum_o F_o^T (H_o E_o^T) F_o.
 // Records (F, E, H = pieces 0..14) are gathered 32 at a time into shared memory.
+// With RHS the same pass also forms the reduced right-hand side of the camera
+// (schur.py:122): rhs_i = -g_i - sum_o F_o^T q_o, q_o = E_o C^-1 b_p staged as piece
+// 15 -- the camera-major gather build_system would otherwise run on its own.
 #define SD_ST 31
 #ifndef SD_STAGES
 #define SD_STAGES 2
 #endif
+template <bool RHS>
 __global__ void __launch_bounds__(128)
 k_schur_diag(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, const double* __restrict__ J,
-             const double* __restrict__ A, const int* __restrict__ dpos, int nc, double* __restrict__ S) {
-  // SD_STAGES-deep cp.async pipeline of 32-record chunks (pieces 0..14: F, E, H)
+             const double* __restrict__ A, const int* __restrict__ dpos, int nc, const double* __restrict__ qo,
+             const double* __restrict__ g_cam, double* __restrict__ rhs, double* __restrict__ S) {
+  // SD_STAGES-deep cp.async pipeline of 32-record chunks (pieces 0..14: F, E, H; 15: q)
   extern __shared__ __align__(16) double sd_smem[];
-  constexpr int CH = 15 * 64;
+  constexpr int CH = (RHS ? 16 : 15) * 64;
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double* wbuf = sd_smem + (size_t)w * SD_STAGES * CH;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -344,13 +349,16 @@ k_schur_diag(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
     double acc[45];
 #pragma unroll
     for (int q = 0; q < 45; ++q) acc[q] = 0.0;
+    double racc[RHS ? 9 : 1];
+#pragma unroll
+    for (int q = 0; q < (RHS ? 9 : 1); ++q) racc[q] = 0.0;
     const int q0 = cam_ptr[i], q1 = cam_ptr[i + 1];
 #pragma unroll
     for (int s = 0; s < SD_STAGES - 1; ++s) {
       int cb = q0 + 32 * s;
       if (cb < q1) {
         bool v = cb + lane < q1;
-        rec_issue<15, 0, 0>(J, v ? cm_list[cb + lane] : 0, v, 0, 0, nullptr, wbuf + s * CH, lane);
+        rec_issue<15, 0, RHS ? 1 : 0>(J, v ? cm_list[cb + lane] : 0, v, 0, 0, qo, wbuf + s * CH, lane);
       } else {
         cp_async_commit();
       }
@@ -363,7 +371,7 @@ k_schur_diag(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
       int nb = base + 32 * (SD_STAGES - 1);
       if (nb < q1) {
         bool vn = nb + lane < q1;
-        rec_issue<15, 0, 0>(J, nidx, vn, 0, 0, nullptr,
+        rec_issue<15, 0, RHS ? 1 : 0>(J, nidx, vn, 0, 0, qo,
                             wbuf + ((c + SD_STAGES - 1) % SD_STAGES) * CH, lane);
       } else {
         cp_async_commit();
@@ -397,12 +405,24 @@ k_schur_diag(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
 #pragma unroll
           for (int l = j; l < 9; ++l) acc[t++] += a0 * f[l] + a1 * f[9 + l];
         }
+        if constexpr (RHS) {
+          double q0 = bsrc[15 * 64], q1 = bsrc[15 * 64 + 1];
+#pragma unroll
+          for (int j = 0; j < 9; ++j) racc[j] += f[j] * q0 + f[9 + j] * q1;
+        }
       }
       __syncwarp();
     }
     cp_async_wait<0>();
 #pragma unroll
     for (int q = 0; q < 45; ++q) acc[q] = warp_sum(acc[q]);
+    if constexpr (RHS) {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) racc[q] = warp_sum(racc[q]);
+      if (lane == 0)
+#pragma unroll
+        for (int j = 0; j < 9; ++j) rhs[(int64_t)i * 9 + j] = -g_cam[(int64_t)i * 9 + j] - racc[j];
+    }
     if (lane == 0) {
       double* out = S + (int64_t)dpos[i] * 81;
       const double* a = A + (int64_t)i * 81;
@@ -846,14 +866,26 @@ k_schur_rows(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, c
   }
 }
 
-static size_t schur_diag_smem() {
-  const size_t sm = sizeof(double) * 4 * SD_STAGES * 15 * 64;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_schur_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
+static size_t schur_diag_smem(bool with_rhs) {
+  const size_t sm = sizeof(double) * 4 * SD_STAGES * (with_rhs ? 16 : 15) * 64;
+  static bool attr[2] = {false, false};
+  if (!attr[with_rhs]) {
+    if (with_rhs) cudaFuncSetAttribute(k_schur_diag<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    else cudaFuncSetAttribute(k_schur_diag<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr[with_rhs] = true;
   }
   return sm;
+}
+
+static void schur_diag_launch(const int* cam_ptr, const int* cm_list, const double* J, const double* A,
+                              const int* dpos, int nc, const double* qo, const double* g_cam, double* rhs, double* S,
+                              cudaStream_t st) {
+  int g = grid_for((int64_t)nc * 32, 128, 8);
+  if (rhs)
+    launch(k_schur_diag<true>, g, 128, schur_diag_smem(true), st, cam_ptr, cm_list, J, A, dpos, nc, qo, g_cam, rhs, S);
+  else
+    launch(k_schur_diag<false>, g, 128, schur_diag_smem(false), st, cam_ptr, cm_list, J, A, dpos, nc, qo, g_cam, rhs,
+           S);
 }
 
 extern "C" int bamg_schur_numeric_rows(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
@@ -863,8 +895,7 @@ extern "C" int bamg_schur_numeric_rows(bamg_ctx* ctx, const int32_t* cam_ptr, co
                                        double* S, void* stream) {
   cudaStream_t st = as_stream(stream);
   if (nc <= 0) return 0;
-  launch(k_schur_diag, grid_for((int64_t)nc * 32, 128, 8), 128, schur_diag_smem(), st, cam_ptr, cm_list, J, A, dpos,
-         nc, S);
+  schur_diag_launch(cam_ptr, cm_list, J, A, dpos, nc, nullptr, nullptr, nullptr, S, st);
   const size_t budget = 200 * 1024;
   size_t fixed = sizeof(SrEntry) * SR_WARPS * SR_QCAP;
   int use_map = (nc <= 40000) ? 1 : 0;
@@ -889,12 +920,11 @@ extern "C" int bamg_schur_numeric_rows(bamg_ctx* ctx, const int32_t* cam_ptr, co
 extern "C" int bamg_schur_numeric(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const double* J,
                                   const double* A, const int32_t* dpos, int32_t nc, const int32_t* up_blk,
                                   const int32_t* up_tpos, int32_t n_up, const int32_t* blk_pair_ptr,
-                                  const int32_t* pair_a, const int32_t* pair_b, double* S, void* stream) {
+                                  const int32_t* pair_a, const int32_t* pair_b, const double* qo, const double* g_cam,
+                                  double* rhs, double* S, void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
-  if (nc)
-    launch(k_schur_diag, grid_for((int64_t)nc * 32, 128, 8), 128, schur_diag_smem(), st, cam_ptr, cm_list, J, A, dpos,
-           nc, S);
+  if (nc) schur_diag_launch(cam_ptr, cm_list, J, A, dpos, nc, qo, g_cam, rhs, S, st);
   if (n_up) {
     int64_t warps = ceil_div(n_up, OFF_GROUPS);
     static const int variant = [] {

@@ -38,7 +38,7 @@ def _schur_diagonal_blocks(sys: SchurSystem):
     dpos = torch.arange(nc, device=D.dev(), dtype=torch.int32)
     sys._own_H()
     D.call("bamg_schur_numeric", st.cam_ptr, st.cm_list, sys._jac._J, sys.A.blocks, dpos, nc,
-           None, None, 0, None, None, None, out)
+           None, None, 0, None, None, None, None, None, None, out)
     return out
 
 

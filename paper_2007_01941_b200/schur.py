@@ -51,7 +51,7 @@ class SchurSystem:
     def __init__(self, A, C, rhs_cam, grad_pt, jac, Cb, mode="implicit"):
         self.A = A
         self.C = C
-        self.rhs_cam = rhs_cam
+        self._rhs = rhs_cam  # None: formed on first use, or by the explicit assembly's diagonal pass
         self.grad_pt = grad_pt
         self.mode = mode
         self.S_explicit = None
@@ -59,6 +59,25 @@ class SchurSystem:
         self._Cb = Cb
         self._W = None
         self._qo = None
+
+    @property
+    def rhs_cam(self):
+        """Reduced right-hand side b_c - W C^-1 b_p (schur.py:122). build_system defers
+        it: the explicit assembly forms it in its camera-major diagonal pass (one
+        sweep over the records instead of two); otherwise the standalone gather runs
+        at first use."""
+        if self._rhs is None:
+            st = self._jac._st
+            self._own_H()
+            rhs = D.empty(self.n_cameras * CAMERA_SIZE)
+            _, gc, _, _ = self._jac.normal_blocks()
+            D.call("bamg_rhs_gather", st.cam_ptr, st.cm_list, self._jac._J, self._qo, gc, self.n_cameras, rhs)
+            self._rhs = rhs
+        return self._rhs
+
+    @rhs_cam.setter
+    def rhs_cam(self, value):
+        self._rhs = value
 
     @property
     def n_cameras(self) -> int:
@@ -125,17 +144,16 @@ def build_system(jac: JacobianBlocks, damping: Damping) -> SchurSystem:
     Cinv = D.empty(npt, 3, 3)
     Cb = D.empty(npt, 3)
     qo = D.empty(max(st.k, 1), 2)
-    rhs = D.empty(nc * CAMERA_SIZE)
     bad = D.empty(1, dtype=torch.int32)
     D.call("bamg_build_system", st.cam_ptr, st.cm_list, st.obs_pt_pm, jac._J, st.k, A_raw, C_raw, gc, gp,
-           damping.cam_diag, damping.pt_diag, nc, npt, A, C, Cinv, Cb, qo, rhs, bad)
+           damping.cam_diag, damping.pt_diag, nc, npt, A, C, Cinv, Cb, qo, None, bad)
     b = int(bad.item())
     if b != 0x7FFFFFFF:
         raise IndefiniteBlockError(b)
     grad_pt = D.empty(npt * POINT_SIZE)
     D.call("bamg_negate", gp, grad_pt, npt * POINT_SIZE)
     Cm = BlockDiagMatrix(C, _inv=Cinv)
-    s = SchurSystem(BlockDiagMatrix(A), Cm, rhs, grad_pt, jac, Cb)
+    s = SchurSystem(BlockDiagMatrix(A), Cm, None, grad_pt, jac, Cb)
     s._qo = qo
     jac._h_owner = weakref.ref(s)  # weak: no jac <-> system reference cycle
     return s
@@ -159,9 +177,15 @@ def schur_explicit(sys: SchurSystem, variant: str = "pairs") -> BlockSparseMatri
                sys.A.blocks, S_ptr, S_col, sym["dpos"], sym["up_off"], sym["up_tpos"], sys.n_cameras, blocks)
     else:
         sym = st.pair_lists
+        rhs = None
+        if sys._rhs is None:  # the diagonal pass forms the right-hand side in the same sweep
+            rhs = D.empty(sys.n_cameras * CAMERA_SIZE)
+        _, gc, _, _ = J.normal_blocks()
         D.call("bamg_schur_numeric", st.cam_ptr, st.cm_list, J._J, sys.A.blocks, sym["dpos"],
                sys.n_cameras, sym["up_blk"], sym["up_tpos"], sym["n_up"], sym["blk_ptr"], sym["pair_a"],
-               sym["pair_b"], blocks)
+               sym["pair_b"], sys._qo, gc, rhs, blocks)
+        if rhs is not None:
+            sys._rhs = rhs
     S = BlockSparseMatrix(sys.n_cameras, sys.n_cameras, CAMERA_SIZE, CAMERA_SIZE, S_ptr, S_col, blocks,
                           _validate=False)
     if _SYMMETRIC:
