@@ -145,6 +145,26 @@ int bamg_schur_numeric(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_
                        int32_t n_up, const int32_t* blk_pair_ptr, const int32_t* pair_a, const int32_t* pair_b,
                        const double* qo, const double* g_cam, double* rhs, double* S, void* stream);
 
+/* point-chunk phased assembly (same sums as bamg_schur_numeric, chunk-then-point order):
+ * chunk_pairs sorts the point pairs by (chunk, S block) -- chunks of consecutive points in
+ * (first camera, point) order holding ~chunk_records observations each -- into pair_a /
+ * pair_b / sorted_key (n_pairs each); out_host = [n_segments, n_chunks, blk_bits,
+ * chunk_records used]. chunk_work builds the work list (int4 per item, capacity
+ * n_segments + 10 n_chunks); out_host[0] = items. numeric_chunked runs the diagonal pass
+ * and the work list; done = nnz scratch words. */
+int bamg_schur_chunk_pairs(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs_cam_pm, const int32_t* S_ptr,
+                           const int32_t* S_col, int32_t nc, int32_t npt, int64_t nnz, int64_t k,
+                           const int32_t* pair_off, int64_t n_pairs, int64_t chunk_records, int32_t* pair_a,
+                           int32_t* pair_b, uint32_t* sorted_key, int64_t* out_host, void* stream);
+int bamg_schur_chunk_work(bamg_ctx* ctx, const int32_t* S_ptr, const int32_t* S_col, int32_t nc,
+                          const uint32_t* sorted_key, int64_t n_pairs, int32_t n_seg, int32_t n_chunks,
+                          int32_t blk_bits, int32_t group_rows, int32_t* work, int64_t work_cap, int64_t* out_host,
+                          void* stream);
+int bamg_schur_numeric_chunked(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const double* J,
+                               const double* A, const int32_t* dpos, int32_t nc, const int32_t* work, int32_t n_work,
+                               const int32_t* pair_a, const int32_t* pair_b, uint32_t* done, int64_t nnz,
+                               const double* qo, const double* g_cam, double* rhs, double* S, void* stream);
+
 /* ---- BSR kernels: blockmat.py:295-299 (matvec), 91-129 (block-diagonal), 270-282 ---- */
 int bamg_bsr_spmv(bamg_ctx* ctx, int32_t bs, const int32_t* ptr, const int32_t* col, const double* blocks,
                   const double* x, double* y, int32_t nbr, double* dot_out_dev, void* stream);

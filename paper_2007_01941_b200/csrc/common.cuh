@@ -262,4 +262,3 @@ __device__ __forceinline__ void rec_issue(const double* __restrict__ J, int o_la
   }
   cp_async_commit();
 }
-

@@ -11,6 +11,8 @@
 // columns of the 9x9 block in registers) -- no atomics, fixed summation order, so
 // S is bit-reproducible run to run. S_ji is written as S_ij^T (exactly symmetric,
 // matching the reference's 0.5 (S + S^T) to roundoff).
+#include <algorithm>
+
 #include "common.cuh"
 #include "ctx.h"
 
@@ -948,3 +950,546 @@ extern "C" int bamg_schur_numeric(bamg_ctx* ctx, const int32_t* cam_ptr, const i
   BAMG_LAUNCH_CHECK();
   return 0;
 }
+
+// ===========================================================================
+// Point-chunk phased assembly (schur.py:128-144, same sums in another order).
+//
+// The block-owned pair lists above read both records of every point pair: 90.5 M
+// pairs x ~450 B at config 4, with no reuse in L2 (a record's ~6 uses are spread
+// over the whole run: ncu read 46 GB for 7.5 GB of records). Here the points are
+// cut into chunks of consecutive points in (first camera, point) order, each chunk
+// holding about `chunk_records` observations (a few tens of MB of records), and the
+// pairs are sorted by (chunk, S block). A work item is one (chunk, block) segment;
+// items run in chunk order, so while a chunk is in flight its records stay in L2
+// and every record comes from DRAM about once. A block's running sum travels
+// through its own S slot: the first segment stores the partial, later segments
+// (later chunks) wait on the block's completion counter, load the partial and add
+// theirs, the last one writes -S_ij and its transpose. Every block is summed in one
+// fixed order (chunk, then point) by one lane group at a time: deterministic, no
+// floating-point atomics.
+
+__global__ void k_point_firstcam(const int* __restrict__ pt_ptr, const int* __restrict__ ocam, int npt, int nc,
+                                 uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npt; p += gridDim.x * blockDim.x) {
+    int s = pt_ptr[p], e = pt_ptr[p + 1];
+    key[p] = (e - s >= 2) ? (uint32_t)ocam[s] : (uint32_t)nc;  // points without pairs last
+    val[p] = (uint32_t)p;
+  }
+}
+
+__global__ void k_chunk_counts(const uint32_t* __restrict__ order, const int* __restrict__ pt_ptr, int npt,
+                               int* __restrict__ cnt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npt; i += gridDim.x * blockDim.x) {
+    int p = (int)order[i];
+    int m = pt_ptr[p + 1] - pt_ptr[p];
+    cnt[i] = m >= 2 ? m : 0;
+  }
+}
+
+// chunk c (in first-camera order) runs at position (c mod K) * ceil(n / K) + c / K:
+// consecutive chunks in the run are K apart in camera order, so they rarely share an
+// S block and a segment seldom waits for the previous chunk's segment of its block
+__global__ void k_chunk_assign(const uint32_t* __restrict__ order, const int* __restrict__ cum, int npt,
+                               int64_t chunk_records, int n_chunks, int stride, int* __restrict__ ch) {
+  int per = (n_chunks + stride - 1) / stride;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npt; i += gridDim.x * blockDim.x) {
+    int c = (int)((int64_t)cum[i] / chunk_records);
+    ch[order[i]] = (c % stride) * per + c / stride;
+  }
+}
+
+// pairs of point p keyed (chunk(p) << blk_bits) | S position; value packed a << 7 | (b - a)
+// (PACKED) or the pair's emission index (payload for a gather)
+template <bool PACKED>
+__global__ void k_pair_emit_chunk(const int* __restrict__ pt_ptr, const int* __restrict__ ocam,
+                                  const int* __restrict__ S_ptr, const int* __restrict__ S_col,
+                                  const int* __restrict__ off, const int* __restrict__ ch, int npt, int blk_bits,
+                                  uint32_t* __restrict__ key, uint32_t* __restrict__ val, int* __restrict__ oa,
+                                  int* __restrict__ ob) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npt; p += gridDim.x * blockDim.x) {
+    int s = pt_ptr[p], e = pt_ptr[p + 1];
+    int pos = off[p];
+    uint32_t hi = (uint32_t)ch[p] << blk_bits;
+    for (int a = s; a < e; ++a) {
+      int ca = ocam[a];
+      const int* cols = S_col + S_ptr[ca];
+      int n = S_ptr[ca + 1] - S_ptr[ca];
+      for (int b = a + 1; b < e; ++b) {
+        int q = lower_bound_i32(cols, n, ocam[b]);
+        key[pos] = hi | (uint32_t)(S_ptr[ca] + q);
+        if (PACKED) {
+          val[pos] = ((uint32_t)a << 7) | (uint32_t)(b - a);
+        } else {
+          val[pos] = (uint32_t)pos;
+          oa[pos] = a;
+          ob[pos] = b;
+        }
+        ++pos;
+      }
+    }
+  }
+}
+
+__global__ void k_seg_heads(const uint32_t* __restrict__ key, int64_t n, int* __restrict__ head) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    head[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
+}
+
+// heads -> segment starts / keys (sid = exclusive scan of the head flags)
+__global__ void k_seg_fill(const uint32_t* __restrict__ key, const int* __restrict__ sid, int64_t n,
+                           int* __restrict__ seg_start, uint32_t* __restrict__ seg_key) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == 0 || key[i] != key[i - 1]) {
+      seg_start[sid[i]] = (int)i;
+      seg_key[sid[i]] = key[i];
+    }
+  }
+}
+
+// per segment: block position (sort key of the ordinal pass), row, transposed position
+__global__ void k_seg_info(const uint32_t* __restrict__ seg_key, int nseg, int blk_bits,
+                           const int* __restrict__ S_ptr, const int* __restrict__ S_col, int nc,
+                           uint32_t* __restrict__ blk_key, uint32_t* __restrict__ iota, int* __restrict__ row,
+                           int* __restrict__ tpos) {
+  uint32_t mask = (blk_bits >= 32) ? 0xFFFFFFFFu : ((1u << blk_bits) - 1u);
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += gridDim.x * blockDim.x) {
+    int q = (int)(seg_key[s] & mask);
+    // row i: last row with S_ptr[i] <= q
+    int lo = 0, hi = nc;
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (S_ptr[mid] <= q) lo = mid; else hi = mid;
+    }
+    int i = lo, j = S_col[q];
+    row[s] = i;
+    tpos[s] = S_ptr[j] + lower_bound_i32(S_col + S_ptr[j], S_ptr[j + 1] - S_ptr[j], i);
+    blk_key[s] = (uint32_t)q;
+    iota[s] = (uint32_t)s;
+  }
+}
+
+// segments sorted by block (stable: chunk order inside a block) -> ordinal and last flag
+__global__ void k_seg_ordinal(const uint32_t* __restrict__ bkey, const uint32_t* __restrict__ bseg, int nseg,
+                              int* __restrict__ ord2) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nseg; i += gridDim.x * blockDim.x) {
+    uint32_t b = bkey[i];
+    int d = 0;
+    while (i - d - 1 >= 0 && bkey[i - d - 1] == b) ++d;
+    bool last = (i + 1 >= nseg) || bkey[i + 1] != b;
+    ord2[bseg[i]] = d * 2 + (last ? 1 : 0);
+  }
+}
+
+// work order keys: pass 1 longest first (8 bits), pass 2 (chunk, row) stable
+__global__ void k_seg_lenkey(const int* __restrict__ seg_start, int nseg, int64_t n_pairs, uint32_t* __restrict__ key,
+                             uint32_t* __restrict__ iota) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += gridDim.x * blockDim.x) {
+    int64_t e = (s + 1 < nseg) ? seg_start[s + 1] : n_pairs;
+    int len = (int)(e - seg_start[s]);
+    key[s] = 255u - (uint32_t)min(len, 255);
+    iota[s] = (uint32_t)s;
+  }
+}
+
+__global__ void k_seg_rowkey(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ seg_key, int nseg,
+                             int blk_bits, const int* __restrict__ row, int row_bits, uint32_t* __restrict__ key,
+                             int* __restrict__ chunk_of) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nseg; i += gridDim.x * blockDim.x) {
+    int s = (int)perm[i];
+    uint32_t c = blk_bits >= 32 ? 0u : (seg_key[s] >> blk_bits);
+    key[i] = row_bits > 0 ? ((c << row_bits) | (uint32_t)row[s]) : c;
+    chunk_of[i] = (int)c;
+  }
+}
+
+// per chunk: padded segment count (multiple of OFF_GROUPS, so no warp batch spans two
+// chunks: a block then never appears twice in one batch)
+__global__ void k_chunk_pad(const int* __restrict__ cptr, int nch, int* __restrict__ padded) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nch; c += gridDim.x * blockDim.x) {
+    int n = cptr[c + 1] - cptr[c];
+    padded[c] = (n + OFF_GROUPS - 1) / OFF_GROUPS * OFF_GROUPS;
+  }
+}
+
+__global__ void k_work_fill(const uint32_t* __restrict__ perm, const int* __restrict__ chunk_of, int nseg,
+                            const int* __restrict__ cptr, const int* __restrict__ wpos, const int* __restrict__ seg_start,
+                            const uint32_t* __restrict__ seg_key, const int* __restrict__ tpos,
+                            const int* __restrict__ ord2, int64_t n_pairs, int blk_bits, int4* __restrict__ work,
+                            int* __restrict__ bad) {
+  uint32_t mask = (blk_bits >= 32) ? 0xFFFFFFFFu : ((1u << blk_bits) - 1u);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nseg; i += gridDim.x * blockDim.x) {
+    int s = (int)perm[i];
+    int c = chunk_of[i];
+    int pos = wpos[c] + (i - cptr[c]);
+    int64_t e = (s + 1 < nseg) ? seg_start[s + 1] : n_pairs;
+    int len = (int)(e - seg_start[s]);
+    int o2 = ord2[s];
+    if (len >= (1 << 21) || (o2 >> 1) >= (1 << 9)) atomicExch(bad, 1);
+    work[pos] = make_int4(seg_start[s], (int)(seg_key[s] & mask), tpos[s],
+                          len | ((o2 >> 1) << 21) | ((o2 & 1) << 30));
+  }
+}
+
+__global__ void k_work_pad_init(int4* __restrict__ work, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    work[i] = make_int4(0, -1, 0, 0);
+}
+
+static int bits_of(int64_t n) {
+  int b = 1;
+  while ((1ll << b) < n) ++b;
+  return b;
+}
+
+extern "C" int bamg_schur_chunk_pairs(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs_cam_pm,
+                                      const int32_t* S_ptr, const int32_t* S_col, int32_t nc, int32_t npt,
+                                      int64_t nnz, int64_t k, const int32_t* pair_off, int64_t n_pairs,
+                                      int64_t chunk_records, int32_t* pair_a, int32_t* pair_b, uint32_t* sorted_key,
+                                      int64_t* out_host, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  const int blk_bits = bits_of(nnz + 1);
+  if (blk_bits > 30) {
+    bamg_set_error("schur chunks: %lld S blocks exceed the 30-bit key", (long long)nnz);
+    return BAMG_ERR_UNSUPPORTED;
+  }
+  const int64_t max_chunks = 1ll << (32 - blk_bits);
+  if (chunk_records < 1) chunk_records = 1;
+  if (ceil_div(k, chunk_records) + 64 > max_chunks) chunk_records = ceil_div(k, max_chunks - 64);
+  out_host[0] = 0;
+  out_host[1] = ceil_div(k > 0 ? k : 1, chunk_records);
+  out_host[2] = blk_bits;
+  out_host[3] = chunk_records;
+  if (n_pairs == 0 || npt == 0) return 0;
+  // 1. chunk of every point: consecutive points in (first camera, point) order
+  uint32_t *pk = nullptr, *pv = nullptr, *spk = nullptr, *spv = nullptr;
+  int *cum = nullptr, *ch = nullptr, *mx = nullptr;
+  BAMG_CUDA_CHECK(cudaMallocAsync(&pk, 4 * (size_t)npt, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&pv, 4 * (size_t)npt, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&spk, 4 * (size_t)npt, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&spv, 4 * (size_t)npt, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&cum, 4 * (size_t)npt + 4, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&ch, 4 * (size_t)npt, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&mx, 8, st));
+  launch(k_point_firstcam, grid_for(npt, 256), 256, 0, st, pt_ptr, obs_cam_pm, npt, nc, pk, pv);
+  int rc = radix_sort_pairs(pk, pv, spk, spv, npt, bits_of((int64_t)nc + 1), st);
+  if (rc) return rc;
+  launch(k_chunk_counts, grid_for(npt, 256), 256, 0, st, spv, pt_ptr, npt, cum);
+  rc = scan_exclusive_int(cum, cum, npt, nullptr, st);
+  if (rc) return rc;
+  {
+    int stride = 8;
+    if (const char* e = getenv("BAMG_SCHUR_CHUNK_STRIDE")) stride = atoi(e) > 0 ? atoi(e) : 1;
+    int nch = (int)ceil_div(k > 0 ? k : 1, chunk_records);
+    if (stride > nch) stride = nch;
+    // positions run up to stride * ceil(nch / stride) - 1
+    out_host[1] = (int64_t)stride * ceil_div(nch, stride);
+    launch(k_chunk_assign, grid_for(npt, 256), 256, 0, st, spv, cum, npt, chunk_records, nch, stride, ch);
+  }
+  // 2. pairs keyed (chunk, block), sorted (stable: point order inside a segment)
+  int h[2] = {0, 0};
+  BAMG_CUDA_CHECK(cudaMemsetAsync(mx, 0, 8, st));
+  launch(k_max_segment, grid_for(npt, 256), 256, 0, st, pt_ptr, npt, mx);
+  BAMG_CUDA_CHECK(cudaMemcpyAsync(h, mx, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+  const bool packed = k < (1ll << 25) && h[0] <= 128;
+  uint32_t *key = nullptr, *val = nullptr, *sval = nullptr;
+  int *oa = nullptr, *ob = nullptr;
+  BAMG_CUDA_CHECK(cudaMallocAsync(&key, 4 * n_pairs, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&val, 4 * n_pairs, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&sval, 4 * n_pairs, st));
+  if (packed) {
+    launch(k_pair_emit_chunk<true>, grid_for(npt, 128), 128, 0, st, pt_ptr, obs_cam_pm, S_ptr, S_col, pair_off, ch,
+           npt, blk_bits, key, val, (int*)nullptr, (int*)nullptr);
+  } else {
+    BAMG_CUDA_CHECK(cudaMallocAsync(&oa, 4 * n_pairs, st));
+    BAMG_CUDA_CHECK(cudaMallocAsync(&ob, 4 * n_pairs, st));
+    launch(k_pair_emit_chunk<false>, grid_for(npt, 128), 128, 0, st, pt_ptr, obs_cam_pm, S_ptr, S_col, pair_off, ch,
+           npt, blk_bits, key, val, oa, ob);
+  }
+  BAMG_LAUNCH_CHECK();
+  rc = radix_sort_pairs(key, val, sorted_key, sval, n_pairs, 32, st);
+  if (rc) return rc;
+  if (packed) {
+    launch(k_unpack_pairs, grid_for(n_pairs, 256), 256, 0, st, (const uint32_t*)sval, n_pairs, pair_a, pair_b);
+  } else {
+    launch(k_gather_pairs, grid_for(n_pairs, 256), 256, 0, st, sval, oa, ob, n_pairs, pair_a, pair_b);
+    cudaFreeAsync(oa, st);
+    cudaFreeAsync(ob, st);
+  }
+  // 3. segment count
+  int* head = (int*)val;  // reuse: n_pairs ints
+  launch(k_seg_heads, grid_for(n_pairs, 256), 256, 0, st, sorted_key, n_pairs, head);
+  int* tot = mx;
+  rc = scan_exclusive_int(head, head, n_pairs, tot, st);
+  if (rc) return rc;
+  BAMG_CUDA_CHECK(cudaMemcpyAsync(h, tot, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+  BAMG_LAUNCH_CHECK();
+  out_host[0] = h[0];
+  for (void* p : {(void*)pk, (void*)pv, (void*)spk, (void*)spv, (void*)cum, (void*)ch, (void*)mx, (void*)key,
+                  (void*)val, (void*)sval})
+    cudaFreeAsync(p, st);
+  return 0;
+}
+
+extern "C" int bamg_schur_chunk_work(bamg_ctx* ctx, const int32_t* S_ptr, const int32_t* S_col, int32_t nc,
+                                     const uint32_t* sorted_key, int64_t n_pairs, int32_t n_seg, int32_t n_chunks,
+                                     int32_t blk_bits, int32_t group_rows, int32_t* work, int64_t work_cap,
+                                     int64_t* out_host, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  out_host[0] = 0;
+  if (n_seg <= 0) return 0;
+  int *sid = nullptr, *seg_start = nullptr, *row = nullptr, *tpos = nullptr, *ord2 = nullptr, *chunk_of = nullptr;
+  int *cptr = nullptr, *padded = nullptr, *bad = nullptr;
+  uint32_t *seg_key = nullptr, *k1 = nullptr, *v1 = nullptr, *k2 = nullptr, *v2 = nullptr;
+  BAMG_CUDA_CHECK(cudaMallocAsync(&sid, 4 * n_pairs, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&seg_start, 4 * (size_t)n_seg, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&seg_key, 4 * (size_t)n_seg, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&row, 4 * (size_t)n_seg, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&tpos, 4 * (size_t)n_seg, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&ord2, 4 * (size_t)n_seg, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&chunk_of, 4 * (size_t)n_seg, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&k1, 4 * (size_t)n_seg, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&v1, 4 * (size_t)n_seg, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&k2, 4 * (size_t)n_seg, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&v2, 4 * (size_t)n_seg, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&cptr, 4 * ((size_t)n_chunks + 1), st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&padded, 4 * ((size_t)n_chunks + 1), st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&bad, 8, st));
+  BAMG_CUDA_CHECK(cudaMemsetAsync(bad, 0, 8, st));
+  launch(k_seg_heads, grid_for(n_pairs, 256), 256, 0, st, sorted_key, n_pairs, sid);
+  int rc = scan_exclusive_int(sid, sid, n_pairs, nullptr, st);
+  if (rc) return rc;
+  launch(k_seg_fill, grid_for(n_pairs, 256), 256, 0, st, sorted_key, sid, n_pairs, seg_start, seg_key);
+  // ordinals: segments of a block in chunk order
+  launch(k_seg_info, grid_for(n_seg, 256), 256, 0, st, seg_key, n_seg, blk_bits, S_ptr, S_col, nc, k1, v1, row, tpos);
+  rc = radix_sort_pairs(k1, v1, k2, v2, n_seg, blk_bits, st);
+  if (rc) return rc;
+  launch(k_seg_ordinal, grid_for(n_seg, 256), 256, 0, st, k2, v2, n_seg, ord2);
+  // work order: (chunk, row) with the longest segments first inside a row
+  launch(k_seg_lenkey, grid_for(n_seg, 256), 256, 0, st, seg_start, n_seg, n_pairs, k1, v1);
+  rc = radix_sort_pairs(k1, v1, k2, v2, n_seg, 8, st);
+  if (rc) return rc;
+  const int chunk_bits = bits_of((int64_t)n_chunks + 1);
+  int row_bits = group_rows ? bits_of((int64_t)nc + 1) : 0;
+  if (chunk_bits + row_bits > 32) row_bits = 0;
+  launch(k_seg_rowkey, grid_for(n_seg, 256), 256, 0, st, v2, seg_key, n_seg, blk_bits, row, row_bits, k1, chunk_of);
+  rc = radix_sort_pairs(k1, v2, k2, v1, n_seg, chunk_bits + row_bits, st);  // v1 = final order
+  if (rc) return rc;
+  launch(k_seg_rowkey, grid_for(n_seg, 256), 256, 0, st, v1, seg_key, n_seg, blk_bits, row, 0, k1, chunk_of);
+  rc = segment_ptr(chunk_of, n_seg, n_chunks, cptr, st);
+  if (rc) return rc;
+  launch(k_chunk_pad, grid_for(n_chunks, 256), 256, 0, st, cptr, n_chunks, padded);
+  int* tot = bad + 1;
+  rc = scan_exclusive_int(padded, padded, n_chunks, tot, st);
+  if (rc) return rc;
+  int h[2] = {0, 0};
+  BAMG_CUDA_CHECK(cudaMemcpyAsync(h, bad, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (h[1] > work_cap) {
+    bamg_set_error("schur chunks: work list %d exceeds capacity %lld", h[1], (long long)work_cap);
+    return BAMG_ERR_UNSUPPORTED;
+  }
+  int4* w4 = reinterpret_cast<int4*>(work);
+  launch(k_work_pad_init, grid_for(h[1], 256), 256, 0, st, w4, (int64_t)h[1]);
+  launch(k_work_fill, grid_for(n_seg, 256), 256, 0, st, v1, chunk_of, n_seg, cptr, padded, seg_start, seg_key, tpos,
+         ord2, n_pairs, blk_bits, w4, bad);
+  BAMG_CUDA_CHECK(cudaMemcpyAsync(h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
+  BAMG_LAUNCH_CHECK();
+  for (void* p : {(void*)sid, (void*)seg_start, (void*)seg_key, (void*)row, (void*)tpos, (void*)ord2,
+                  (void*)chunk_of, (void*)k1, (void*)v1, (void*)k2, (void*)v2, (void*)cptr, (void*)padded,
+                  (void*)bad})
+    cudaFreeAsync(p, st);
+  if (h[0]) {
+    bamg_set_error("schur chunks: a segment exceeds 2^21 pairs or a block 512 chunks");
+    return BAMG_ERR_UNSUPPORTED;
+  }
+  out_host[0] = h[1];
+  return 0;
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Work item (int4): x = first pair, y = S position of the upper block (-1: padding),
+// z = transposed position, w = length | ordinal << 21 | last << 30. Warps take
+// batches of OFF_GROUPS items from a global counter (dispensed in work order, so a
+// segment only ever waits on segments owned by running warps: no deadlock).
+// Measured at c4 (profiles/r2/schur_experiments.md): DRAM read 46 -> 14.4 GB, but
+// 8.6 ms against the block-owned kernel's 7.6 ms -- 4.5 M short segments (20 pairs
+// on average) pay the per-batch latency chain four times as often.
+__global__ void __launch_bounds__(128)
+k_schur_chunked(const int4* __restrict__ work, int n_work, const int* __restrict__ pair_a,
+                const int* __restrict__ pair_b, const double* __restrict__ J, unsigned* __restrict__ done,
+                unsigned* __restrict__ next_batch, double* __restrict__ S) {
+  extern __shared__ __align__(16) double smem_offp[];
+  int lane = threadIdx.x & 31;
+  double* wsm = smem_offp + (threadIdx.x >> 5) * OFFP_WARP_DOUBLES;
+  int grp = lane / 3, c3 = lane - 3 * grp;
+  int c0 = 3 * c3;
+  const int fb_lo = (RF + c0) >> 1, fb_hi = (RF + 9 + c0) >> 1;
+  const bool lo_odd = (RF + c0) & 1;
+  const int ig = lane >> 1;
+  const int* ilist = (lane & 1) ? pair_b : pair_a;
+  const int n_batches = (n_work + OFF_GROUPS - 1) / OFF_GROUPS;
+  for (;;) {
+    int bt = 0;
+    if (lane == 0) bt = (int)atomicAdd(next_batch, 1u);
+    bt = __shfl_sync(FULL_MASK, bt, 0);
+    if (bt >= n_batches) break;
+    int u = bt * OFF_GROUPS + grp;
+    int4 wi = make_int4(0, -1, 0, 0);
+    if (grp < OFF_GROUPS && u < n_work) wi = work[u];
+    bool active = wi.y >= 0;
+    int q0 = wi.x, blk = wi.y;
+    int len = active ? (wi.w & ((1 << 21) - 1)) : 0;
+    unsigned ord = (unsigned)(wi.w >> 21) & 511u;
+    bool last = (wi.w >> 30) & 1;
+    int maxlen = len;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(FULL_MASK, maxlen, o));
+    int src = 3 * ig < 31 ? 3 * ig : 31;
+    int iq0 = __shfl_sync(FULL_MASK, q0, src);
+    int ilen = __shfl_sync(FULL_MASK, len, src);
+    if (lane >= 2 * OFF_GROUPS) ilen = 0;
+    int nrec = (ilen > 0) ? ilist[iq0] : -1;
+#pragma unroll
+    for (int t = 0; t < OFFP_STAGES - 1; ++t) {
+      int rec = nrec;
+      nrec = (t + 1 < ilen) ? ilist[iq0 + t + 1] : -1;
+      if (t < maxlen) offp_issue(wsm + t * OFFP_STAGE_DOUBLES, J, rec, lane);
+      else cp_async_commit();
+    }
+    // the block's running sum from the previous chunk (records are already in flight)
+    double acc[27];
+    if (active && ord > 0) {
+      while (ld_acquire_u32(done + blk) < ord) __nanosleep(64);
+      const double* sp = S + (int64_t)blk * 81 + c0;
+#pragma unroll
+      for (int r = 0; r < 9; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[r * 3 + c] = __ldcg(sp + r * 9 + c);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 27; ++q) acc[q] = 0.0;
+    }
+    __syncwarp();
+    for (int s = 0; s < maxlen; ++s) {
+      int t = s + OFFP_STAGES - 1;
+      int rec = nrec;
+      nrec = (t + 1 < ilen) ? ilist[iq0 + t + 1] : -1;
+      if (t < maxlen) offp_issue(wsm + (t % OFFP_STAGES) * OFFP_STAGE_DOUBLES, J, rec, lane);
+      else cp_async_commit();
+      cp_async_wait<OFFP_STAGES - 1>();
+      __syncwarp();
+      if (s < len) {
+        const double* stg = wsm + (s % OFFP_STAGES) * OFFP_STAGE_DOUBLES;
+        const double2* ra = reinterpret_cast<const double2*>(stg + grp * OFFP_RS);
+        const double2* rb = reinterpret_cast<const double2*>(stg + (OFF_GROUPS + grp) * OFFP_RS);
+        double fa[18], ha[6], eb[6];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+          double2 v = ra[RF / 2 + k];
+          fa[2 * k] = v.x;
+          fa[2 * k + 1] = v.y;
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          double2 v = ra[RH / 2 + k], w = rb[RE / 2 + k];
+          ha[2 * k] = v.x;
+          ha[2 * k + 1] = v.y;
+          eb[2 * k] = w.x;
+          eb[2 * k + 1] = w.y;
+        }
+        double2 p0 = rb[fb_lo], p1 = rb[fb_lo + 1];
+        double2 s0 = rb[fb_hi], s1 = rb[fb_hi + 1];
+        double b0[3], b1[3];
+        b0[0] = lo_odd ? p0.y : p0.x;
+        b0[1] = lo_odd ? p1.x : p0.y;
+        b0[2] = lo_odd ? p1.y : p1.x;
+        b1[0] = lo_odd ? s0.x : s0.y;
+        b1[1] = lo_odd ? s0.y : s1.x;
+        b1[2] = lo_odd ? s1.x : s1.y;
+        double g00 = ha[0] * eb[0] + ha[1] * eb[1] + ha[2] * eb[2];
+        double g01 = ha[0] * eb[3] + ha[1] * eb[4] + ha[2] * eb[5];
+        double g10 = ha[3] * eb[0] + ha[4] * eb[1] + ha[5] * eb[2];
+        double g11 = ha[3] * eb[3] + ha[4] * eb[4] + ha[5] * eb[5];
+        double z0[3], z1[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          z0[c] = g00 * b0[c] + g01 * b1[c];
+          z1[c] = g10 * b0[c] + g11 * b1[c];
+        }
+#pragma unroll
+        for (int r = 0; r < 9; ++r) {
+          double fr0 = fa[r], fr1 = fa[9 + r];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) acc[r * 3 + c] += fr0 * z0[c] + fr1 * z1[c];
+        }
+      }
+      __syncwarp();
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+    if (active) {
+      double* sij = S + (int64_t)blk * 81;
+      if (last) {
+        double* sji = S + (int64_t)wi.z * 81;
+#pragma unroll
+        for (int r = 0; r < 9; ++r)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            double v = -acc[r * 3 + c];
+            sij[r * 9 + c0 + c] = v;
+            sji[(c0 + c) * 9 + r] = v;
+          }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 9; ++r)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) __stcg(sij + r * 9 + c0 + c, acc[r * 3 + c]);
+      }
+    }
+    if (active && !last) __threadfence();
+    __syncwarp();
+    if (active && !last && c3 == 0) st_release_u32(done + blk, ord + 1);
+  }
+}
+
+extern "C" int bamg_schur_numeric_chunked(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
+                                          const double* J, const double* A, const int32_t* dpos, int32_t nc,
+                                          const int32_t* work, int32_t n_work, const int32_t* pair_a,
+                                          const int32_t* pair_b, uint32_t* done, int64_t nnz, const double* qo,
+                                          const double* g_cam, double* rhs, double* S, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (nc) schur_diag_launch(cam_ptr, cm_list, J, A, dpos, nc, qo, g_cam, rhs, S, st);
+  if (n_work > 0) {
+    BAMG_CUDA_CHECK(cudaMemsetAsync(done, 0, sizeof(uint32_t) * (size_t)nnz, st));
+    unsigned* ctr = ctx->counters + BAMG_CTR_MISC;
+    BAMG_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(unsigned), st));
+    const size_t sm = 4 * OFFP_WARP_DOUBLES * sizeof(double);
+    static int grid = 0;
+    if (!grid) {
+      BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_schur_chunked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      int per_sm = 0;
+      BAMG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_schur_chunked, 128, sm));
+      grid = bamg_num_sms() * (per_sm > 0 ? per_sm : 1);
+    }
+    int64_t batches = ceil_div(n_work, OFF_GROUPS);
+    int g = (int)std::min<int64_t>(grid, ceil_div(batches, 4));
+    launch(k_schur_chunked, g, 128, sm, st, reinterpret_cast<const int4*>(work), n_work, pair_a, pair_b, J,
+           done, ctr, S);
+  }
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+

@@ -189,6 +189,36 @@ class ObsStructure:
         return self._symop
 
     @property
+    def chunk_plan(self):
+        """Point-chunk phased pair lists (schur.cu, bamg_schur_chunk_*): pairs sorted by
+        (chunk, S block), one work item per (chunk, block) segment."""
+        if getattr(self, "_chunks", None) is None:
+            S_ptr, S_col, nnz, _ = self.covis
+            sym = getattr(self, "_pairs", None) or self.symbolic
+            pair_off = D.empty(max(self.npt, 1), dtype=torch.int32)
+            dpos = D.empty(max(self.nc, 1), dtype=torch.int32)
+            up_off = D.empty(max(self.nc, 1), dtype=torch.int32)
+            sizes = np.zeros(4, dtype=np.int64)
+            D.call("bamg_schur_symbolic_sizes", self.pt_ptr, S_ptr, S_col, self.nc, self.npt,
+                   pair_off, dpos, up_off, sizes.ctypes.data)
+            n_pairs = int(sizes[0])
+            pair_a = D.empty(max(n_pairs, 1), dtype=torch.int32)
+            pair_b = D.empty(max(n_pairs, 1), dtype=torch.int32)
+            skey = D.empty(max(n_pairs, 1), dtype=torch.int32)
+            D.call("bamg_schur_chunk_pairs", self.pt_ptr, self.obs_cam_pm, S_ptr, S_col, self.nc, self.npt, nnz,
+                   self.k, pair_off, n_pairs, _CHUNK_RECORDS, pair_a, pair_b, skey, sizes.ctypes.data)
+            n_seg, n_chunks, blk_bits = int(sizes[0]), int(sizes[1]), int(sizes[2])
+            cap = n_seg + 10 * n_chunks
+            work = D.empty(max(cap, 1), 4, dtype=torch.int32)
+            out = np.zeros(1, dtype=np.int64)
+            D.call("bamg_schur_chunk_work", S_ptr, S_col, self.nc, skey, n_pairs, n_seg, n_chunks, blk_bits,
+                   _CHUNK_GROUP_ROWS, work, cap, out.ctypes.data)
+            del skey
+            self._chunks = dict(pair_a=pair_a, pair_b=pair_b, work=work, n_work=int(out[0]), n_seg=n_seg,
+                                n_chunks=n_chunks, dpos=sym["dpos"], done=D.empty(max(nnz, 1), dtype=torch.int32))
+        return self._chunks
+
+    @property
     def pair_lists(self):
         """Per-block point-pair lists (the block-owned alternative assembly)."""
         if getattr(self, "_pairs", None) is None:
@@ -217,6 +247,8 @@ def _copy_stream():
 
 
 _EAGER_STRUCTURE = __import__("os").environ.get("BAMG_EAGER_STRUCTURE", "1") == "1"
+_CHUNK_RECORDS = int(__import__("os").environ.get("BAMG_SCHUR_CHUNK", "150000"))  # observations per point chunk
+_CHUNK_GROUP_ROWS = int(__import__("os").environ.get("BAMG_SCHUR_CHUNK_ROWS", "1"))
 
 
 class BundleProblem:

@@ -171,7 +171,17 @@ def schur_explicit(sys: SchurSystem, variant: str = "pairs") -> BlockSparseMatri
     blocks = D.empty(nnz, CAMERA_SIZE, CAMERA_SIZE)
     J = sys._jac
     sys._own_H()
-    if variant == "rows":
+    if variant == "chunks":
+        ch = st.chunk_plan
+        rhs = None
+        if sys._rhs is None:
+            rhs = D.empty(sys.n_cameras * CAMERA_SIZE)
+        _, gc, _, _ = J.normal_blocks()
+        D.call("bamg_schur_numeric_chunked", st.cam_ptr, st.cm_list, J._J, sys.A.blocks, ch["dpos"], sys.n_cameras,
+               ch["work"], ch["n_work"], ch["pair_a"], ch["pair_b"], ch["done"], nnz, sys._qo, gc, rhs, blocks)
+        if rhs is not None:
+            sys._rhs = rhs
+    elif variant == "rows":
         sym = st.symbolic
         D.call("bamg_schur_numeric_rows", st.cam_ptr, st.cm_list, st.pt_ptr, st.obs_cam_pm, st.obs_pt_pm, J._J,
                sys.A.blocks, S_ptr, S_col, sym["dpos"], sym["up_off"], sym["up_tpos"], sys.n_cameras, blocks)

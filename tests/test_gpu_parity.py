@@ -101,6 +101,21 @@ def test_schur_explicit(case):
     assert block_rel(H(S2.blocks), H(S.blocks)) <= 1e-12
     S3 = SC.schur_explicit(s)
     assert np.array_equal(H(S3.blocks), H(S.blocks))
+    # point-chunk phased assembly, cut into several chunks (partial sums handed over
+    # between chunks through the S slots)
+    from paper_2007_01941_b200 import problem as PR
+
+    st, old = prob.structure, PR._CHUNK_RECORDS
+    try:
+        PR._CHUNK_RECORDS, st._chunks = max(8, st.k // 7), None
+        S4 = SC.schur_explicit(s, variant="chunks")
+        assert st.chunk_plan["n_chunks"] >= 4
+        S5 = SC.schur_explicit(s, variant="chunks")
+    finally:
+        PR._CHUNK_RECORDS, st._chunks = old, None
+    assert block_rel(H(S4.blocks), g["S_blocks"]) <= 1e-10
+    assert block_rel(H(S4.blocks), H(S.blocks)) <= 1e-12
+    assert np.array_equal(H(S5.blocks), H(S4.blocks))
     # implicit operator == explicit operator (schur.py:84-91)
     rng = np.random.default_rng(0)
     x = rng.normal(size=S.shape[0])

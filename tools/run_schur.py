@@ -21,6 +21,12 @@ def main(config=4, variants="rows,pairs", reps=3):
     if "pairs" in variants:
         _ = st.pair_lists
     torch.cuda.synchronize()
+    if "chunks" in variants:
+        t0 = time.perf_counter()
+        ch = st.chunk_plan
+        torch.cuda.synchronize()
+        print(f"chunk plan: {(time.perf_counter() - t0) * 1e3:.1f} ms, segments {ch['n_seg']}, "
+              f"work {ch['n_work']}, chunks {ch['n_chunks']}", flush=True)
     for v in variants.split(","):
         SC.schur_explicit(s, variant=v)
         torch.cuda.synchronize()

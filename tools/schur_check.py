@@ -27,6 +27,7 @@ def main(which="ring"):
     obj, jac = P.evaluate(prob)
     s = P.build_system(jac, P.Damping.from_jacobian(jac, 1e4))
     _ = prob.structure.pair_lists
+    _ = prob.structure.chunk_plan
     torch.cuda.synchronize()
     vs = [a for a in sys.argv[2:] if not a.startswith("--")]
     out = {}
