@@ -96,7 +96,7 @@ int bamg_normal_blocks(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_
                        double* g_pt, void* stream);
 int bamg_damping(bamg_ctx* ctx, const double* A_raw, const double* C_raw, int32_t nc, int32_t npt, double radius,
                  double* d_cam, double* d_pt, void* stream);
-int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* obs_pt_pm,
+int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* pt_ptr,
                       double* J, int64_t k, const double* A_raw, const double* C_raw, const double* g_cam,
                       const double* g_pt, const double* d_cam, const double* d_pt, int32_t nc, int32_t npt,
                       double* A, double* C, double* Cinv, double* Cb, double* qo, double* rhs,

@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(128)
 k_bsr_spmv(const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ blocks,
            const double* __restrict__ x, double* __restrict__ y, int nbr, double* partials, unsigned int* counter,
            double* dot_out) {
+  PDL_ENTRY();
   __shared__ double scratch[33];
   int lane = threadIdx.x & 31;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -126,6 +127,7 @@ template <int BS>
 __global__ void __launch_bounds__(128)
 k_bsr_residual(const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ blocks,
                const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r, int nbr) {
+  PDL_ENTRY();
   int lane = threadIdx.x & 31;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -146,6 +148,7 @@ __global__ void __launch_bounds__(128)
 k_cheb_step(const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ blocks,
             const double* __restrict__ x_in, const double* __restrict__ b, const double* __restrict__ Dinv,
             double* __restrict__ d, double* __restrict__ x_out, int nbr, double c1, double c2, int divide) {
+  PDL_ENTRY();
   int lane = threadIdx.x & 31;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -236,6 +239,7 @@ extern "C" int bamg_cheb_step(bamg_ctx* ctx, int32_t bs, const int32_t* ptr, con
 __global__ void __launch_bounds__(256, 1)
 k_prolong(const int* __restrict__ agg, const double* __restrict__ P, const double* __restrict__ xc, int nf, int bs,
           double* __restrict__ y, int accumulate) {
+  PDL_ENTRY();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)nf * bs; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = t / bs;
     int r = (int)(t - i * bs);
@@ -396,6 +400,7 @@ extern "C" int bamg_block_chol_inv(bamg_ctx* ctx, const double* M, int32_t n, in
 // y_b = M_b x_b (block-diagonal apply), bs arbitrary
 __global__ void k_blockdiag_apply(const double* __restrict__ M, const double* __restrict__ x, int n, int bs,
                                   double* __restrict__ y) {
+  PDL_ENTRY();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * bs; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t b = t / bs;
     int r = (int)(t - b * bs);
@@ -767,6 +772,7 @@ extern "C" int bamg_coarse_factor(bamg_ctx* ctx, const int32_t* ptr, const int32
 
 // y = M x for dense n x n (warp per row)
 __global__ void k_gemv(const double* __restrict__ M, const double* __restrict__ x, int n, double* __restrict__ y) {
+  PDL_ENTRY();
   int lane = threadIdx.x & 31;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;

@@ -22,6 +22,37 @@ static inline void launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t sme
   k<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
 }
 
+// Programmatic dependent launch (PDL) for the kernel chains of the V-cycle and PCG
+// graphs: launch_pdl sets the programmatic-stream-serialization attribute, so in a
+// captured graph the edge to the previous kernel becomes programmatic and the next
+// kernel's CTAs are launched while the previous one drains. Every kernel launched
+// this way starts with PDL_ENTRY(): griddepcontrol.wait (returns once the
+// predecessor grid has completed and its writes are visible -- nothing is read
+// early) and launch_dependents (lets the successor's launch begin). BAMG_PDL=0
+// turns the attribute off (A/B).
+bool bamg_pdl_enabled();
+template <typename... KArgs, typename... Args>
+static inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  if (!bamg_pdl_enabled()) {
+    launch(k, grid, block, smem, st, std::forward<Args>(args)...);
+    return;
+  }
+  g_bamg_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+#define PDL_ENTRY() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+
 #define BAMG_WARP 32
 #define FULL_MASK 0xffffffffu
 

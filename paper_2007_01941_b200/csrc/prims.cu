@@ -1,6 +1,7 @@
 // Primitives: stable LSD radix sort, exclusive scan, segment pointers, gathers,
 // deterministic reductions, context / error plumbing.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -28,6 +29,14 @@ extern "C" int bamg_last_error(char* buf, size_t n) {
   strncpy(buf, g_err, n - 1);
   buf[n - 1] = 0;
   return (int)strlen(g_err);
+}
+
+bool bamg_pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BAMG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 int bamg_num_sms() {
@@ -429,6 +438,7 @@ extern "C" int bamg_gather_i32(bamg_ctx* ctx, const int32_t* src, const int32_t*
 __global__ void __launch_bounds__(RED_THREADS)
 k_dot(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
       double* partials, unsigned int* counter, double* out) {
+  PDL_ENTRY();
   __shared__ double scratch[33];
   double s = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -476,7 +486,7 @@ k_absmax(const double* __restrict__ x, int64_t n, double* partials, unsigned int
 
 int dot_dev(bamg_ctx* ctx, const double* x, const double* y, int64_t n, double* out, cudaStream_t st) {
   int g = grid_for(n, RED_THREADS, 4);
-  launch(k_dot, g, RED_THREADS, 0, st, x, y, n, ctx->partials, ctx->counters + BAMG_CTR_DOT, out);
+  launch_pdl(k_dot, g, RED_THREADS, 0, st, x, y, n, ctx->partials, ctx->counters + BAMG_CTR_DOT, out);
   BAMG_LAUNCH_CHECK();
   return 0;
 }

@@ -744,33 +744,6 @@ __device__ __forceinline__ bool chol_inv3(const double* C, double* Ci) {
   return true;
 }
 
-// Thread per point: C = C_raw + D_p, factor, C^-1, b_p = -g_p, Cb = C^-1 b_p.
-__global__ void k_points_factor(const double* __restrict__ C_raw, const double* __restrict__ d_pt,
-                                const double* __restrict__ g_pt, int npt, double* __restrict__ C,
-                                double* __restrict__ Cinv, double* __restrict__ Cb, int* __restrict__ bad_min) {
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npt; p += gridDim.x * blockDim.x) {
-    double c[9], ci[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) c[q] = C_raw[(int64_t)p * 9 + q];
-    c[0] += d_pt[3 * p];
-    c[4] += d_pt[3 * p + 1];
-    c[8] += d_pt[3 * p + 2];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) C[(int64_t)p * 9 + q] = c[q];
-    if (!chol_inv3(c, ci)) {
-      atomicMin(bad_min, p);
-#pragma unroll
-      for (int q = 0; q < 9; ++q) ci[q] = 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < 9; ++q) Cinv[(int64_t)p * 9 + q] = ci[q];
-    double b0 = -g_pt[3 * p], b1 = -g_pt[3 * p + 1], b2 = -g_pt[3 * p + 2];
-    Cb[3 * p] = ci[0] * b0 + ci[1] * b1 + ci[2] * b2;
-    Cb[3 * p + 1] = ci[3] * b0 + ci[4] * b1 + ci[5] * b2;
-    Cb[3 * p + 2] = ci[6] * b0 + ci[7] * b1 + ci[8] * b2;
-  }
-}
-
 // Thread per observation: H = E C_p^-1 (into the record) and q = E C_p^-1 b_p.
 __global__ void k_obs_H(const int* __restrict__ opt, const double* __restrict__ Cinv, const double* __restrict__ Cb,
                         int64_t k, double* __restrict__ J, double* __restrict__ qo) {
@@ -794,6 +767,84 @@ __global__ void k_obs_H(const int* __restrict__ opt, const double* __restrict__ 
     rp[RR / 2] = res;
     reinterpret_cast<double2*>(qo)[o] =
         make_double2(e[0] * x0 + e[1] * x1 + e[2] * x2, e[3] * x0 + e[4] * x1 + e[5] * x2);
+  }
+}
+
+// k_points_factor + k_obs_H in one pass: 32 consecutive points per warp, a lane per
+// point factors C (C = C_raw + D_p, batched 3x3 Cholesky inverse, b_p = -g_p), parks C^-1 and C^-1 b_p in
+// shared memory, then the lanes walk the points' contiguous observations (coalesced
+// record accesses) and form H = E C^-1 and q = E C^-1 b_p (same arithmetic as k_obs_H).
+__global__ void __launch_bounds__(128)
+k_points_H_warp(const int* __restrict__ pt_ptr, const double* __restrict__ C_raw, const double* __restrict__ d_pt,
+                const double* __restrict__ g_pt, int npt, double* __restrict__ C, double* __restrict__ Cinv,
+                double* __restrict__ Cb, int* __restrict__ bad_min, double* __restrict__ J, double* __restrict__ qo) {
+  __shared__ double cib[4][32 * 12];
+  __shared__ int sbuf[4][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int p0 = warp * 32; p0 < npt; p0 += nwarps * 32) {
+    const int np = min(32, npt - p0);
+    const int p = p0 + lane;
+    if (lane < np) sbuf[w][lane] = pt_ptr[p0 + lane];
+    if (lane == 0) sbuf[w][np] = pt_ptr[p0 + np];
+    if (lane < np) {
+      double c[9], ci[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) c[q] = C_raw[(int64_t)p * 9 + q];
+      c[0] += d_pt[3 * p];
+      c[4] += d_pt[3 * p + 1];
+      c[8] += d_pt[3 * p + 2];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) C[(int64_t)p * 9 + q] = c[q];
+      if (!chol_inv3(c, ci)) {
+        atomicMin(bad_min, p);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) ci[q] = 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 9; ++q) Cinv[(int64_t)p * 9 + q] = ci[q];
+      double b0 = -g_pt[3 * p], b1 = -g_pt[3 * p + 1], b2 = -g_pt[3 * p + 2];
+      double x0 = ci[0] * b0 + ci[1] * b1 + ci[2] * b2;
+      double x1 = ci[3] * b0 + ci[4] * b1 + ci[5] * b2;
+      double x2 = ci[6] * b0 + ci[7] * b1 + ci[8] * b2;
+      Cb[3 * p] = x0;
+      Cb[3 * p + 1] = x1;
+      Cb[3 * p + 2] = x2;
+      double* cb = cib[w] + 12 * lane;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) cb[q] = ci[q];
+      cb[9] = x0;
+      cb[10] = x1;
+      cb[11] = x2;
+    }
+    __syncwarp();
+    const int r0 = sbuf[w][0], r1 = sbuf[w][np];
+    for (int o = r0 + lane; o < r1; o += 32) {
+      int lo = 0, hi = np;
+      while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (sbuf[w][mid] <= o) lo = mid; else hi = mid;
+      }
+      const double* ci = cib[w] + 12 * lo;
+      double2* rp = reinterpret_cast<double2*>(J + (int64_t)o * REC);
+      double2 e01 = rp[RE / 2], e23 = rp[RE / 2 + 1], e45 = rp[RE / 2 + 2];
+      double2 res = rp[RR / 2];  // rewritten with H[4..5]: the shared sector is stored whole
+      double e[6] = {e01.x, e01.y, e23.x, e23.y, e45.x, e45.y};
+      double h[6];
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc)
+          h[r * 3 + cc] = e[r * 3] * ci[cc] + e[r * 3 + 1] * ci[3 + cc] + e[r * 3 + 2] * ci[6 + cc];
+      rp[RH / 2] = make_double2(h[0], h[1]);
+      rp[RH / 2 + 1] = make_double2(h[2], h[3]);
+      rp[RH / 2 + 2] = make_double2(h[4], h[5]);
+      rp[RR / 2] = res;
+      reinterpret_cast<double2*>(qo)[o] =
+          make_double2(e[0] * ci[9] + e[1] * ci[10] + e[2] * ci[11], e[3] * ci[9] + e[4] * ci[10] + e[5] * ci[11]);
+    }
+    __syncwarp();
   }
 }
 
@@ -892,7 +943,7 @@ static size_t cam_gather_smem() {
 }
 
 extern "C" int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
-                                 const int32_t* obs_pt_pm, double* J, int64_t k, const double* A_raw,
+                                 const int32_t* pt_ptr, double* J, int64_t k, const double* A_raw,
                                  const double* C_raw, const double* g_cam, const double* g_pt, const double* d_cam,
                                  const double* d_pt, int32_t nc, int32_t npt, double* A, double* C, double* Cinv,
                                  double* Cb, double* qo, double* rhs, int32_t* bad_min_dev, void* stream) {
@@ -902,8 +953,8 @@ extern "C" int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const in
   BAMG_CUDA_CHECK(cudaMemcpyAsync(bad_min_dev, &big, sizeof(int), cudaMemcpyHostToDevice, st));
   if (nc) launch(k_add_diag, grid_for((int64_t)nc * 81, 256), 256, 0, st, A_raw, d_cam, nc, 9, A);
   if (npt)
-    launch(k_points_factor, grid_for(npt, 128, 16), 128, 0, st, C_raw, d_pt, g_pt, npt, C, Cinv, Cb, bad_min_dev);
-  if (k) launch(k_obs_H, grid_for(k, 256, 8), 256, 0, st, obs_pt_pm, Cinv, Cb, k, J, qo);
+    launch(k_points_H_warp, grid_for((int64_t)ceil_div(npt, 32) * 32, 128, 16), 128, 0, st, pt_ptr, C_raw, d_pt, g_pt,
+           npt, C, Cinv, Cb, bad_min_dev, J, qo);
   if (nc && rhs)  // rhs == NULL: formed later by bamg_rhs_gather or the Schur diagonal pass
     launch(k_cam_gather, grid_for((int64_t)nc * 32, 128, 8), 128, cam_gather_smem(), st, cam_ptr, cm_list, J, qo,
            g_cam, nullptr, nullptr, nc, rhs);
@@ -1007,8 +1058,8 @@ extern "C" int bamg_back_substitute(bamg_ctx* ctx, const int32_t* pt_ptr, const 
                                     double* dp, void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
-  if (npt) launch(k_point_wtx, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, obs_cam_pm, J, Cinv, dc, grad_pt, npt, dp,
-                  nullptr);
+  if (npt) launch(k_point_wtx, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, obs_cam_pm, J, Cinv, dc, grad_pt, npt,
+                  dp, nullptr);
   BAMG_LAUNCH_CHECK();
   return 0;
 }

@@ -17,6 +17,7 @@ int dot_dev(bamg_ctx* ctx, const double* x, const double* y, int64_t n, double* 
 
 // y = x (copy)
 __global__ void k_copy(const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = x[i];
 }
@@ -26,6 +27,7 @@ __global__ void __launch_bounds__(256)
 k_pcg_update_dev(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                  const double* __restrict__ ap, const double* __restrict__ rz, const double* __restrict__ pap,
                  int64_t n, double* partials, unsigned int* counter, double* rr_out) {
+  PDL_ENTRY();
   __shared__ double scratch[33];
   double a = (*rz) / (*pap);
   double s = 0.0;
@@ -42,6 +44,7 @@ k_pcg_update_dev(double* __restrict__ x, double* __restrict__ r, const double* _
 // p = z + (rz_new / rz_old) p
 __global__ void k_xpby_dev(const double* __restrict__ z, const double* __restrict__ rz_new,
                            const double* __restrict__ rz_old, double* __restrict__ p, int64_t n) {
+  PDL_ENTRY();
   double beta = (*rz_new) / (*rz_old);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = z[i] + beta * p[i];
@@ -156,6 +159,7 @@ k_sym9_upper(const int* __restrict__ ptr, const int* __restrict__ col, const int
              const int* __restrict__ tpos, const int* __restrict__ cbeg, const int* __restrict__ crow, int nch,
              const double* __restrict__ blocks, const double* __restrict__ x, double* __restrict__ T,
              double* __restrict__ yup, int blk_policy) {
+  PDL_ENTRY();
   __shared__ double red[4][27 * 9];
   const uint64_t pb = l2_policy(blk_policy), pt = l2_policy(L2_LAST);
   int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -211,6 +215,7 @@ k_sym9_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const i
               const double* __restrict__ Dinv, double* __restrict__ d, const double* __restrict__ x_in,
               double* __restrict__ out, double c1, double c2, int divide, double* partials, unsigned int* counter,
               double* dot_out) {
+  PDL_ENTRY();
   __shared__ double scratch[33];
   const uint64_t pt = l2_policy(L2_LAST);
   int lane = threadIdx.x & 31;
@@ -284,6 +289,7 @@ __global__ void __launch_bounds__(128)
 k_sym16_upper(const int* __restrict__ ptr, const int* __restrict__ col, const int* __restrict__ dpos,
               const int* __restrict__ tpos, const int* __restrict__ cbeg, const int* __restrict__ crow, int nch, const double* __restrict__ blocks,
               const double* __restrict__ x, double* __restrict__ T, double* __restrict__ yup, int blk_policy) {
+  PDL_ENTRY();
   const uint64_t pb = l2_policy(blk_policy), pt = l2_policy(L2_LAST);
   int lane = threadIdx.x & 31;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -342,6 +348,7 @@ k_sym16_finish(const int* __restrict__ ptr, const int* __restrict__ dpos, const 
                int mode, const double* __restrict__ b, const double* __restrict__ Dinv, double* __restrict__ d,
                const double* __restrict__ x_in, double* __restrict__ out, double c1, double c2, int divide,
                double* partials, unsigned int* counter, double* dot_out) {
+  PDL_ENTRY();
   __shared__ double scratch[33];
   const uint64_t pt = l2_policy(L2_LAST);
   int lane = threadIdx.x & 31;
@@ -423,23 +430,23 @@ static void sym_apply(bamg_ctx* ctx, const bamg_symop* S, const double* blocks, 
   double* part = ctx ? ctx->partials : nullptr;
   unsigned* ctr = ctx ? ctx->counters + BAMG_CTR_SPMV : nullptr;
   if (S->bs == 16) {
-    launch(k_sym16_upper, sym_grid(S->nch), 128, 0, st, S->ptr, S->col, S->dpos, (const int*)S->tpos,
+    launch_pdl(k_sym16_upper, sym_grid(S->nch), 128, 0, st, S->ptr, S->col, S->dpos, (const int*)S->tpos,
            (const int*)S->cbeg,
            (const int*)S->crow, S->nch, blocks, x, S->T, S->yup, sym_block_policy(S));
     int g = grid_for((int64_t)((S->nbr + 1) / 2) * 32, 128, 16);
     if (dot_out && g > BAMG_MAX_PARTIALS) g = BAMG_MAX_PARTIALS;
-    launch(k_sym16_finish, g, 128, 0, st, S->ptr, S->dpos, (const int*)S->tpos, (const double*)S->T,
+    launch_pdl(k_sym16_finish, g, 128, 0, st, S->ptr, S->dpos, (const int*)S->tpos, (const double*)S->T,
            (const int*)S->ucptr, (const double*)S->yup, S->nbr, mode, b, Dinv, d, x, out, c1, c2, divide, part, ctr,
            dot_out);
     return;
   }
-  launch(k_sym9_upper, sym_grid(S->nch), 128, 0, st, S->ptr, S->col, S->dpos, (const int*)S->tpos,
+  launch_pdl(k_sym9_upper, sym_grid(S->nch), 128, 0, st, S->ptr, S->col, S->dpos, (const int*)S->tpos,
          (const int*)S->cbeg, (const int*)S->crow, S->nch, blocks, x, S->T, S->yup, sym_block_policy(S));
   // one row per warp (the hardware balances CTAs over SMs as rows finish); the
   // fused dot's grid is capped by the partials buffer and strides instead
   int g = (int)ceil_div(S->nbr, 4);
   if (dot_out && g > BAMG_MAX_PARTIALS) g = BAMG_MAX_PARTIALS;
-  launch(k_sym9_finish<SYM_FB>, g, 128, 0, st, S->ptr, S->dpos, (const int*)S->tpos, (const double*)S->T, (const int*)S->ucptr,
+  launch_pdl(k_sym9_finish<SYM_FB>, g, 128, 0, st, S->ptr, S->dpos, (const int*)S->tpos, (const double*)S->T, (const int*)S->ucptr,
          (const double*)S->yup, S->nbr, mode, b, Dinv, d, x, out, c1, c2, divide, part, ctr, dot_out);
 }
 
@@ -612,6 +619,7 @@ __global__ void __launch_bounds__(128)
 k_spmv16_chunks(const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ blocks,
                 const double* __restrict__ x, const int* __restrict__ cbeg, const int* __restrict__ crow, int nch,
                 int CH, double* __restrict__ partial) {
+  PDL_ENTRY();
   int lane = threadIdx.x & 31;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -636,6 +644,7 @@ k_row16_cta(const int* __restrict__ ptr, const int* __restrict__ col, const doub
             const double* __restrict__ x, int nbr, int mode, const double* __restrict__ b,
             const double* __restrict__ Dinv, double* __restrict__ d, double* __restrict__ out, double c1, double c2,
             int divide) {
+  PDL_ENTRY();
   __shared__ double part[4][16];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int row = blockIdx.x;
@@ -673,6 +682,7 @@ __global__ void __launch_bounds__(128)
 k_rows16_finish(const int* __restrict__ cptr, const double* __restrict__ partial, int nbr, int mode,
                 const double* __restrict__ b, const double* __restrict__ Dinv, double* __restrict__ d,
                 const double* __restrict__ x_in, double* __restrict__ out, double c1, double c2, int divide) {
+  PDL_ENTRY();
   int lane = threadIdx.x & 31;
   int half = lane >> 4, r = lane & 15;
   int row0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2;
@@ -715,6 +725,7 @@ template <int BS>
 __global__ void __launch_bounds__(128, 1)
 k_restrict_warp(const int* __restrict__ agg_ptr, const int* __restrict__ members, const double* __restrict__ P,
                 const double* __restrict__ r, int nagg, double* __restrict__ bc) {
+  PDL_ENTRY();
   int lane = threadIdx.x & 31;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -1007,12 +1018,12 @@ static int mg_alloc(bamg_mg* m, cudaStream_t st) {
 template <int BS>
 static void cheb_launch(const MgLevelPlan& L, const double* x_in, double* x_out, double c1, double c2, int divide,
                         bool with_A, cudaStream_t st) {
-  launch(k_cheb_step<BS>, spmv_grid(L.nbr), 128, 0, st, L.ptr, L.col, with_A ? L.blocks : nullptr, x_in, L.b, L.Dinv,
+  launch_pdl(k_cheb_step<BS>, spmv_grid(L.nbr), 128, 0, st, L.ptr, L.col, with_A ? L.blocks : nullptr, x_in, L.b, L.Dinv,
          L.d, x_out, L.nbr, c1, c2, divide);
 }
 
 static void chunk_spmv(const MgLevelPlan& L, const double* x, cudaStream_t st) {
-  launch(k_spmv16_chunks, grid_for((int64_t)L.nch * 32, 128, 16), 128, 0, st, L.ptr, L.col, L.blocks, x, L.cbeg,
+  launch_pdl(k_spmv16_chunks, grid_for((int64_t)L.nch * 32, 128, 16), 128, 0, st, L.ptr, L.col, L.blocks, x, L.cbeg,
          L.crow, L.nch, L.CH, L.partial);
 }
 
@@ -1021,7 +1032,7 @@ static int finish_grid(int nbr) { return grid_for((int64_t)((nbr + 1) / 2) * 32,
 static void cheb(const MgLevelPlan& L, const double* x_in, double* x_out, double c1, double c2, int divide,
                  bool with_A, cudaStream_t st) {
   if (with_A && L.rowcta) {
-    launch(k_row16_cta, L.nbr, 128, 0, st, L.ptr, L.col, L.blocks, x_in, L.nbr, 1, L.b, L.Dinv, L.d, x_out, c1, c2,
+    launch_pdl(k_row16_cta, L.nbr, 128, 0, st, L.ptr, L.col, L.blocks, x_in, L.nbr, 1, L.b, L.Dinv, L.d, x_out, c1, c2,
            divide);
     return;
   }
@@ -1031,7 +1042,7 @@ static void cheb(const MgLevelPlan& L, const double* x_in, double* x_out, double
   }
   if (with_A && L.CH) {
     chunk_spmv(L, x_in, st);
-    launch(k_rows16_finish, finish_grid(L.nbr), 128, 0, st, L.cptr, L.partial, L.nbr, 1, L.b, L.Dinv, L.d, x_in,
+    launch_pdl(k_rows16_finish, finish_grid(L.nbr), 128, 0, st, L.cptr, L.partial, L.nbr, 1, L.b, L.Dinv, L.d, x_in,
            x_out, c1, c2, divide);
     return;
   }
@@ -1043,22 +1054,27 @@ static void cheb(const MgLevelPlan& L, const double* x_in, double* x_out, double
 }
 
 // Smoother (multigrid.py:308-328); returns the buffer holding the result.
-static double* smooth(MgLevelPlan& L, double* x, cudaStream_t st) {
+// `final_out` (optional): the buffer the last step writes (the plan's output vector,
+// so no copy follows the cycle).
+static double* smooth(MgLevelPlan& L, double* x, cudaStream_t st, double* final_out = nullptr) {
   double rho = 1.0 / L.sigma;
   double* cur;
   double* spare;
+  const bool one = L.iterations <= 1 && final_out;
   if (x == nullptr) {
-    cheb(L, nullptr, L.x, 0.0, L.theta, 1, false, st);  // d = D^-1 b / theta ; x = d
-    cur = L.x;
+    double* out = one ? final_out : L.x;
+    cheb(L, nullptr, out, 0.0, L.theta, 1, false, st);  // d = D^-1 b / theta ; x = d
+    cur = out;
     spare = L.xs;
   } else {
-    double* out = (x == L.x) ? L.xs : L.x;
+    double* out = one ? final_out : ((x == L.x) ? L.xs : L.x);
     cheb(L, x, out, 0.0, L.theta, 1, true, st);  // r = b - A x ; d = D^-1 r / theta ; x += d
     cur = out;
     spare = x;
   }
   for (int it = 0; it < L.iterations - 1; ++it) {
     double rho_next = 1.0 / (2.0 * L.sigma - rho);
+    if (final_out && it == L.iterations - 2) spare = final_out;
     cheb(L, cur, spare, rho_next * rho, 2.0 * rho_next / L.delta, 0, true, st);
     double* t = cur;
     cur = spare;
@@ -1070,7 +1086,7 @@ static double* smooth(MgLevelPlan& L, double* x, cudaStream_t st) {
 
 static void residual(const MgLevelPlan& L, const double* x, cudaStream_t st) {
   if (L.rowcta) {
-    launch(k_row16_cta, L.nbr, 128, 0, st, L.ptr, L.col, L.blocks, x, L.nbr, 0, L.b, nullptr, nullptr, L.r, 0.0, 0.0,
+    launch_pdl(k_row16_cta, L.nbr, 128, 0, st, L.ptr, L.col, L.blocks, x, L.nbr, 0, L.b, nullptr, nullptr, L.r, 0.0, 0.0,
            0);
     return;
   }
@@ -1080,15 +1096,15 @@ static void residual(const MgLevelPlan& L, const double* x, cudaStream_t st) {
   }
   if (L.CH) {
     chunk_spmv(L, x, st);
-    launch(k_rows16_finish, finish_grid(L.nbr), 128, 0, st, L.cptr, L.partial, L.nbr, 0, L.b, nullptr, nullptr,
+    launch_pdl(k_rows16_finish, finish_grid(L.nbr), 128, 0, st, L.cptr, L.partial, L.nbr, 0, L.b, nullptr, nullptr,
            nullptr, L.r, 0.0, 0.0, 0);
     return;
   }
   int g = spmv_grid(L.nbr);
   switch (L.bs) {
-    case 9: launch(k_bsr_residual<9>, g, 128, 0, st, L.ptr, L.col, L.blocks, x, L.b, L.r, L.nbr); break;
-    case 16: launch(k_bsr_residual<16>, g, 128, 0, st, L.ptr, L.col, L.blocks, x, L.b, L.r, L.nbr); break;
-    default: launch(k_bsr_residual<1>, g, 128, 0, st, L.ptr, L.col, L.blocks, x, L.b, L.r, L.nbr); break;
+    case 9: launch_pdl(k_bsr_residual<9>, g, 128, 0, st, L.ptr, L.col, L.blocks, x, L.b, L.r, L.nbr); break;
+    case 16: launch_pdl(k_bsr_residual<16>, g, 128, 0, st, L.ptr, L.col, L.blocks, x, L.b, L.r, L.nbr); break;
+    default: launch_pdl(k_bsr_residual<1>, g, 128, 0, st, L.ptr, L.col, L.blocks, x, L.b, L.r, L.nbr); break;
   }
 }
 
@@ -1096,26 +1112,28 @@ static void residual(const MgLevelPlan& L, const double* x, cudaStream_t st) {
 static double* vcycle(bamg_mg* m, size_t l, cudaStream_t st) {
   MgLevelPlan& L = m->lv[l];
   if (L.inv) {
-    launch(k_gemv, grid_for((int64_t)L.n * 32, 128, 8), 128, 0, st, L.inv, L.b, L.n, L.x);
-    return L.x;
+    double* out = l == 0 ? m->out : L.x;
+    launch_pdl(k_gemv, grid_for((int64_t)L.n * 32, 128, 8), 128, 0, st, L.inv, L.b, L.n, out);
+    return out;
   }
   double* x = smooth(L, nullptr, st);
   residual(L, x, st);
   MgLevelPlan& C = m->lv[l + 1];
   if (L.bs == 9)
-    launch(k_restrict_warp<9>, grid_for((int64_t)L.n_agg * 32, 128, 16), 128, 0, st, L.agg_ptr, L.members, L.P, L.r,
+    launch_pdl(k_restrict_warp<9>, grid_for((int64_t)L.n_agg * 32, 128, 16), 128, 0, st, L.agg_ptr, L.members, L.P, L.r,
            L.n_agg, C.b);
   else
-    launch(k_restrict_warp<16>, grid_for((int64_t)L.n_agg * 32, 128, 16), 128, 0, st, L.agg_ptr, L.members, L.P,
+    launch_pdl(k_restrict_warp<16>, grid_for((int64_t)L.n_agg * 32, 128, 16), 128, 0, st, L.agg_ptr, L.members, L.P,
            L.r, L.n_agg, C.b);
   double* xc = vcycle(m, l + 1, st);
-  launch(k_prolong, grid_for((int64_t)L.n, 256), 256, 0, st, L.agg, L.P, xc, L.nbr, L.bs, x, 1);
-  return smooth(L, x, st);
+  launch_pdl(k_prolong, grid_for((int64_t)L.n, 256), 256, 0, st, L.agg, L.P, xc, L.nbr, L.bs, x, 1);
+  return smooth(L, x, st, l == 0 ? m->out : nullptr);
 }
 
 static int mg_record(bamg_mg* m, cudaStream_t st) {
   double* res = vcycle(m, 0, st);
-  BAMG_CUDA_CHECK(cudaMemcpyAsync(m->out, res, sizeof(double) * (size_t)m->lv[0].n, cudaMemcpyDeviceToDevice, st));
+  if (res != m->out)
+    BAMG_CUDA_CHECK(cudaMemcpyAsync(m->out, res, sizeof(double) * (size_t)m->lv[0].n, cudaMemcpyDeviceToDevice, st));
   return 0;
 }
 
@@ -1272,6 +1290,7 @@ __global__ void k_pcg_g_rz0(PcgDev* s, int max_it, cudaGraphConditionalHandle hw
 // tolerance, forcing (solver.py:104-120, ForcingCriterion.satisfied 52-59)
 __global__ void k_pcg_g_check1(PcgDev* s, double* qh, double rtol, double tau, cudaGraphConditionalHandle hw,
                                cudaGraphConditionalHandle hif) {
+  PDL_ENTRY();
   if (threadIdx.x | blockIdx.x) return;
   int i = ++s->it;
   double pap = s->pap;
@@ -1314,6 +1333,7 @@ __global__ void k_pcg_g_check1(PcgDev* s, double* qh, double rtol, double tau, c
 
 // after z = M r and <r, z>: preconditioner checks (solver.py:121-125), last iteration
 __global__ void k_pcg_g_check2(PcgDev* s, int max_it) {
+  PDL_ENTRY();
   if (threadIdx.x | blockIdx.x) return;
   double rzn = s->rzn;
   if (!isfinite(rzn)) {
@@ -1333,6 +1353,7 @@ __global__ void k_pcg_g_check2(PcgDev* s, int max_it) {
 
 // after p = z + (rz_next / rz) p: rz <- rz_next, loop condition
 __global__ void k_pcg_g_next(PcgDev* s, cudaGraphConditionalHandle hw) {
+  PDL_ENTRY();
   if (threadIdx.x | blockIdx.x) return;
   s->rz = s->rzn;
   cudaGraphSetConditional(hw, s->done ? 0u : 1u);
@@ -1374,7 +1395,7 @@ static int pcg_graph(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const ba
       vj_apply_dev(vj, r, z, cs);
       return 0;
     }
-    launch(k_blockdiag_apply, grid_for(n, 256), 256, 0, cs, pbj_inv, (const double*)r, nbr, bs, z);
+    launch_pdl(k_blockdiag_apply, grid_for(n, 256), 256, 0, cs, pbj_inv, (const double*)r, nbr, bs, z);
     return 0;
   };
   auto spmv_dot = [&](cudaStream_t cs) {
@@ -1386,9 +1407,9 @@ static int pcg_graph(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const ba
     if (g > BAMG_MAX_PARTIALS) g = BAMG_MAX_PARTIALS;
     unsigned* ctr = ctx->counters + BAMG_CTR_SPMV;
     switch (bs) {
-      case 9: launch(k_bsr_spmv<9>, g, 128, 0, cs, ptr, col, blocks, (const double*)p, ap, nbr, ctx->partials, ctr, &dev->pap); break;
-      case 16: launch(k_bsr_spmv<16>, g, 128, 0, cs, ptr, col, blocks, (const double*)p, ap, nbr, ctx->partials, ctr, &dev->pap); break;
-      default: launch(k_bsr_spmv<1>, g, 128, 0, cs, ptr, col, blocks, (const double*)p, ap, nbr, ctx->partials, ctr, &dev->pap); break;
+      case 9: launch_pdl(k_bsr_spmv<9>, g, 128, 0, cs, ptr, col, blocks, (const double*)p, ap, nbr, ctx->partials, ctr, &dev->pap); break;
+      case 16: launch_pdl(k_bsr_spmv<16>, g, 128, 0, cs, ptr, col, blocks, (const double*)p, ap, nbr, ctx->partials, ctr, &dev->pap); break;
+      default: launch_pdl(k_bsr_spmv<1>, g, 128, 0, cs, ptr, col, blocks, (const double*)p, ap, nbr, ctx->partials, ctr, &dev->pap); break;
     }
   };
 
@@ -1408,12 +1429,12 @@ static int pcg_graph(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const ba
     long long c0 = g_bamg_launches.load();
     cudaMemsetAsync(x, 0, sizeof(double) * n, cs);
     dot_dev(ctx, b, b, n, bb, cs);
-    launch(k_copy, grid_for(n, 256), 256, 0, cs, b, r, n);
+    launch_pdl(k_copy, grid_for(n, 256), 256, 0, cs, b, r, n);
     launch(k_pcg_g_init, 1, 32, 0, cs, (const double*)bb, dev, qh);
     if ((rc = precond(cs))) break;
     dot_dev(ctx, r, z, n, &dev->rz, cs);
     launch(k_pcg_g_rz0, 1, 32, 0, cs, dev, max_it, hw);
-    launch(k_copy, grid_for(n, 256), 256, 0, cs, (const double*)z, p, n);
+    launch_pdl(k_copy, grid_for(n, 256), 256, 0, cs, (const double*)z, p, n);
     k_init = (int)(g_bamg_launches.load() - c0);
     // WHILE node after the init segment
     cudaStreamCaptureStatus cst;
@@ -1437,10 +1458,10 @@ static int pcg_graph(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const ba
     if (cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) { rc = BAMG_ERR_CUDA; break; }
     c0 = g_bamg_launches.load();
     spmv_dot(cs);
-    launch(k_pcg_update_dev, grid_for(n, 256, 4), 256, 0, cs, x, r, (const double*)p, (const double*)ap,
+    launch_pdl(k_pcg_update_dev, grid_for(n, 256, 4), 256, 0, cs, x, r, (const double*)p, (const double*)ap,
            (const double*)&dev->rz, (const double*)&dev->pap, n, ctx->partials, ctx->counters + BAMG_CTR_PCG0,
            &dev->rr);
-    launch(k_pcg_g_check1, 1, 32, 0, cs, dev, qh, rtol, tau, hw, hif);
+    launch_pdl(k_pcg_g_check1, 1, 32, 0, cs, dev, qh, rtol, tau, hw, hif);
     k_body = (int)(g_bamg_launches.load() - c0);
     if (cudaStreamGetCaptureInfo(cs, &cst, nullptr, &cg, &deps, &ndeps)) { rc = BAMG_ERR_CUDA; break; }
     cudaGraphNodeParams ip = {};
@@ -1458,10 +1479,10 @@ static int pcg_graph(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const ba
     c0 = g_bamg_launches.load();
     if ((rc = precond(cs))) break;
     dot_dev(ctx, r, z, n, &dev->rzn, cs);
-    launch(k_pcg_g_check2, 1, 32, 0, cs, dev, max_it);
-    launch(k_xpby_dev, grid_for(n, 256), 256, 0, cs, (const double*)z, (const double*)&dev->rzn,
+    launch_pdl(k_pcg_g_check2, 1, 32, 0, cs, dev, max_it);
+    launch_pdl(k_xpby_dev, grid_for(n, 256), 256, 0, cs, (const double*)z, (const double*)&dev->rzn,
            (const double*)&dev->rz, p, n);
-    launch(k_pcg_g_next, 1, 32, 0, cs, dev, hw);
+    launch_pdl(k_pcg_g_next, 1, 32, 0, cs, dev, hw);
     k_tail = (int)(g_bamg_launches.load() - c0);
     if (cudaStreamEndCapture(cs, &tail)) { rc = BAMG_ERR_CUDA; break; }
   } while (0);
@@ -1572,7 +1593,7 @@ extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, c
       BAMG_LAUNCH_CHECK();
       return 0;
     }
-    launch(k_blockdiag_apply, grid_for(n, 256), 256, 0, st, pbj_inv, in, nbr, bs, out);
+    launch_pdl(k_blockdiag_apply, grid_for(n, 256), 256, 0, st, pbj_inv, in, nbr, bs, out);
     BAMG_LAUNCH_CHECK();
     return 0;
   };
@@ -1585,9 +1606,9 @@ extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, c
     if (g > BAMG_MAX_PARTIALS) g = BAMG_MAX_PARTIALS;
     unsigned* ctr = ctx->counters + BAMG_CTR_SPMV;
     switch (bs) {
-      case 9: launch(k_bsr_spmv<9>, g, 128, 0, st, ptr, col, blocks, v, out, nbr, ctx->partials, ctr, dot); break;
-      case 16: launch(k_bsr_spmv<16>, g, 128, 0, st, ptr, col, blocks, v, out, nbr, ctx->partials, ctr, dot); break;
-      default: launch(k_bsr_spmv<1>, g, 128, 0, st, ptr, col, blocks, v, out, nbr, ctx->partials, ctr, dot); break;
+      case 9: launch_pdl(k_bsr_spmv<9>, g, 128, 0, st, ptr, col, blocks, v, out, nbr, ctx->partials, ctr, dot); break;
+      case 16: launch_pdl(k_bsr_spmv<16>, g, 128, 0, st, ptr, col, blocks, v, out, nbr, ctx->partials, ctr, dot); break;
+      default: launch_pdl(k_bsr_spmv<1>, g, 128, 0, st, ptr, col, blocks, v, out, nbr, ctx->partials, ctr, dot); break;
     }
   };
   int rc;
@@ -1596,7 +1617,7 @@ extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, c
   BAMG_CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
   rc = dot_dev(ctx, b, b, n, sc + 4, st);
   if (rc) return rc;
-  launch(k_copy, grid_for(n, 256), 256, 0, st, b, r, n);
+  launch_pdl(k_copy, grid_for(n, 256), 256, 0, st, b, r, n);
   BAMG_CUDA_CHECK(cudaMemcpyAsync(hs + 4, sc + 4, sizeof(double), cudaMemcpyDeviceToHost, st));
   BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
   double b_norm = sqrt(hs[4]);
@@ -1616,12 +1637,12 @@ extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, c
   double rz = hs[slot];
   if (!isfinite(rz)) { *err_out = 5; *err_iter_out = 0; return 0; }
   if (rz <= 0.0) { *err_out = 1; *err_value_out = rz; *err_iter_out = 0; return 0; }
-  launch(k_copy, grid_for(n, 256), 256, 0, st, z, p, n);
+  launch_pdl(k_copy, grid_for(n, 256), 256, 0, st, z, p, n);
   double q_val = 0.0, rel = 1.0;
   bool pending = false;  // an rz_next on the device not yet checked on the host
   for (int i = 1; i <= max_it; ++i) {
     spmv_dot(p, ap, sc + 0);
-    launch(k_pcg_update_dev, grid_for(n, 256, 4), 256, 0, st, x, r, p, ap, sc + slot, sc + 0, n, ctx->partials,
+    launch_pdl(k_pcg_update_dev, grid_for(n, 256, 4), 256, 0, st, x, r, p, ap, sc + slot, sc + 0, n, ctx->partials,
            ctx->counters + BAMG_CTR_PCG0, sc + 1);
     BAMG_CUDA_CHECK(cudaMemcpyAsync(hs, sc, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
     BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -1654,7 +1675,7 @@ extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, c
     int nslot = (slot == 2) ? 3 : 2;
     rc = dot_dev(ctx, r, z, n, sc + nslot, st);
     if (rc) return rc;
-    launch(k_xpby_dev, grid_for(n, 256), 256, 0, st, z, sc + nslot, sc + slot, p, n);
+    launch_pdl(k_xpby_dev, grid_for(n, 256), 256, 0, st, z, sc + nslot, sc + slot, p, n);
     slot = nslot;
     pending = true;
   }
@@ -1766,7 +1787,7 @@ extern "C" int bamg_lanczos_lmax(bamg_ctx* ctx, int32_t bs, int32_t nbr, const i
   int g = grid_for(n, 256);
   BAMG_CUDA_CHECK(cudaMemsetAsync(qprev, 0, sizeof(double) * n, st));
   // q0 = v / sqrt(v . D v)
-  launch(k_blockdiag_apply, g, 256, 0, st, D, v0, nbr, bs, Dz);
+  launch_pdl(k_blockdiag_apply, g, 256, 0, st, D, v0, nbr, bs, Dz);
   int rc = dot_dev(ctx, v0, Dz, n, tmp + 0, st);
   if (rc) return rc;
   launch(k_scale_rsqrt_dev, g, 256, 0, st, v0, tmp, 0, basis, n);
@@ -1779,9 +1800,9 @@ extern "C" int bamg_lanczos_lmax(bamg_ctx* ctx, int32_t bs, int32_t nbr, const i
     unsigned* ctr = ctx->counters + BAMG_CTR_SPMV;
     if (sym && sym->bs == bs) sym_apply(ctx, sym, blocks, q, 0, nullptr, nullptr, nullptr, u, 0.0, 0.0, 0, sc + s, st);
     else switch (bs) {
-      case 9: launch(k_bsr_spmv<9>, sg, 128, 0, st, ptr, col, blocks, q, u, nbr, ctx->partials, ctr, sc + s); break;
-      case 16: launch(k_bsr_spmv<16>, sg, 128, 0, st, ptr, col, blocks, q, u, nbr, ctx->partials, ctr, sc + s); break;
-      default: launch(k_bsr_spmv<1>, sg, 128, 0, st, ptr, col, blocks, q, u, nbr, ctx->partials, ctr, sc + s); break;
+      case 9: launch_pdl(k_bsr_spmv<9>, sg, 128, 0, st, ptr, col, blocks, q, u, nbr, ctx->partials, ctr, sc + s); break;
+      case 16: launch_pdl(k_bsr_spmv<16>, sg, 128, 0, st, ptr, col, blocks, q, u, nbr, ctx->partials, ctr, sc + s); break;
+      default: launch_pdl(k_bsr_spmv<1>, sg, 128, 0, st, ptr, col, blocks, q, u, nbr, ctx->partials, ctr, sc + s); break;
     }
     // z = D^-1 u - alpha q - beta_prev q_prev   (beta_prev = sqrt(beta2[s-1]))
     if (s > 0) launch(k_sqrt_slot, 1, 1, 0, st, sc, 8 + s - 1, 40 + s - 1);

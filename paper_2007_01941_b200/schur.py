@@ -145,7 +145,7 @@ def build_system(jac: JacobianBlocks, damping: Damping) -> SchurSystem:
     Cb = D.empty(npt, 3)
     qo = D.empty(max(st.k, 1), 2)
     bad = D.empty(1, dtype=torch.int32)
-    D.call("bamg_build_system", st.cam_ptr, st.cm_list, st.obs_pt_pm, jac._J, st.k, A_raw, C_raw, gc, gp,
+    D.call("bamg_build_system", st.cam_ptr, st.cm_list, st.pt_ptr, jac._J, st.k, A_raw, C_raw, gc, gp,
            damping.cam_diag, damping.pt_diag, nc, npt, A, C, Cinv, Cb, qo, None, bad)
     b = int(bad.item())
     if b != 0x7FFFFFFF:

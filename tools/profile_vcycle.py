@@ -21,6 +21,13 @@ r = D.f64(np.random.default_rng(1).standard_normal(h.levels[0].scalar_dim))
 for _ in range(3):
     h.apply(r)
 torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(20):
+    h.apply(r)
+e1.record()
+torch.cuda.synchronize()
+print(f"per V-cycle (events, 20 back to back): {e0.elapsed_time(e1) / 20 * 1e3:.1f} us")
 reps = 10
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(reps):
@@ -37,5 +44,5 @@ for e in prof.events():
 tot = sum(v[1] for v in agg.values())
 print(f"per V-cycle: kernel sum {tot / reps:.1f} us; levels {[l.scalar_dim for l in h.levels]}; "
       f"nnz {[l.explicit.n_block_entries for l in h.levels]}")
-for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:20]:
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:30]:
     print(f"  {k[:40]:40s} n/cycle={v[0] / reps:5.1f} {v[1] / reps:8.1f} us")
