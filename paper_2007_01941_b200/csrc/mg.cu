@@ -857,7 +857,10 @@ k_aggregate_spec(const int* __restrict__ G_ptr, const int* __restrict__ G_col, c
   double* sval = shh;                                           // AH_NB * AH_B * AH_K
   int* scol = reinterpret_cast<int*>(sval + AH_NB * AH_B * AH_K);  // AH_NB * AH_B * AH_K
   int* slen = scol + AH_NB * AH_B * AH_K;                       // AH_NB * AH_B
-  int* agg = slen + AH_NB * AH_B;                               // n
+  int* sd_ex = slen + AH_NB * AH_B;                             // AH_B * AH_K examined entries
+  int* sd_code = sd_ex + AH_B * AH_K;                           // AH_B * AH_K their state code
+  int* sd_dec = sd_code + AH_B * AH_K;                          // AH_B decisions (-3: none usable)
+  int* agg = sd_dec + AH_B;                                     // n
   int* size = agg + n;                                          // n
   const int lane = threadIdx.x;
   for (int i = lane; i < n; i += 32) {
@@ -880,15 +883,16 @@ k_aggregate_spec(const int* __restrict__ G_ptr, const int* __restrict__ G_col, c
     const int i_me = b * AH_B + lane;
     const int* hc = scol + (slot * AH_B + lane) * AH_K;
     const double* hv = sval + (slot * AH_B + lane) * AH_K;
-    // ---- phase 1: every lane decides its node from the batch-start state
-    int ex[AH_K];     // examined entries (node ids; -1 unused)
-    int exa[AH_K];    // their aggregate at decision time
-    int dec = -1;     // chosen partner / aggregate member
-    bool spec = false;  // a usable speculative decision (false: visit cooperatively at its turn)
+    // ---- phase 1: every lane decides its node from the batch-start state and
+    // records what the decision read: each examined entry with a state code
+    // (-1 unassigned, a assigned to eligible aggregate a, a | 1 << 30 assigned to a
+    // full one -- fixed for good, sizes only grow)
+    int dec = -3;
+    int ex[AH_K], code[AH_K];
 #pragma unroll
     for (int e = 0; e < AH_K; ++e) {
       ex[e] = -1;
-      exa[e] = -1;
+      code[e] = -1;
     }
     if (lane < iend && agg[i_me] < 0) {
       const int len = slen[slot * AH_B + lane];
@@ -910,17 +914,13 @@ k_aggregate_spec(const int* __restrict__ G_ptr, const int* __restrict__ G_col, c
 #pragma unroll
         for (int e = AH_K - 1; e >= 0; --e)
           if (el[e]) f = e;
+        int last = AH_K - 1;
         if (f < 0) {
-          spec = len <= AH_K;  // no eligible neighbour at all: stays unassigned for now
-          // examined: the whole (short) row
-#pragma unroll
-          for (int e = 0; e < AH_K; ++e) {
-            ex[e] = jj[e];
-            exa[e] = aa[e];
-          }
+          if (len <= AH_K) dec = -1;  // no eligible neighbour at all: stays unassigned for now
         } else {
           double gf = gg[f];
-          int cu = -1, last = f;
+          int cu = -1;
+          last = f;
 #pragma unroll
           for (int e = 0; e < AH_K; ++e) {
             if (e >= f && jj[e] >= 0 && gg[e] == gf) {
@@ -929,63 +929,60 @@ k_aggregate_spec(const int* __restrict__ G_ptr, const int* __restrict__ G_col, c
             }
           }
           bool tail = jj[AH_K - 1] >= 0 && gg[AH_K - 1] == gf;
-          if (cu >= 0) {
-            dec = jj[cu];
-            spec = true;
-          } else if (!(tail && len > AH_K)) {
-            dec = jj[f];
-            spec = true;
-          }
-#pragma unroll
-          for (int e = 0; e < AH_K; ++e)
-            if (e <= last) {
-              ex[e] = jj[e];
-              exa[e] = aa[e];
-            }
+          if (cu >= 0) dec = jj[cu];
+          else if (!(tail && len > AH_K)) dec = jj[f];
         }
+#pragma unroll
+        for (int e = 0; e < AH_K; ++e)
+          if (e <= last) {
+            ex[e] = jj[e];
+            code[e] = aa[e] < 0 ? -1 : (el[e] ? aa[e] : (aa[e] | (1 << 30)));
+          }
       }
     }
-    // ---- phase 2: commit in index order
+#pragma unroll
+    for (int e = 0; e < AH_K; ++e) {
+      sd_ex[lane * AH_K + e] = ex[e];
+      sd_code[lane * AH_K + e] = code[e];
+    }
+    sd_dec[lane] = dec;
+    __syncwarp();
+    // ---- phase 2: commit in index order, warp-uniform. At its turn a node's
+    // speculative decision stands iff none of its examined entries changed state
+    // since the batch start: unassigned -> assigned, or eligible -> full (both are
+    // monotone); lanes 0..AH_K-1 check one entry each. Otherwise the node is
+    // visited cooperatively with the current state.
     for (int ii = 0; ii < iend; ++ii) {
       const int i = b * AH_B + ii;
-      __syncwarp();
       if (agg[i] >= 0) continue;  // partnered by an earlier commit (or before the batch)
-      bool ok = __shfl_sync(FULL_MASK, spec ? 1 : 0, ii) != 0;
-      int bj;
+      int bj = sd_dec[ii];
+      bool ok = bj != -3;
       if (ok) {
-        bj = __shfl_sync(FULL_MASK, dec, ii);
-      } else {
+        bool ch = false;
+        if (lane < AH_K) {
+          const int j = sd_ex[ii * AH_K + lane], c = sd_code[ii * AH_K + lane];
+          if (j >= 0) ch = (c < 0) ? (agg[j] >= 0) : (!(c >> 30) && size[c] >= max_size);
+        }
+        ok = __ballot_sync(FULL_MASK, ch) == 0u;
+      }
+      if (!ok)
         bj = agg_visit_coop(i, G_ptr, G_col, G_val, scol + (slot * AH_B + ii) * AH_K,
                             sval + (slot * AH_B + ii) * AH_K, slen[slot * AH_B + ii], agg, size, max_size, lane);
-      }
       if (bj < 0) continue;  // nothing eligible: left for the post-pass
-      int aj = agg[bj];
-      int a_new, sz_new;
-      if (aj < 0) {
-        a_new = nagg;
-        sz_new = 2;
-      } else {
-        a_new = aj;
-        sz_new = size[aj] + 1;
-      }
+      const int aj = agg[bj];
       __syncwarp();
       if (lane == 0) {
-        agg[i] = a_new;
-        if (aj < 0) agg[bj] = a_new;
-        size[a_new] = sz_new;
+        if (aj < 0) {
+          agg[i] = nagg;
+          agg[bj] = nagg;
+          size[nagg] = 2;
+        } else {
+          agg[i] = aj;
+          size[aj] += 1;
+        }
       }
       if (aj < 0) ++nagg;
-      // later lanes whose examined entries this commit touched decide again at their turn
-      const bool became_full = sz_new >= max_size;
-      if (lane > ii && spec) {
-        bool hit = false;
-#pragma unroll
-        for (int e = 0; e < AH_K; ++e) {
-          int j = ex[e];
-          hit |= j >= 0 && (j == i || j == bj || (became_full && exa[e] == a_new));
-        }
-        if (hit) spec = false;
-      }
+      __syncwarp();
     }
     __syncwarp();
     if (b + AH_NB < nbt) ah_issue(b + AH_NB, hcol_g, hval_g, hlen_g, scol, sval, slen, lane);
@@ -1078,7 +1075,8 @@ extern "C" int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t
     }();
     const int n_pad = ((n + AH_B - 1) / AH_B) * AH_B;
     const size_t smh = (size_t)AH_NB * AH_B * AH_K * (sizeof(double) + sizeof(int)) +
-                       (size_t)AH_NB * AH_B * sizeof(int) + 2 * sizeof(int) * (size_t)n;
+                       (size_t)AH_NB * AH_B * sizeof(int) + (size_t)AH_B * (2 * AH_K + 1) * sizeof(int) +
+                       2 * sizeof(int) * (size_t)n;
     if (head_on && smh <= 220 * 1024) {
       int *hcol = nullptr, *hlen = nullptr;
       double* hval = nullptr;

@@ -1,7 +1,7 @@
 """Per-kernel device time of ONE bench step (evaluate + linear solve) at a config,
 after warm-up, from torch.profiler's CUDA activity (dev tool; not a bench number).
 
-  python tools/step_profile.py [config=4] [top=45]
+  python tools/step_profile.py [config=4] [top=45] [detail=kernel,kernel]
 """
 
 import sys
@@ -17,7 +17,7 @@ from paper_2007_01941_b200 import multigrid as MG  # noqa: E402
 from paper_2007_01941_b200 import solver  # noqa: E402
 
 
-def main(config=4, top=45):
+def main(config=4, top=45, detail=""):
     sc = bench.scene_for(int(config))
     prob = P.BundleProblem(*sc.arrays())
     cfg = P.SolveConfig(**bench.CFG)
@@ -54,6 +54,10 @@ def main(config=4, top=45):
         a[0] += 1
         a[1] += e.device_time_total
     tot = sum(v[1] for v in agg.values())
+    for name in filter(None, detail.split(",")):  # individual launches of these kernels, in order
+        evs = sorted((e for e in prof.events() if e.device_type.name == "CUDA" and name in e.name),
+                     key=lambda e: e.time_range.start)
+        print(f"  {name}: " + " ".join(f"{e.device_time_total:.0f}" for e in evs) + " us")
     print(f"config {config}: wall {wall * 1e3:.2f} ms, kernel sum {tot / 1e3:.2f} ms, cg {out[2].iterations}, "
           f"levels {[l.scalar_dim for l in out[6].levels]}")
     for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:int(top)]:
