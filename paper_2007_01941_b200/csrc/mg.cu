@@ -546,7 +546,7 @@ k_aggregate_ring(const int* __restrict__ G_ptr, const int* __restrict__ G_col, c
 // exhaustive scan -- both with the ring kernel's exact rules.
 #define AH_K 8
 #define AH_B 32
-#define AH_NB 8
+#define AH_NB 4
 
 __global__ void k_agg_heads(const int* __restrict__ G_ptr, const int* __restrict__ col_s,
                             const double* __restrict__ val_s, const unsigned* __restrict__ unsorted, int n,
@@ -862,10 +862,14 @@ k_aggregate_spec(const int* __restrict__ G_ptr, const int* __restrict__ G_col, c
   int* sd_dec = sd_code + AH_B * AH_K;                          // AH_B decisions (-3: none usable)
   int* agg = sd_dec + AH_B;                                     // n
   int* size = agg + n;                                          // n
+  unsigned* pmask = reinterpret_cast<unsigned*>(size + n);      // n: lanes of a round pairing with node j
+  unsigned* jmask = pmask + n;                                  // n: lanes of a round joining aggregate a
   const int lane = threadIdx.x;
   for (int i = lane; i < n; i += 32) {
     agg[i] = -1;
     size[i] = 0;
+    pmask[i] = 0u;
+    jmask[i] = 0u;
   }
   const int nbt = (n + AH_B - 1) / AH_B;
 #pragma unroll 1
@@ -875,6 +879,10 @@ k_aggregate_spec(const int* __restrict__ G_ptr, const int* __restrict__ G_col, c
   }
   __syncwarp();
   int nagg = 0;
+  const unsigned lt = (1u << lane) - 1u;
+#ifdef AGG_STATS
+  int st_turn = 0, st_coop = 0, st_nospec = 0;
+#endif
   for (int b = 0; b < nbt; ++b) {
     cp_async_wait<AH_NB - 1>();
     __syncwarp();
@@ -947,48 +955,129 @@ k_aggregate_spec(const int* __restrict__ G_ptr, const int* __restrict__ G_col, c
     }
     sd_dec[lane] = dec;
     __syncwarp();
-    // ---- phase 2: commit in index order, warp-uniform. At its turn a node's
-    // speculative decision stands iff none of its examined entries changed state
-    // since the batch start: unassigned -> assigned, or eligible -> full (both are
-    // monotone); lanes 0..AH_K-1 check one entry each. Otherwise the node is
-    // visited cooperatively with the current state.
-    for (int ii = 0; ii < iend; ++ii) {
-      const int i = b * AH_B + ii;
-      if (agg[i] >= 0) continue;  // partnered by an earlier commit (or before the batch)
-      int bj = sd_dec[ii];
-      bool ok = bj != -3;
-      if (ok) {
+    // ---- phase 2: commit in index order, in rounds. A decision stands iff none of
+    // the entries it read changed state since the batch start (unassigned ->
+    // assigned, eligible -> full; both monotone). A round starts at lane p: every
+    // later lane whose decision still stands publishes its effect (pair with node d:
+    // pmask[d] |= lane bit; join aggregate a: jmask[a] |= lane bit), then each lane
+    // checks the effects of the EARLIER lanes of the round on what it read (an
+    // examined node assigned by an earlier lane's own node or pairing, an examined
+    // aggregate filled by earlier joins, its own node taken as a partner). Lanes
+    // p .. q-1 before the first conflict commit together -- exactly what the
+    // one-at-a-time scan does for them -- and lane q is resolved alone with the
+    // current state (cooperative visit if its decision no longer stands).
+    int p = 0;
+    while (p < iend) {
+      const bool inr = lane >= p && lane < iend;
+      const bool assigned = inr && agg[i_me] >= 0;
+      const int d = sd_dec[lane];
+      bool pend = inr && !assigned && d != -3;
+      if (pend) {
         bool ch = false;
-        if (lane < AH_K) {
-          const int j = sd_ex[ii * AH_K + lane], c = sd_code[ii * AH_K + lane];
-          if (j >= 0) ch = (c < 0) ? (agg[j] >= 0) : (!(c >> 30) && size[c] >= max_size);
-        }
-        ok = __ballot_sync(FULL_MASK, ch) == 0u;
+#pragma unroll
+        for (int e = 0; e < AH_K; ++e)
+          if (ex[e] >= 0) ch |= (code[e] < 0) ? (agg[ex[e]] >= 0) : (!(code[e] >> 30) && size[code[e]] >= max_size);
+        pend = !ch;
       }
-      if (!ok)
-        bj = agg_visit_coop(i, G_ptr, G_col, G_val, scol + (slot * AH_B + ii) * AH_K,
-                            sval + (slot * AH_B + ii) * AH_K, slen[slot * AH_B + ii], agg, size, max_size, lane);
-      if (bj < 0) continue;  // nothing eligible: left for the post-pass
-      const int aj = agg[bj];
+      int tgt = -1;
+      bool pair = false;
+      if (pend && d >= 0) {
+        const int a = agg[d];
+        pair = a < 0;
+        tgt = pair ? d : a;
+        if (pair) atomicOr(pmask + d, 1u << lane);
+        else atomicOr(jmask + a, 1u << lane);
+      }
+      const unsigned C = __ballot_sync(FULL_MASK, pend && d >= 0);  // lanes whose commit changes state
       __syncwarp();
-      if (lane == 0) {
-        if (aj < 0) {
-          agg[i] = nagg;
-          agg[bj] = nagg;
-          size[nagg] = 2;
+      bool conflict = inr && !assigned && !pend;
+      if (pend) {
+        if (pmask[i_me] & lt) conflict = true;  // taken as an earlier lane's partner
+#pragma unroll
+        for (int e = 0; e < AH_K; ++e) {
+          const int j = ex[e];
+          if (j < 0) continue;
+          const int l = j - b * AH_B;
+          if (l >= 0 && l < lane && ((C >> l) & 1u)) conflict = true;  // node of an earlier committer
+          if (pmask[j] & lt) conflict = true;                          // an earlier lane's partner
+          const int c = code[e];
+          if (c >= 0 && !(c >> 30) && __popc(jmask[c] & lt) >= max_size - size[c]) conflict = true;
+        }
+      }
+      const unsigned cm = __ballot_sync(FULL_MASK, conflict);
+      const int q = cm ? __ffs(cm) - 1 : iend;
+      const unsigned range = (q >= 32 ? 0xffffffffu : ((1u << q) - 1u)) & ~((1u << p) - 1u);
+      const unsigned pairs = __ballot_sync(FULL_MASK, pend && d >= 0 && pair) & range;
+      __syncwarp();
+      if (((range >> lane) & 1u) && pend && d >= 0) {
+        if (pair) {
+          const int id = nagg + __popc(pairs & lt);
+          agg[i_me] = id;
+          agg[d] = id;
+          size[id] = 2;
         } else {
-          agg[i] = aj;
-          size[aj] += 1;
+          agg[i_me] = tgt;
+          const unsigned jm = jmask[tgt] & range;
+          if (lane == __ffs(jm) - 1) size[tgt] += __popc(jm);
         }
       }
-      if (aj < 0) ++nagg;
+      nagg += __popc(pairs);
       __syncwarp();
+      if (pend && d >= 0) {
+        if (pair) pmask[d] = 0u;
+        else jmask[tgt] = 0u;
+      }
+      __syncwarp();
+#ifdef AGG_STATS
+      ++st_turn;
+#endif
+      if (q < iend) {  // lane q alone, with the current state
+        const int ii = q, i = b * AH_B + q;
+        if (agg[i] < 0) {
+          int bj = sd_dec[ii];
+          bool ok = bj != -3;
+          if (ok) {
+            bool ch = false;
+            if (lane < AH_K) {
+              const int jx = sd_ex[ii * AH_K + lane], c = sd_code[ii * AH_K + lane];
+              if (jx >= 0) ch = (c < 0) ? (agg[jx] >= 0) : (!(c >> 30) && size[c] >= max_size);
+            }
+            ok = __ballot_sync(FULL_MASK, ch) == 0u;
+          }
+#ifdef AGG_STATS
+          if (!ok) ++st_coop;
+#endif
+          if (!ok)
+            bj = agg_visit_coop(i, G_ptr, G_col, G_val, scol + (slot * AH_B + ii) * AH_K,
+                                sval + (slot * AH_B + ii) * AH_K, slen[slot * AH_B + ii], agg, size, max_size, lane);
+          if (bj >= 0) {
+            const int aj = agg[bj];
+            __syncwarp();
+            if (lane == 0) {
+              if (aj < 0) {
+                agg[i] = nagg;
+                agg[bj] = nagg;
+                size[nagg] = 2;
+              } else {
+                agg[i] = aj;
+                size[aj] += 1;
+              }
+            }
+            if (aj < 0) ++nagg;
+          }
+        }
+        __syncwarp();
+      }
+      p = q + 1;
     }
     __syncwarp();
     if (b + AH_NB < nbt) ah_issue(b + AH_NB, hcol_g, hval_g, hlen_g, scol, sval, slen, lane);
     else cp_async_commit();
   }
   cp_async_wait<0>();
+#ifdef AGG_STATS
+  if (lane == 0) printf("agg_spec n=%d turns=%d coop=%d nospec=%d\n", n, st_turn, st_coop, st_nospec);
+#endif
   // post-pass over leftovers in index order (multigrid.py:164-175)
   for (int i = 0; i < n; ++i) {
     __syncwarp();
@@ -1076,8 +1165,15 @@ extern "C" int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t
     const int n_pad = ((n + AH_B - 1) / AH_B) * AH_B;
     const size_t smh = (size_t)AH_NB * AH_B * AH_K * (sizeof(double) + sizeof(int)) +
                        (size_t)AH_NB * AH_B * sizeof(int) + (size_t)AH_B * (2 * AH_K + 1) * sizeof(int) +
-                       2 * sizeof(int) * (size_t)n;
-    if (head_on && smh <= 220 * 1024) {
+                       4 * sizeof(int) * (size_t)n;
+    static int smem_optin = 0;
+    if (!smem_optin) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+        smem_optin = 220 * 1024;
+    }
+    if (head_on && smh <= (size_t)smem_optin) {
       int *hcol = nullptr, *hlen = nullptr;
       double* hval = nullptr;
       BAMG_CUDA_CHECK(cudaMallocAsync(&hcol, sizeof(int) * (size_t)n_pad * AH_K, st));
