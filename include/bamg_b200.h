@@ -101,6 +101,15 @@ int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_l
                       const double* g_pt, const double* d_cam, const double* d_pt, int32_t nc, int32_t npt,
                       double* A, double* C, double* Cinv, double* Cb, double* qo, double* rhs,
                       int32_t* bad_min_dev, void* stream);
+/* A = A_raw + diag(d) (bs x bs blocks): the damped camera blocks, formed on demand */
+int bamg_add_block_diag(bamg_ctx* ctx, const double* raw, const double* d, int32_t n, int32_t bs, double* out,
+                        void* stream);
+/* One camera-major pass over the records (schur.py:38-47, 99-125, 128-144): dA = diag(sum F^T F)
+ * (dA_raw, optional), D = clip(dA, 1e-6, 1e32) / radius (d_cam, optional), and with S != NULL the
+ * diagonal blocks S[dpos[i]] = sum F^T (I - H E^T) F + D and rhs = -sum F^T (r + q) (optional). */
+int bamg_camera_pass(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const double* J, const double* qo,
+                     int32_t nc, double radius, const int32_t* dpos, double* S, double* rhs, double* d_cam,
+                     double* dA_raw, void* stream);
 /* rhs == NULL in bamg_build_system skips the right-hand side (formed later by
  * bamg_rhs_gather, or by bamg_schur_numeric's diagonal pass in the same sweep) */
 int bamg_rhs_gather(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const double* J, const double* qo,

@@ -715,6 +715,16 @@ __global__ void k_add_diag(const double* __restrict__ raw, const double* __restr
   }
 }
 
+// A = A_raw + diag(d) for n blocks of size bs (the damped camera blocks on demand)
+extern "C" int bamg_add_block_diag(bamg_ctx* ctx, const double* raw, const double* d, int32_t n, int32_t bs,
+                                   double* out, void* stream) {
+  (void)ctx;
+  if (n > 0)
+    launch(k_add_diag, grid_for((int64_t)n * bs * bs, 256), 256, 0, as_stream(stream), raw, d, n, bs, out);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
 // 3x3 Cholesky + L^-T L^-1 (blockmat.py:95-115). Returns false if not PD.
 __device__ __forceinline__ bool chol_inv3(const double* C, double* Ci) {
   double l00 = C[0];

@@ -1493,3 +1493,208 @@ extern "C" int bamg_schur_numeric_chunked(bamg_ctx* ctx, const int32_t* cam_ptr,
   return 0;
 }
 
+
+// ---------------------------------------------------------------------------
+// One camera-major pass for everything the camera side of a linear solve needs
+// from the observation records (schur.py:38-47, 99-125, 128-144):
+//   dA_i  = diag(sum_o F_o^T F_o)                 (normal_diagonal, problem.py:262-269)
+//   D_i   = clip(dA_i, 1e-6, 1e32) / radius        (Damping.from_jacobian)
+//   S_ii  = sum_o F_o^T (I - H_o E_o^T) F_o + D_i  (= A_i + D_i - sum W C^-1 W^T, one sum)
+//   rhs_i = -sum_o F_o^T (r_o + q_o)               (= -g_i - sum W C^-1 b_p)
+// Three lanes per observation, ten observations per warp step; lane (g, c) owns
+// columns 3c..3c+2 of the 9x9 block (27 accumulators instead of the 45 + 9 + 9 a lane
+// per observation would hold, so the pass runs at 4 CTAs / SM instead of 1). The
+// records (all 16 pieces) and q stream through a CF_STAGES-deep cp.async pipeline;
+// at the end the ten groups' partials are added in group order (deterministic).
+// WITH_S = false: only dA / D (the damping of a Jacobian whose S is not assembled).
+#define CF_G 10
+#define CF_P 17                   // 16 record pieces + q
+#define CF_PD (CF_P * CF_G * 2)   // doubles per stage
+#ifndef CF_STAGES
+#define CF_STAGES 4
+#endif
+
+#ifndef CF_MINB
+#define CF_MINB 3
+#endif
+template <bool WITH_S>
+__global__ void __launch_bounds__(128, CF_MINB)
+k_cam_fused(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, const double* __restrict__ J,
+            const double* __restrict__ qo, int nc, double radius, const int* __restrict__ dpos,
+            double* __restrict__ S, double* __restrict__ rhs, double* __restrict__ d_cam,
+            double* __restrict__ dA_out) {
+  extern __shared__ __align__(16) double cf_smem[];
+  const int lane = threadIdx.x & 31;
+  double* wbuf = cf_smem + (size_t)(threadIdx.x >> 5) * CF_STAGES * CF_PD;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int g = lane / 3, c = lane - 3 * (lane / 3);
+  // copy slots: 10 obs x 17 pieces = 170 chunks, 6 per lane (the piece of slot s is fixed)
+  auto issue = [&](int q_lo, int q_hi, int idx_lane, double* buf) {
+#pragma unroll
+    for (int it = 0; it < 6; ++it) {
+      const int s = lane + 32 * it;
+      const int ob = s / CF_P, pc = s - CF_P * (s / CF_P);
+      const int o = __shfl_sync(FULL_MASK, idx_lane, ob < CF_G ? ob : 0);
+      if (s < CF_P * CF_G && q_lo + ob < q_hi && (WITH_S || pc < 9)) {
+        const double* src = pc < 16 ? J + (int64_t)o * REC + 2 * pc : qo + 2 * (int64_t)o;
+        cp_async16(buf + pc * (2 * CF_G) + 2 * ob, src);
+      }
+    }
+    cp_async_commit();
+  };
+  for (int i = warp; i < nc; i += nwarps) {
+    const int q0 = cam_ptr[i], q1 = cam_ptr[i + 1];
+    double acc[27], dA[3], rr[3];
+#pragma unroll
+    for (int t = 0; t < 27; ++t) acc[t] = 0.0;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) dA[t] = rr[t] = 0.0;
+    // observation ids: lane l < 10 holds obs l of a step; CF_STAGES - 1 steps issued ahead
+    int nidx = 0;
+#pragma unroll
+    for (int t = 0; t < CF_STAGES - 1; ++t) {
+      const int b = q0 + CF_G * t;
+      const int id = (lane < CF_G && b + lane < q1) ? cm_list[b + lane] : 0;
+      if (b < q1) issue(b, q1, id, wbuf + t * CF_PD);
+      else cp_async_commit();
+    }
+    {
+      const int b = q0 + CF_G * (CF_STAGES - 1);
+      nidx = (lane < CF_G && b + lane < q1) ? cm_list[b + lane] : 0;
+    }
+    int st = 0;
+    for (int base = q0; base < q1; base += CF_G, ++st) {
+      const int nb = base + CF_G * (CF_STAGES - 1);
+      if (nb < q1) issue(nb, q1, nidx, wbuf + ((st + CF_STAGES - 1) % CF_STAGES) * CF_PD);
+      else cp_async_commit();
+      {
+        const int b = nb + CF_G;
+        nidx = (lane < CF_G && b + lane < q1) ? cm_list[b + lane] : 0;
+      }
+      cp_async_wait<CF_STAGES - 1>();
+      __syncwarp();
+      if (g < CF_G && base + g < q1) {
+        const double* bf = wbuf + (st % CF_STAGES) * CF_PD + 2 * g;
+        auto pcv = [&](int pc) { return *reinterpret_cast<const double2*>(bf + pc * (2 * CF_G)); };
+        double f[18];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+          double2 v = pcv(k);
+          f[2 * k] = v.x;
+          f[2 * k + 1] = v.y;
+        }
+        // own columns of F (rows 0 and 1)
+        double f0[3], f1[3];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {  // selects, not a dynamic index (keeps f in registers)
+          f0[t] = c == 0 ? f[t] : (c == 1 ? f[3 + t] : f[6 + t]);
+          f1[t] = c == 0 ? f[9 + t] : (c == 1 ? f[12 + t] : f[15 + t]);
+          dA[t] += f0[t] * f0[t] + f1[t] * f1[t];
+        }
+        if constexpr (WITH_S) {
+          double e[6], h[6];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            double2 ve = pcv(RE / 2 + k), vh = pcv(RH / 2 + k);
+            e[2 * k] = ve.x;
+            e[2 * k + 1] = ve.y;
+            h[2 * k] = vh.x;
+            h[2 * k + 1] = vh.y;
+          }
+          const double2 r = pcv(RR / 2), q = pcv(16);
+          const double u0 = r.x + q.x, u1 = r.y + q.y;
+#pragma unroll
+          for (int t = 0; t < 3; ++t) rr[t] += f0[t] * u0 + f1[t] * u1;
+          // G' = I - H E^T
+          const double m00 = 1.0 - (h[0] * e[0] + h[1] * e[1] + h[2] * e[2]);
+          const double m01 = -(h[0] * e[3] + h[1] * e[4] + h[2] * e[5]);
+          const double m10 = -(h[3] * e[0] + h[4] * e[1] + h[5] * e[2]);
+          const double m11 = 1.0 - (h[3] * e[3] + h[4] * e[4] + h[5] * e[5]);
+          double z0[3], z1[3];
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            z0[t] = m00 * f0[t] + m01 * f1[t];
+            z1[t] = m10 * f0[t] + m11 * f1[t];
+          }
+#pragma unroll
+          for (int j = 0; j < 9; ++j)
+#pragma unroll
+            for (int t = 0; t < 3; ++t) acc[j * 3 + t] += f[j] * z0[t] + f[9 + j] * z1[t];
+        }
+      }
+      __syncwarp();
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+    // group partials -> shared memory (the stage buffers are free now), added in group order
+    constexpr int NV = WITH_S ? 33 : 3;
+    double* red = wbuf;  // [CF_G][3][NV]
+    if (g < CF_G) {
+      double* my = red + (g * 3 + c) * NV;
+#pragma unroll
+      for (int t = 0; t < 3; ++t) my[t] = dA[t];
+      if constexpr (WITH_S) {
+#pragma unroll
+        for (int t = 0; t < 3; ++t) my[3 + t] = rr[t];
+#pragma unroll
+        for (int t = 0; t < 27; ++t) my[6 + t] = acc[t];
+      }
+    }
+    __syncwarp();
+    // lane l < 9: column l -- its raw diagonal, damping, rhs, and its column of S_ii
+    if (lane < 9) {
+      const int cc = lane / 3, t = lane - 3 * (lane / 3);
+      double da = 0.0, rv = 0.0;
+      for (int gg = 0; gg < CF_G; ++gg) {
+        const double* p = red + (gg * 3 + cc) * NV;
+        da += p[t];
+        if constexpr (WITH_S) rv += p[3 + t];
+      }
+      double d = fmin(fmax(da, 1e-6), 1e32);
+      if (d != d) d = da;
+      d = d / radius;
+      if (d_cam) d_cam[(int64_t)i * 9 + lane] = d;
+      if (dA_out) dA_out[(int64_t)i * 9 + lane] = da;
+      if constexpr (WITH_S) {
+        if (rhs) rhs[(int64_t)i * 9 + lane] = -rv;
+        // S_ii[j][l], j <= l, from column l's owner; mirrored to [l][j]
+        double* out = S + (int64_t)dpos[i] * 81;
+        for (int j = 0; j <= lane; ++j) {
+          double v = 0.0;
+          for (int gg = 0; gg < CF_G; ++gg) v += red[(gg * 3 + cc) * NV + 6 + j * 3 + t];
+          if (j == lane) v += d;
+          out[j * 9 + lane] = v;
+          out[lane * 9 + j] = v;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+extern "C" int bamg_camera_pass(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const double* J,
+                                const double* qo, int32_t nc, double radius, const int32_t* dpos, double* S,
+                                double* rhs, double* d_cam, double* dA_raw, void* stream) {
+  (void)ctx;
+  cudaStream_t st = as_stream(stream);
+  if (nc <= 0) return 0;
+  const size_t sm = sizeof(double) * 4 * CF_STAGES * CF_PD;
+  static bool attr[2] = {false, false};
+  const int g = grid_for((int64_t)nc * 32, 128, 16);
+  if (S) {
+    if (!attr[1]) {
+      BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_cam_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      attr[1] = true;
+    }
+    launch(k_cam_fused<true>, g, 128, sm, st, cam_ptr, cm_list, J, qo, nc, radius, dpos, S, rhs, d_cam, dA_raw);
+  } else {
+    if (!attr[0]) {
+      BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_cam_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      attr[0] = true;
+    }
+    launch(k_cam_fused<false>, g, 128, sm, st, cam_ptr, cm_list, J, qo, nc, radius, dpos, S, rhs, d_cam, dA_raw);
+  }
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}

@@ -37,6 +37,12 @@ def _schur_diagonal_blocks(sys: SchurSystem):
     out = D.empty(nc, CAMERA_SIZE, CAMERA_SIZE)
     dpos = torch.arange(nc, device=D.dev(), dtype=torch.int32)
     sys._own_H()
+    if sys._damping is not None and sys._A is None:  # one camera-major pass: S_ii, rhs, damping
+        # (a materialised A is authoritative: the caller may have changed it)
+        from .schur import _camera_pass
+
+        _camera_pass(sys, dpos, out)
+        return out
     D.call("bamg_schur_numeric", st.cam_ptr, st.cm_list, sys._jac._J, sys.A.blocks, dpos, nc,
            None, None, 0, None, None, None, None, None, None, out)
     return out

@@ -440,6 +440,7 @@ class JacobianBlocks:
         self.n_cameras, self.n_points = n_cameras, n_points
         self.cam_index, self.pt_index = cam_index, pt_index
         self._normal = None
+        self._pnormal = None
         self._h_owner = None  # weakref to the SchurSystem whose C^-1 produced the H slots
 
     @property
@@ -458,16 +459,28 @@ class JacobianBlocks:
     def weight(self):
         return self._st.to_input_order(self._w.reshape(-1, 1)).reshape(-1)
 
-    def normal_blocks(self):
-        """(A_raw (nc,9,9), g_cam (nc,9), C_raw (np,3,3), g_pt (np,3)) -- undamped."""
-        if self._normal is None:
-            nc, npt = self.n_cameras, self.n_points
-            A = D.empty(nc, 9, 9)
-            gc = D.empty(nc, 9)
+    def point_normal(self):
+        """(C_raw (np,3,3), g_pt (np,3)): the point half of normal_blocks (point-major pass)."""
+        if self._pnormal is None:
+            npt = self.n_points
             C = D.empty(npt, 3, 3)
             gp = D.empty(npt, 3)
             st = self._st
-            D.call("bamg_normal_blocks", st.cam_ptr, st.cm_list, st.pt_ptr, self._J, nc, npt, A, gc, C, gp)
+            D.call("bamg_normal_blocks", st.cam_ptr, st.cm_list, st.pt_ptr, self._J, 0, npt, None, None, C, gp)
+            self._pnormal = (C, gp)
+        return self._pnormal
+
+    def normal_blocks(self):
+        """(A_raw (nc,9,9), g_cam (nc,9), C_raw (np,3,3), g_pt (np,3)) -- undamped. The
+        linear solve does not need the camera blocks themselves (its camera-major pass
+        forms D, S_ii and the right-hand side directly); they are formed here on demand."""
+        if self._normal is None:
+            nc = self.n_cameras
+            A = D.empty(nc, 9, 9)
+            gc = D.empty(nc, 9)
+            C, gp = self.point_normal()
+            st = self._st
+            D.call("bamg_normal_blocks", st.cam_ptr, st.cm_list, st.pt_ptr, self._J, nc, 0, A, gc, None, None)
             self._normal = (A, gc, C, gp)
         return self._normal
 

@@ -23,22 +23,40 @@ _DIAG_MAX = 1e32  # schur.py:22
 
 
 class Damping:
-    """Additive diagonal scaled by the trust radius (schur.py:25-55)."""
+    """Additive diagonal scaled by the trust radius (schur.py:25-55).
 
-    def __init__(self, radius, cam_diag, pt_diag):
+    The camera half is formed lazily: the explicit assembly's camera-major pass
+    produces it alongside S_ii (no separate pass over the records); reading
+    ``cam_diag`` before that runs a diagonal-only camera pass."""
+
+    def __init__(self, radius, cam_diag, pt_diag, jac=None):
         self.radius = radius
-        self.cam_diag = cam_diag
+        self._cam = cam_diag
         self.pt_diag = pt_diag
+        self._jac = jac
+
+    @property
+    def cam_diag(self):
+        if self._cam is None:
+            jac, st = self._jac, self._jac._st
+            dc = D.empty(jac.n_cameras, CAMERA_SIZE)
+            D.call("bamg_camera_pass", st.cam_ptr, st.cm_list, jac._J, None, jac.n_cameras, float(self.radius), None,
+                   None, None, dc, None)
+            self._cam = dc
+        return self._cam
+
+    @cam_diag.setter
+    def cam_diag(self, value):
+        self._cam = value
 
     @staticmethod
     def from_jacobian(jac: JacobianBlocks, radius: float) -> "Damping":
         if not radius > 0:
             raise ValueError(f"trust radius must be positive, got {radius}")
-        A, _, C, _ = jac.normal_blocks()
-        dc = D.empty(jac.n_cameras, CAMERA_SIZE)
+        C, _ = jac.point_normal()
         dp = D.empty(jac.n_points, POINT_SIZE)
-        D.call("bamg_damping", A, C, jac.n_cameras, jac.n_points, float(radius), dc, dp)
-        return Damping(radius, dc, dp)
+        D.call("bamg_damping", None, C, 0, jac.n_points, float(radius), None, dp)
+        return Damping(radius, None, dp, jac)
 
     @staticmethod
     def zero(n_cameras: int, n_points: int) -> "Damping":
@@ -48,8 +66,9 @@ class Damping:
 class SchurSystem:
     """Block factors after point elimination (schur.py:58-96)."""
 
-    def __init__(self, A, C, rhs_cam, grad_pt, jac, Cb, mode="implicit"):
-        self.A = A
+    def __init__(self, A, C, rhs_cam, grad_pt, jac, Cb, mode="implicit", damping=None):
+        self._A = A  # None: A_raw + D formed on first use (the explicit path never needs it)
+        self._damping = damping
         self.C = C
         self._rhs = rhs_cam  # None: formed on first use, or by the explicit assembly's diagonal pass
         self.grad_pt = grad_pt
@@ -80,8 +99,21 @@ class SchurSystem:
         self._rhs = value
 
     @property
+    def A(self) -> BlockDiagMatrix:
+        if self._A is None:
+            A_raw, _, _, _ = self._jac.normal_blocks()
+            A = D.empty(self.n_cameras, CAMERA_SIZE, CAMERA_SIZE)
+            D.call("bamg_add_block_diag", A_raw, self._damping.cam_diag, self.n_cameras, CAMERA_SIZE, A)
+            self._A = BlockDiagMatrix(A)
+        return self._A
+
+    @A.setter
+    def A(self, value):
+        self._A = value
+
+    @property
     def n_cameras(self) -> int:
-        return self.A.n_blocks
+        return self._jac.n_cameras
 
     @property
     def n_points(self) -> int:
@@ -136,24 +168,24 @@ class SchurSystem:
 
 def build_system(jac: JacobianBlocks, damping: Damping) -> SchurSystem:
     """Assemble A, C (factored), rhs and the point gradient (schur.py:99-125)."""
-    nc, npt = jac.n_cameras, jac.n_points
+    npt = jac.n_points
     st = jac._st
-    A_raw, gc, C_raw, gp = jac.normal_blocks()
-    A = D.empty(nc, 9, 9)
+    C_raw, gp = jac.point_normal()
     C = D.empty(npt, 3, 3)
     Cinv = D.empty(npt, 3, 3)
     Cb = D.empty(npt, 3)
     qo = D.empty(max(st.k, 1), 2)
     bad = D.empty(1, dtype=torch.int32)
-    D.call("bamg_build_system", st.cam_ptr, st.cm_list, st.pt_ptr, jac._J, st.k, A_raw, C_raw, gc, gp,
-           damping.cam_diag, damping.pt_diag, nc, npt, A, C, Cinv, Cb, qo, None, bad)
+    # point half only: the damped camera blocks A are formed on demand (SchurSystem.A)
+    D.call("bamg_build_system", st.cam_ptr, st.cm_list, st.pt_ptr, jac._J, st.k, None, C_raw, None, gp,
+           None, damping.pt_diag, 0, npt, None, C, Cinv, Cb, qo, None, bad)
     b = int(bad.item())
     if b != 0x7FFFFFFF:
         raise IndefiniteBlockError(b)
     grad_pt = D.empty(npt * POINT_SIZE)
     D.call("bamg_negate", gp, grad_pt, npt * POINT_SIZE)
     Cm = BlockDiagMatrix(C, _inv=Cinv)
-    s = SchurSystem(BlockDiagMatrix(A), Cm, None, grad_pt, jac, Cb)
+    s = SchurSystem(None, Cm, None, grad_pt, jac, Cb, damping=damping)
     s._qo = qo
     jac._h_owner = weakref.ref(s)  # weak: no jac <-> system reference cycle
     return s
@@ -171,29 +203,40 @@ def schur_explicit(sys: SchurSystem, variant: str = "pairs") -> BlockSparseMatri
     blocks = D.empty(nnz, CAMERA_SIZE, CAMERA_SIZE)
     J = sys._jac
     sys._own_H()
+    # a materialised A is authoritative (the caller may have changed it): then the
+    # assembly's own diagonal pass runs on it
+    fused = sys._damping is not None and sys._A is None and variant in ("chunks", "pairs")
+    if fused:  # diagonal blocks, right-hand side and camera damping in one camera-major pass
+        _camera_pass(sys, st.pair_lists["dpos"] if variant == "pairs" else st.chunk_plan["dpos"], blocks)
+    nc_diag = 0 if fused else sys.n_cameras  # otherwise the assembly's own diagonal pass (needs A)
     if variant == "chunks":
         ch = st.chunk_plan
         rhs = None
-        if sys._rhs is None:
-            rhs = D.empty(sys.n_cameras * CAMERA_SIZE)
-        _, gc, _, _ = J.normal_blocks()
-        D.call("bamg_schur_numeric_chunked", st.cam_ptr, st.cm_list, J._J, sys.A.blocks, ch["dpos"], sys.n_cameras,
-               ch["work"], ch["n_work"], ch["pair_a"], ch["pair_b"], ch["done"], nnz, sys._qo, gc, rhs, blocks)
+        gc = None
+        if not fused:
+            _, gc, _, _ = J.normal_blocks()
+            if sys._rhs is None:
+                rhs = D.empty(sys.n_cameras * CAMERA_SIZE)
+        D.call("bamg_schur_numeric_chunked", st.cam_ptr, st.cm_list, J._J, None if fused else sys.A.blocks,
+               ch["dpos"], nc_diag, ch["work"], ch["n_work"], ch["pair_a"], ch["pair_b"], ch["done"], nnz, sys._qo,
+               gc, rhs, blocks)
         if rhs is not None:
             sys._rhs = rhs
     elif variant == "rows":
         sym = st.symbolic
         D.call("bamg_schur_numeric_rows", st.cam_ptr, st.cm_list, st.pt_ptr, st.obs_cam_pm, st.obs_pt_pm, J._J,
                sys.A.blocks, S_ptr, S_col, sym["dpos"], sym["up_off"], sym["up_tpos"], sys.n_cameras, blocks)
-    else:
+    else:  # off-diagonal blocks from the per-block pair lists
         sym = st.pair_lists
         rhs = None
-        if sys._rhs is None:  # the diagonal pass forms the right-hand side in the same sweep
-            rhs = D.empty(sys.n_cameras * CAMERA_SIZE)
-        _, gc, _, _ = J.normal_blocks()
-        D.call("bamg_schur_numeric", st.cam_ptr, st.cm_list, J._J, sys.A.blocks, sym["dpos"],
-               sys.n_cameras, sym["up_blk"], sym["up_tpos"], sym["n_up"], sym["blk_ptr"], sym["pair_a"],
-               sym["pair_b"], sys._qo, gc, rhs, blocks)
+        gc = None
+        if not fused:
+            _, gc, _, _ = J.normal_blocks()
+            if sys._rhs is None:
+                rhs = D.empty(sys.n_cameras * CAMERA_SIZE)
+        D.call("bamg_schur_numeric", st.cam_ptr, st.cm_list, J._J, None if fused else sys.A.blocks, sym["dpos"],
+               nc_diag, sym["up_blk"], sym["up_tpos"], sym["n_up"], sym["blk_ptr"], sym["pair_a"], sym["pair_b"],
+               sys._qo, gc, rhs, blocks)
         if rhs is not None:
             sys._rhs = rhs
     S = BlockSparseMatrix(sys.n_cameras, sys.n_cameras, CAMERA_SIZE, CAMERA_SIZE, S_ptr, S_col, blocks,
@@ -201,6 +244,20 @@ def schur_explicit(sys: SchurSystem, variant: str = "pairs") -> BlockSparseMatri
     if _SYMMETRIC:
         S._symop = st.symop  # S_ji == S_ij^T bit for bit: half-storage products
     return S
+
+
+def _camera_pass(sys: SchurSystem, dpos, blocks):
+    """Diagonal blocks S_ii, the right-hand side and (if still pending) the camera
+    damping in one camera-major pass over the records (bamg_camera_pass)."""
+    st, J, dmp = sys._jac._st, sys._jac, sys._damping
+    rhs = D.empty(sys.n_cameras * CAMERA_SIZE) if sys._rhs is None else None
+    dc = D.empty(sys.n_cameras, CAMERA_SIZE) if dmp is not None and dmp._cam is None else None
+    D.call("bamg_camera_pass", st.cam_ptr, st.cm_list, J._J, sys._qo, sys.n_cameras, float(dmp.radius), dpos, blocks,
+           rhs, dc, None)
+    if rhs is not None:
+        sys._rhs = rhs
+    if dc is not None:
+        dmp._cam = dc
 
 
 _SYMMETRIC = __import__("os").environ.get("BAMG_SYM_SPMV", "1") == "1"
@@ -218,7 +275,8 @@ def covisibility_block_count(sys: SchurSystem) -> int:
 def choose_mode(sys: SchurSystem) -> str:
     """Cheaper matvec route by stored-entry flop count; ties explicit (schur.py:162-168)."""
     explicit_cost = 2 * covisibility_block_count(sys) * CAMERA_SIZE**2
-    implicit_cost = 2 * (sys.A.nnz_scalar() + 2 * sys._jac._st.k * CAMERA_SIZE * POINT_SIZE + sys.C.nnz_scalar())
+    a_nnz = sys.n_cameras * CAMERA_SIZE**2  # sys.A.nnz_scalar() without forming A
+    implicit_cost = 2 * (a_nnz + 2 * sys._jac._st.k * CAMERA_SIZE * POINT_SIZE + sys.C.nnz_scalar())
     return "explicit" if explicit_cost <= implicit_cost else "implicit"
 
 
