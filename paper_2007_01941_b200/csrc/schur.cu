@@ -1511,7 +1511,7 @@ extern "C" int bamg_schur_numeric_chunked(bamg_ctx* ctx, const int32_t* cam_ptr,
 #define CF_P 17                   // 16 record pieces + q
 #define CF_PD (CF_P * CF_G * 2)   // doubles per stage
 #ifndef CF_STAGES
-#define CF_STAGES 4
+#define CF_STAGES 6
 #endif
 
 #ifndef CF_MINB
@@ -1529,16 +1529,25 @@ k_cam_fused(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, co
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int g = lane / 3, c = lane - 3 * (lane / 3);
-  // copy slots: 10 obs x 17 pieces = 170 chunks, 6 per lane (the piece of slot s is fixed)
+  // copy slots: 10 obs x 17 pieces = 170 chunks, 6 per lane; slot s = lane + 32 it has a
+  // fixed (observation, piece), decoded once
+  int s_ob[6], s_pc[6], s_dst[6];
+#pragma unroll
+  for (int it = 0; it < 6; ++it) {
+    const int s = lane + 32 * it;
+    s_ob[it] = s < CF_P * CF_G ? s / CF_P : (1 << 20);  // no slot
+    s_pc[it] = s - CF_P * (s / CF_P);
+    s_dst[it] = s_pc[it] * (2 * CF_G) + 2 * s_ob[it];
+  }
   auto issue = [&](int q_lo, int q_hi, int idx_lane, double* buf) {
+    const int nval = q_hi - q_lo;  // observations of this step (>= 1)
 #pragma unroll
     for (int it = 0; it < 6; ++it) {
-      const int s = lane + 32 * it;
-      const int ob = s / CF_P, pc = s - CF_P * (s / CF_P);
+      const int ob = s_ob[it], pc = s_pc[it];
       const int o = __shfl_sync(FULL_MASK, idx_lane, ob < CF_G ? ob : 0);
-      if (s < CF_P * CF_G && q_lo + ob < q_hi && (WITH_S || pc < 9)) {
+      if (ob < nval && (WITH_S || pc < 9)) {
         const double* src = pc < 16 ? J + (int64_t)o * REC + 2 * pc : qo + 2 * (int64_t)o;
-        cp_async16(buf + pc * (2 * CF_G) + 2 * ob, src);
+        cp_async16(buf + s_dst[it], src);
       }
     }
     cp_async_commit();
@@ -1584,12 +1593,14 @@ k_cam_fused(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list, co
           f[2 * k] = v.x;
           f[2 * k + 1] = v.y;
         }
-        // own columns of F (rows 0 and 1)
+        // own columns of F (rows 0 and 1), read again from shared memory (element e of
+        // the flattened F sits at piece e / 2, half e % 2)
         double f0[3], f1[3];
 #pragma unroll
-        for (int t = 0; t < 3; ++t) {  // selects, not a dynamic index (keeps f in registers)
-          f0[t] = c == 0 ? f[t] : (c == 1 ? f[3 + t] : f[6 + t]);
-          f1[t] = c == 0 ? f[9 + t] : (c == 1 ? f[12 + t] : f[15 + t]);
+        for (int t = 0; t < 3; ++t) {
+          const int e0 = 3 * c + t, e1 = 9 + 3 * c + t;
+          f0[t] = bf[(e0 >> 1) * (2 * CF_G) + (e0 & 1)];
+          f1[t] = bf[(e1 >> 1) * (2 * CF_G) + (e1 & 1)];
           dA[t] += f0[t] * f0[t] + f1[t] * f1[t];
         }
         if constexpr (WITH_S) {
