@@ -359,6 +359,11 @@ int32_t bamg_mg_level_kind(const bamg_mg* mg, int32_t level);
  * blocks when mg == NULL); one host synchronisation per iteration. err codes:
  * 1 PreconditionerNotSPD, 2/3/4/5 CgDivergence (operator non-finite / curvature /
  * residual non-finite / preconditioner non-finite). */
+/* optional: build the PCG graph of a later bamg_pcg_run with the same arguments now (host
+ * capture / re-target overlaps device work in flight) */
+int bamg_pcg_prepare(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const bamg_vj* vj, int32_t bs, int32_t nbr,
+                     const int32_t* ptr, const int32_t* col, const double* blocks, const double* b, double* x,
+                     double tau, int32_t max_it, double rtol, double* work, const bamg_symop* sym, void* stream);
 int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const bamg_vj* vj, int32_t bs, int32_t nbr,
                  const int32_t* ptr,
                  const int32_t* col, const double* blocks, const double* b, double* x, double tau, int32_t max_it,

@@ -1361,11 +1361,49 @@ __global__ void k_pcg_g_next(PcgDev* s, cudaGraphConditionalHandle hw) {
 
 static cudaGraphExec_t g_pcg_parked = nullptr;  // last PCG executable: re-targeted by the next solve
 
-static int pcg_graph(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const bamg_vj* vj, int32_t bs, int32_t nbr,
+// A PCG graph built ahead of its launch (bamg_pcg_prepare): the host-side capture and
+// re-target then run while the device finishes the setup; bamg_pcg_run launches it
+// when called with the same arguments.
+struct PcgPlan {
+  bool valid = false;
+  bamg_mg* mg = nullptr;
+  const double* pbj = nullptr;
+  const bamg_vj* vj = nullptr;
+  int bs = 0, nbr = 0, max_it = 0;
+  const int *ptr = nullptr, *col = nullptr;
+  const double *blocks = nullptr, *b = nullptr;
+  double *x = nullptr, *work = nullptr;
+  double tau = 0.0, rtol = 0.0;
+  const bamg_symop* sym = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  PcgDev* dev = nullptr;
+  double* qh = nullptr;
+  int k_init = 0, k_body = 0, k_tail = 0;
+  bool same(bamg_mg* mg_, const double* pbj_, const bamg_vj* vj_, int bs_, int nbr_, const int* ptr_, const int* col_,
+            const double* blocks_, const double* b_, double* x_, double tau_, int max_it_, double rtol_, double* work_,
+            const bamg_symop* sym_) const {
+    return valid && mg == mg_ && pbj == pbj_ && vj == vj_ && bs == bs_ && nbr == nbr_ && ptr == ptr_ && col == col_ &&
+           blocks == blocks_ && b == b_ && x == x_ && tau == tau_ && max_it == max_it_ && rtol == rtol_ &&
+           work == work_ && sym == sym_;
+  }
+};
+static PcgPlan g_pcg_plan;
+
+static void pcg_plan_drop(cudaStream_t st) {  // an unlaunched plan: keep its executable for re-targeting
+  if (!g_pcg_plan.valid) return;
+  if (g_pcg_plan.exec) {
+    if (g_pcg_parked) cudaGraphExecDestroy(g_pcg_parked);
+    g_pcg_parked = g_pcg_plan.exec;
+  }
+  cudaFreeAsync(g_pcg_plan.dev, st);
+  cudaFreeAsync(g_pcg_plan.qh, st);
+  g_pcg_plan = PcgPlan();
+}
+
+static int pcg_build(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const bamg_vj* vj, int32_t bs, int32_t nbr,
                      const int32_t* ptr, const int32_t* col, const double* blocks, const double* b, double* x,
-                     double tau, int32_t max_it, double rtol, double* work, int32_t* iterations_out,
-                     int32_t* reason_out, double* rel_out, double* q_hist, int32_t* err_out, double* err_value_out,
-                     int32_t* err_iter_out, const bamg_symop* sym, cudaStream_t st) {
+                     double tau, int32_t max_it, double rtol, double* work, const bamg_symop* sym, cudaStream_t st) {
+  pcg_plan_drop(st);
   int64_t n = (int64_t)nbr * bs;
   double* r = work;
   double* z = work + n;
@@ -1524,11 +1562,51 @@ static int pcg_graph(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const ba
     }
   }
   cudaGraphDestroy(graph);
-  BAMG_CUDA_CHECK(cudaGraphLaunch(exec, st));
+  PcgPlan& P = g_pcg_plan;
+  P.valid = true;
+  P.mg = mg;
+  P.pbj = pbj_inv;
+  P.vj = vj;
+  P.bs = bs;
+  P.nbr = nbr;
+  P.ptr = ptr;
+  P.col = col;
+  P.blocks = blocks;
+  P.b = b;
+  P.x = x;
+  P.tau = tau;
+  P.max_it = max_it;
+  P.rtol = rtol;
+  P.work = work;
+  P.sym = sym;
+  P.exec = exec;
+  P.dev = dev;
+  P.qh = qh;
+  P.k_init = k_init;
+  P.k_body = k_body;
+  P.k_tail = k_tail;
+  return 0;
+}
+
+static int pcg_graph(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const bamg_vj* vj, int32_t bs, int32_t nbr,
+                     const int32_t* ptr, const int32_t* col, const double* blocks, const double* b, double* x,
+                     double tau, int32_t max_it, double rtol, double* work, int32_t* iterations_out,
+                     int32_t* reason_out, double* rel_out, double* q_hist, int32_t* err_out, double* err_value_out,
+                     int32_t* err_iter_out, const bamg_symop* sym, cudaStream_t st) {
+  if (!g_pcg_plan.same(mg, pbj_inv, vj, bs, nbr, ptr, col, blocks, b, x, tau, max_it, rtol, work, sym)) {
+    int rc = pcg_build(ctx, mg, pbj_inv, vj, bs, nbr, ptr, col, blocks, b, x, tau, max_it, rtol, work, sym, st);
+    if (rc) return rc;
+  }
+  PcgPlan P = g_pcg_plan;
+  g_pcg_plan = PcgPlan();  // consumed
+  PcgDev* dev = P.dev;
+  double* qh = P.qh;
+  BAMG_CUDA_CHECK(cudaGraphLaunch(P.exec, st));
   PcgDev h;
   BAMG_CUDA_CHECK(cudaMemcpyAsync(&h, dev, sizeof(PcgDev), cudaMemcpyDeviceToHost, st));
   BAMG_CUDA_CHECK(cudaStreamSynchronize(st));
-  g_pcg_parked = exec;
+  if (g_pcg_parked) cudaGraphExecDestroy(g_pcg_parked);
+  g_pcg_parked = P.exec;
   int its = h.it;
   if (its > 0) BAMG_CUDA_CHECK(cudaMemcpy(q_hist + 1, qh + 1, sizeof(double) * (size_t)its, cudaMemcpyDeviceToHost));
   q_hist[0] = 0.0;
@@ -1537,7 +1615,7 @@ static int pcg_graph(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const ba
   // launch accounting: init + every body + every executed tail
   int tails = its - ((h.err >= 2 && h.err <= 4) || (h.done && h.err == 0 && h.reason != 2) ? 1 : 0);
   if (tails < 0) tails = 0;
-  g_bamg_launches.fetch_add((long long)k_init + (long long)its * k_body + (long long)tails * k_tail);
+  g_bamg_launches.fetch_add((long long)P.k_init + (long long)its * P.k_body + (long long)tails * P.k_tail);
   *err_out = h.err;
   *err_value_out = h.errv;
   *err_iter_out = h.erri;
@@ -1546,6 +1624,23 @@ static int pcg_graph(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const ba
   *rel_out = h.rel;
   BAMG_LAUNCH_CHECK();
   return 0;
+}
+
+// Build (capture / re-target) the PCG graph of a later bamg_pcg_run with the same
+// arguments now, so the host work overlaps device work still in flight. Optional.
+extern "C" int bamg_pcg_prepare(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const bamg_vj* vj, int32_t bs,
+                                int32_t nbr, const int32_t* ptr, const int32_t* col, const double* blocks,
+                                const double* b, double* x, double tau, int32_t max_it, double rtol, double* work,
+                                const bamg_symop* sym, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if ((sym && bs != sym->bs) || max_it < 0 || (mg && mg_prepare(mg, st) == 0 && mg->lv[0].n != (int64_t)nbr * bs))
+    return 0;  // bamg_pcg_run takes another path (or reports the error) itself
+  static const bool host_loop = [] {
+    const char* e = getenv("BAMG_PCG_HOSTLOOP");
+    return e && e[0] == '1';
+  }();
+  if (host_loop) return 0;
+  return pcg_build(ctx, mg, pbj_inv, vj, bs, nbr, ptr, col, blocks, b, x, tau, max_it, rtol, work, sym, st);
 }
 
 extern "C" int bamg_pcg_run(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const bamg_vj* vj, int32_t bs, int32_t nbr,

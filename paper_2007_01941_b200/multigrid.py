@@ -536,6 +536,13 @@ class MgHierarchy:
     def n_levels(self) -> int:
         return len(self.levels)
 
+    def check(self) -> None:
+        """The coarsest factorisation's not-PD test when build_hierarchy deferred it."""
+        cf = getattr(self, "_pending_cf", None)
+        if cf is not None:
+            self._pending_cf = None
+            _coarse_check(cf)
+
     def apply(self, r):
         """One V-cycle from a zero initial guess (multigrid.py:366-368)."""
         r = D.f64(r).reshape(-1)
@@ -635,7 +642,8 @@ def _smoother_finish(pend) -> None:
 
 
 def build_hierarchy(sys: SchurSystem, nullspace: DenseTall, strength: StrengthMatrix, *, max_coarse_dim: int = 400,
-                    max_ratio: float = 0.7, max_aggregate: int = 20, seed: int = _LANCZOS_SEED) -> MgHierarchy:
+                    max_ratio: float = 0.7, max_aggregate: int = 20, seed: int = _LANCZOS_SEED,
+                    _defer_check: bool = False) -> MgHierarchy:
     """Coarsen the reduced camera system (multigrid.py:371-441)."""
     s_explicit = sys.ensure_explicit()
     level0 = MgLevel(0, sys.matvec, sys.n_cameras * CAMERA_SIZE, sys, s_explicit, nullspace)
@@ -695,7 +703,10 @@ def build_hierarchy(sys: SchurSystem, nullspace: DenseTall, strength: StrengthMa
     if h._plan is not None:
         h._plan.prepare()
     D.phase("mg.plan")
-    _coarse_check(cf)
+    if _defer_check:  # the caller runs h.check() after queuing more host work (solver.linear_solve)
+        h._pending_cf = cf
+    else:
+        _coarse_check(cf)
     D.phase("mg.coarse")
     return h
 
