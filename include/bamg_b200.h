@@ -85,7 +85,7 @@ int bamg_visibility_strength(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_
 
 /* ---- residuals / Jacobians: problem.py:202-219 (_project_arrays), 272-326 (evaluate) ---- */
 /* J: (k, 32) observation records [F 2x9 | E 2x3 | H 2x3 | r 2] (H filled by build_system) */
-int bamg_evaluate(bamg_ctx* ctx, const double* cams, const double* pts, const int32_t* obs_cam,
+int bamg_evaluate(bamg_ctx* ctx, const double* cams, int32_t nc, const double* pts, const int32_t* obs_cam,
                   const int32_t* obs_pt, const double* pixels, int64_t k, int32_t huber, int32_t with_jacobian,
                   double* J, double* w, uint8_t* behind, double* objective_dev, int32_t* n_behind_dev,
                   void* stream);
@@ -123,8 +123,8 @@ int bamg_implicit_matvec(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* c
                          const double* x, int32_t nc, int32_t npt, double* qo, double* y, void* stream);
 /* schur.py:171-173 back_substitute */
 int bamg_back_substitute(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs_cam_pm, const double* J,
-                         const double* Cinv, const double* grad_pt, const double* dc, int32_t npt, double* dp,
-                         void* stream);
+                         const double* Cinv, const double* grad_pt, const double* dc, int32_t nc, int32_t npt,
+                         double* dp, void* stream);
 /* schur.py:114-116 W blocks in reference BSR order (API view) */
 int bamg_materialize_W(bamg_ctx* ctx, const int32_t* cm_list, const double* J, int64_t k, double* W,
                        void* stream);

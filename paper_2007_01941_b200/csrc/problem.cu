@@ -36,6 +36,21 @@ __global__ void k_take_u32(const uint32_t* __restrict__ src, const uint32_t* __r
 
 // Builds the point-major permutation and the camera-major list (problem.py:84-86
 // keeps input order; only the device layout changes).
+// rows of 9 doubles -> rows of 10 (80 B, 16 B aligned): per-observation gathers of a
+// camera's 9 values then take five 16 B loads instead of nine 8 B ones (each load
+// instruction of a warp touches up to 32 lines: the L1 wavefront count is the limit)
+__global__ void k_pad9(const double* __restrict__ src, int n, double* __restrict__ dst) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * 10;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = t / 10;
+    int c = (int)(t - r * 10);
+    dst[t] = c < 9 ? src[r * 9 + c] : 0.0;
+  }
+}
+static inline void pad9(const double* src, int n, double* dst, cudaStream_t st) {
+  launch(k_pad9, grid_for((int64_t)n * 10, 256), 256, 0, st, src, n, dst);
+}
+
 extern "C" int bamg_obs_orders(bamg_ctx* ctx, const int32_t* cam_idx, const int32_t* pt_idx, int64_t k,
                                int32_t nc, int32_t npt, int32_t* pm_perm, int32_t* obs_cam_pm,
                                int32_t* obs_pt_pm, int32_t* pt_ptr, int32_t* cm_list, int32_t* cam_ptr,
@@ -407,10 +422,15 @@ k_evaluate(const double* __restrict__ cams, const double* __restrict__ pts, cons
   };
   auto gather = [&](int64_t tt) {
     if (tt < k) {
-      const double* c = cams + (int64_t)ic * 9;
+      const double2* c = reinterpret_cast<const double2*>(cams + (int64_t)ic * 10);  // padded rows
       const double* x = pts + (int64_t)ip * 3;
 #pragma unroll
-      for (int q = 0; q < 9; ++q) cam[q] = __ldg(c + q);
+      for (int q = 0; q < 4; ++q) {
+        double2 v = __ldg(c + q);
+        cam[2 * q] = v.x;
+        cam[2 * q + 1] = v.y;
+      }
+      cam[8] = __ldg(cams + (int64_t)ic * 10 + 8);
 #pragma unroll
       for (int q = 0; q < 3; ++q) X[q] = __ldg(x + q);
       px[0] = __ldg(pix + 2 * tt);
@@ -519,15 +539,19 @@ k_evaluate(const double* __restrict__ cams, const double* __restrict__ pts, cons
   grid_finish(partials, counter, acc, scratch, objective);
 }
 
-extern "C" int bamg_evaluate(bamg_ctx* ctx, const double* cams, const double* pts, const int32_t* obs_cam,
+extern "C" int bamg_evaluate(bamg_ctx* ctx, const double* cams, int32_t nc, const double* pts, const int32_t* obs_cam,
                              const int32_t* obs_pt, const double* pixels, int64_t k, int32_t huber,
                              int32_t with_jacobian, double* J, double* w, uint8_t* behind, double* objective_dev,
                              int32_t* n_behind_dev, void* stream) {
   cudaStream_t st = as_stream(stream);
   BAMG_CUDA_CHECK(cudaMemsetAsync(n_behind_dev, 0, sizeof(int), st));
   int g = grid_for(k, EVAL_THREADS, 8);
-  launch(k_evaluate, g, EVAL_THREADS, 0, st, cams, pts, obs_cam, obs_pt, pixels, k, huber, with_jacobian, J, w,
-         behind, n_behind_dev, ctx->partials, ctx->counters + BAMG_CTR_OBJ, objective_dev);
+  double* cams10 = nullptr;  // camera rows padded to 80 B
+  BAMG_CUDA_CHECK(cudaMallocAsync(&cams10, sizeof(double) * 10 * (size_t)(nc > 0 ? nc : 1), st));
+  if (nc > 0) pad9(cams, nc, cams10, st);
+  launch(k_evaluate, g, EVAL_THREADS, 0, st, (const double*)cams10, pts, obs_cam, obs_pt, pixels, k, huber,
+         with_jacobian, J, w, behind, n_behind_dev, ctx->partials, ctx->counters + BAMG_CTR_OBJ, objective_dev);
+  BAMG_CUDA_CHECK(cudaFreeAsync(cams10, st));
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -995,7 +1019,7 @@ extern "C" int bamg_obs_H(bamg_ctx* ctx, const int32_t* obs_pt_pm, const double*
 }
 
 // Per point: u_p = sum_o E_o^T (F_o x_cam(o)); v_p = Cinv u_p (or Cinv (base - u_p));
-// q_o = E_o v_p.
+// q_o = E_o v_p. x: camera rows padded to 10 doubles (pad9).
 __global__ void k_point_wtx(const int* __restrict__ pt_ptr, const int* __restrict__ ocam, const double* __restrict__ J,
                             const double* __restrict__ Cinv, const double* __restrict__ x, const double* __restrict__ base,
                             int npt, double* __restrict__ v_out, double* __restrict__ qo) {
@@ -1003,7 +1027,14 @@ __global__ void k_point_wtx(const int* __restrict__ pt_ptr, const int* __restric
     double u[3] = {0, 0, 0};
     for (int o = pt_ptr[p]; o < pt_ptr[p + 1]; ++o) {
       const double2* rp = reinterpret_cast<const double2*>(J + (int64_t)o * REC);
-      const double* xc = x + (int64_t)ocam[o] * 9;
+      const double2* xc2 = reinterpret_cast<const double2*>(x + (int64_t)ocam[o] * 10);  // padded rows
+      double xc[10];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        double2 v = __ldg(xc2 + c);
+        xc[2 * c] = v.x;
+        xc[2 * c + 1] = v.y;
+      }
       double t0 = 0.0, t1 = 0.0;
 #pragma unroll
       for (int c = 0; c < 9; ++c) {
@@ -1048,8 +1079,12 @@ extern "C" int bamg_implicit_matvec(bamg_ctx* ctx, const int32_t* cam_ptr, const
                                     double* qo, double* y, void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
-  if (npt) launch(k_point_wtx, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, obs_cam_pm, J, Cinv, x, nullptr, npt,
-                  nullptr, qo);
+  double* x10 = nullptr;  // camera vector padded to 80 B rows for k_point_wtx's gathers
+  BAMG_CUDA_CHECK(cudaMallocAsync(&x10, sizeof(double) * 10 * (size_t)(nc > 0 ? nc : 1), st));
+  if (nc) pad9(x, nc, x10, st);
+  if (npt) launch(k_point_wtx, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, obs_cam_pm, J, Cinv, (const double*)x10,
+                  nullptr, npt, nullptr, qo);
+  BAMG_CUDA_CHECK(cudaFreeAsync(x10, st));
   if (nc)
     launch(k_cam_gather, grid_for((int64_t)nc * 32, 128, 8), 128, cam_gather_smem(), st, cam_ptr, cm_list, J, qo,
            nullptr, A, x, nc, y);
@@ -1064,12 +1099,16 @@ __global__ void k_neg(const double* __restrict__ a, double* __restrict__ b, int6
 }
 
 extern "C" int bamg_back_substitute(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs_cam_pm, const double* J,
-                                    const double* Cinv, const double* grad_pt, const double* dc, int32_t npt,
-                                    double* dp, void* stream) {
+                                    const double* Cinv, const double* grad_pt, const double* dc, int32_t nc,
+                                    int32_t npt, double* dp, void* stream) {
   (void)ctx;
   cudaStream_t st = as_stream(stream);
-  if (npt) launch(k_point_wtx, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, obs_cam_pm, J, Cinv, dc, grad_pt, npt,
-                  dp, nullptr);
+  double* x10 = nullptr;  // dc padded to 80 B camera rows for k_point_wtx's gathers
+  BAMG_CUDA_CHECK(cudaMallocAsync(&x10, sizeof(double) * 10 * (size_t)(nc > 0 ? nc : 1), st));
+  if (nc > 0) pad9(dc, nc, x10, st);
+  if (npt) launch(k_point_wtx, grid_for(npt, 128, 16), 128, 0, st, pt_ptr, obs_cam_pm, J, Cinv, (const double*)x10,
+                  grad_pt, npt, dp, nullptr);
+  BAMG_CUDA_CHECK(cudaFreeAsync(x10, st));
   BAMG_LAUNCH_CHECK();
   return 0;
 }

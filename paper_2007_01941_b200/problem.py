@@ -521,7 +521,7 @@ def evaluate(problem: BundleProblem, camera_params=None, points=None, with_jacob
     else:
         J = w = None
     if k:
-        D.call("bamg_evaluate", cams, pts, st.obs_cam_pm, st.obs_pt_pm, st.pix_pm, k, huber,
+        D.call("bamg_evaluate", cams, cams.shape[0], pts, st.obs_cam_pm, st.obs_pt_pm, st.pix_pm, k, huber,
                1 if with_jacobian else 0, J, w, behind, obj, nb)
         host = res.cpu()
         n_behind = int(host[1:].view(torch.int32)[0])
@@ -549,7 +549,7 @@ def _objective_dev(problem: BundleProblem, cams, pts, obj_out, n_behind_out) -> 
         return
     huber = 1 if problem.loss == "huber" else 0
     behind = D.empty(k, dtype=torch.uint8)
-    D.call("bamg_evaluate", cams, pts, st.obs_cam_pm, st.obs_pt_pm, st.pix_pm, k, huber, 0, None, None, behind,
+    D.call("bamg_evaluate", cams, cams.shape[0], pts, st.obs_cam_pm, st.obs_pt_pm, st.pix_pm, k, huber, 0, None, None, behind,
            obj_out, n_behind_out)
 
 

@@ -286,7 +286,7 @@ def back_substitute(sys: SchurSystem, delta_cam):
     dc = D.f64(delta_cam).reshape(-1)
     dp = D.empty(sys.n_points * POINT_SIZE)
     D.call("bamg_back_substitute", st.pt_ptr, st.obs_cam_pm, sys._jac._J, sys.C._inv, sys.grad_pt,
-           dc, sys.n_points, dp)
+           dc, sys.n_cameras, sys.n_points, dp)
     return dp
 
 
