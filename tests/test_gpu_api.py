@@ -190,11 +190,12 @@ def test_midsize_scene_matches_oracle(P, which):
     np.testing.assert_array_equal(H(agg.assignment), O.aggregate(Go)[0])
     h = P.build_hierarchy(s, P.gauge_nullspace(prob), G)
     lv = O.hierarchy(os_, O.gauge_nullspace(op.cams), Go)
-    assert [l.scalar_dim for l in h.levels][:2] == [l.dim for l in lv][:2]
+    assert [l.scalar_dim for l in h.levels] == [l.dim for l in lv]
     x, rep = P.pcg(s.matvec, h.apply, s.rhs_cam, tau=1e-30, max_iterations=20000, residual_tolerance=1e-6)
     xo, repo = O.pcg(os_.matvec, lambda r: O.vcycle(lv, 0, None, r), os_.rhs, 1e-30, 20000, 1e-6)
-    assert abs(rep.iterations - repo.iterations) <= 2, (rep.iterations, repo.iterations)
-    assert relerr(H(x), xo) <= 1e-3
+    assert abs(rep.iterations - repo.iterations) <= 1, (rep.iterations, repo.iterations)
+    # both solutions meet rel-res 1e-6; they differ by the solvers' own residual error
+    assert relerr(H(x), xo) <= 1e-4
 
 
 def test_lm_trial_decision_on_device(P):
