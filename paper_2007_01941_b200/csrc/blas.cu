@@ -384,7 +384,7 @@ extern "C" int bamg_block_chol_inv(bamg_ctx* ctx, const double* M, int32_t n, in
   (void)ctx;
   cudaStream_t st = as_stream(stream);
   int big = 0x7fffffff;
-  BAMG_CUDA_CHECK(cudaMemcpyAsync(bad_min_dev, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+  set_i32(bad_min_dev, big, st);  // device-side: no pageable host copy in the stream
   if (n <= 0) return 0;
   if (bs > 32 || bs < 1) {
     bamg_set_error("block_chol_inv: block size %d outside [1, 32]", bs);

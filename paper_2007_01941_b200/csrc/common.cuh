@@ -84,6 +84,10 @@ static inline int grid_for(int64_t n, int threads, int per_sm = 8) {
   return (int)(want < cap ? want : cap);
 }
 
+// one int32 device slot <- v (a kernel, not a pageable host->device copy)
+__global__ void k_set_i32(int* p, int v);
+void set_i32(int* p, int v, cudaStream_t st);
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);

@@ -39,6 +39,11 @@ bool bamg_pdl_enabled() {
   return on;
 }
 
+__global__ void k_set_i32(int* p, int v) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *p = v;
+}
+void set_i32(int* p, int v, cudaStream_t st) { launch(k_set_i32, 1, 32, 0, st, p, v); }
+
 int bamg_num_sms() {
   static int sms = 0;
   if (!sms) {

@@ -984,7 +984,7 @@ extern "C" int bamg_build_system(bamg_ctx* ctx, const int32_t* cam_ptr, const in
   (void)ctx;
   cudaStream_t st = as_stream(stream);
   int big = 0x7fffffff;
-  BAMG_CUDA_CHECK(cudaMemcpyAsync(bad_min_dev, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+  set_i32(bad_min_dev, big, st);  // device-side: no pageable host copy in the stream
   if (nc) launch(k_add_diag, grid_for((int64_t)nc * 81, 256), 256, 0, st, A_raw, d_cam, nc, 9, A);
   if (npt)
     launch(k_points_H_warp, grid_for((int64_t)ceil_div(npt, 32) * 32, 128, 16), 128, 0, st, pt_ptr, C_raw, d_pt, g_pt,

@@ -520,9 +520,16 @@ def evaluate(problem: BundleProblem, camera_params=None, points=None, with_jacob
         J, w = D.empty(max(k, 1), JacobianBlocks.REC)[:k], D.empty(k)
     else:
         J = w = None
+    jac = None
     if k:
         D.call("bamg_evaluate", cams, cams.shape[0], pts, st.obs_cam_pm, st.obs_pt_pm, st.pix_pm, k, huber,
                1 if with_jacobian else 0, J, w, behind, obj, nb)
+        if with_jacobian:
+            # the points' normal blocks depend on the Jacobian alone: queued ahead of the
+            # objective readback so the device works through the host round trip
+            jac = JacobianBlocks._from_records(st, J, w, problem.n_cameras, problem.n_points, problem._ci,
+                                               problem._pi)
+            jac.point_normal()
         host = res.cpu()
         n_behind = int(host[1:].view(torch.int32)[0])
         objective = float(host[0])
@@ -534,8 +541,9 @@ def evaluate(problem: BundleProblem, camera_params=None, points=None, with_jacob
         raise BehindCameraError(idx)
     if not with_jacobian:
         return objective, None
-    return objective, JacobianBlocks._from_records(st, J, w, problem.n_cameras, problem.n_points, problem._ci,
-                                                   problem._pi)
+    if jac is None:
+        jac = JacobianBlocks._from_records(st, J, w, problem.n_cameras, problem.n_points, problem._ci, problem._pi)
+    return objective, jac
 
 
 def _objective_dev(problem: BundleProblem, cams, pts, obj_out, n_behind_out) -> None:
