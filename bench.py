@@ -205,9 +205,8 @@ def gpu_arm(args, rank, world):
 
     def structure():
         pr = P.BundleProblem(*dev_in)
-        G = P.visibility_strength(pr)  # once per problem (solver.py:221-230)
-        _ = pr.structure.symbolic
         _ = pr.structure.pair_lists
+        G = P.visibility_strength(pr)  # once per problem (solver.py:221-230)
         MG._aggregate_cached(G, cfg.mg_max_aggregate)
         return pr, G
 

@@ -133,11 +133,17 @@ int bamg_materialize_W(bamg_ctx* ctx, const int32_t* cm_list, const double* J, i
 int bamg_schur_symbolic_sizes(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* S_ptr, const int32_t* S_col,
                               int32_t nc, int32_t npt, int32_t* pair_off, int32_t* dpos, int32_t* up_off,
                               int64_t* out_host, void* stream);
-int bamg_schur_symbolic(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs_cam_pm, const int32_t* S_ptr,
+int bamg_schur_symbolic(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs_cam_pm, const int32_t* obs_pt_pm,
+                        const int32_t* S_ptr,
                         const int32_t* S_col, int32_t nc, int32_t npt, int64_t nnz, const int32_t* pair_off,
                         int64_t n_pairs, const int32_t* dpos, const int32_t* up_off, int32_t* pair_a,
                         int32_t* pair_b, int32_t* blk_pair_ptr, int32_t* up_blk, int32_t* up_row,
                         int32_t* up_tpos, void* stream);
+/* shared-point counts per S slot from the pair lists (list lengths, mirrored;
+ * diagonal = camera degree): the strength pass without a sweep of the observations */
+int bamg_shared_from_pairs(bamg_ctx* ctx, const int32_t* up_blk, const int32_t* up_tpos, int32_t n_up,
+                           const int32_t* blk_pair_ptr, const int32_t* dpos, const int32_t* cam_ptr, int32_t nc,
+                           int32_t* shared_cnt, void* stream);
 /* reorder the upper-block work list by descending pair count (load balance) */
 int bamg_schur_order_upper(bamg_ctx* ctx, int32_t* up_blk, int32_t* up_row, int32_t* up_tpos, int32_t n_up,
                            const int32_t* blk_pair_ptr, const int32_t* pair_a, void* stream);
@@ -347,6 +353,9 @@ int bamg_symop_cheb_step(bamg_ctx* ctx, const bamg_symop* sym, const double* blo
                          const double* b, const double* Dinv, double* d, double* x_out, double c1, double c2,
                          int32_t divide, void* stream);
 int bamg_mg_set_symmetric(bamg_mg* mg, int32_t level, const bamg_symop* sym);
+/* coarse V-cycle tail as one persistent cooperative kernel: levels whose 16x16
+ * operator is at most max_mb MB (0 disables; -1 = BAMG_VTAIL_MB, default 0) */
+int bamg_mg_set_tail(bamg_mg* m, int32_t max_mb);
 int bamg_mg_use_graph(bamg_mg* mg, int32_t on);
 /* arena + graph ahead of the first bamg_mg_apply (optional; apply prepares lazily) */
 int bamg_mg_prepare(bamg_ctx* ctx, bamg_mg* mg, void* stream);

@@ -269,27 +269,32 @@ k_radix_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ v
     __syncwarp();
   }
   __syncthreads();
-  // per-digit exclusive prefix over warps, and the digit's total in the tile
+  // per-digit exclusive prefix over warps (thread d owns digit d), then a block-wide
+  // exclusive scan of the digit totals: where each digit starts in the tile
+  static_assert(RS_WARPS * 32 == 256, "one thread per digit");
   __shared__ int dstart[257];
-  for (int d = threadIdx.x; d < 256; d += blockDim.x) {
+  __shared__ int wtot[RS_WARPS];
+  {
+    const int d = threadIdx.x;
     int run = 0;
+#pragma unroll
     for (int q = 0; q < RS_WARPS; ++q) {
       int c = wcount[q][d];
       wcount[q][d] = run;
       run += c;
     }
-    dstart[d + 1] = run;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {  // exclusive prefix over digits: where each digit starts in the tile
-    int s = 0;
-    dstart[0] = 0;
-    for (int d = 0; d < 256; ++d) {
-      int c = dstart[d + 1];
-      dstart[d] = s;
-      s += c;
+    int incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(FULL_MASK, incl, o);
+      if (lane >= o) incl += t;
     }
-    dstart[256] = s;
+    if (lane == 31) wtot[w] = incl;
+    __syncthreads();
+    int off = 0;
+    for (int q = 0; q < w; ++q) off += wtot[q];
+    dstart[d] = off + incl - run;
+    if (d == 255) dstart[256] = off + incl;
   }
   __syncthreads();
   __shared__ uint32_t skey[RS_TILE];

@@ -28,12 +28,6 @@ __global__ void k_iota(uint32_t* a, int64_t n) {
     a[i] = (uint32_t)i;
 }
 
-__global__ void k_take_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ idx, int64_t n,
-                           uint32_t* __restrict__ dst) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = src[idx[i]];
-}
-
 // Builds the point-major permutation and the camera-major list (problem.py:84-86
 // keeps input order; only the device layout changes).
 // rows of 9 doubles -> rows of 10 (80 B, 16 B aligned): per-observation gathers of a
@@ -51,6 +45,50 @@ static inline void pad9(const double* src, int n, double* dst, cudaStream_t st) 
   launch(k_pad9, grid_for((int64_t)n * 10, 256), 256, 0, st, src, n, dst);
 }
 
+// Point-major order by counting: per-point histogram -> pt_ptr, scatter into the
+// point segments (atomic slots: arbitrary order inside a segment), then every
+// element finds its place by ranking its segment on (camera, caller index) -- the
+// (point, camera) order is total once duplicates are tie-broken by caller index, so
+// the result is the stable sort's, deterministic. Segments are short (a point's
+// observations), so the quadratic rank costs less than five radix passes.
+__global__ void k_count_i32(const int* __restrict__ key, int64_t k, int* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[key[i]], 1);
+}
+
+__global__ void k_pt_scatter(const int* __restrict__ cam_idx, const int* __restrict__ pt_idx, int64_t k,
+                             const int* __restrict__ pt_ptr, int* __restrict__ fill, int* __restrict__ tcam,
+                             int* __restrict__ tperm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+    int p = pt_idx[i];
+    int pos = pt_ptr[p] + atomicAdd(&fill[p], 1);
+    tcam[pos] = cam_idx[i];
+    tperm[pos] = (int)i;
+  }
+}
+
+__global__ void k_segment_ids(const int* __restrict__ ptr, int n, int* __restrict__ ids) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
+    for (int q = ptr[p]; q < ptr[p + 1]; ++q) ids[q] = p;
+}
+
+__global__ void k_pt_rank(const int* __restrict__ pt_ptr, const int* __restrict__ obs_pt_pm, int64_t k,
+                          const int* __restrict__ tcam, const int* __restrict__ tperm, int* __restrict__ obs_cam_pm,
+                          int* __restrict__ pm_perm) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < k; q += (int64_t)gridDim.x * blockDim.x) {
+    int p = obs_pt_pm[q];
+    int s = pt_ptr[p], e = pt_ptr[p + 1];
+    int c = tcam[q], t = tperm[q];
+    int r = 0;
+    for (int u = s; u < e; ++u) {
+      int cu = tcam[u];
+      r += (cu < c) || (cu == c && tperm[u] < t);
+    }
+    obs_cam_pm[s + r] = c;
+    pm_perm[s + r] = t;
+  }
+}
+
 extern "C" int bamg_obs_orders(bamg_ctx* ctx, const int32_t* cam_idx, const int32_t* pt_idx, int64_t k,
                                int32_t nc, int32_t npt, int32_t* pm_perm, int32_t* obs_cam_pm,
                                int32_t* obs_pt_pm, int32_t* pt_ptr, int32_t* cm_list, int32_t* cam_ptr,
@@ -62,36 +100,36 @@ extern "C" int bamg_obs_orders(bamg_ctx* ctx, const int32_t* cam_idx, const int3
     BAMG_CUDA_CHECK(cudaMemsetAsync(cam_ptr, 0, sizeof(int) * (nc + 1), st));
     return 0;
   }
-  uint32_t *iota = nullptr, *k1 = nullptr, *v1 = nullptr, *kk = nullptr, *cm_keys = nullptr;
+  uint32_t *iota = nullptr, *cm_keys = nullptr;
+  int *cnt = nullptr, *tcam = nullptr, *tperm = nullptr;
   BAMG_CUDA_CHECK(cudaMallocAsync(&iota, 4 * k, st));
-  BAMG_CUDA_CHECK(cudaMallocAsync(&k1, 4 * k, st));
-  BAMG_CUDA_CHECK(cudaMallocAsync(&v1, 4 * k, st));
-  BAMG_CUDA_CHECK(cudaMallocAsync(&kk, 4 * k, st));
   BAMG_CUDA_CHECK(cudaMallocAsync(&cm_keys, 4 * k, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&tcam, 4 * k, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&tperm, 4 * k, st));
+  BAMG_CUDA_CHECK(cudaMallocAsync(&cnt, 4 * ((size_t)npt + 1), st));
   int g = grid_for(k, 256);
-  launch(k_iota, g, 256, 0, st, iota, k);
-  int rc;
-  // (a) stable by camera
-  rc = radix_sort_pairs((const uint32_t*)cam_idx, iota, k1, v1, k, bits_for(nc), st);
+  // (a) point segments by counting
+  BAMG_CUDA_CHECK(cudaMemsetAsync(cnt, 0, 4 * ((size_t)npt + 1), st));
+  launch(k_count_i32, g, 256, 0, st, pt_idx, k, cnt);
+  int rc = scan_exclusive_int(cnt, pt_ptr, (int64_t)npt + 1, nullptr, st);
   if (rc) return rc;
-  // (b) stable by point -> (point, camera) order
-  launch(k_take_u32, g, 256, 0, st, (const uint32_t*)pt_idx, v1, k, kk);
-  rc = radix_sort_pairs(kk, v1, (uint32_t*)obs_pt_pm, (uint32_t*)pm_perm, k, bits_for(npt), st);
-  if (rc) return rc;
-  launch(k_take_u32, g, 256, 0, st, (const uint32_t*)cam_idx, (const uint32_t*)pm_perm, k, (uint32_t*)obs_cam_pm);
+  BAMG_CUDA_CHECK(cudaMemsetAsync(cnt, 0, 4 * (size_t)npt, st));
+  launch(k_pt_scatter, g, 256, 0, st, cam_idx, pt_idx, k, pt_ptr, cnt, tcam, tperm);
+  launch(k_segment_ids, grid_for(npt, 256), 256, 0, st, pt_ptr, npt, obs_pt_pm);
+  // (b) inside each point: (camera, caller index) order
+  launch(k_pt_rank, g, 256, 0, st, pt_ptr, obs_pt_pm, k, tcam, tperm, obs_cam_pm, pm_perm);
   // (c) point-major positions stably by camera -> (camera, point) order
+  launch(k_iota, g, 256, 0, st, iota, k);
   rc = radix_sort_pairs((const uint32_t*)obs_cam_pm, iota, cm_keys, (uint32_t*)cm_list, k, bits_for(nc), st);
-  if (rc) return rc;
-  rc = segment_ptr(obs_pt_pm, k, npt, pt_ptr, st);
   if (rc) return rc;
   rc = segment_ptr((const int*)cm_keys, k, nc, cam_ptr, st);
   if (rc) return rc;
   BAMG_LAUNCH_CHECK();
   cudaFreeAsync(iota, st);
-  cudaFreeAsync(k1, st);
-  cudaFreeAsync(v1, st);
-  cudaFreeAsync(kk, st);
   cudaFreeAsync(cm_keys, st);
+  cudaFreeAsync(tcam, st);
+  cudaFreeAsync(tperm, st);
+  cudaFreeAsync(cnt, st);
   return 0;
 }
 

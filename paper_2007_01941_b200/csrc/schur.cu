@@ -74,6 +74,32 @@ __global__ void k_pair_emit_packed(const int* __restrict__ pt_ptr, const int* __
   }
 }
 
+// Same output as k_pair_emit_packed with a thread per observation a instead of per
+// point (29 M threads with at most m - 1 pairs each, against 4.5 M with up to
+// m (m - 1) / 2): a's pairs start at pair_off[p] + t (m - 1) - t (t - 1) / 2 for a at
+// index t of its point's segment; the partner cameras ascend, so each slot search
+// starts past the previous one.
+__global__ void k_pair_emit_obs(const int* __restrict__ pt_ptr, const int* __restrict__ obs_pt_pm,
+                                const int* __restrict__ ocam, const int* __restrict__ S_ptr,
+                                const int* __restrict__ S_col, const int* __restrict__ off, int64_t k,
+                                uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < k; a += (int64_t)gridDim.x * blockDim.x) {
+    int p = obs_pt_pm[a];
+    int s = pt_ptr[p], e = pt_ptr[p + 1];
+    int t = (int)a - s, m = e - s;
+    int64_t pos = (int64_t)off[p] + (int64_t)t * (m - 1) - (int64_t)t * (t - 1) / 2;
+    int ca = ocam[a];
+    int r0 = S_ptr[ca], n = S_ptr[ca + 1] - r0;
+    const int* cols = S_col + r0;
+    int q = -1;
+    for (int b = (int)a + 1; b < e; ++b, ++pos) {
+      q += 1 + lower_bound_i32(cols + q + 1, n - q - 1, ocam[b]);
+      key[pos] = (uint32_t)(r0 + q);
+      val[pos] = ((uint32_t)a << 7) | (uint32_t)(b - (int)a);
+    }
+  }
+}
+
 __global__ void k_unpack_pairs(const uint32_t* __restrict__ v, int64_t n, int* __restrict__ pa, int* __restrict__ pb) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     uint32_t x = v[i];
@@ -158,6 +184,7 @@ extern "C" int bamg_schur_symbolic_sizes(bamg_ctx* ctx, const int32_t* pt_ptr, c
 }
 
 extern "C" int bamg_schur_symbolic(bamg_ctx* ctx, const int32_t* pt_ptr, const int32_t* obs_cam_pm,
+                                   const int32_t* obs_pt_pm,
                                    const int32_t* S_ptr, const int32_t* S_col, int32_t nc, int32_t npt,
                                    int64_t nnz, const int32_t* pair_off, int64_t n_pairs, const int32_t* dpos,
                                    const int32_t* up_off, int32_t* pair_a, int32_t* pair_b, int32_t* blk_pair_ptr,
@@ -190,8 +217,8 @@ extern "C" int bamg_schur_symbolic(bamg_ctx* ctx, const int32_t* pt_ptr, const i
       BAMG_CUDA_CHECK(cudaMallocAsync(&val, 4 * n_pairs, st));
       BAMG_CUDA_CHECK(cudaMallocAsync(&skey, 4 * n_pairs, st));
       BAMG_CUDA_CHECK(cudaMallocAsync(&sval, 4 * n_pairs, st));
-      launch(k_pair_emit_packed, grid_for(npt, 128), 128, 0, st, pt_ptr, obs_cam_pm, S_ptr, S_col, pair_off, npt, key,
-             val);
+      launch(k_pair_emit_obs, grid_for(n_obs, 256), 256, 0, st, pt_ptr, obs_pt_pm, obs_cam_pm, S_ptr, S_col, pair_off,
+             n_obs, key, val);
       int bits = 1;
       while ((1ll << bits) < nnz) ++bits;
       int rc = radix_sort_pairs(key, val, skey, sval, n_pairs, bits, st);
@@ -232,6 +259,37 @@ extern "C" int bamg_schur_symbolic(bamg_ctx* ctx, const int32_t* pt_ptr, const i
   cudaFreeAsync(perm, st);
   cudaFreeAsync(oa, st);
   cudaFreeAsync(ob, st);
+  return 0;
+}
+
+// Shared-point counts per covisibility slot from the pair lists (a block's list has
+// one pair per shared point): upper slot and its mirror = list length, diagonal =
+// the camera's observation count -- what k_shared_counts derives from the
+// observations in a separate pass.
+__global__ void k_shared_from_pairs(const int* __restrict__ up_blk, const int* __restrict__ up_tpos, int n_up,
+                                    const int* __restrict__ blk_ptr, const int* __restrict__ dpos,
+                                    const int* __restrict__ cam_ptr, int nc, int* __restrict__ shared) {
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n_up + nc; u += gridDim.x * blockDim.x) {
+    if (u < n_up) {
+      int q = up_blk[u];
+      int len = blk_ptr[q + 1] - blk_ptr[q];
+      shared[q] = len;
+      shared[up_tpos[u]] = len;
+    } else {
+      int i = u - n_up;
+      shared[dpos[i]] = cam_ptr[i + 1] - cam_ptr[i];
+    }
+  }
+}
+
+extern "C" int bamg_shared_from_pairs(bamg_ctx* ctx, const int32_t* up_blk, const int32_t* up_tpos, int32_t n_up,
+                                      const int32_t* blk_pair_ptr, const int32_t* dpos, const int32_t* cam_ptr,
+                                      int32_t nc, int32_t* shared_cnt, void* stream) {
+  (void)ctx;
+  if (n_up + nc <= 0) return 0;
+  launch(k_shared_from_pairs, grid_for((int64_t)n_up + nc, 256), 256, 0, as_stream(stream), up_blk, up_tpos, n_up,
+         blk_pair_ptr, dpos, cam_ptr, nc, shared_cnt);
+  BAMG_LAUNCH_CHECK();
   return 0;
 }
 

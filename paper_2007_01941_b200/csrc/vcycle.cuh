@@ -782,6 +782,215 @@ __global__ void k_chunk_fill(const int* __restrict__ ptr, const int* __restrict_
 }
 
 // ---------------------------------------------------------------------------
+// Coarse V-cycle tail as ONE persistent kernel. Below some level every operator is
+// small (tens of MB or less): its products, Jacobi steps, restriction, prolongation
+// and the coarsest dense solve are each a few microseconds of work behind a
+// dependent launch. The plan records those steps as a list of ops once (the same
+// recursion that launches them, in recording mode) and replays the list inside one
+// cooperative grid, a grid-wide barrier between consecutive ops. Each op computes
+// exactly what its kernel computes (same row partition and summation order), so the
+// result is bit-identical to the launched form. Vectors written inside the kernel are
+// read with ld.global.cg (L2, not the incoherent L1 / read-only paths).
+#include <cooperative_groups.h>
+
+enum { TOP_CHEB = 0, TOP_ROW = 1, TOP_RESTRICT = 2, TOP_PROLONG = 3, TOP_GEMV = 4 };
+
+struct TailOp {
+  int type = 0, nbr = 0, mode = 0, divide = 0;
+  const int* ptr = nullptr;
+  const int* col = nullptr;
+  const double* blocks = nullptr;
+  const double* x = nullptr;  // product / update input (CHEB: may be null)
+  const double* b = nullptr;
+  const double* Dinv = nullptr;
+  double* d = nullptr;
+  double* out = nullptr;
+  double c1 = 0.0, c2 = 0.0;
+  const int* agg_ptr = nullptr;
+  const int* members = nullptr;
+  const double* P = nullptr;
+  const int* agg = nullptr;
+  int n_agg = 0, n = 0, bs = 16, pad = 0;
+  const double* inv = nullptr;
+};
+
+__device__ __forceinline__ double tail_blocks16(const int* __restrict__ col, const double* __restrict__ blocks,
+                                                const double* x, int b, int b1, int lane) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const int cp = 2 * (lane & 7);
+  for (; b + 1 < b1; b += 2) {
+    const double2* A0 = reinterpret_cast<const double2*>(blocks + (int64_t)b * 256) + lane;
+    const double2* A1 = reinterpret_cast<const double2*>(blocks + (int64_t)(b + 1) * 256) + lane;
+    double2 u0 = __ldg(A0), u1 = __ldg(A0 + 32), u2 = __ldg(A0 + 64), u3 = __ldg(A0 + 96);
+    double2 v0 = __ldg(A1), v1 = __ldg(A1 + 32), v2 = __ldg(A1 + 64), v3 = __ldg(A1 + 96);
+    double2 xa = __ldcg(reinterpret_cast<const double2*>(x + (int64_t)__ldg(col + b) * 16 + cp));
+    double2 xb = __ldcg(reinterpret_cast<const double2*>(x + (int64_t)__ldg(col + b + 1) * 16 + cp));
+    a0 = fma(u0.x, xa.x, fma(u0.y, xa.y, a0));
+    a1 = fma(u1.x, xa.x, fma(u1.y, xa.y, a1));
+    a2 = fma(u2.x, xa.x, fma(u2.y, xa.y, a2));
+    a3 = fma(u3.x, xa.x, fma(u3.y, xa.y, a3));
+    a0 = fma(v0.x, xb.x, fma(v0.y, xb.y, a0));
+    a1 = fma(v1.x, xb.x, fma(v1.y, xb.y, a1));
+    a2 = fma(v2.x, xb.x, fma(v2.y, xb.y, a2));
+    a3 = fma(v3.x, xb.x, fma(v3.y, xb.y, a3));
+  }
+  if (b < b1) {
+    const double2* A0 = reinterpret_cast<const double2*>(blocks + (int64_t)b * 256) + lane;
+    double2 u0 = __ldg(A0), u1 = __ldg(A0 + 32), u2 = __ldg(A0 + 64), u3 = __ldg(A0 + 96);
+    double2 xa = __ldcg(reinterpret_cast<const double2*>(x + (int64_t)__ldg(col + b) * 16 + cp));
+    a0 = fma(u0.x, xa.x, fma(u0.y, xa.y, a0));
+    a1 = fma(u1.x, xa.x, fma(u1.y, xa.y, a1));
+    a2 = fma(u2.x, xa.x, fma(u2.y, xa.y, a2));
+    a3 = fma(u3.x, xa.x, fma(u3.y, xa.y, a3));
+  }
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+    a0 += __shfl_xor_sync(FULL_MASK, a0, o);
+    a1 += __shfl_xor_sync(FULL_MASK, a1, o);
+    a2 += __shfl_xor_sync(FULL_MASK, a2, o);
+    a3 += __shfl_xor_sync(FULL_MASK, a3, o);
+  }
+  int src = 8 * (lane & 3);
+  double s0 = __shfl_sync(FULL_MASK, a0, src);
+  double s1 = __shfl_sync(FULL_MASK, a1, src);
+  double s2 = __shfl_sync(FULL_MASK, a2, src);
+  double s3 = __shfl_sync(FULL_MASK, a3, src);
+  int k = (lane >> 2) & 3;
+  return k == 0 ? s0 : (k == 1 ? s1 : (k == 2 ? s2 : s3));
+}
+
+// k_row16_cta's row, CTA-cooperative (4 warps)
+__device__ __forceinline__ void tail_row16(const TailOp& o, int row, double (*part)[16], int lane, int w) {
+  int b0 = __ldg(o.ptr + row), b1 = __ldg(o.ptr + row + 1);
+  int q = (b1 - b0 + 3) >> 2;
+  int lo = min(b0 + w * q, b1), hi = min(lo + q, b1);
+  double v = tail_blocks16(o.col, o.blocks, o.x, lo, hi, lane);
+  if (lane < 16) part[w][lane] = v;
+  __syncthreads();
+  if (w == 0) {
+    int r = lane & 15;
+    double ax = ((part[0][r] + part[1][r]) + part[2][r]) + part[3][r];
+    int64_t e = (int64_t)row * 16 + r;
+    double rr = __ldcg(o.b + e) - ax;
+    if (o.mode == 0) {
+      if (lane < 16) o.out[e] = rr;
+    } else {
+      double z = 0.0;
+      const double* Di = o.Dinv + e * 16;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) z = fma(__ldg(Di + c), __shfl_sync(FULL_MASK, rr, c, 16), z);
+      if (lane < 16) {
+        double dn = o.divide ? z / o.c2 : o.c1 * __ldcg(o.d + e) + o.c2 * z;
+        o.d[e] = dn;
+        o.out[e] = __ldcg(o.x + e) + dn;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(128) k_vcycle_tail(const TailOp* __restrict__ ops, int nops) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double part[4][16];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int k = 0; k < nops; ++k) {
+    const TailOp o = ops[k];
+    switch (o.type) {
+      case TOP_ROW:
+        for (int row = blockIdx.x; row < o.nbr; row += gridDim.x) tail_row16(o, row, part, lane, w);
+        break;
+      case TOP_CHEB:  // k_cheb_step<16> without the product (x_in null)
+        for (int row = gwarp; row < o.nbr; row += nwarps) {
+          int64_t base = (int64_t)row * 16;
+          double rr = (lane < 16) ? __ldcg(o.b + base + lane) : 0.0;
+          double z = 0.0;
+          const double* Di = o.Dinv + (int64_t)row * 256 + (lane < 16 ? lane : 0) * 16;
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            double rc = __shfl_sync(FULL_MASK, rr, c);
+            if (lane < 16) z = fma(__ldg(Di + c), rc, z);
+          }
+          if (lane < 16) {
+            double dn = o.divide ? z / o.c2 : o.c1 * __ldcg(o.d + base + lane) + o.c2 * z;
+            o.d[base + lane] = dn;
+            o.out[base + lane] = (o.x ? __ldcg(o.x + base + lane) : 0.0) + dn;
+          }
+        }
+        break;
+      case TOP_RESTRICT: {  // k_restrict_warp<16>
+        int c = lane & 15, h = lane >> 4;
+        for (int a = gwarp; a < o.n_agg; a += nwarps) {
+          int q = __ldg(o.agg_ptr + a) + h, q1 = __ldg(o.agg_ptr + a + 1);
+          double s = 0.0;
+          for (; q + 2 < q1; q += 4) {
+            int64_t i0 = __ldg(o.members + q), i1 = __ldg(o.members + q + 2);
+            double u0[16], u1[16], r0[16], r1[16];
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) {
+              u0[kk] = __ldg(o.P + (i0 * 16 + kk) * 16 + c);
+              u1[kk] = __ldg(o.P + (i1 * 16 + kk) * 16 + c);
+              r0[kk] = __ldcg(o.x + i0 * 16 + kk);
+              r1[kk] = __ldcg(o.x + i1 * 16 + kk);
+            }
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) s = fma(u0[kk], r0[kk], s);
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) s = fma(u1[kk], r1[kk], s);
+          }
+          if (q < q1) {
+            int64_t i0 = __ldg(o.members + q);
+            double u0[16], r0[16];
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) {
+              u0[kk] = __ldg(o.P + (i0 * 16 + kk) * 16 + c);
+              r0[kk] = __ldcg(o.x + i0 * 16 + kk);
+            }
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) s = fma(u0[kk], r0[kk], s);
+          }
+          s += __shfl_down_sync(FULL_MASK, s, 16);
+          if (lane < 16) o.out[(int64_t)a * 16 + c] = s;
+        }
+        break;
+      }
+      case TOP_PROLONG: {  // k_prolong, accumulate
+        int64_t tot = (int64_t)o.nbr * o.bs;
+        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+             t += (int64_t)gridDim.x * blockDim.x) {
+          int64_t i = t / o.bs;
+          int r = (int)(t - i * o.bs);
+          const double2* pp = reinterpret_cast<const double2*>(o.P + (i * o.bs + r) * 16);
+          const double2* xa = reinterpret_cast<const double2*>(o.x + (int64_t)__ldg(o.agg + i) * 16);
+          double2 pv[8], xv[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            pv[c] = __ldg(pp + c);
+            xv[c] = __ldcg(xa + c);
+          }
+          double s = 0.0;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) s = fma(pv[c].y, xv[c].y, fma(pv[c].x, xv[c].x, s));
+          o.out[t] = __ldcg(o.out + t) + s;
+        }
+        break;
+      }
+      case TOP_GEMV:  // k_gemv
+        for (int i = gwarp; i < o.n; i += nwarps) {
+          double s = 0.0;
+          for (int c = lane; c < o.n; c += 32) s = fma(__ldg(o.inv + (int64_t)i * o.n + c), __ldcg(o.b + c), s);
+          s = warp_sum(s);
+          if (lane == 0) o.out[i] = s;
+        }
+        break;
+    }
+    if (k + 1 < nops) grid.sync();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // MG plan
 
 struct MgLevelPlan {
@@ -810,6 +1019,8 @@ struct MgLevelPlan {
   bool rowcta = false;
   // work
   double *b = nullptr, *x = nullptr, *xs = nullptr, *d = nullptr, *r = nullptr;
+  // set while the plan records the coarse tail: steps are appended, not launched
+  std::vector<TailOp>* rec = nullptr;
 };
 
 struct bamg_mg {
@@ -823,6 +1034,14 @@ struct bamg_mg {
   bool dirty = true;
   bool use_graph = false;
   long long graph_kernels = 0;
+  // coarse tail (levels >= tail_from) as one persistent kernel
+  int tail_mb = -1;  // size cap per level operator (MB); -1: BAMG_VTAIL_MB / default
+  int tail_from = -1;
+  bool tail_recording = false;
+  std::vector<TailOp> tail_host;
+  TailOp* tail_ops = nullptr;
+  double* tail_result = nullptr;
+  int tail_grid = 0;
 };
 
 extern "C" bamg_mg* bamg_mg_create(int32_t n_levels) {
@@ -856,6 +1075,11 @@ static cudaGraphExec_t take_parked_exec() {
 static void mg_free_work(bamg_mg* m) {
   if (m->arena) cudaFreeAsync(m->arena, m->arena_stream);
   m->arena = nullptr;
+  if (m->tail_ops) cudaFreeAsync(m->tail_ops, m->arena_stream);
+  m->tail_ops = nullptr;
+  m->tail_from = -1;
+  m->tail_host.clear();
+  m->tail_result = nullptr;
   for (auto& L : m->lv) L.b = L.x = L.xs = L.d = L.r = nullptr;
   m->in = m->out = nullptr;
   if (m->exec) park_exec(m->exec);
@@ -906,6 +1130,7 @@ extern "C" int bamg_mg_set_level(bamg_mg* m, int32_t level, int32_t bs, int32_t 
 }
 
 int scan_exclusive_int(const int* in, int* out, int64_t n, int* total, cudaStream_t st);
+static int mg_plan_tail(bamg_mg* m, const std::vector<int>& nnzb, cudaStream_t st);
 
 static int mg_alloc(bamg_mg* m, cudaStream_t st) {
   mg_free_work(m);
@@ -1012,7 +1237,7 @@ static int mg_alloc(bamg_mg* m, cudaStream_t st) {
     L.d = p; p += n;
     L.r = p; p += n;
   }
-  return 0;
+  return mg_plan_tail(m, nnzb, st);
 }
 
 template <int BS>
@@ -1031,6 +1256,25 @@ static int finish_grid(int nbr) { return grid_for((int64_t)((nbr + 1) / 2) * 32,
 
 static void cheb(const MgLevelPlan& L, const double* x_in, double* x_out, double c1, double c2, int divide,
                  bool with_A, cudaStream_t st) {
+  if (L.rec) {
+    TailOp o;
+    o.type = with_A ? TOP_ROW : TOP_CHEB;
+    o.mode = 1;
+    o.nbr = L.nbr;
+    o.ptr = L.ptr;
+    o.col = L.col;
+    o.blocks = L.blocks;
+    o.x = x_in;
+    o.b = L.b;
+    o.Dinv = L.Dinv;
+    o.d = L.d;
+    o.out = x_out;
+    o.c1 = c1;
+    o.c2 = c2;
+    o.divide = divide;
+    L.rec->push_back(o);
+    return;
+  }
   if (with_A && L.rowcta) {
     launch_pdl(k_row16_cta, L.nbr, 128, 0, st, L.ptr, L.col, L.blocks, x_in, L.nbr, 1, L.b, L.Dinv, L.d, x_out, c1, c2,
            divide);
@@ -1085,6 +1329,20 @@ static double* smooth(MgLevelPlan& L, double* x, cudaStream_t st, double* final_
 }
 
 static void residual(const MgLevelPlan& L, const double* x, cudaStream_t st) {
+  if (L.rec) {
+    TailOp o;
+    o.type = TOP_ROW;
+    o.mode = 0;
+    o.nbr = L.nbr;
+    o.ptr = L.ptr;
+    o.col = L.col;
+    o.blocks = L.blocks;
+    o.x = x;
+    o.b = L.b;
+    o.out = L.r;
+    L.rec->push_back(o);
+    return;
+  }
   if (L.rowcta) {
     launch_pdl(k_row16_cta, L.nbr, 128, 0, st, L.ptr, L.col, L.blocks, x, L.nbr, 0, L.b, nullptr, nullptr, L.r, 0.0, 0.0,
            0);
@@ -1111,14 +1369,62 @@ static void residual(const MgLevelPlan& L, const double* x, cudaStream_t st) {
 // V-cycle at level l from x = 0; returns the buffer holding x_l.
 static double* vcycle(bamg_mg* m, size_t l, cudaStream_t st) {
   MgLevelPlan& L = m->lv[l];
+  if ((int)l == m->tail_from && !m->tail_recording) {
+    // the recorded coarse tail: one cooperative launch (no PDL edge: every CTA must be
+    // resident at once)
+    g_bamg_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(m->tail_grid);
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_vcycle_tail, (const TailOp*)m->tail_ops, (int)m->tail_host.size());
+    return m->tail_result;
+  }
   if (L.inv) {
     double* out = l == 0 ? m->out : L.x;
+    if (L.rec) {
+      TailOp o;
+      o.type = TOP_GEMV;
+      o.n = L.n;
+      o.inv = L.inv;
+      o.b = L.b;
+      o.out = out;
+      L.rec->push_back(o);
+      return out;
+    }
     launch_pdl(k_gemv, grid_for((int64_t)L.n * 32, 128, 8), 128, 0, st, L.inv, L.b, L.n, out);
     return out;
   }
   double* x = smooth(L, nullptr, st);
   residual(L, x, st);
   MgLevelPlan& C = m->lv[l + 1];
+  if (L.rec) {
+    TailOp o;
+    o.type = TOP_RESTRICT;
+    o.agg_ptr = L.agg_ptr;
+    o.members = L.members;
+    o.P = L.P;
+    o.x = L.r;
+    o.n_agg = L.n_agg;
+    o.out = C.b;
+    L.rec->push_back(o);
+    double* xc = vcycle(m, l + 1, st);
+    TailOp q;
+    q.type = TOP_PROLONG;
+    q.agg = L.agg;
+    q.P = L.P;
+    q.x = xc;
+    q.nbr = L.nbr;
+    q.bs = L.bs;
+    q.out = x;
+    L.rec->push_back(q);
+    return smooth(L, x, st, l == 0 ? m->out : nullptr);
+  }
   if (L.bs == 9)
     launch_pdl(k_restrict_warp<9>, grid_for((int64_t)L.n_agg * 32, 128, 16), 128, 0, st, L.agg_ptr, L.members, L.P, L.r,
            L.n_agg, C.b);
@@ -1128,6 +1434,54 @@ static double* vcycle(bamg_mg* m, size_t l, cudaStream_t st) {
   double* xc = vcycle(m, l + 1, st);
   launch_pdl(k_prolong, grid_for((int64_t)L.n, 256), 256, 0, st, L.agg, L.P, xc, L.nbr, L.bs, x, 1);
   return smooth(L, x, st, l == 0 ? m->out : nullptr);
+}
+
+// Coarse tail: the first level from which every level is a 16x16 operator of at most
+// BAMG_VTAIL_MB MB (default 0: off) or the coarsest dense solve, if there is a smoothing
+// level among them. Records the tail's steps (the launch recursion in recording
+// mode: same buffers, same coefficients) and uploads them.
+static int vtail_mb() {
+  static int mb = -1;
+  if (mb < 0) {
+    const char* e = getenv("BAMG_VTAIL_MB");
+    mb = e ? atoi(e) : 0;  // off by default: measured slower than the launched levels
+  }
+  return mb;
+}
+
+static int mg_plan_tail(bamg_mg* m, const std::vector<int>& nnzb, cudaStream_t st) {
+  m->tail_from = -1;
+  const int nl = (int)m->lv.size();
+  const int64_t cap = (int64_t)(m->tail_mb >= 0 ? m->tail_mb : vtail_mb()) << 20;
+  int from = nl;
+  for (int l = nl - 1; l >= 1; --l) {
+    const MgLevelPlan& L = m->lv[l];
+    bool ok = L.inv ? (l == nl - 1) : (L.bs == 16 && L.ptr && L.Dinv && L.agg_ptr && (int64_t)nnzb[l] * 2048 <= cap);
+    if (!ok) break;
+    from = l;
+  }
+  if (cap <= 0 || from >= nl - 1 || !m->lv[nl - 1].inv) return 0;
+  for (int l = from; l < nl; ++l) m->lv[l].rec = &m->tail_host;
+  m->tail_recording = true;
+  m->tail_from = from;
+  m->tail_result = vcycle(m, from, st);
+  m->tail_recording = false;
+  for (int l = from; l < nl; ++l) m->lv[l].rec = nullptr;
+  size_t bytes = sizeof(TailOp) * m->tail_host.size();
+  BAMG_CUDA_CHECK(cudaMallocAsync(&m->tail_ops, bytes, st));
+  BAMG_CUDA_CHECK(cudaMemcpyAsync(m->tail_ops, m->tail_host.data(), bytes, cudaMemcpyHostToDevice, st));
+  static int grid = 0;
+  if (!grid) {
+    int per_sm = 0;
+    BAMG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vcycle_tail, 128, 0));
+    const char* e = getenv("BAMG_VTAIL_CTAS");
+    int want = e ? atoi(e) : 4;
+    if (per_sm > want) per_sm = want;
+    if (per_sm < 1) per_sm = 1;
+    grid = per_sm * bamg_num_sms();
+  }
+  m->tail_grid = grid;
+  return 0;
 }
 
 static int mg_record(bamg_mg* m, cudaStream_t st) {
@@ -1200,6 +1554,12 @@ extern "C" int bamg_mg_set_symmetric(bamg_mg* m, int32_t level, const bamg_symop
   return 0;
 }
 
+extern "C" int bamg_mg_set_tail(bamg_mg* m, int32_t max_mb) {
+  m->tail_mb = max_mb;
+  m->dirty = true;
+  return 0;
+}
+
 extern "C" int bamg_mg_use_graph(bamg_mg* m, int32_t on) {
   m->use_graph = on != 0;
   m->dirty = true;
@@ -1209,6 +1569,7 @@ extern "C" int bamg_mg_use_graph(bamg_mg* m, int32_t on) {
 extern "C" int32_t bamg_mg_level_kind(const bamg_mg* m, int32_t level) {
   if (!m || m->dirty || level < 0 || level >= (int)m->lv.size()) return -1;
   const MgLevelPlan& L = m->lv[level];
+  if (m->tail_from >= 0 && level >= m->tail_from && !L.inv) return 5;
   if (L.inv) return 4;
   if (L.rowcta) return 1;
   if (L.sym) return 0;

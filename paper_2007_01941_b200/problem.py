@@ -131,8 +131,13 @@ class ObsStructure:
         if self._strength is None:
             S_ptr, S_col, nnz, max_row = self.covis
             cnt = D.empty(max(nnz, 1), dtype=torch.int32)
-            D.call("bamg_shared_counts", self.cam_ptr, self.cm_list, self.obs_pt_pm, self.pt_ptr,
-                   self.obs_cam_pm, self.nc, S_ptr, S_col, max_row, cnt)
+            pl = getattr(self, "_pairs", None)
+            if pl is not None:  # list lengths: no sweep of the observations
+                D.call("bamg_shared_from_pairs", pl["up_blk"], pl["up_tpos"], pl["n_up"], pl["blk_ptr"], pl["dpos"],
+                       self.cam_ptr, self.nc, cnt)
+            else:
+                D.call("bamg_shared_counts", self.cam_ptr, self.cm_list, self.obs_pt_pm, self.pt_ptr,
+                       self.obs_cam_pm, self.nc, S_ptr, S_col, max_row, cnt)
             deg = D.empty(self.nc, dtype=torch.int32)
             G_ptr = D.empty(self.nc + 1, dtype=torch.int32)
             ng = nnz - self.nc
@@ -164,7 +169,7 @@ class ObsStructure:
             out["pair_a"] = D.empty(max(n_pairs, 1), dtype=torch.int32)
             out["pair_b"] = D.empty(max(n_pairs, 1), dtype=torch.int32)
             out["blk_ptr"] = D.empty(nnz + 1, dtype=torch.int32)
-        D.call("bamg_schur_symbolic", self.pt_ptr, self.obs_cam_pm, S_ptr, S_col, self.nc, self.npt,
+        D.call("bamg_schur_symbolic", self.pt_ptr, self.obs_cam_pm, self.obs_pt_pm, S_ptr, S_col, self.nc, self.npt,
                nnz, pair_off, n_pairs, dpos, up_off, out.get("pair_a"), out.get("pair_b"), out.get("blk_ptr"),
                up_blk, up_row, up_tpos)
         return out
@@ -329,9 +334,9 @@ class BundleProblem:
             # aggregation scan (side stream) and the Schur pair lists
             from . import multigrid
 
+            st.pair_lists  # first: the strength pass then reads the shared counts off its lists
             G = multigrid.visibility_strength(self)
             multigrid._aggregate_prefetch(G, 20)
-            st.pair_lists
 
     # -- reference attributes (device tensors, caller order) --
     @property
