@@ -74,6 +74,13 @@ int bamg_covis_count(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_li
 int bamg_covis_fill(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* obs_pt_pm,
                     const int32_t* pt_ptr, const int32_t* obs_cam_pm, int32_t nc, const int32_t* S_ptr,
                     int32_t* S_col, void* stream);
+/* count pass that keeps each row's bitmap (nc x ceil(nc/32) words) for the fill */
+int bamg_covis_count_keep(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* obs_pt_pm,
+                          const int32_t* pt_ptr, const int32_t* obs_cam_pm, int32_t nc, int32_t* row_counts,
+                          uint32_t* bitmaps, void* stream);
+/* S columns from the kept bitmaps (replaces the fill pass's second sweep) */
+int bamg_covis_compact(bamg_ctx* ctx, const uint32_t* bitmaps, int32_t nc, const int32_t* S_ptr, int32_t* S_col,
+                       void* stream);
 int bamg_shared_counts(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list, const int32_t* obs_pt_pm,
                        const int32_t* pt_ptr, const int32_t* obs_cam_pm, int32_t nc, const int32_t* S_ptr,
                        const int32_t* S_col, int32_t max_row, int32_t* shared_cnt, void* stream);

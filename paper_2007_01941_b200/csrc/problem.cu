@@ -141,7 +141,8 @@ extern "C" int bamg_obs_orders(bamg_ctx* ctx, const int32_t* cam_idx, const int3
 __global__ void k_covis_rows(const int* __restrict__ cam_ptr, const int* __restrict__ cm_list,
                              const int* __restrict__ obs_pt_pm, const int* __restrict__ pt_ptr,
                              const int* __restrict__ obs_cam_pm, int nc, int* __restrict__ counts,
-                             const int* __restrict__ S_ptr, int* __restrict__ S_col) {
+                             const int* __restrict__ S_ptr, int* __restrict__ S_col,
+                             unsigned* __restrict__ bm_out) {
   extern __shared__ unsigned int bm[];
   int words = (nc + 31) >> 5;
   for (int i = blockIdx.x; i < nc; i += gridDim.x) {
@@ -158,7 +159,10 @@ __global__ void k_covis_rows(const int* __restrict__ cam_ptr, const int* __restr
     __syncthreads();
     if (S_col == nullptr) {
       int c = 0;
-      for (int w = threadIdx.x; w < words; w += blockDim.x) c += __popc(bm[w]);
+      for (int w = threadIdx.x; w < words; w += blockDim.x) {
+        c += __popc(bm[w]);
+        if (bm_out) bm_out[(int64_t)i * words + w] = bm[w];
+      }
       c = warp_sum_int(c);
       __shared__ int red[32];
       if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
@@ -196,6 +200,62 @@ __global__ void k_covis_rows(const int* __restrict__ cam_ptr, const int* __restr
   }
 }
 
+// Fill from the row bitmaps the count pass kept (nc x ceil(nc/32) words): warp per
+// row, lanes compact set bits in column order -- no second sweep of the observations.
+__global__ void k_covis_compact(const unsigned* __restrict__ bm, int nc, const int* __restrict__ S_ptr,
+                                int* __restrict__ S_col) {
+  const int words = (nc + 31) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = warp; i < nc; i += nwarps) {
+    const unsigned* row = bm + (int64_t)i * words;
+    int out = S_ptr[i];
+    for (int w0 = 0; w0 < words; w0 += 32) {
+      int w = w0 + lane;
+      unsigned v = (w < words) ? row[w] : 0u;
+      int c = __popc(v);
+      int incl = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(FULL_MASK, incl, o);
+        if (lane >= o) incl += t;
+      }
+      int pos = out + incl - c;
+      while (v) {
+        int b = __ffs(v) - 1;
+        v &= v - 1;
+        S_col[pos++] = w * 32 + b;
+      }
+      out += __shfl_sync(FULL_MASK, incl, 31);
+    }
+  }
+}
+
+extern "C" int bamg_covis_count_keep(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
+                                     const int32_t* obs_pt_pm, const int32_t* pt_ptr, const int32_t* obs_cam_pm,
+                                     int32_t nc, int32_t* row_counts, uint32_t* bitmaps, void* stream) {
+  (void)ctx;
+  size_t sm = sizeof(unsigned) * ((nc + 31) / 32);
+  if (sm > 200 * 1024) {
+    bamg_set_error("covisibility bitmap for %d cameras exceeds shared memory", nc);
+    return BAMG_ERR_UNSUPPORTED;
+  }
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_covis_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  launch(k_covis_rows, grid_for(nc, 1, 16), 256, sm, as_stream(stream), cam_ptr, cm_list, obs_pt_pm, pt_ptr,
+         obs_cam_pm, nc, row_counts, nullptr, nullptr, bitmaps);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int bamg_covis_compact(bamg_ctx* ctx, const uint32_t* bitmaps, int32_t nc, const int32_t* S_ptr,
+                                  int32_t* S_col, void* stream) {
+  (void)ctx;
+  if (nc <= 0) return 0;
+  launch(k_covis_compact, grid_for((int64_t)nc * 32, 256), 256, 0, as_stream(stream), bitmaps, nc, S_ptr, S_col);
+  BAMG_LAUNCH_CHECK();
+  return 0;
+}
+
 extern "C" int bamg_covis_count(bamg_ctx* ctx, const int32_t* cam_ptr, const int32_t* cm_list,
                                 const int32_t* obs_pt_pm, const int32_t* pt_ptr, const int32_t* obs_cam_pm,
                                 int32_t nc, int32_t* row_counts, void* stream) {
@@ -207,7 +267,7 @@ extern "C" int bamg_covis_count(bamg_ctx* ctx, const int32_t* cam_ptr, const int
   }
   if (sm > 48 * 1024) cudaFuncSetAttribute(k_covis_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   launch(k_covis_rows, grid_for(nc, 1, 16), 256, sm, as_stream(stream), cam_ptr, cm_list, obs_pt_pm, pt_ptr,
-                                                                    obs_cam_pm, nc, row_counts, nullptr, nullptr);
+         obs_cam_pm, nc, row_counts, nullptr, nullptr, nullptr);
   BAMG_LAUNCH_CHECK();
   return 0;
 }
@@ -219,7 +279,7 @@ extern "C" int bamg_covis_fill(bamg_ctx* ctx, const int32_t* cam_ptr, const int3
   size_t sm = sizeof(unsigned) * ((nc + 31) / 32);
   if (sm > 48 * 1024) cudaFuncSetAttribute(k_covis_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   launch(k_covis_rows, grid_for(nc, 1, 16), 256, sm, as_stream(stream), cam_ptr, cm_list, obs_pt_pm, pt_ptr,
-                                                                    obs_cam_pm, nc, nullptr, S_ptr, S_col);
+         obs_cam_pm, nc, nullptr, S_ptr, S_col, nullptr);
   BAMG_LAUNCH_CHECK();
   return 0;
 }

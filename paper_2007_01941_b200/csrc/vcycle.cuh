@@ -8,6 +8,7 @@
 // Included at the end of blas.cu (same translation unit as the kernels it launches).
 #include <math.h>
 
+#include <chrono>
 #include <vector>
 
 int dot_dev(bamg_ctx* ctx, const double* x, const double* y, int64_t n, double* out, cudaStream_t st);
@@ -721,10 +722,14 @@ k_rows16_finish(const int* __restrict__ cptr, const double* __restrict__ partial
 // loads are in flight per warp; the halves combine once at the end (fixed order).
 // (min-blocks 1: without it ptxas holds the kernel at 32 registers and interleaves
 // every load with its fma, one member's row in flight at a time)
-template <int BS>
+// CHEB: the coarse level's first smoothing step (x = 0: d = D^-1 b / theta, x = d,
+// k_cheb_step without the product) in the same warp, on the 16 values it just formed
+// -- one launch per level less, same arithmetic.
+template <int BS, bool CHEB = false>
 __global__ void __launch_bounds__(128, 1)
 k_restrict_warp(const int* __restrict__ agg_ptr, const int* __restrict__ members, const double* __restrict__ P,
-                const double* __restrict__ r, int nagg, double* __restrict__ bc) {
+                const double* __restrict__ r, int nagg, double* __restrict__ bc, const double* __restrict__ Dinv = nullptr,
+                double* __restrict__ dc = nullptr, double* __restrict__ xc = nullptr, double theta = 1.0) {
   PDL_ENTRY();
   int lane = threadIdx.x & 31;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -761,6 +766,21 @@ k_restrict_warp(const int* __restrict__ agg_ptr, const int* __restrict__ members
     }
     s += __shfl_down_sync(FULL_MASK, s, 16);
     if (lane < 16) bc[(int64_t)a * 16 + c] = s;
+    if constexpr (CHEB) {
+      double rr = lane < 16 ? s : 0.0;
+      double z = 0.0;
+      const double* Di = Dinv + (int64_t)a * 256 + (lane < 16 ? lane : 0) * 16;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        double rk = __shfl_sync(FULL_MASK, rr, k);
+        if (lane < 16) z = fma(Di[k], rk, z);
+      }
+      if (lane < 16) {
+        double dn = z / theta;
+        dc[(int64_t)a * 16 + lane] = dn;
+        xc[(int64_t)a * 16 + lane] = 0.0 + dn;
+      }
+    }
   }
 }
 
@@ -1300,14 +1320,15 @@ static void cheb(const MgLevelPlan& L, const double* x_in, double* x_out, double
 // Smoother (multigrid.py:308-328); returns the buffer holding the result.
 // `final_out` (optional): the buffer the last step writes (the plan's output vector,
 // so no copy follows the cycle).
-static double* smooth(MgLevelPlan& L, double* x, cudaStream_t st, double* final_out = nullptr) {
+static double* smooth(MgLevelPlan& L, double* x, cudaStream_t st, double* final_out = nullptr,
+                      bool first_done = false) {
   double rho = 1.0 / L.sigma;
   double* cur;
   double* spare;
   const bool one = L.iterations <= 1 && final_out;
   if (x == nullptr) {
     double* out = one ? final_out : L.x;
-    cheb(L, nullptr, out, 0.0, L.theta, 1, false, st);  // d = D^-1 b / theta ; x = d
+    if (!first_done) cheb(L, nullptr, out, 0.0, L.theta, 1, false, st);  // d = D^-1 b / theta ; x = d
     cur = out;
     spare = L.xs;
   } else {
@@ -1367,7 +1388,7 @@ static void residual(const MgLevelPlan& L, const double* x, cudaStream_t st) {
 }
 
 // V-cycle at level l from x = 0; returns the buffer holding x_l.
-static double* vcycle(bamg_mg* m, size_t l, cudaStream_t st) {
+static double* vcycle(bamg_mg* m, size_t l, cudaStream_t st, bool first_done = false) {
   MgLevelPlan& L = m->lv[l];
   if ((int)l == m->tail_from && !m->tail_recording) {
     // the recorded coarse tail: one cooperative launch (no PDL edge: every CTA must be
@@ -1400,7 +1421,7 @@ static double* vcycle(bamg_mg* m, size_t l, cudaStream_t st) {
     launch_pdl(k_gemv, grid_for((int64_t)L.n * 32, 128, 8), 128, 0, st, L.inv, L.b, L.n, out);
     return out;
   }
-  double* x = smooth(L, nullptr, st);
+  double* x = smooth(L, nullptr, st, nullptr, first_done);
   residual(L, x, st);
   MgLevelPlan& C = m->lv[l + 1];
   if (L.rec) {
@@ -1425,13 +1446,27 @@ static double* vcycle(bamg_mg* m, size_t l, cudaStream_t st) {
     L.rec->push_back(q);
     return smooth(L, x, st, l == 0 ? m->out : nullptr);
   }
-  if (L.bs == 9)
-    launch_pdl(k_restrict_warp<9>, grid_for((int64_t)L.n_agg * 32, 128, 16), 128, 0, st, L.agg_ptr, L.members, L.P, L.r,
-           L.n_agg, C.b);
-  else
-    launch_pdl(k_restrict_warp<16>, grid_for((int64_t)L.n_agg * 32, 128, 16), 128, 0, st, L.agg_ptr, L.members, L.P,
-           L.r, L.n_agg, C.b);
-  double* xc = vcycle(m, l + 1, st);
+  // the coarse level's first smoothing step rides on the restriction (not into the
+  // coarsest solve, nor into a level the recorded tail runs)
+  const bool fuse = !C.inv && C.bs == 16 && C.Dinv && C.iterations >= 1 && C.x &&
+                    !((int)(l + 1) == m->tail_from && !m->tail_recording);
+  const int rg = grid_for((int64_t)L.n_agg * 32, 128, 16);
+  if (L.bs == 9) {
+    if (fuse)
+      launch_pdl(k_restrict_warp<9, true>, rg, 128, 0, st, L.agg_ptr, L.members, L.P, L.r, L.n_agg, C.b, C.Dinv, C.d,
+                 C.x, C.theta);
+    else
+      launch_pdl(k_restrict_warp<9>, rg, 128, 0, st, L.agg_ptr, L.members, L.P, L.r, L.n_agg, C.b, nullptr, nullptr,
+                 nullptr, 1.0);
+  } else {
+    if (fuse)
+      launch_pdl(k_restrict_warp<16, true>, rg, 128, 0, st, L.agg_ptr, L.members, L.P, L.r, L.n_agg, C.b, C.Dinv, C.d,
+                 C.x, C.theta);
+    else
+      launch_pdl(k_restrict_warp<16>, rg, 128, 0, st, L.agg_ptr, L.members, L.P, L.r, L.n_agg, C.b, nullptr, nullptr,
+                 nullptr, 1.0);
+  }
+  double* xc = vcycle(m, l + 1, st, fuse);
   launch_pdl(k_prolong, grid_for((int64_t)L.n, 256), 256, 0, st, L.agg, L.P, xc, L.nbr, L.bs, x, 1);
   return smooth(L, x, st, l == 0 ? m->out : nullptr);
 }
@@ -1902,19 +1937,30 @@ static int pcg_build(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const ba
     return rc;
   }
   cudaStreamDestroy(cs);
+  static const bool timing = getenv("BAMG_PCG_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto t0 = now();
+  int how = 0;
   cudaGraphExec_t exec = nullptr;
   if (g_pcg_parked) {
     cudaGraphExecUpdateResultInfo info;
     if (cudaGraphExecUpdate(g_pcg_parked, graph, &info) == cudaSuccess) {
       exec = g_pcg_parked;
+      how = 1;
     } else {
       cudaGetLastError();
       cudaGraphExecDestroy(g_pcg_parked);
+      how = 2;
     }
     g_pcg_parked = nullptr;
   }
+  auto t1 = now();
   if (!exec) {
     cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    if (timing)
+      fprintf(stderr, "[pcg] update %s %.2f ms, instantiate %.2f ms\n", how == 1 ? "ok" : (how == 2 ? "failed" : "none"),
+              std::chrono::duration<double, std::milli>(t1 - t0).count(),
+              std::chrono::duration<double, std::milli>(now() - t1).count());
     if (e != cudaSuccess) {
       cudaGraphDestroy(graph);
       cudaFreeAsync(dev, st);
@@ -1922,6 +1968,8 @@ static int pcg_build(bamg_ctx* ctx, bamg_mg* mg, const double* pbj_inv, const ba
       BAMG_CUDA_CHECK(e);
     }
   }
+  else if (timing)
+    fprintf(stderr, "[pcg] update ok %.2f ms\n", std::chrono::duration<double, std::milli>(t1 - t0).count());
   cudaGraphDestroy(graph);
   PcgPlan& P = g_pcg_plan;
   P.valid = true;

@@ -113,15 +113,26 @@ class ObsStructure:
         """(S_ptr, S_col, nnz, max_row): covisibility incl. the diagonal, sorted."""
         if self._covis is None:
             counts = D.empty(self.nc + 1, dtype=torch.int32)
-            D.call("bamg_covis_count", self.cam_ptr, self.cm_list, self.obs_pt_pm, self.pt_ptr,
-                   self.obs_cam_pm, self.nc, counts)
+            words = (self.nc + 31) // 32
+            keep = self.nc * words * 4 <= _COVIS_KEEP_BYTES
+            bm = D.empty(max(self.nc * words, 1), dtype=torch.int32) if keep else None
+            if keep:  # the fill then compacts these bitmaps instead of sweeping the observations again
+                D.call("bamg_covis_count_keep", self.cam_ptr, self.cm_list, self.obs_pt_pm, self.pt_ptr,
+                       self.obs_cam_pm, self.nc, counts, bm)
+            else:
+                D.call("bamg_covis_count", self.cam_ptr, self.cm_list, self.obs_pt_pm, self.pt_ptr,
+                       self.obs_cam_pm, self.nc, counts)
             max_row = int(counts[: self.nc].max().item()) if self.nc else 0
             total = D.empty(1, dtype=torch.int32)
             D.call("bamg_scan_exclusive_i32", counts, counts, self.nc + 1, total)
             nnz = int(counts[self.nc].item())
             S_col = D.empty(max(nnz, 1), dtype=torch.int32)
-            D.call("bamg_covis_fill", self.cam_ptr, self.cm_list, self.obs_pt_pm, self.pt_ptr,
-                   self.obs_cam_pm, self.nc, counts, S_col)
+            if keep:
+                D.call("bamg_covis_compact", bm, self.nc, counts, S_col)
+                del bm
+            else:
+                D.call("bamg_covis_fill", self.cam_ptr, self.cm_list, self.obs_pt_pm, self.pt_ptr,
+                       self.obs_cam_pm, self.nc, counts, S_col)
             self._covis = (counts, S_col[:nnz], nnz, max_row)
         return self._covis
 
@@ -252,6 +263,7 @@ def _copy_stream():
 
 
 _EAGER_STRUCTURE = __import__("os").environ.get("BAMG_EAGER_STRUCTURE", "1") == "1"
+_COVIS_KEEP_BYTES = 256 << 20  # row bitmaps kept between the covisibility count and fill passes
 _CHUNK_RECORDS = int(__import__("os").environ.get("BAMG_SCHUR_CHUNK", "150000"))  # observations per point chunk
 _CHUNK_GROUP_ROWS = int(__import__("os").environ.get("BAMG_SCHUR_CHUNK_ROWS", "1"))
 

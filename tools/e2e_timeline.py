@@ -2,7 +2,8 @@
 evaluate -> linear solve -> D2H), from torch.profiler's CUDA activity (dev tool):
 the copies, the largest kernels and the idle gaps, in start order.
 
-  python tools/e2e_timeline.py [config=4] [min_us=200]
+  python tools/e2e_timeline.py [config=4] [min_us=200] [from_us] [to_us]
+(with a window, every activity inside it is listed)
 """
 import sys
 
@@ -16,7 +17,7 @@ import paper_2007_01941_b200 as P  # noqa: E402
 from paper_2007_01941_b200 import solver  # noqa: E402
 
 
-def main(config=4, min_us=200.0):
+def main(config=4, min_us=200.0, w0=None, w1=None):
     sc = bench.scene_for(int(config))
     cfg = P.SolveConfig(**bench.CFG)
     host = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in sc.arrays()]
@@ -46,9 +47,10 @@ def main(config=4, min_us=200.0):
         gap = s - busy_end
         if gap > 0:
             idle += gap
-        if gap >= float(min_us):
+        inwin = w0 is not None and float(w0) <= s - t0 <= float(w1)
+        if gap >= float(min_us) or (inwin and gap >= 3):
             print(f"  gap {gap:9.1f} us", flush=True)
-        if d >= float(min_us) or "Memcpy" in e.name and d >= 20:
+        if inwin or d >= float(min_us) or "Memcpy" in e.name and d >= 20:
             print(f"  {s - t0:9.1f} +{d:8.1f} us  {e.name.split('(')[0][:60]}")
         busy_end = max(busy_end, e.time_range.end)
     print(f"config {config}: span {busy_end - t0:.1f} us, device idle {idle:.1f} us, {len(ev)} activities")
