@@ -879,14 +879,20 @@ __device__ __forceinline__ double tail_blocks16(const int* __restrict__ col, con
   return k == 0 ? s0 : (k == 1 ? s1 : (k == 2 ? s2 : s3));
 }
 
-// k_row16_cta's row, CTA-cooperative (4 warps)
-__device__ __forceinline__ void tail_row16(const TailOp& o, int row, double (*part)[16], int lane, int w) {
+// 4-warp group barrier (named barrier 1 + group; barrier 0 stays __syncthreads)
+__device__ __forceinline__ void group_sync(int grp) {
+  asm volatile("bar.sync %0, 128;" ::"r"(grp + 1) : "memory");
+}
+
+// k_row16_cta's row, cooperative over a group of 4 warps (a 128-thread CTA, or one
+// of the 4-warp groups of a larger CTA: same partition, same summation order)
+__device__ __forceinline__ void tail_row16(const TailOp& o, int row, double (*part)[16], int lane, int w, int grp) {
   int b0 = __ldg(o.ptr + row), b1 = __ldg(o.ptr + row + 1);
   int q = (b1 - b0 + 3) >> 2;
   int lo = min(b0 + w * q, b1), hi = min(lo + q, b1);
   double v = tail_blocks16(o.col, o.blocks, o.x, lo, hi, lane);
   if (lane < 16) part[w][lane] = v;
-  __syncthreads();
+  group_sync(grp);
   if (w == 0) {
     int r = lane & 15;
     double ax = ((part[0][r] + part[1][r]) + part[2][r]) + part[3][r];
@@ -906,21 +912,28 @@ __device__ __forceinline__ void tail_row16(const TailOp& o, int row, double (*pa
       }
     }
   }
-  __syncthreads();
+  group_sync(grp);
 }
 
-__global__ void __launch_bounds__(128) k_vcycle_tail(const TailOp* __restrict__ ops, int nops) {
+// CLUSTER = false: one cooperative grid (128-thread CTAs, grid-wide barrier);
+// CLUSTER = true: ONE thread-block cluster of up to 16 CTAs of 512 threads (4-warp
+// row groups), cluster barrier between ops -- the coarse levels' data are a few MB,
+// read from L2 by 16 SMs at a fraction of a grid barrier's cost.
+template <bool CLUSTER>
+__global__ void __launch_bounds__(CLUSTER ? 512 : 128) k_vcycle_tail(const TailOp* __restrict__ ops, int nops) {
   namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  __shared__ double part[4][16];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __shared__ double part_all[CLUSTER ? 16 : 4][16];
+  const int lane = threadIdx.x & 31, wt = threadIdx.x >> 5, w = wt & 3, grp = wt >> 2;
+  const int ngrp = blockDim.x >> 7;
+  double(*part)[16] = part_all + 4 * grp;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int k = 0; k < nops; ++k) {
     const TailOp o = ops[k];
     switch (o.type) {
       case TOP_ROW:
-        for (int row = blockIdx.x; row < o.nbr; row += gridDim.x) tail_row16(o, row, part, lane, w);
+        for (int row = blockIdx.x * ngrp + grp; row < o.nbr; row += gridDim.x * ngrp)
+          tail_row16(o, row, part, lane, w, grp);
         break;
       case TOP_CHEB:  // k_cheb_step<16> without the product (x_in null)
         for (int row = gwarp; row < o.nbr; row += nwarps) {
@@ -1006,7 +1019,10 @@ __global__ void __launch_bounds__(128) k_vcycle_tail(const TailOp* __restrict__ 
         }
         break;
     }
-    if (k + 1 < nops) grid.sync();
+    if (k + 1 < nops) {
+      if constexpr (CLUSTER) cg::this_cluster().sync();
+      else cg::this_grid().sync();
+    }
   }
 }
 
@@ -1062,6 +1078,7 @@ struct bamg_mg {
   TailOp* tail_ops = nullptr;
   double* tail_result = nullptr;
   int tail_grid = 0;
+  bool tail_cluster = true;
 };
 
 extern "C" bamg_mg* bamg_mg_create(int32_t n_levels) {
@@ -1396,14 +1413,25 @@ static double* vcycle(bamg_mg* m, size_t l, cudaStream_t st, bool first_done = f
     g_bamg_launches.fetch_add(1, std::memory_order_relaxed);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(m->tail_grid);
-    cfg.blockDim = dim3(128);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
+    if (m->tail_cluster) {
+      cfg.blockDim = dim3(512);
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = m->tail_grid;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+    } else {
+      cfg.blockDim = dim3(128);
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+    }
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_vcycle_tail, (const TailOp*)m->tail_ops, (int)m->tail_host.size());
+    if (m->tail_cluster)
+      cudaLaunchKernelEx(&cfg, k_vcycle_tail<true>, (const TailOp*)m->tail_ops, (int)m->tail_host.size());
+    else
+      cudaLaunchKernelEx(&cfg, k_vcycle_tail<false>, (const TailOp*)m->tail_ops, (int)m->tail_host.size());
     return m->tail_result;
   }
   if (L.inv) {
@@ -1505,17 +1533,29 @@ static int mg_plan_tail(bamg_mg* m, const std::vector<int>& nnzb, cudaStream_t s
   size_t bytes = sizeof(TailOp) * m->tail_host.size();
   BAMG_CUDA_CHECK(cudaMallocAsync(&m->tail_ops, bytes, st));
   BAMG_CUDA_CHECK(cudaMemcpyAsync(m->tail_ops, m->tail_host.data(), bytes, cudaMemcpyHostToDevice, st));
-  static int grid = 0;
+  static int grid = 0, cluster = -1;
+  if (cluster < 0) {
+    const char* e = getenv("BAMG_VTAIL_MODE");
+    cluster = !(e && strcmp(e, "grid") == 0);
+  }
   if (!grid) {
-    int per_sm = 0;
-    BAMG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vcycle_tail, 128, 0));
-    const char* e = getenv("BAMG_VTAIL_CTAS");
-    int want = e ? atoi(e) : 4;
-    if (per_sm > want) per_sm = want;
-    if (per_sm < 1) per_sm = 1;
-    grid = per_sm * bamg_num_sms();
+    if (cluster) {
+      const char* e = getenv("BAMG_VTAIL_CTAS");
+      grid = e ? atoi(e) : 16;
+      if (grid > 8)
+        BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_vcycle_tail<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    } else {
+      int per_sm = 0;
+      BAMG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vcycle_tail<false>, 128, 0));
+      const char* e = getenv("BAMG_VTAIL_CTAS");
+      int want = e ? atoi(e) : 4;
+      if (per_sm > want) per_sm = want;
+      if (per_sm < 1) per_sm = 1;
+      grid = per_sm * bamg_num_sms();
+    }
   }
   m->tail_grid = grid;
+  m->tail_cluster = cluster != 0;
   return 0;
 }
 

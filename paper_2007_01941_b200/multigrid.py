@@ -263,18 +263,27 @@ def galerkin(P: BlockSparseMatrix, A: BlockSparseMatrix, agg: Aggregation) -> Bl
     """sym(P^T A P) + decoupled-dof patch (multigrid.py:409-411, 444-471)."""
     na, n = agg.n_aggregates, A.n_block_rows
     ptr, mem = agg.member_lists()
-    counts = D.empty(na + 1, dtype=torch.int32)
-    D.call("bamg_galerkin_pattern", ptr, mem, A._ptr, A._col, agg._a32, na, counts, None)
-    D.call("bamg_scan_exclusive_i32", counts, counts, na + 1, None)
-    nnzc = int(counts[na].item())
-    Ccol = D.empty(max(nnzc, 1), dtype=torch.int32)
-    D.call("bamg_galerkin_pattern", ptr, mem, A._ptr, A._col, agg._a32, na, counts, Ccol)
     nnzf = A.n_block_entries
-    fine_sorted = D.empty(max(nnzf, 1), dtype=torch.int32)
-    cblk_ptr = D.empty(nnzc + 1, dtype=torch.int32)
-    fine_row = D.empty(max(nnzf, 1), dtype=torch.int32)
-    D.call("bamg_galerkin_map", A._ptr, A._col, agg._a32, n, nnzf, counts, Ccol, nnzc, fine_sorted, cblk_ptr,
-           fine_row)
+    # the coarse pattern and the fine -> coarse block map depend on the fine pattern
+    # and the aggregation only: kept on the aggregation, so the level-0 ones (whose
+    # aggregation is cached per problem) are built once per problem, not per step
+    key = (A._ptr.data_ptr(), A._col.data_ptr(), n, nnzf)
+    cache = getattr(agg, "_galerkin_symbolic", None)
+    if cache is not None and cache[0] == key:
+        _, counts, Ccol, nnzc, fine_sorted, cblk_ptr, fine_row = cache
+    else:
+        counts = D.empty(na + 1, dtype=torch.int32)
+        D.call("bamg_galerkin_pattern", ptr, mem, A._ptr, A._col, agg._a32, na, counts, None)
+        D.call("bamg_scan_exclusive_i32", counts, counts, na + 1, None)
+        nnzc = int(counts[na].item())
+        Ccol = D.empty(max(nnzc, 1), dtype=torch.int32)
+        D.call("bamg_galerkin_pattern", ptr, mem, A._ptr, A._col, agg._a32, na, counts, Ccol)
+        fine_sorted = D.empty(max(nnzf, 1), dtype=torch.int32)
+        cblk_ptr = D.empty(nnzc + 1, dtype=torch.int32)
+        fine_row = D.empty(max(nnzf, 1), dtype=torch.int32)
+        D.call("bamg_galerkin_map", A._ptr, A._col, agg._a32, n, nnzf, counts, Ccol, nnzc, fine_sorted, cblk_ptr,
+               fine_row)
+        agg._galerkin_symbolic = (key, counts, Ccol, nnzc, fine_sorted, cblk_ptr, fine_row)
     out = D.empty(max(nnzc, 1), NULLSPACE_DIM, NULLSPACE_DIM)
     D.call("bamg_galerkin_numeric", A.row_block_size, cblk_ptr, fine_sorted, fine_row, A._col, A.blocks, P.blocks,
            nnzf, na, counts, Ccol, nnzc, P.padded_count, out)

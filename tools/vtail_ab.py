@@ -19,7 +19,7 @@ out = solver.linear_solve(prob, jac, 1e4, cfg)
 h = out[6]
 r = D.f64(np.random.default_rng(1).standard_normal(h.levels[0].scalar_dim))
 ref = None
-for mb in (0, 32, 96, 256, 0, 96):
+for mb in [int(v) for v in (sys.argv[2].split(",") if len(sys.argv) > 2 else "0,2,16,32,0,16".split(","))]:
     _lib.call("bamg_mg_set_tail", h._plan.handle, mb)
     h._plan.prepare()
     kinds = [int(_lib.lib().bamg_mg_level_kind(h._plan.handle, li)) for li in range(h.n_levels)]
