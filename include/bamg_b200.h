@@ -396,6 +396,41 @@ int bamg_lanczos_lmax(bamg_ctx* ctx, int32_t bs, int32_t nbr, const int32_t* ptr
  * later, so several levels share one readback */
 int bamg_lanczos_finish(const double* ab_host, int32_t steps, double* lambda_out, int32_t* status);
 
+/* ---- device-side synthetic scenes, BASELINE configs 3-5 ----
+ * The model of the reference's host generator (synth.py:92-558: look-at camera frames,
+ * visibility draw, pixel noise, centre-preserving start perturbation) with the
+ * distributions of SURVEY App. C (scenes.py is the numpy statement used for the goldens).
+ * kind: 3 city, 4 large, 5 loop. params_host (8 doubles, host memory): [side, n_clusters,
+ * cam_sigma, pt_sigma, z_max, lam, radius (= grid cell), bridge_frac]. Counter-based RNG:
+ * every draw is a function of (seed, stream, index).
+ * layout: cam_centre (nc,3), cam_rt (nc,24: R, t, R0, t0), cam_truth / cam_init (nc,9),
+ *   cam_cell (nc) grid cell of each camera, pts_true / pts_init (npts,3), n_pick (npts)
+ *   requested cameras, aux (npts,2) loop run placement.
+ * visibility: cell_ptr / cell_cams = cameras grouped by cell (kinds 3, 4); sel
+ *   (npts x 32) the surviving cameras of each point sorted by camera, cnt (npts; 0 when
+ *   fewer than two survive), cam_used (nc) / pt_used (npts) 0/1 flags, info[0] = points
+ *   whose in-radius candidates overflowed the 2048-entry cache (must be 0).
+ * emit: obs_off = exclusive scan of cnt, cam_map / pt_map = exclusive scans of the used
+ *   flags; writes the compacted problem arrays (observations point-major). */
+int bamg_scene_grid_cells(int32_t kind, int32_t nc, int64_t npts, const double* params_host);
+int bamg_scene_layout(bamg_ctx* ctx, int32_t kind, int64_t seed, int32_t nc, int64_t npts,
+                      const double* params_host, double* cam_centre, double* cam_rt, double* cam_truth,
+                      double* cam_init, uint32_t* cam_cell, double* pts_true, double* pts_init,
+                      int32_t* n_pick, int32_t* aux, void* stream);
+int bamg_scene_visibility(bamg_ctx* ctx, int32_t kind, int64_t seed, int32_t nc, int64_t npts,
+                          const double* params_host, int32_t k_nn, const double* cam_centre,
+                          const double* cam_rt, const double* pts_true, const double* pts_init,
+                          const int32_t* n_pick, const int32_t* aux, const int32_t* cell_ptr,
+                          const uint32_t* cell_cams, int32_t* sel, int32_t* cnt, int32_t* cam_used,
+                          int32_t* pt_used, int32_t* info, void* stream);
+int bamg_scene_emit(bamg_ctx* ctx, int64_t seed, int32_t nc, int64_t npts, const int32_t* cnt,
+                    const int32_t* obs_off, const int32_t* sel, const int32_t* cam_used,
+                    const int32_t* cam_map, const int32_t* pt_map, const double* cam_rt,
+                    const double* cam_truth, const double* cam_init, const double* pts_true,
+                    const double* pts_init, int64_t* cam_index, int64_t* pt_index, double* pixels,
+                    double* out_cam_truth, double* out_cam_init, double* out_pts_true,
+                    double* out_pts_init, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

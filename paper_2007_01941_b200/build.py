@@ -18,7 +18,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "csrc", "_obj")
 LIB = os.path.join(HERE, "libbamg_b200.so")
-SOURCES = ["prims.cu", "problem.cu", "schur.cu", "blas.cu", "mg.cu", "driver.cu", "blockmat.cu", "balio.cpp"]
+SOURCES = ["prims.cu", "problem.cu", "schur.cu", "blas.cu", "mg.cu", "driver.cu", "blockmat.cu", "scenegen.cu", "balio.cpp"]
 HEADERS = ["common.cuh", "ctx.h", "vcycle.cuh", os.path.join("..", "..", "include", "bamg_b200.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

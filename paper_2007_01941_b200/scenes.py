@@ -389,3 +389,105 @@ def random_problem(seed, n_cameras=5, n_points=15, pixel_noise=0.5, decoupled=Fa
     if pixel_noise:
         pix = pix + rng.normal(0, pixel_noise, pix.shape)
     return Scene("random", cams, pts, ci, pi, pix)
+
+
+# -- device-side generation (configs 3-5) ---------------------------------------
+
+
+@dataclasses.dataclass
+class DeviceScene:
+    """A generated scene resident in HBM (torch tensors): `arrays()` goes straight into
+    `BundleProblem` with no host round trip; `to_host()` gives the numpy `Scene`."""
+
+    name: str
+    camera_params: "object"
+    points: "object"
+    cam_index: "object"
+    pt_index: "object"
+    pixels: "object"
+    truth_cameras: "object"
+    truth_points: "object"
+    notes: str = ""
+
+    n_cameras = property(lambda self: self.camera_params.shape[0])
+    n_points = property(lambda self: self.points.shape[0])
+    n_observations = property(lambda self: self.cam_index.shape[0])
+
+    def arrays(self):
+        return (self.camera_params, self.points, self.cam_index, self.pt_index, self.pixels)
+
+    def to_host(self) -> Scene:
+        h = lambda t: t.cpu().numpy()  # noqa: E731
+        return Scene(self.name, h(self.camera_params), h(self.points), h(self.cam_index), h(self.pt_index),
+                     h(self.pixels), h(self.truth_cameras), h(self.truth_points), self.notes)
+
+
+# per-config defaults: the numbers of `city`, `large` and `loop` above
+_DEVICE_DEFAULTS = {
+    3: dict(n_cameras=4000, n_points=1_000_000, side=200.0, z_max=20.0, lam=4.0, radius=15.0, k_nearest=48),
+    4: dict(n_cameras=13_000, n_points=4_500_000, side=1000.0, n_clusters=40, cam_sigma=5.0, pt_sigma=10.0,
+            z_max=10.0, lam=4.5, radius=60.0, k_nearest=160),
+    5: dict(n_cameras=8000, n_points=2_000_000, bridge_frac=0.005),
+}
+
+
+def device_config(n: int, seed: int = 0, **kw) -> DeviceScene:
+    """Configs 3-5 generated on the GPU (csrc/scenegen.cu).
+
+    Same model and distributions as `city` / `large` / `loop` (camera frames, the
+    k-nearest in-front candidate rule, 2+Poisson / 2+geometric draws, `_finish`'s
+    filters, pixel noise and the centre-preserving start), but drawn from a
+    counter-based generator on the device, so the scene differs draw by draw from the
+    numpy one (the goldens stay tied to the numpy scenes). Deterministic in `seed`.
+    """
+    import torch
+
+    from . import _device as D
+    from . import _lib
+
+    if n not in _DEVICE_DEFAULTS:
+        raise ValueError("device_config generates configs 3, 4 and 5")
+    p = dict(_DEVICE_DEFAULTS[n])
+    unknown = set(kw) - set(p)
+    if unknown:
+        raise TypeError(f"unknown scene parameter(s) {sorted(unknown)}")
+    p.update(kw)
+    nc, npts = int(p["n_cameras"]), int(p["n_points"])
+    params = torch.tensor([p.get("side", 0.0), p.get("n_clusters", 1), p.get("cam_sigma", 0.0),
+                           p.get("pt_sigma", 0.0), p.get("z_max", 0.0), p.get("lam", 0.0),
+                           p.get("radius", 1.0), p.get("bridge_frac", 0.0)], dtype=torch.float64)
+    i32, u32 = torch.int32, torch.int32  # u32 buffers carried as int32 tensors
+    centre, cam_rt = D.empty(nc, 3), D.empty(nc, 24)
+    truth, init = D.empty(nc, 9), D.empty(nc, 9)
+    cell = D.empty(nc, dtype=u32)
+    pts, pts0 = D.empty(npts, 3), D.empty(npts, 3)
+    n_pick, aux = D.empty(npts, dtype=i32), D.empty(npts, 2, dtype=i32)
+    D.call("bamg_scene_layout", n, seed, nc, npts, params, centre, cam_rt, truth, init, cell, pts, pts0, n_pick, aux)
+    n_cells = _lib.call("bamg_scene_grid_cells", n, nc, npts, params)
+    cell_ptr = D.empty(n_cells + 1, dtype=i32)
+    cell_cams = D.empty(nc, dtype=u32)
+    if n != 5:
+        ids = torch.arange(nc, dtype=i32, device=D.dev())
+        cell_sorted = D.empty(nc, dtype=u32)
+        D.call("bamg_sort_pairs_u32", cell, ids, cell_sorted, cell_cams, nc, max(1, int(n_cells).bit_length()))
+        D.call("bamg_segment_ptr", cell_sorted, nc, n_cells, cell_ptr)
+    sel, cnt = D.empty(npts, 32, dtype=i32), D.empty(npts, dtype=i32)
+    cam_used, pt_used, info = D.empty(nc, dtype=i32), D.empty(npts, dtype=i32), D.empty(1, dtype=i32)
+    D.call("bamg_scene_visibility", n, seed, nc, npts, params, int(p.get("k_nearest", 0)), centre, cam_rt, pts, pts0,
+           n_pick, aux, cell_ptr, cell_cams, sel, cnt, cam_used, pt_used, info)
+    obs_off, cam_map, pt_map = D.empty(npts, dtype=i32), D.empty(nc, dtype=i32), D.empty(npts, dtype=i32)
+    totals = D.empty(3, dtype=i32)
+    D.call("bamg_scan_exclusive_i32", cnt, obs_off, npts, totals[0:1])
+    D.call("bamg_scan_exclusive_i32", cam_used, cam_map, nc, totals[1:2])
+    D.call("bamg_scan_exclusive_i32", pt_used, pt_map, npts, totals[2:3])
+    k, nc_kept, np_kept, over = (int(v) for v in torch.cat([totals, info]).cpu().numpy())
+    if over:
+        raise RuntimeError(f"scene generation: {over} point(s) had more than 2048 cameras in range")
+    ci, pi = D.empty(k, dtype=torch.int64), D.empty(k, dtype=torch.int64)
+    pix = D.empty(k, 2)
+    o_truth, o_init = D.empty(nc_kept, 9), D.empty(nc_kept, 9)
+    o_pts, o_pts0 = D.empty(np_kept, 3), D.empty(np_kept, 3)
+    D.call("bamg_scene_emit", seed, nc, npts, cnt, obs_off, sel, cam_used, cam_map, pt_map, cam_rt, truth, init,
+           pts, pts0, ci, pi, pix, o_truth, o_init, o_pts, o_pts0)
+    name = {3: "city", 4: "large", 5: "loop"}[n] + "-device"
+    return DeviceScene(name, o_init, o_pts0, ci, pi, pix, o_truth, o_pts, f"seed {seed}, {p}")
