@@ -282,10 +282,11 @@ double bamg_tridiag_max_eig(const double* a_host, const double* b_host, int32_t 
 /* ---- driver helpers: rotation.py:124-137 canonicalize (solver.py:290, problem.py:106) ---- */
 int bamg_canonicalize(bamg_ctx* ctx, double* cams, int32_t n, int32_t stride, void* stream);
 /* solver.py:276-301 LM trial decision on the device: t_dev = [rhs.dc, dc.S dc, g_p.C^-1 g_p,
- * dc.dc, dp.dp, f, f_new] (device scalars), n_behind_dev = the candidate's behind-camera
+ * dc.dc, dp.dp, f, f_new, radius] (device scalars), n_behind_dev = the candidate's behind-camera
  * count. Computes decrease (schur.py:176-188), rho, accepted = rho > min_rho; on accept
  * copies the candidate into (cams, pts) and canonicalises the rotations. out_dev =
- * [rho, accepted, decrease, step_norm, f_new] -- one readback per LM trial. */
+ * [rho, accepted, decrease, step_norm, f_new, radius'] (6 doubles) with the trust-region
+ * update of solver.py:134-149 applied to the radius -- one readback per LM trial. */
 int bamg_lm_trial(bamg_ctx* ctx, const double* t_dev, const int32_t* n_behind_dev, double min_rho, double* cams,
                   const double* cand_cams, int32_t nc, double* pts, const double* cand_pts, int32_t npt,
                   double* out_dev, void* stream);

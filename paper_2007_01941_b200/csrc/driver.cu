@@ -37,7 +37,10 @@ __global__ void k_canonicalize(double* __restrict__ cams, int n, int stride) {
 //   accepted = rho > min_rho: params <- candidate, rotations canonicalised
 // Every thread evaluates the (uniform) decision; the arithmetic is the host's
 // IEEE sequence (explicit _rn operations, no contraction). out = [rho, accepted,
-// decrease, step_norm, f_new (f when behind)]. The radius update stays on the host.
+// decrease, step_norm, f_new (f when behind), radius']: the trust-region update
+// (solver.py:134-149) radius' = radius / max(1/3, 1 - (2 rho - 1)^3) on acceptance,
+// radius / 2 otherwise, from the device slot t[7]. The cube is formed in double-double
+// and rounded once, like the host's correctly rounded pow(x, 3).
 __global__ void k_lm_trial(const double* __restrict__ t, const int* __restrict__ n_behind, double min_rho,
                            double* __restrict__ cams, const double* __restrict__ cand_cams, int nc,
                            double* __restrict__ pts, const double* __restrict__ cand_pts, int npt,
@@ -54,6 +57,17 @@ __global__ void k_lm_trial(const double* __restrict__ t, const int* __restrict__
     out[2] = dec;
     out[3] = __dsqrt_rn(__dadd_rn(t[3], t[4]));
     out[4] = fn;
+    double rad = t[7];
+    if (acc) {
+      double u = __dsub_rn(__dmul_rn(2.0, rho), 1.0);
+      double hi = __dmul_rn(u, u), lo = __fma_rn(u, u, -hi);
+      double p = __dmul_rn(hi, u), e = __fma_rn(hi, u, -p);
+      double cube = __dadd_rn(p, __dadd_rn(e, __dmul_rn(lo, u)));
+      rad = __ddiv_rn(rad, fmax(1.0 / 3.0, __dsub_rn(1.0, cube)));
+    } else {
+      rad = __ddiv_rn(rad, 2.0);
+    }
+    out[5] = rad;
   }
   if (!acc) return;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;

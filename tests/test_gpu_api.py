@@ -214,11 +214,11 @@ def test_lm_trial_decision_on_device(P):
     cand[1, :3] = [4.0, 0.0, 0.0]  # |aa| > pi: canonicalised on acceptance
     pts0, cpts = rng.normal(size=(npt, 3)), rng.normal(size=(npt, 3))
 
-    def run(tvals, behind, min_rho=1e-3):
+    def run(tvals, behind, min_rho=1e-3, radius=1e4):
         cams, pts = D.f64(cams0.copy()), D.f64(pts0.copy())
-        t = D.f64(np.array(tvals + [0.0]))
+        t = D.f64(np.array(tvals + [radius]))
         nb = D.i32(np.array([behind], dtype=np.int32))
-        out = D.empty(5)
+        out = D.empty(6)
         D.call("bamg_lm_trial", t, nb, min_rho, cams, D.f64(cand), nc, pts, D.f64(cpts), npt, out)
         return H(out), H(cams), H(pts)
 
@@ -243,6 +243,20 @@ def test_lm_trial_decision_on_device(P):
     # nonpositive model decrease: rho = -inf
     out, _, _ = run([0.0, 2.0, 0.0, dcn, dpn, f, fn], 0)
     assert out[0] == -np.inf and out[1] == 0.0
+    # the trust-region update (solver.py:134-149) on the device, bit for bit the host's
+    # TrustRegion.accept / reject: decrease = 1 and f_new = 0 make rho = f / 2 exactly
+    rng = np.random.default_rng(5)
+    for rho_want in [1e-3 + 1e-9, 0.25, 0.5, 0.75, 1.0, 1.7, 3.0] + list(rng.uniform(0.002, 2.0, 200)):
+        for radius in (1e4, 3.3333e-7, float(rng.uniform(1e-3, 1e6))):
+            out, _, _ = run([1.0, 0.0, 0.0, dcn, dpn, 2.0 * rho_want, 0.0], 0, radius=radius)
+            assert out[0] == rho_want and out[1] == 1.0
+            tr = P.TrustRegion(radius=radius)
+            tr.accept(rho_want)
+            assert out[5] == tr.radius, (rho_want, radius)
+    out, _, _ = run([a, b, c, dcn, dpn, f, 11.0], 0, radius=7.0)
+    tr = P.TrustRegion(radius=7.0)
+    tr.reject()
+    assert out[1] == 0.0 and out[5] == tr.radius
 
 
 def test_pinned_inputs_match_host_inputs(P):
