@@ -1121,6 +1121,201 @@ k_aggregate_spec(const int* __restrict__ G_ptr, const int* __restrict__ G_col, c
   }
 }
 
+// ---------------------------------------------------------------------------
+// Low-latency sequential form of the same scan (identical decisions). On the coarse
+// levels the neighbours of a node sit a few indices away, so most of a speculative
+// batch conflicts and its rounds cost ~500 cycles per node. Here every lane runs the
+// SAME one-node-at-a-time decision redundantly from shared memory (broadcast loads,
+// no shuffles, no ballots): the dependent chain per node is agg[j] -> size[agg[j]]
+// -> the head rule -> one store, ~100-150 cycles; the next node's head entries are
+// state independent and are loaded ahead. Visits the head cannot decide (tie run
+// past the head, no eligible head entry in a longer row, unsorted row) fall back to
+// the cooperative visit of k_aggregate_head.
+__global__ void __launch_bounds__(32)
+k_aggregate_seq(const int* __restrict__ G_ptr, const int* __restrict__ G_col, const double* __restrict__ G_val,
+                const int* __restrict__ hcol_g, const double* __restrict__ hval_g, const int* __restrict__ hlen_g,
+                int n, int max_size, int* __restrict__ agg_g, int* __restrict__ size_g, int* __restrict__ n_agg_out) {
+  extern __shared__ __align__(16) double shh[];
+  double* sval = shh;                                              // AH_NB * AH_B * AH_K
+  int* scol = reinterpret_cast<int*>(sval + AH_NB * AH_B * AH_K);  // AH_NB * AH_B * AH_K
+  int* slen = scol + AH_NB * AH_B * AH_K;                          // AH_NB * AH_B
+  int* agg = slen + AH_NB * AH_B;                                  // n
+  int* size = agg + n;                                             // n
+  const int lane = threadIdx.x;
+  for (int i = lane; i < n; i += 32) {
+    agg[i] = -1;
+    size[i] = 0;
+  }
+  const int nbt = (n + AH_B - 1) / AH_B;
+#pragma unroll 1
+  for (int b = 0; b < AH_NB; ++b) {
+    if (b < nbt) ah_issue(b, hcol_g, hval_g, hlen_g, scol, sval, slen, lane);
+    else cp_async_commit();
+  }
+  __syncwarp();
+  int nagg = 0;
+  for (int b = 0; b < nbt; ++b) {
+    cp_async_wait<AH_NB - 1>();
+    __syncwarp();
+    const int slot = b % AH_NB;
+    const int iend = min(AH_B, n - b * AH_B);
+    int ii = 0;
+    while (ii < iend) {  // warp uniform
+      // fast path, lane 0 alone (same-thread ordering, no warp synchronisation per
+      // node): the top head entry is not tied with the second one, so it wins as soon
+      // as it is eligible -- pair if unassigned, join if its aggregate has room
+      int stop = iend, nagg0 = nagg;
+      if (lane == 0) {
+        int k = ii;
+        int nj0 = scol[(slot * AH_B + k) * AH_K];
+        double2 ng = *reinterpret_cast<const double2*>(sval + (slot * AH_B + k) * AH_K);
+        for (; k < iend; ++k) {
+          const int i = b * AH_B + k;
+          const int self = agg[i];
+          const int j0 = nj0;
+          const double2 g = ng;
+          if (k + 1 < iend) {  // the next node's top entries (state independent)
+            nj0 = scol[(slot * AH_B + k + 1) * AH_K];
+            ng = *reinterpret_cast<const double2*>(sval + (slot * AH_B + k + 1) * AH_K);
+          }
+          if (self >= 0) continue;
+          if (j0 >= 0 && g.x != g.y) {
+            const int a0 = agg[j0];
+            if (a0 < 0) {
+              agg[i] = nagg0;
+              agg[j0] = nagg0;
+              size[nagg0] = 2;
+              ++nagg0;
+              continue;
+            }
+            if (size[a0] < max_size) {
+              agg[i] = a0;
+              size[a0] += 1;
+              continue;
+            }
+          }
+          break;  // the general rule decides this node
+        }
+        stop = k;
+      }
+      stop = __shfl_sync(FULL_MASK, stop, 0);
+      nagg = __shfl_sync(FULL_MASK, nagg0, 0);
+      __syncwarp();
+      ii = stop + 1;
+      if (stop >= iend) break;
+      // general rule for node `stop`, every lane redundantly (broadcast loads)
+      const int i = b * AH_B + stop;
+      const int* hc = scol + (slot * AH_B + stop) * AH_K;
+      const double* hv = sval + (slot * AH_B + stop) * AH_K;
+      const int len = slen[slot * AH_B + stop];
+      int jj[AH_K], aa[AH_K];
+      double gg[AH_K];
+#pragma unroll
+      for (int e = 0; e < AH_K; ++e) {
+        jj[e] = hc[e];
+        gg[e] = hv[e];
+      }
+#pragma unroll
+      for (int e = 0; e < AH_K; ++e) aa[e] = jj[e] >= 0 ? agg[jj[e]] : -1;
+      int dec = -3;
+      if (jj[0] != -2) {
+        bool el[AH_K];
+#pragma unroll
+        for (int e = 0; e < AH_K; ++e) el[e] = jj[e] >= 0 && (aa[e] < 0 || size[aa[e]] < max_size);
+        int f = -1;
+#pragma unroll
+        for (int e = AH_K - 1; e >= 0; --e)
+          if (el[e]) f = e;
+        if (f < 0) {
+          if (len <= AH_K) dec = -1;  // no eligible neighbour: left for the post-pass
+        } else {
+          double gf = 0.0;
+#pragma unroll
+          for (int e = 0; e < AH_K; ++e)
+            if (e == f) gf = gg[e];
+          int cu = -1, jf = -1;
+#pragma unroll
+          for (int e = AH_K - 1; e >= 0; --e) {
+            if (e == f) jf = jj[e];
+            if (e >= f && jj[e] >= 0 && gg[e] == gf && el[e] && aa[e] < 0) cu = jj[e];
+          }
+          const bool tail = jj[AH_K - 1] >= 0 && gg[AH_K - 1] == gf;
+          if (cu >= 0) dec = cu;
+          else if (!(tail && len > AH_K)) dec = jf;
+        }
+      }
+      int bj = dec;
+      if (dec == -3) bj = agg_visit_coop(i, G_ptr, G_col, G_val, hc, hv, len, agg, size, max_size, lane);
+      if (bj >= 0) {
+        const int aj = agg[bj];  // every lane reads the pre-update value
+        __syncwarp();
+        if (lane == 0) {
+          if (aj < 0) {
+            agg[i] = nagg;
+            agg[bj] = nagg;
+            size[nagg] = 2;
+          } else {
+            agg[i] = aj;
+            size[aj] += 1;
+          }
+        }
+        if (aj < 0) ++nagg;
+        __syncwarp();
+      }
+    }
+    __syncwarp();  // every lane is done with this slot before it is refilled
+    if (b + AH_NB < nbt) ah_issue(b + AH_NB, hcol_g, hval_g, hlen_g, scol, sval, slen, lane);
+    else cp_async_commit();
+  }
+  cp_async_wait<0>();
+  // post-pass over leftovers in index order (multigrid.py:164-175); a leftover's visit
+  // assigns only itself, so the unassigned set of a 32-node window is read once
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    __syncwarp();
+    unsigned todo = __ballot_sync(FULL_MASK, i0 + lane < n && agg[i0 + lane] < 0);
+    while (todo) {
+      const int i = i0 + __ffs(todo) - 1;
+      todo &= todo - 1;
+      Cand best{0.0, 0, -1};
+      for (int q = G_ptr[i] + lane; q < G_ptr[i + 1]; q += 32) {
+        int j = G_col[q];
+        int a = agg[j];
+        if (a >= 0 && size[a] <= max_size) {
+          Cand c{G_val[q], 0, j};
+          if (better(c, best)) best = c;
+        }
+      }
+      best = warp_best(best);
+      __syncwarp();
+      if (lane == 0) {
+        if (best.j >= 0) {
+          int a = agg[best.j];
+          agg[i] = a;
+          size[a] += 1;
+        } else {
+          agg[i] = nagg;
+          size[nagg] = 1;
+        }
+      }
+      if (best.j < 0) ++nagg;
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  int mx = 0;
+  for (int i = lane; i < n; i += 32) {
+    agg_g[i] = agg[i];
+    size_g[i] = size[i];
+    if (i < nagg) mx = max(mx, size[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL_MASK, mx, o));
+  if (lane == 0) {
+    n_agg_out[0] = nagg;
+    n_agg_out[1] = mx;
+  }
+}
+
 extern "C" int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t* G_col, const double* G_val,
                               int32_t n, int32_t max_size, int32_t* agg, int32_t* size_work, int32_t* n_agg_dev,
                               int64_t nnz_cap, void* stream) {
@@ -1190,7 +1385,22 @@ extern "C" int bamg_aggregate(bamg_ctx* ctx, const int32_t* G_ptr, const int32_t
         const char* e = getenv("BAMG_AGG_SPEC");
         return !(e && e[0] == '0');
       }();
-      if (spec_on) {
+      // default: the low-latency sequential scan (config 4: level 0 2.8 -> 1.8 ms, coarse
+      // levels 2.5 -> 1.1 ms; config 5: 6.0 -> 1.0 and 3.6 -> 0.8 ms against the
+      // speculative rounds, tools/agg_ab.py); BAMG_AGG_SEQ=0 selects the speculative kernel
+      static const bool use_seq = [] {
+        const char* e = getenv("BAMG_AGG_SEQ");
+        return !(e && e[0] == '0');
+      }();
+      if (use_seq) {
+        static size_t qattr = 0;
+        if (smh > qattr) {
+          BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smh));
+          qattr = smh;
+        }
+        launch(k_aggregate_seq, 1, 32, smh, st, G_ptr, (const int*)col_s, (const double*)val_s, (const int*)hcol,
+               (const double*)hval, (const int*)hlen, n, max_size, agg, size_work, n_agg_dev);
+      } else if (spec_on) {
         static size_t sattr = 0;
         if (smh > sattr) {
           BAMG_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smh));

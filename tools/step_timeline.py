@@ -2,7 +2,7 @@
 start order with its stream, duration and the idle gap before it on the device, plus
 the total idle time (host synchronisations / launch latency show up as gaps).
 
-  python tools/step_timeline.py [config=4] [min_gap_us=15]
+  python tools/step_timeline.py [config=4] [min_gap_us=15] [dump_path]   (dump: every activity)
 """
 import sys
 
@@ -16,7 +16,7 @@ from paper_2007_01941_b200 import multigrid as MG  # noqa: E402
 from paper_2007_01941_b200 import solver  # noqa: E402
 
 
-def main(config=4, min_gap=15.0):
+def main(config=4, min_gap=15.0, dump=None):
     sc = bench.scene_for(int(config))
     prob = P.BundleProblem(*sc.arrays())
     cfg = P.SolveConfig(**bench.CFG)
@@ -46,6 +46,11 @@ def main(config=4, min_gap=15.0):
         if gap >= float(min_gap):
             print(f"  gap {gap:8.1f} us before {e.name.split('(')[0][:40]:40s} at {s - t0:9.1f}")
         busy_end = max(busy_end, e.time_range.end)
+    if dump:
+        with open(dump, "w") as fh:
+            for e in ev:
+                fh.write(f"{e.time_range.start - t0:10.1f} {e.time_range.end - e.time_range.start:9.1f} "
+                         f"{e.name.split('(')[0][:60]}\n")
     print(f"config {config}: span {busy_end - t0:.1f} us, device idle {idle:.1f} us, {len(ev)} activities")
 
 
