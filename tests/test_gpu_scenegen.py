@@ -174,3 +174,26 @@ def test_config4_full_size_on_device_solves():
     S = sys_.ensure_explicit()
     assert 2.0e6 < S.blocks.shape[0] < 3.0e6
     assert cg.iterations <= 30 and cg.relative_residual <= 1e-6
+
+
+@pytest.mark.parametrize("n, pts_band, obs_band", [(3, (0.93e6, 1.0e6), (4.6e6, 5.7e6)), (5, (1.95e6, 2.0e6), (7.5e6, 8.5e6))])
+def test_configs_3_and_5_full_size_on_device_solve(n, pts_band, obs_band):
+    """BASELINE configs 3 and 5 at full size from the device generator: sizes next to the
+    numpy scenes' (977 k points / 5.12 M observations; 2.0 M / 8.0 M) and the multigrid
+    PCG of the first LM linear solve converges within the numpy scenes' counts + 3."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2007_01941_b200 as P
+    from paper_2007_01941_b200 import scenes
+
+    sc = scenes.device_config(n, seed=0)
+    assert pts_band[0] < sc.n_points <= pts_band[1], sc.n_points
+    assert obs_band[0] < sc.n_observations < obs_band[1], sc.n_observations
+    prob = P.BundleProblem(*sc.arrays())
+    cfg = P.SolveConfig(preconditioner="multigrid", tau=1e-30, cg_max_iterations=200, cg_residual_tolerance=1e-6)
+    obj, jac = P.evaluate(prob)
+    dc, dp, cg, *_ = P.solver.linear_solve(prob, jac, 1e4, cfg)
+    assert cg.relative_residual <= 1e-6
+    assert cg.iterations <= {3: 15, 5: 27}[n] + 3, cg.iterations
