@@ -1154,6 +1154,9 @@ k_aggregate_seq(const int* __restrict__ G_ptr, const int* __restrict__ G_col, co
   }
   __syncwarp();
   int nagg = 0;
+#ifdef AGG_STATS
+  int st_slow = 0, st_coop = 0, st_none = 0;
+#endif
   for (int b = 0; b < nbt; ++b) {
     cp_async_wait<AH_NB - 1>();
     __syncwarp();
@@ -1174,13 +1177,13 @@ k_aggregate_seq(const int* __restrict__ G_ptr, const int* __restrict__ G_col, co
           const int self = agg[i];
           const int j0 = nj0;
           const double2 g = ng;
+          const int a0 = agg[j0 >= 0 ? j0 : 0];  // issued with the load above, used only when j0 >= 0
           if (k + 1 < iend) {  // the next node's top entries (state independent)
             nj0 = scol[(slot * AH_B + k + 1) * AH_K];
             ng = *reinterpret_cast<const double2*>(sval + (slot * AH_B + k + 1) * AH_K);
           }
           if (self >= 0) continue;
           if (j0 >= 0 && g.x != g.y) {
-            const int a0 = agg[j0];
             if (a0 < 0) {
               agg[i] = nagg0;
               agg[j0] = nagg0;
@@ -1204,6 +1207,9 @@ k_aggregate_seq(const int* __restrict__ G_ptr, const int* __restrict__ G_col, co
       ii = stop + 1;
       if (stop >= iend) break;
       // general rule for node `stop`, every lane redundantly (broadcast loads)
+#ifdef AGG_STATS
+      ++st_slow;
+#endif
       const int i = b * AH_B + stop;
       const int* hc = scol + (slot * AH_B + stop) * AH_K;
       const double* hv = sval + (slot * AH_B + stop) * AH_K;
@@ -1245,6 +1251,10 @@ k_aggregate_seq(const int* __restrict__ G_ptr, const int* __restrict__ G_col, co
         }
       }
       int bj = dec;
+#ifdef AGG_STATS
+      if (dec == -3) ++st_coop;
+      if (dec == -1) ++st_none;
+#endif
       if (dec == -3) bj = agg_visit_coop(i, G_ptr, G_col, G_val, hc, hv, len, agg, size, max_size, lane);
       if (bj >= 0) {
         const int aj = agg[bj];  // every lane reads the pre-update value
@@ -1268,6 +1278,9 @@ k_aggregate_seq(const int* __restrict__ G_ptr, const int* __restrict__ G_col, co
     else cp_async_commit();
   }
   cp_async_wait<0>();
+#ifdef AGG_STATS
+  if (lane == 0) printf("agg_seq n=%d slow=%d coop=%d none=%d\n", n, st_slow, st_coop, st_none);
+#endif
   // post-pass over leftovers in index order (multigrid.py:164-175); a leftover's visit
   // assigns only itself, so the unassigned set of a 32-node window is read once
   for (int i0 = 0; i0 < n; i0 += 32) {
