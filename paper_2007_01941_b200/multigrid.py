@@ -157,12 +157,23 @@ class Aggregation:
 
 def aggregate(strength: StrengthMatrix, max_size: int = 20) -> Aggregation:
     """Greedy pairwise aggregation (multigrid.py:127-176), bit-exact scan order."""
+    return _aggregate_finish(_aggregate_launch(strength, max_size))
+
+
+def _aggregate_launch(strength: StrengthMatrix, max_size: int):
+    """Queue the scan (no readback): the caller may issue other work in its shadow."""
     n = strength.n
     agg = D.empty(max(n, 1), dtype=torch.int32)
     work = D.empty(max(n, 1), dtype=torch.int32)
     na = D.empty(2, dtype=torch.int32)
     D.call("bamg_aggregate", strength.indptr, strength._col, strength._val, n, int(max_size), agg, work, na,
            strength._col.numel())
+    return strength, agg, work, na
+
+
+def _aggregate_finish(pending) -> Aggregation:
+    strength, agg, work, na = pending
+    n = strength.n
     # one readback: aggregate count, largest aggregate, and a pending strength flag
     vals = (torch.cat([na, strength._flags[:1]]) if strength._flags is not None else na).tolist()
     if strength._flags is not None and vals[2]:
@@ -666,12 +677,35 @@ def build_hierarchy(sys: SchurSystem, nullspace: DenseTall, strength: StrengthMa
     main = torch.cuda.current_stream()
     side = _side_stream() if _OVERLAP else None
     pend = []
+    deferred = None  # (level, event): a smoother setup waiting to be issued
+
+    def issue_deferred():
+        # ~75 launches (one C call): issued while the main stream is busy with the next
+        # level's single-warp aggregation scan, not in front of it
+        nonlocal deferred
+        if deferred is None:
+            return
+        lvl, ev = deferred
+        deferred = None
+        if side is None:
+            return
+        side.wait_event(ev)
+        with torch.cuda.stream(side):
+            p = _smoother_launch(lvl, seed)
+        if p is not None:
+            pend.append(p)
+            jac = p[1]  # allocated on the side stream, used by V-cycles on the main one
+            for t in (jac.blocks, jac._inv, jac._chol):
+                t.record_stream(main)
+
     while levels[-1].scalar_dim > max_coarse_dim:
         cur = levels[-1]
         if cur.index == 0:
             agg = _aggregate_cached(strength, max_aggregate)
         else:
-            agg = aggregate(_operator_strength(cur.explicit), max_size=max_aggregate)
+            scan = _aggregate_launch(_operator_strength(cur.explicit), max_aggregate)
+            issue_deferred()
+            agg = _aggregate_finish(scan)
         D.phase("mg.aggregate")
         ratio = (agg.n_aggregates * NULLSPACE_DIM) / cur.scalar_dim
         if ratio > max_ratio:
@@ -687,14 +721,8 @@ def build_hierarchy(sys: SchurSystem, nullspace: DenseTall, strength: StrengthMa
                               K_next))
         K = K_next
         if side is not None:
-            side.wait_stream(main)
-            with torch.cuda.stream(side):
-                p = _smoother_launch(cur, seed)
-            if p is not None:
-                pend.append(p)
-                jac = p[1]  # allocated on the side stream, used by V-cycles on the main one
-                for t in (jac.blocks, jac._inv, jac._chol):
-                    t.record_stream(main)
+            deferred = (cur, main.record_event())
+    issue_deferred()
     # The coarsest factorisation is queued first; the smoothers' readback then waits
     # for the side stream only, and the native plan (work arena, V-cycle graph capture
     # / re-target: host work) is prepared while the factorisation runs. The errors
