@@ -364,13 +364,11 @@ def gpu_arm(args, rank, world):
     torch.cuda.synchronize()
     # hygiene: collect now and park the survivors in the permanent generation, so a
     # collection inside the timed steps only looks at the objects those steps create (a
-    # step leaves no reference cycles behind: tools/find_cycles.py). What remains in the
-    # per-step log is external: on the GPU boxes one e2e step in ~15 (about once a second)
-    # takes +30 ms and very rarely +350-500 ms while the device-timed steps next to it do
-    # not move -- a 1 Hz poller on the box holding the driver lock against this loop's
-    # blocking calls (graph instantiation, stream-ordered allocation, readbacks)
+    # step leaves no reference cycles behind: tools/find_cycles.py). The per-step log
+    # below is the evidence for host-side interference on a busy box
     gc.collect()
-    gc.freeze()
+    if os.environ.get("BAMG_BENCH_GC_FREEZE", "1") == "1":
+        gc.freeze()
     e0.record()
     t_host = time.perf_counter()
     for it in range(max(1, args.steps)):
