@@ -280,7 +280,8 @@ def test_chebyshev_matches_oracle(P):
     (1, 300, 6, 20, 4), (2, 2000, 12, 20, 8), (3, 700, 30, 3, 3), (4, 500, 9, 2, 5), (5, 4000, 40, 20, 16),
     (6, 1500, 3, 20, 2)])
 def test_aggregate_speculative_scan_matches_oracle(P, seed, n, deg, max_size, levels):
-    """The speculative batch scan (k_aggregate_spec) against the oracle's sequential
+    """The aggregation scan (k_aggregate_seq by default; the speculative batch scan
+    k_aggregate_spec under BAMG_AGG_SEQ=0) against the oracle's sequential
     greedy scan (multigrid.py:127-176) on random graphs built to collide: local
     neighbourhoods (consecutive nodes are neighbours, as coarse aggregates are),
     few distinct strengths (ties everywhere), rows longer than the 8-entry head,
@@ -302,3 +303,24 @@ def test_aggregate_speculative_scan_matches_oracle(P, seed, n, deg, max_size, le
     want, na = O.aggregate(g, max_size)
     assert agg.n_aggregates == na
     np.testing.assert_array_equal(D().host(agg.assignment), want)
+
+
+def test_aggregate_alternative_kernels_still_match():
+    """The scan kernels that are no longer the default (speculative rounds, BAMG_AGG_SEQ=0;
+    cooperative head scan, BAMG_AGG_SPEC=0 as well) stay bit-exact: the aggregation tests
+    of this file re-run in a subprocess with the environment switches set (they are read
+    once per process)."""
+    import os
+    import subprocess
+    import sys
+
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    here = os.path.abspath(__file__)
+    for env in ({"BAMG_AGG_SEQ": "0"}, {"BAMG_AGG_SEQ": "0", "BAMG_AGG_SPEC": "0"}):
+        p = subprocess.run([sys.executable, "-m", "pytest", here, "-q", "-x", "-k",
+                            "aggregate_known_answers or aggregate_speculative_scan"],
+                           env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, (env, p.stdout[-2000:], p.stderr[-2000:])
