@@ -1124,13 +1124,15 @@ k_aggregate_spec(const int* __restrict__ G_ptr, const int* __restrict__ G_col, c
 // ---------------------------------------------------------------------------
 // Low-latency sequential form of the same scan (identical decisions). On the coarse
 // levels the neighbours of a node sit a few indices away, so most of a speculative
-// batch conflicts and its rounds cost ~500 cycles per node. Here every lane runs the
-// SAME one-node-at-a-time decision redundantly from shared memory (broadcast loads,
-// no shuffles, no ballots): the dependent chain per node is agg[j] -> size[agg[j]]
-// -> the head rule -> one store, ~100-150 cycles; the next node's head entries are
-// state independent and are loaded ahead. Visits the head cannot decide (tie run
-// past the head, no eligible head entry in a longer row, unsorted row) fall back to
-// the cooperative visit of k_aggregate_head.
+// batch conflicts and its rounds cost ~500 cycles per node. Here lane 0 alone walks the
+// batch's unassigned nodes (a register mask, built by one ballot per batch) and decides
+// every node whose top head entry is not tied with the second one: one state load, the
+// decision, the stores -- same-thread ordering, no warp synchronisation per node. ncu:
+// ~24 instructions per node at ~7.7 cycles each (fixed-latency dependency waits 3.2,
+// shared-memory scoreboard 2.9), i.e. the single-warp issue limit of a dependent chain.
+// Ties, ineligible tops and unsorted rows take the general head rule (every lane
+// redundantly, broadcast loads, no shuffles) or the cooperative row visit of
+// k_aggregate_head.
 __global__ void __launch_bounds__(32)
 k_aggregate_seq(const int* __restrict__ G_ptr, const int* __restrict__ G_col, const double* __restrict__ G_val,
                 const int* __restrict__ hcol_g, const double* __restrict__ hval_g, const int* __restrict__ hlen_g,
@@ -1139,7 +1141,8 @@ k_aggregate_seq(const int* __restrict__ G_ptr, const int* __restrict__ G_col, co
   double* sval = shh;                                              // AH_NB * AH_B * AH_K
   int* scol = reinterpret_cast<int*>(sval + AH_NB * AH_B * AH_K);  // AH_NB * AH_B * AH_K
   int* slen = scol + AH_NB * AH_B * AH_K;                          // AH_NB * AH_B
-  int* agg = slen + AH_NB * AH_B;                                  // n
+  int* tops = slen + AH_NB * AH_B;                                 // AH_B: the current batch's top entries
+  int* agg = tops + AH_B;                                          // n
   int* size = agg + n;                                             // n
   const int lane = threadIdx.x;
   for (int i = lane; i < n; i += 32) {
@@ -1162,50 +1165,57 @@ k_aggregate_seq(const int* __restrict__ G_ptr, const int* __restrict__ G_col, co
     __syncwarp();
     const int slot = b % AH_NB;
     const int iend = min(AH_B, n - b * AH_B);
-    int ii = 0;
-    while (ii < iend) {  // warp uniform
+    const int base = b * AH_B;
+    // per batch, all lanes: each node's deciding top entry (-1: tied with the second entry,
+    // no entry, or an unsorted row -> the general rule) and the unassigned nodes' mask
+    {
+      const int j0 = scol[(slot * AH_B + lane) * AH_K];
+      const double2 g = *reinterpret_cast<const double2*>(sval + (slot * AH_B + lane) * AH_K);
+      tops[lane] = (j0 >= 0 && g.x != g.y) ? j0 : -1;
+    }
+    unsigned todo = __ballot_sync(FULL_MASK, lane < iend && agg[base + lane] < 0);
+    __syncwarp();
+    while (todo) {  // warp uniform
       // fast path, lane 0 alone (same-thread ordering, no warp synchronisation per
-      // node): the top head entry is not tied with the second one, so it wins as soon
-      // as it is eligible -- pair if unassigned, join if its aggregate has room
-      int stop = iend, nagg0 = nagg;
+      // node): an untied top entry wins as soon as it is eligible -- pair if unassigned,
+      // join if its aggregate has room. The batch's unassigned nodes are a register
+      // mask (a partner inside the batch clears its own bit), so the dependent chain
+      // per node is one state load, the decision, the stores.
+      int stop = -1, nagg0 = nagg;
       if (lane == 0) {
-        int k = ii;
-        int nj0 = scol[(slot * AH_B + k) * AH_K];
-        double2 ng = *reinterpret_cast<const double2*>(sval + (slot * AH_B + k) * AH_K);
-        for (; k < iend; ++k) {
-          const int i = b * AH_B + k;
-          const int self = agg[i];
-          const int j0 = nj0;
-          const double2 g = ng;
-          const int a0 = agg[j0 >= 0 ? j0 : 0];  // issued with the load above, used only when j0 >= 0
-          if (k + 1 < iend) {  // the next node's top entries (state independent)
-            nj0 = scol[(slot * AH_B + k + 1) * AH_K];
-            ng = *reinterpret_cast<const double2*>(sval + (slot * AH_B + k + 1) * AH_K);
+        unsigned t = todo;
+        while (t) {
+          const int k = __ffs(t) - 1;
+          const int j0 = tops[k];
+          if (j0 < 0) {
+            stop = k;
+            break;
           }
-          if (self >= 0) continue;
-          if (j0 >= 0 && g.x != g.y) {
-            if (a0 < 0) {
-              agg[i] = nagg0;
-              agg[j0] = nagg0;
-              size[nagg0] = 2;
-              ++nagg0;
-              continue;
-            }
-            if (size[a0] < max_size) {
-              agg[i] = a0;
-              size[a0] += 1;
-              continue;
-            }
+          const int a0 = agg[j0];
+          if (a0 < 0) {
+            agg[base + k] = nagg0;
+            agg[j0] = nagg0;
+            size[nagg0] = 2;
+            ++nagg0;
+            t &= t - 1;
+            const unsigned d = (unsigned)(j0 - base);
+            if (d < 32u) t &= ~(1u << d);
+            continue;
           }
-          break;  // the general rule decides this node
+          if (size[a0] < max_size) {
+            agg[base + k] = a0;
+            size[a0] += 1;
+            t &= t - 1;
+            continue;
+          }
+          stop = k;  // its aggregate is full: the general rule looks further
+          break;
         }
-        stop = k;
       }
       stop = __shfl_sync(FULL_MASK, stop, 0);
       nagg = __shfl_sync(FULL_MASK, nagg0, 0);
       __syncwarp();
-      ii = stop + 1;
-      if (stop >= iend) break;
+      if (stop < 0) break;
       // general rule for node `stop`, every lane redundantly (broadcast loads)
 #ifdef AGG_STATS
       ++st_slow;
@@ -1272,6 +1282,8 @@ k_aggregate_seq(const int* __restrict__ G_ptr, const int* __restrict__ G_col, co
         if (aj < 0) ++nagg;
         __syncwarp();
       }
+      // the nodes after `stop` that are still unassigned (the visit above may have taken one)
+      todo = __ballot_sync(FULL_MASK, lane > stop && lane < iend && agg[base + lane] < 0);
     }
     __syncwarp();  // every lane is done with this slot before it is refilled
     if (b + AH_NB < nbt) ah_issue(b + AH_NB, hcol_g, hval_g, hlen_g, scol, sval, slen, lane);
