@@ -86,3 +86,25 @@ def test_compute_without_gpu_fails_loudly():
 
     with pytest.raises(_lib.NativeError):
         problem.BundleProblem([[0.0] * 9], [[0.0, 0.0, 1.0]], [0], [0], [[0.0, 0.0]])
+
+
+def test_device_scene_arguments_checked_before_any_gpu_work():
+    """scenes.device_config validates the configuration number and parameter names on
+    the host (no CUDA needed for that), and the scene entry points are exported."""
+    import ctypes
+
+    import pytest
+
+    from paper_2007_01941_b200 import _lib, scenes
+
+    with pytest.raises(ValueError):
+        scenes.device_config(2)
+    with pytest.raises(TypeError):
+        scenes.device_config(4, n_camera=10)
+    L = _lib.lib()
+    for name in ("bamg_scene_grid_cells", "bamg_scene_layout", "bamg_scene_visibility", "bamg_scene_emit"):
+        assert hasattr(L, name)
+    # the grid-size helper is pure host code: city defaults -> ceil(200 / 15) + 1 cells a side
+    p = (ctypes.c_double * 8)(200.0, 1, 0, 0, 20.0, 4.0, 15.0, 0.0)
+    assert L.bamg_scene_grid_cells(3, 4000, 1_000_000, ctypes.addressof(p)) == 15 * 15
+    assert L.bamg_scene_grid_cells(7, 4000, 1_000_000, ctypes.addressof(p)) == -1
